@@ -1,0 +1,258 @@
+"""Generate tests/golden/* by running the REFERENCE itself (poromgr).
+
+Run in the build container only (the reference is not on the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python oracle/make_golden.py
+
+It imports /root/reference/pkg/src read-only, applies the two adapter shims
+SURVEY.md §8c prescribes (FieldLayout.restrict downgrade for the mgr.py:359
+interleave bug; a hand-built hierarchy for the 4-field config), configures
+the parity smoother (npartitions >= n, i.e. l1-Jacobi) and dumps every setup
+product, one preconditioner application and a GMRES solve.  Small cases are
+stored as full arrays; large ones as SHA-256 digests of the canonical bytes
+(zeros normalised to +0.0) plus the vectors.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = os.environ.get("POROMGR_SRC", "/root/reference/pkg/src")
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+OUT = os.path.join(REPO, "tests", "golden")
+sys.path.insert(0, REF)
+sys.path.insert(0, REPO)
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+import numba  # noqa: E402
+import scipy  # noqa: E402
+import poromgr.sparse as psp  # noqa: E402
+
+_orig_restrict = psp.FieldLayout.restrict
+
+
+def _restrict(self, idx):  # shim 1: mgr.py:359 x sparse.py:180-189
+    try:
+        return _orig_restrict(self, idx)
+    except ValueError:
+        return psp.FieldLayout(self.field_of[idx], self.entity_of[idx], psp.Ordering.FIELD_BLOCKED)
+
+
+psp.FieldLayout.restrict = _restrict
+
+from poromgr import mgr as pmgr  # noqa: E402
+from poromgr.amg import AmgConfig, amg_setup, amg_vcycle, strength_graph  # noqa: E402
+from poromgr.krylov import GmresConfig, gmres  # noqa: E402
+from poromgr.smoothers import PartitionSet, l1_diagonal, l1_gs_sweep  # noqa: E402
+from poromgr.sparse import (CfSplitting, CsrMatrix, Field, FieldLayout, extract_blocks,  # noqa: E402
+                            matvec, sparsify, spgemm, subtract)
+
+from paper_1904_05960_b200 import problems  # noqa: E402
+
+JACOBI = 10 ** 9
+VERSIONS = dict(numpy=np.__version__, scipy=scipy.__version__, numba=numba.__version__)
+
+
+def digest(ro, ci, v=None) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(ro, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(ci, dtype=np.int32).tobytes())
+    if v is not None:
+        vv = np.ascontiguousarray(v, dtype=np.float64) + 0.0
+        h.update(vv.tobytes())
+    return h.hexdigest()
+
+
+def dcsr(m: CsrMatrix) -> str:
+    return digest(m.row_offsets, m.col_indices, m.values)
+
+
+def put_csr(d, key, m: CsrMatrix):
+    d[key + "_ro"] = m.row_offsets
+    d[key + "_ci"] = m.col_indices
+    d[key + "_v"] = m.values
+    d[key + "_shape"] = np.array(m.shape)
+
+
+def parity_config(levels, f_parts=JACOBI, t_parts=JACOBI):
+    return pmgr.MgrConfig(levels=levels,
+                          amg_f_relax=AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=f_parts),
+                          amg_terminal=AmgConfig(strength_threshold=0.25, npartitions=t_parts))
+
+
+def levels_for(pb, n_max):
+    if pb.cell_fields == (problems.FIELD_P,):
+        return (pmgr.MgrLevelSpec({Field.U}, {Field.P}, f_relax="amg", n_max=n_max),)
+    return (pmgr.MgrLevelSpec({Field.U}, {Field.S, Field.P}, f_relax="amg", n_max=n_max),
+            pmgr.MgrLevelSpec({Field.S}, {Field.P}, f_relax="jacobi", n_max=None))
+
+
+def setup_4field(A, layout, n_max, cfg):
+    """Shim 2: U -> S2 -> S1 -> P built from reference primitives
+    (mgr.py:300-326 containers)."""
+    cur, lay = A, layout
+    levs = []
+    order = [(problems.FIELD_U, "amg", n_max), (problems.FIELD_S2, "jacobi", None),
+             (problems.FIELD_S, "jacobi", None)]
+    for tag, relax, nm in order:
+        fspec = {Field.U} if tag == problems.FIELD_U else {Field.S}
+        spec = pmgr.MgrLevelSpec(fspec, {Field.P}, f_relax=relax, n_max=nm)
+        split = CfSplitting(lay.field_of != tag)
+        blocks = extract_blocks(cur, split)
+        P, R = pmgr.build_transfers(blocks, split, spec, cfg.ideal_size_cap)
+        f_relax = pmgr._build_f_relax(blocks[0], spec, cfg)
+        coarse = pmgr.build_coarse(cur, lay, split, blocks, P, R, spec)
+        levs.append(pmgr._MgrLevel(cur, lay, split, blocks, P, R, f_relax, None, spec))
+        lay = FieldLayout(lay.field_of[split.c_rows()], lay.entity_of[split.c_rows()])
+        cur = coarse
+    term = amg_setup(cur, cfg.amg_terminal)
+    return pmgr.MgrHierarchy(levs, cur, "amg", term, 1, "pre")
+
+
+def dump_amg(d, prefix, h, full):
+    d[prefix + "sizes"] = np.array(h.level_sizes())
+    for i, lv in enumerate(h.levels):
+        k = f"{prefix}L{i}_"
+        if full:
+            d[k + "isc"] = lv.split.is_c
+            put_csr(d, k + "P", lv.P)
+            put_csr(d, k + "A", lv.A)
+            d[k + "dtilde"] = lv.dtilde
+        else:
+            d[k + "isc_sha"] = hashlib.sha256(lv.split.is_c.tobytes()).hexdigest()
+            d[k + "P_sha"] = dcsr(lv.P)
+            d[k + "A_sha"] = dcsr(lv.A)
+            d[k + "dtilde_sha"] = hashlib.sha256((lv.dtilde + 0.0).tobytes()).hexdigest()
+    if full:
+        put_csr(d, prefix + "coarse", h.coarse_A)
+    else:
+        d[prefix + "coarse_sha"] = dcsr(h.coarse_A)
+
+
+def dump_problem(tag, pb, n_max, full, restart=100, four_field=False):
+    A = CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    lay = FieldLayout(pb.field_of, pb.entity_of)
+    if four_field:
+        cfg = parity_config(())
+        h = setup_4field(A, lay, n_max, cfg)
+    else:
+        cfg = parity_config(levels_for(pb, n_max))
+        h = pmgr.mgr_setup(A, lay, cfg)
+    d = {}
+    d["input_sha"] = np.array(digest(pb.row_offsets, pb.col_indices, pb.values))
+    d["rhs_sha"] = np.array(hashlib.sha256(pb.rhs.tobytes()).hexdigest())
+    d["mgr_sizes"] = np.array(h.level_sizes())
+    for i, lv in enumerate(h.levels):
+        k = f"mgr{i}_"
+        nxt = h.levels[i + 1].A if i + 1 < len(h.levels) else h.terminal_A
+        if full:
+            d[k + "isc"] = lv.split.is_c
+            put_csr(d, k + "P", lv.P)
+            put_csr(d, k + "coarse", nxt)
+        else:
+            d[k + "isc_sha"] = hashlib.sha256(lv.split.is_c.tobytes()).hexdigest()
+            d[k + "P_sha"] = dcsr(lv.P)
+            d[k + "coarse_sha"] = dcsr(nxt)
+        if isinstance(lv.f_relax, pmgr._AmgFRelax):
+            dump_amg(d, k + "amg_", lv.f_relax.hierarchy, full)
+    dump_amg(d, "term_", h.terminal_solver, full)
+    rng = np.random.default_rng(1234)
+    v = rng.standard_normal(pb.n)
+    d["apply_v"] = v
+    d["apply_z"] = pmgr.mgr_apply(h, v)
+    x, st = gmres(lambda y: matvec(A, y), h.apply, pb.rhs,
+                  cfg=GmresConfig(restart=restart, max_iters=1000, rtol=1e-6))
+    d["gmres_iters"] = np.array(st.iterations)
+    d["gmres_hist"] = st.residual_history
+    d["gmres_x"] = x
+    d["gmres_conv"] = np.array(st.converged)
+    d["versions"] = np.array(json.dumps(VERSIONS))
+    path = os.path.join(OUT, f"ref_{tag}.npz")
+    np.savez_compressed(path, **d)
+    print(tag, pb.n, pb.nnz, "levels", h.level_sizes(), "its", st.iterations, "->", path,
+          os.path.getsize(path) // 1024, "KiB")
+
+
+def dump_units():
+    """Kernel-level cases on the reference's own fixture shapes."""
+    sys.path.insert(0, os.path.join(os.path.dirname(REF), "tests"))
+    from common import diag_dominant_random, laplacian_2d
+
+    d = {}
+    rng = np.random.default_rng(7)
+    # spgemm (structural) / subtract / sparsify on random two-field matrices
+    for t in range(6):
+        A = diag_dominant_random(rng, 40, density=0.15)
+        B = diag_dominant_random(rng, 40, density=0.15)
+        put_csr(d, f"u{t}_A", A)
+        put_csr(d, f"u{t}_B", B)
+        put_csr(d, f"u{t}_AB", spgemm(A, B))
+        put_csr(d, f"u{t}_AmB", subtract(A, B))
+        ent = np.repeat(np.arange(20, dtype=np.int32), 2)
+        lay = FieldLayout(np.tile([1, 2], 20).astype(np.int8), ent)
+        d[f"u{t}_ent"] = ent
+        for nm in (0, 2, 4):
+            put_csr(d, f"u{t}_sp{nm}", sparsify(A, lay, nm))
+        # Galerkin product with scipy semantics, as amg.py:200-202
+        sA, sB = A.to_scipy(), B.to_scipy()
+        put_csr(d, f"u{t}_gal", CsrMatrix.from_scipy((sB.T @ sA @ sB).tocsr()))
+        # hybrid l1-GS sweeps with 1, 3 and n partitions
+        b = rng.standard_normal(40)
+        x = rng.standard_normal(40)
+        d[f"u{t}_b"] = b
+        d[f"u{t}_x"] = x
+        for npart in (1, 3, JACOBI):
+            parts = PartitionSet.contiguous(40, npart)
+            dt = l1_diagonal(A, parts)
+            d[f"u{t}_dt{min(npart, 99)}"] = dt
+            d[f"u{t}_gsf{min(npart, 99)}"] = l1_gs_sweep(A, b, x, "forward", parts, dt)
+            d[f"u{t}_gsb{min(npart, 99)}"] = l1_gs_sweep(A, b, x, "backward", parts, dt)
+    # AMG on anisotropic 2-D Laplacians (test_amg.py's fixture family)
+    for t, (nx, eps) in enumerate(((12, 1.0), (16, 0.01), (20, 1.0))):
+        L = laplacian_2d(nx, eps_y=eps)
+        put_csr(d, f"lap{t}_A", L)
+        S = strength_graph(L, 0.25)
+        put_csr(d, f"lap{t}_S", S)
+        for npart in (1, JACOBI):
+            h = amg_setup(L, AmgConfig(npartitions=npart))
+            tag = f"lap{t}_p{min(npart, 99)}_"
+            dump_amg(d, tag, h, True)
+            b = np.random.default_rng(t).standard_normal(L.nrows)
+            d[tag + "b"] = b
+            d[tag + "vcyc"] = amg_vcycle(h, b, np.zeros(L.nrows))
+            x, st = gmres(lambda y: matvec(L, y), lambda y: amg_vcycle(h, y, np.zeros(L.nrows)), b,
+                          cfg=GmresConfig(restart=30, max_iters=200, rtol=1e-8))
+            d[tag + "its"] = np.array(st.iterations)
+            d[tag + "hist"] = st.residual_history
+            d[tag + "x"] = x
+    d["versions"] = np.array(json.dumps(VERSIONS))
+    path = os.path.join(OUT, "ref_units.npz")
+    np.savez_compressed(path, **d)
+    print("units ->", path, os.path.getsize(path) // 1024, "KiB")
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    which = sys.argv[1:] or ["units", "c1_6", "c2_6", "c4_4", "c1_16", "c2_32"]
+    if "units" in which:
+        dump_units()
+    if "c1_6" in which:
+        dump_problem("c1_6", problems.make_c1(seed=3, n=6), None, True)
+    if "c2_6" in which:
+        dump_problem("c2_6", problems.make_c2(seed=5, n=6), 4, True)
+    if "c4_4" in which:
+        dump_problem("c4_4", problems.make_c4(seed=9, n=4), 4, True, four_field=True)
+    if "c1_16" in which:
+        dump_problem("c1_16", problems.make_c1(seed=0, n=16), None, False)
+    if "c2_32" in which:
+        dump_problem("c2_32", problems.make_c2(seed=0, n=32), 4, False)
+
+
+if __name__ == "__main__":
+    main()

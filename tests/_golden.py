@@ -1,0 +1,81 @@
+"""Helpers shared by the parity tests: load golden fixtures, digests,
+oracle hierarchies for the generated problems (test infrastructure)."""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+
+from oracle import oracle as O
+from paper_1904_05960_b200 import problems
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+JACOBI = 10 ** 9
+
+
+def load(tag):
+    return np.load(os.path.join(GOLDEN, f"ref_{tag}.npz"))
+
+
+def digest(ro, ci, v=None) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(ro, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(ci, dtype=np.int32).tobytes())
+    if v is not None:
+        h.update((np.ascontiguousarray(v, dtype=np.float64) + 0.0).tobytes())
+    return h.hexdigest()
+
+
+def dcsr(m) -> str:
+    return digest(m.ro, m.ci, m.v)
+
+
+def vec_sha(v) -> str:
+    return hashlib.sha256((np.ascontiguousarray(v, dtype=np.float64) + 0.0).tobytes()).hexdigest()
+
+
+def get_csr(d, key):
+    shape = d[key + "_shape"]
+    return O.Csr(int(shape[0]), int(shape[1]), d[key + "_ro"], d[key + "_ci"], d[key + "_v"])
+
+
+# problem tag -> (generator call, n_max, four_field)
+CASES = {
+    "c1_6": (lambda: problems.make_c1(seed=3, n=6), None, False),
+    "c2_6": (lambda: problems.make_c2(seed=5, n=6), 4, False),
+    "c4_4": (lambda: problems.make_c4(seed=9, n=4), 4, True),
+    "c1_16": (lambda: problems.make_c1(seed=0, n=16), None, False),
+    "c2_32": (lambda: problems.make_c2(seed=0, n=32), 4, False),
+}
+
+
+def oracle_levels(pb, n_max, four_field):
+    U, S, P, S2 = problems.FIELD_U, problems.FIELD_S, problems.FIELD_P, problems.FIELD_S2
+    if four_field:
+        return (O.MgrLevelSpec(frozenset({U}), frozenset({S, S2, P}), "amg", 1, n_max),
+                O.MgrLevelSpec(frozenset({S2}), frozenset({S, P}), "jacobi", 1, None),
+                O.MgrLevelSpec(frozenset({S}), frozenset({P}), "jacobi", 1, None))
+    if pb.cell_fields == (P,):
+        return (O.MgrLevelSpec(frozenset({U}), frozenset({P}), "amg", 1, n_max),)
+    return (O.MgrLevelSpec(frozenset({U}), frozenset({S, P}), "amg", 1, n_max),
+            O.MgrLevelSpec(frozenset({S}), frozenset({P}), "jacobi", 1, None))
+
+
+def oracle_config(levels, parts=JACOBI):
+    return O.MgrConfig(levels=levels,
+                       amg_f_relax=O.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=parts),
+                       amg_terminal=O.AmgConfig(strength_threshold=0.25, npartitions=parts))
+
+
+def problem_csr(pb):
+    return O.Csr(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+
+
+def oracle_hierarchy(tag):
+    gen, n_max, four = CASES[tag]
+    pb = gen()
+    cfg = oracle_config(oracle_levels(pb, n_max, four))
+    h = O.mgr_setup(problem_csr(pb), pb.field_of, pb.entity_of, cfg)
+    return pb, h

@@ -1,0 +1,120 @@
+"""Pin the CPU oracle to the reference: every golden fixture produced by
+oracle/make_golden.py (running poromgr itself) must be reproduced bitwise for
+patterns/setup values, and to 1e-12 for applies and solves."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests._golden import (CASES, dcsr, digest, get_csr, load, oracle_hierarchy, vec_sha)
+
+
+@pytest.fixture(scope="module")
+def units():
+    return load("units")
+
+
+def same_csr(a, b):
+    assert (a.nrows, a.ncols) == (b.nrows, b.ncols)
+    assert np.array_equal(a.ro, b.ro)
+    assert np.array_equal(a.ci, b.ci)
+    assert np.array_equal(a.v, b.v)
+
+
+@pytest.mark.parametrize("t", range(6))
+def test_spgemm_subtract_sparsify_bitwise(units, t):
+    A, B = get_csr(units, f"u{t}_A"), get_csr(units, f"u{t}_B")
+    same_csr(O.spgemm(A, B, True), get_csr(units, f"u{t}_AB"))
+    same_csr(O.subtract(A, B), get_csr(units, f"u{t}_AmB"))
+    for nm in (0, 2, 4):
+        same_csr(O.sparsify(A, units[f"u{t}_ent"], nm), get_csr(units, f"u{t}_sp{nm}"))
+    # Galerkin B^T A B with scipy's zero dropping
+    same_csr(O.galerkin(B, O.transpose(B), A), get_csr(units, f"u{t}_gal"))
+
+
+@pytest.mark.parametrize("t", range(6))
+@pytest.mark.parametrize("npart", [1, 3, 10 ** 9])
+def test_hybrid_l1gs_bitwise(units, t, npart):
+    A = get_csr(units, f"u{t}_A")
+    b, x = units[f"u{t}_b"], units[f"u{t}_x"]
+    starts = O.partition_starts(A.nrows, npart)
+    dt = O.l1_diagonal(A, starts)
+    k = min(npart, 99)
+    assert np.array_equal(dt, units[f"u{t}_dt{k}"])
+    assert np.array_equal(O.l1_sweep(A, b, x, starts, dt, True), units[f"u{t}_gsf{k}"])
+    assert np.array_equal(O.l1_sweep(A, b, x, starts, dt, False), units[f"u{t}_gsb{k}"])
+
+
+def check_amg(d, prefix, h, full):
+    sizes = d[prefix + "sizes"]
+    assert list(h.level_sizes()) == list(sizes)
+    for i, lv in enumerate(h.levels):
+        k = f"{prefix}L{i}_"
+        if full:
+            assert np.array_equal(lv.is_c, d[k + "isc"])
+            same_csr(lv.P, get_csr(d, k + "P"))
+            same_csr(lv.A, get_csr(d, k + "A"))
+            assert np.array_equal(lv.dtilde, d[k + "dtilde"])
+        else:
+            import hashlib
+            assert hashlib.sha256(lv.is_c.tobytes()).hexdigest() == str(d[k + "isc_sha"])
+            assert dcsr(lv.P) == str(d[k + "P_sha"])
+            assert dcsr(lv.A) == str(d[k + "A_sha"])
+            assert vec_sha(lv.dtilde) == str(d[k + "dtilde_sha"])
+    if full:
+        same_csr(h.coarse_A, get_csr(d, prefix + "coarse"))
+    else:
+        assert dcsr(h.coarse_A) == str(d[prefix + "coarse_sha"])
+
+
+@pytest.mark.parametrize("t", range(3))
+@pytest.mark.parametrize("npart", [1, 10 ** 9])
+def test_amg_laplacian(units, t, npart):
+    L = get_csr(units, f"lap{t}_A")
+    mask = O.strength_mask(L, 0.25, np.zeros(L.nrows, dtype=np.int32))
+    same_csr(O.mask_to_pattern(L, mask), get_csr(units, f"lap{t}_S"))
+    h = O.amg_setup(L, O.AmgConfig(npartitions=npart))
+    tag = f"lap{t}_p{min(npart, 99)}_"
+    check_amg(units, tag, h, True)
+    b = units[tag + "b"]
+    z = O.amg_vcycle(h, b, np.zeros(L.nrows))
+    assert np.allclose(z, units[tag + "vcyc"], rtol=1e-12, atol=1e-12 * np.abs(z).max())
+    x, its, hist, conv = O.gmres(lambda y: O.spmv(L, y), lambda y: O.amg_vcycle(h, y, np.zeros(L.nrows)),
+                                 b, restart=30, max_iters=200, rtol=1e-8)
+    assert conv and its == int(units[tag + "its"])
+    assert np.allclose(hist, units[tag + "hist"], rtol=1e-8)
+
+
+@pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16",
+                                 pytest.param("c2_32", marks=pytest.mark.slow)])
+def test_mgr_problem(tag):
+    d = load(tag)
+    full = "mgr0_isc" in d.files
+    pb, h = oracle_hierarchy(tag)
+    assert digest(pb.row_offsets, pb.col_indices, pb.values) == str(d["input_sha"])
+    assert list(h.level_sizes()) == list(d["mgr_sizes"])
+    import hashlib
+    for i, lv in enumerate(h.levels):
+        k = f"mgr{i}_"
+        nxt = h.levels[i + 1].A if i + 1 < len(h.levels) else h.terminal_A
+        if full:
+            assert np.array_equal(lv.is_c, d[k + "isc"])
+            same_csr(lv.P, get_csr(d, k + "P"))
+            same_csr(nxt, get_csr(d, k + "coarse"))
+        else:
+            assert hashlib.sha256(lv.is_c.tobytes()).hexdigest() == str(d[k + "isc_sha"])
+            assert dcsr(lv.P) == str(d[k + "P_sha"])
+            assert dcsr(nxt) == str(d[k + "coarse_sha"])
+        if lv.f_relax is not None and lv.f_relax[0] == "amg":
+            check_amg(d, k + "amg_", lv.f_relax[1], full)
+    check_amg(d, "term_", h.terminal, full)
+    z = h.apply(d["apply_v"])
+    zr = d["apply_z"]
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+    A = O.Csr(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    x, its, hist, conv = O.gmres(lambda y: O.spmv(A, y), h.apply, pb.rhs, restart=100,
+                                 max_iters=1000, rtol=1e-6)
+    assert conv == bool(d["gmres_conv"])
+    assert its == int(d["gmres_iters"])
+    xr = d["gmres_x"]
+    assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
