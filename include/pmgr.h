@@ -1,0 +1,190 @@
+/*
+ * pmgr.h -- C ABI of libpmgr.so, the B200-native (sm_100a) MGR-preconditioned
+ * GMRES hot path of arxiv/paper_1904_05960 (reference package `poromgr`).
+ *
+ * The reference has no FFI: its surface is the in-process Python API of
+ * /root/reference/pkg/src/poromgr.  Each entry point below replaces one of
+ * those Python functions (cited per declaration); the Python package
+ * paper_1904_05960_b200 binds them through ctypes and reproduces the
+ * reference signatures, exceptions and messages on top.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  `stream` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream).  Pointers named *_dev are device
+ *    pointers; *_host are host pointers.
+ *  - Every call returns a pmgr_status.  On error, pmgr_last_error() gives a
+ *    thread-local message and pmgr_last_error_index() the offending row (or
+ *    -1); the Python layer maps codes to the reference exception types.
+ *  - CSR: int64 row offsets, int32 column indices (strictly increasing per
+ *    row), fp64 values -- the reference CsrMatrix dtypes (sparse.py:81-83).
+ *  - Handles own device memory; apply/solve calls are asynchronous on the
+ *    given stream and read-only over the hierarchy (one workspace per
+ *    handle; use one handle per concurrent caller).
+ */
+#ifndef PMGR_H
+#define PMGR_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PMGR_API __attribute__((visibility("default")))
+#else
+#define PMGR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PMGR_OK = 0,
+    PMGR_ERR_INVALID = 1,           /* ValueError (dimension, config, pattern)          */
+    PMGR_ERR_SINGULAR_DIAG = 2,     /* ValueError "singular diagonal: zero or missing entry at row N" (sparse.py:407) */
+    PMGR_ERR_L1_VANISHES = 3,       /* ValueError "l1 diagonal vanishes at row N" (smoothers.py:105) */
+    PMGR_ERR_DENSE_CAP = 4,         /* RuntimeError coarsest level too large (amg.py:208-209) */
+    PMGR_ERR_CUDA = 5,              /* RuntimeError from the CUDA runtime               */
+    PMGR_ERR_NOT_SUPPORTED = 6,     /* NotImplementedError (option outside the hot path) */
+    PMGR_ERR_OOM = 7,               /* MemoryError                                       */
+    PMGR_ERR_INTERP_DIAG = 8,       /* ValueError "direct interpolation requires nonzero diagonals" (amg.py:137-138) */
+    PMGR_ERR_FIELDS = 9             /* ValueError level spec fields vs present fields (mgr.py:338-344) */
+} pmgr_status;
+
+typedef struct pmgr_csr pmgr_csr;     /* device CSR matrix              (CsrMatrix, sparse.py:65)      */
+typedef struct pmgr_amg pmgr_amg;     /* classical AMG hierarchy        (AmgHierarchy, amg.py:60)      */
+typedef struct pmgr_mgr pmgr_mgr;     /* MGR hierarchy                  (MgrHierarchy, mgr.py:313)     */
+
+/* ---- library ---------------------------------------------------------- */
+PMGR_API int pmgr_version(void);
+PMGR_API const char *pmgr_last_error(void);
+PMGR_API int64_t pmgr_last_error_index(void);
+/* Number of kernel launches issued by this library so far (bench evidence). */
+PMGR_API int64_t pmgr_launch_count(void);
+
+/* ---- sparse core (sparse.py) ------------------------------------------- */
+/* Copy a CSR matrix (host or device arrays) into library-owned device memory.
+ * Validates like CsrMatrix._validate (sparse.py:86-101) when validate != 0.
+ * Replaces CsrMatrix(...) construction + to_scipy(). */
+PMGR_API int pmgr_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_offsets,
+                    const int32_t *col_indices, const double *values, int on_device,
+                    int validate, void *stream, pmgr_csr **out);
+PMGR_API int pmgr_csr_destroy(pmgr_csr *A);
+PMGR_API int pmgr_csr_info(const pmgr_csr *A, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+/* Copy the three CSR arrays out (host or device destination pointers). */
+PMGR_API int pmgr_csr_download(const pmgr_csr *A, int64_t *row_offsets, int32_t *col_indices,
+                      double *values, int to_device, void *stream);
+/* y = A x, replaces sparse.matvec (sparse.py:261-266). */
+PMGR_API int pmgr_spmv(const pmgr_csr *A, const double *x_dev, double *y_dev, void *stream);
+
+/* ---- classical AMG (amg.py) -------------------------------------------- */
+typedef struct {
+    double strength_threshold;   /* AmgConfig.strength_threshold (amg.py:37)  */
+    int32_t max_levels;          /* AmgConfig.max_levels                      */
+    int32_t coarse_size_cutoff;  /* AmgConfig.coarse_size_cutoff              */
+    int32_t num_functions;       /* AmgConfig.num_functions                   */
+    int32_t cycles;              /* AmgConfig.cycles                          */
+    int64_t npartitions;         /* AmgConfig.npartitions (>= n: l1-Jacobi)   */
+} pmgr_amg_cfg;
+
+/* Replaces amg_setup (amg.py:184-211). */
+PMGR_API int pmgr_amg_setup(const pmgr_csr *A, const pmgr_amg_cfg *cfg, void *stream, pmgr_amg **out);
+PMGR_API int pmgr_amg_destroy(pmgr_amg *h);
+/* Level count L (fine levels) ; sizes has L+1 entries (AmgHierarchy.level_sizes). */
+PMGR_API int pmgr_amg_num_levels(const pmgr_amg *h, int32_t *nlevels);
+PMGR_API int pmgr_amg_level_sizes(const pmgr_amg *h, int64_t *sizes);
+PMGR_API int pmgr_amg_flagged_rows(const pmgr_amg *h, int64_t *flagged);
+/* out = amg_vcycle(h, b, x) (amg.py:214-231); x_dev may be NULL for x = 0. */
+PMGR_API int pmgr_amg_vcycle(pmgr_amg *h, const double *b_dev, const double *x_dev, double *out_dev,
+                    void *stream);
+/* Parity export of level `level`: what = 0 A_l, 1 P_l, 2 coarsest A.  Returns
+ * a new pmgr_csr handle owned by the caller. */
+PMGR_API int pmgr_amg_export_csr(const pmgr_amg *h, int32_t level, int32_t what, void *stream,
+                        pmgr_csr **out);
+/* what = 0: is_c (int8, n_l), 1: dtilde (fp64, n_l); host destination. */
+PMGR_API int pmgr_amg_export_vec(const pmgr_amg *h, int32_t level, int32_t what, void *host_out,
+                        void *stream);
+
+/* ---- MGR (mgr.py) ------------------------------------------------------ */
+enum { PMGR_INTERP_INJECTION_ONLY = 0, PMGR_INTERP_INJECTION_JACOBI = 1, PMGR_INTERP_IDEAL = 2 };
+enum { PMGR_RESTRICT_INJECTION = 0, PMGR_RESTRICT_JACOBI = 1, PMGR_RESTRICT_IDEAL = 2 };
+enum { PMGR_FRELAX_NONE = 0, PMGR_FRELAX_JACOBI = 1, PMGR_FRELAX_AMG = 2, PMGR_FRELAX_EXACT = 3 };
+enum { PMGR_SMOOTHER_NONE = 0, PMGR_SMOOTHER_HBGS = 1, PMGR_SMOOTHER_ILU = 2 };
+
+typedef struct {                 /* MgrLevelSpec (mgr.py:53-83)                 */
+    uint64_t f_mask;             /* bit t set: field tag t is F on this level     */
+    uint64_t c_mask;             /* bit t set: field tag t is C on this level     */
+    int32_t interp;              /* PMGR_INTERP_*                                 */
+    int32_t restrict_;           /* PMGR_RESTRICT_*                               */
+    int32_t f_relax;             /* PMGR_FRELAX_*                                 */
+    int32_t f_relax_sweeps;
+    int32_t global_smoother;     /* PMGR_SMOOTHER_* (only NONE on this path)      */
+    int32_t n_max;               /* < 0: no dropping (n_max=None)                 */
+    int32_t quasi_impes;
+    int32_t amg_num_functions;   /* F-relax AMG functions (3 when F = {U})        */
+} pmgr_level_spec;
+
+typedef struct {                 /* MgrConfig (mgr.py:86-123)                     */
+    int32_t terminal_cycles;
+    int32_t f_relax_post;        /* 0: "pre", 1: "post"                           */
+    pmgr_amg_cfg amg_f_relax;
+    pmgr_amg_cfg amg_terminal;
+} pmgr_mgr_cfg;
+
+/* Replaces mgr_setup (mgr.py:329-371).  field_of (int8) / entity_of (int32)
+ * are host arrays of length n (FieldLayout, sparse.py:167-216). */
+PMGR_API int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                   const pmgr_level_spec *levels, int32_t nlevels, const pmgr_mgr_cfg *cfg,
+                   void *stream, pmgr_mgr **out);
+PMGR_API int pmgr_mgr_destroy(pmgr_mgr *h);
+/* MgrHierarchy.level_sizes (mgr.py:325): nlevels_built + 1 sizes. */
+PMGR_API int pmgr_mgr_num_levels(const pmgr_mgr *h, int32_t *nlevels);
+PMGR_API int pmgr_mgr_level_sizes(const pmgr_mgr *h, int64_t *sizes);
+/* z = mgr_apply(h, v) (mgr.py:399-429), device vectors. */
+PMGR_API int pmgr_mgr_apply(pmgr_mgr *h, const double *v_dev, double *z_dev, void *stream);
+/* Parity export: what = 0 P_l, 1 next coarse operator; returns a new handle. */
+PMGR_API int pmgr_mgr_export_csr(const pmgr_mgr *h, int32_t level, int32_t what, void *stream,
+                        pmgr_csr **out);
+/* what = 0: is_c (int8) of level `level` into host memory. */
+PMGR_API int pmgr_mgr_export_vec(const pmgr_mgr *h, int32_t level, int32_t what, void *host_out,
+                        void *stream);
+/* AMG hierarchy used by level `level` (-1: terminal); borrowed pointer. */
+PMGR_API int pmgr_mgr_amg(const pmgr_mgr *h, int32_t level, const pmgr_amg **out);
+
+/* ---- Krylov (krylov.py) ------------------------------------------------ */
+typedef struct {                 /* GmresConfig (krylov.py:18-29)                 */
+    int32_t restart;
+    int32_t max_iters;
+    double rtol;
+    double atol;
+} pmgr_gmres_cfg;
+
+typedef struct {                 /* SolveStats (krylov.py:32-36)                  */
+    int32_t iterations;
+    int32_t converged;
+    int32_t history_len;         /* entries written to `history`                  */
+    int32_t restarts;
+} pmgr_gmres_stats;
+
+/* Right-preconditioned restarted GMRES (krylov.py:39-117) with A and M both
+ * library objects: the whole solve runs on the device.  M may be NULL
+ * (identity).  x_dev holds x0 on entry (nonzero_x0 != 0) and the solution
+ * on exit.  history_host receives residual_history (capacity history_cap). */
+PMGR_API int pmgr_gmres(const pmgr_csr *A, pmgr_mgr *M, const double *b_dev, double *x_dev,
+               int nonzero_x0, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats,
+               double *history_host, int32_t history_cap, void *stream);
+/* Same solve with HOST b / x buffers: the host<->device copies are part of
+ * the call (the end-to-end entry point a reference-side binding would use). */
+PMGR_API int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_host, double *x_host,
+                    int nonzero_x0, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats,
+                    double *history_host, int32_t history_cap, void *stream);
+
+/* Device BLAS-1 helpers used by the generic (Python-callable) GMRES path:
+ * h[k] = V_k . w for k < nvec (V row-major nvec x n); w -= sum_k h[k] V_k. */
+PMGR_API int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const double *w_dev,
+                  double *h_dev, void *stream);
+PMGR_API int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h_dev,
+                   double *w_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMGR_H */

@@ -1,0 +1,307 @@
+// capi.cu -- the extern "C" surface declared in include/pmgr.h.
+//
+// Every entry point catches pmgr::Error and converts it into a status code
+// plus a thread-local message / row index that the Python layer turns back
+// into the reference's exception (ValueError / RuntimeError / ...).
+#include <cstring>
+#include <string>
+
+#include "hier.cuh"
+
+namespace {
+thread_local std::string g_msg;
+thread_local int64_t g_index = -1;
+
+int set_error(const pmgr::Error &e) {
+    g_msg = e.msg;
+    g_index = e.index;
+    return (int)e.code;
+}
+
+template <class F>
+int guard(F &&f) {
+    try {
+        f();
+        return PMGR_OK;
+    } catch (const pmgr::Error &e) {
+        return set_error(e);
+    } catch (const std::bad_alloc &) {
+        g_msg = "host allocation failed";
+        g_index = -1;
+        return PMGR_ERR_OOM;
+    } catch (const std::exception &e) {
+        g_msg = e.what();
+        g_index = -1;
+        return PMGR_ERR_CUDA;
+    }
+}
+
+cudaStream_t S(void *p) { return (cudaStream_t)p; }
+
+void require(bool ok, const char *msg) {
+    if (!ok) pmgr::fail(PMGR_ERR_INVALID, msg);
+}
+
+void init_pool() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    PMGR_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    PMGR_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    PMGR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done = true;
+}
+
+pmgr_csr *wrap(std::shared_ptr<pmgr::Csr> m) {
+    auto *h = new pmgr_csr;
+    h->m = std::move(m);
+    return h;
+}
+
+const pmgr::AmgLevel &amg_level(const pmgr_amg *h, int32_t level) {
+    if (level < 0 || level >= (int32_t)h->levels.size()) pmgr::fail(PMGR_ERR_INVALID, "AMG level out of range");
+    return h->levels[level];
+}
+}  // namespace
+
+extern "C" {
+
+int pmgr_version(void) { return 1; }
+const char *pmgr_last_error(void) { return g_msg.c_str(); }
+int64_t pmgr_last_error_index(void) { return g_index; }
+int64_t pmgr_launch_count(void) { return pmgr::g_launches.load(); }
+
+int pmgr_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *row_offsets,
+                    const int32_t *col_indices, const double *values, int on_device, int validate,
+                    void *stream, pmgr_csr **out) {
+    return guard([&] {
+        require(out != nullptr, "out handle is NULL");
+        require(nrows >= 0 && ncols >= 0 && nnz >= 0, "negative dimension");
+        require(nnz < (int64_t)2147483647, "nnz exceeds the per-device int32 limit");
+        init_pool();
+        auto m = std::make_shared<pmgr::Csr>();
+        m->alloc(nrows, ncols, nnz);
+        cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        PMGR_CUDA(cudaMemcpyAsync(m->ro.p, row_offsets, sizeof(int64_t) * (nrows + 1), k, S(stream)));
+        if (nnz) {
+            PMGR_CUDA(cudaMemcpyAsync(m->ci.p, col_indices, sizeof(int32_t) * nnz, k, S(stream)));
+            PMGR_CUDA(cudaMemcpyAsync(m->v.p, values, sizeof(double) * nnz, k, S(stream)));
+        }
+        if (validate) pmgr::csr_validate(m->view(), S(stream));
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        *out = wrap(std::move(m));
+    });
+}
+
+int pmgr_csr_destroy(pmgr_csr *A) {
+    return guard([&] { delete A; });
+}
+
+int pmgr_csr_info(const pmgr_csr *A, int64_t *nrows, int64_t *ncols, int64_t *nnz) {
+    return guard([&] {
+        require(A != nullptr, "NULL matrix");
+        if (nrows) *nrows = A->m->nrows;
+        if (ncols) *ncols = A->m->ncols;
+        if (nnz) *nnz = A->m->nnz;
+    });
+}
+
+int pmgr_csr_download(const pmgr_csr *A, int64_t *row_offsets, int32_t *col_indices, double *values,
+                      int to_device, void *stream) {
+    return guard([&] {
+        require(A != nullptr, "NULL matrix");
+        const pmgr::Csr &m = *A->m;
+        cudaMemcpyKind k = to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (row_offsets)
+            PMGR_CUDA(cudaMemcpyAsync(row_offsets, m.ro.p, sizeof(int64_t) * (m.nrows + 1), k, S(stream)));
+        if (m.nnz && col_indices)
+            PMGR_CUDA(cudaMemcpyAsync(col_indices, m.ci.p, sizeof(int32_t) * m.nnz, k, S(stream)));
+        if (m.nnz && values) PMGR_CUDA(cudaMemcpyAsync(values, m.v.p, sizeof(double) * m.nnz, k, S(stream)));
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+int pmgr_spmv(const pmgr_csr *A, const double *x_dev, double *y_dev, void *stream) {
+    return guard([&] {
+        require(A != nullptr, "NULL matrix");
+        pmgr::spmv(A->m->view(), x_dev, y_dev, S(stream));
+    });
+}
+
+// ---------------------------------------------------------------- AMG
+int pmgr_amg_setup(const pmgr_csr *A, const pmgr_amg_cfg *cfg, void *stream, pmgr_amg **out) {
+    return guard([&] {
+        require(A && cfg && out, "NULL argument");
+        init_pool();
+        auto h = pmgr::amg_build(A->m, *cfg, S(stream));
+        *out = h.release();
+    });
+}
+
+int pmgr_amg_destroy(pmgr_amg *h) {
+    return guard([&] { delete h; });
+}
+
+int pmgr_amg_num_levels(const pmgr_amg *h, int32_t *nlevels) {
+    return guard([&] { *nlevels = (int32_t)h->levels.size(); });
+}
+
+int pmgr_amg_level_sizes(const pmgr_amg *h, int64_t *sizes) {
+    return guard([&] {
+        size_t i = 0;
+        for (; i < h->levels.size(); ++i) sizes[i] = h->levels[i].A->nrows;
+        sizes[i] = h->coarse->nrows;
+    });
+}
+
+int pmgr_amg_flagged_rows(const pmgr_amg *h, int64_t *flagged) {
+    return guard([&] { *flagged = h->flagged; });
+}
+
+int pmgr_amg_vcycle(pmgr_amg *h, const double *b_dev, const double *x_dev, double *out_dev, void *stream) {
+    return guard([&] {
+        require(h != nullptr, "NULL hierarchy");
+        pmgr::amg_cycle(*h, b_dev, x_dev, out_dev, S(stream));
+    });
+}
+
+int pmgr_amg_export_csr(const pmgr_amg *h, int32_t level, int32_t what, void *stream, pmgr_csr **out) {
+    return guard([&] {
+        auto m = std::make_shared<pmgr::Csr>();
+        if (what == 2) {
+            pmgr::csr_copy(h->coarse->view(), *m, S(stream));
+        } else {
+            const pmgr::AmgLevel &L = amg_level(h, level);
+            pmgr::csr_copy(what == 0 ? L.A->view() : L.P.view(), *m, S(stream));
+        }
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        *out = wrap(std::move(m));
+    });
+}
+
+int pmgr_amg_export_vec(const pmgr_amg *h, int32_t level, int32_t what, void *host_out, void *stream) {
+    return guard([&] {
+        const pmgr::AmgLevel &L = amg_level(h, level);
+        const int64_t n = L.A->nrows;
+        if (what == 0)
+            PMGR_CUDA(cudaMemcpyAsync(host_out, L.is_c.p, n, cudaMemcpyDeviceToHost, S(stream)));
+        else
+            PMGR_CUDA(cudaMemcpyAsync(host_out, L.dtilde.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(stream)));
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+// ---------------------------------------------------------------- MGR
+int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                   const pmgr_level_spec *levels, int32_t nlevels, const pmgr_mgr_cfg *cfg, void *stream,
+                   pmgr_mgr **out) {
+    return guard([&] {
+        require(A && field_of && entity_of && cfg && out, "NULL argument");
+        require(nlevels >= 0 && (nlevels == 0 || levels), "bad level list");
+        init_pool();
+        auto h = pmgr::mgr_build(A->m, field_of, entity_of, levels, nlevels, *cfg, S(stream));
+        *out = h.release();
+    });
+}
+
+int pmgr_mgr_destroy(pmgr_mgr *h) {
+    return guard([&] { delete h; });
+}
+
+int pmgr_mgr_num_levels(const pmgr_mgr *h, int32_t *nlevels) {
+    return guard([&] { *nlevels = (int32_t)h->levels.size(); });
+}
+
+int pmgr_mgr_level_sizes(const pmgr_mgr *h, int64_t *sizes) {
+    return guard([&] {
+        size_t i = 0;
+        for (; i < h->levels.size(); ++i) sizes[i] = h->levels[i].n;
+        sizes[i] = h->terminal_A->nrows;
+    });
+}
+
+int pmgr_mgr_apply(pmgr_mgr *h, const double *v_dev, double *z_dev, void *stream) {
+    return guard([&] {
+        require(h != nullptr, "NULL hierarchy");
+        pmgr::mgr_apply(*h, v_dev, z_dev, S(stream));
+    });
+}
+
+int pmgr_mgr_export_csr(const pmgr_mgr *h, int32_t level, int32_t what, void *stream, pmgr_csr **out) {
+    return guard([&] {
+        require(level >= 0 && level < (int32_t)h->levels.size(), "MGR level out of range");
+        auto m = std::make_shared<pmgr::Csr>();
+        if (what == 0) {
+            pmgr::csr_copy(h->levels[level].P.view(), *m, S(stream));
+        } else {
+            const pmgr::Csr &nx = (level + 1 < (int32_t)h->levels.size()) ? *h->levels[level + 1].A : *h->terminal_A;
+            pmgr::csr_copy(nx.view(), *m, S(stream));
+        }
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        *out = wrap(std::move(m));
+    });
+}
+
+int pmgr_mgr_export_vec(const pmgr_mgr *h, int32_t level, int32_t what, void *host_out, void *stream) {
+    return guard([&] {
+        require(level >= 0 && level < (int32_t)h->levels.size(), "MGR level out of range");
+        require(what == 0, "unknown vector");
+        const pmgr::MgrLevel &L = h->levels[level];
+        PMGR_CUDA(cudaMemcpyAsync(host_out, L.is_c.p, L.n, cudaMemcpyDeviceToHost, S(stream)));
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+int pmgr_mgr_amg(const pmgr_mgr *h, int32_t level, const pmgr_amg **out) {
+    return guard([&] {
+        if (level < 0) {
+            *out = h->terminal.get();
+        } else {
+            require(level < (int32_t)h->levels.size(), "MGR level out of range");
+            *out = h->levels[level].amg.get();
+        }
+    });
+}
+
+// ---------------------------------------------------------------- GMRES
+int pmgr_gmres(const pmgr_csr *A, pmgr_mgr *M, const double *b_dev, double *x_dev, int nonzero_x0,
+               const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, double *history_host, int32_t history_cap,
+               void *stream) {
+    return guard([&] {
+        require(A && cfg && stats && b_dev && x_dev, "NULL argument");
+        require(cfg->restart <= 1000, "restart above 1000 is not supported");
+        pmgr::gmres_device(A, M, b_dev, x_dev, nonzero_x0, *cfg, *stats, history_host, history_cap, S(stream));
+    });
+}
+
+int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_host, double *x_host, int nonzero_x0,
+                    const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, double *history_host,
+                    int32_t history_cap, void *stream) {
+    return guard([&] {
+        require(A && cfg && stats && b_host && x_host, "NULL argument");
+        require(cfg->restart <= 1000, "restart above 1000 is not supported");
+        const int64_t n = A->m->nrows;
+        pmgr::TBuf<double> b(n, S(stream)), x(n, S(stream));
+        PMGR_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, S(stream)));
+        if (nonzero_x0)
+            PMGR_CUDA(cudaMemcpyAsync(x.p, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, S(stream)));
+        else
+            PMGR_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, S(stream)));
+        pmgr::gmres_device(A, M, b.p, x.p, nonzero_x0, *cfg, *stats, history_host, history_cap, S(stream));
+        PMGR_CUDA(cudaMemcpyAsync(x_host, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(stream)));
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const double *w_dev, double *h_dev, void *stream) {
+    return guard([&] { pmgr::multidot(V_dev, n, nvec, w_dev, h_dev, S(stream)); });
+}
+
+int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h_dev, double *w_dev,
+                   void *stream) {
+    return guard([&] { pmgr::multiaxpy(V_dev, n, nvec, h_dev, w_dev, S(stream)); });
+}
+
+}  // extern "C"

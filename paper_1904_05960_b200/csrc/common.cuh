@@ -1,0 +1,256 @@
+// common.cuh -- shared infrastructure of libpmgr (B200 / sm_100a).
+//
+// Error model, device buffers, device CSR, launch bookkeeping and the warp
+// primitives every kernel uses.  The setup kernels need bitwise-reproducible
+// arithmetic: they use the explicit round-to-nearest
+// intrinsics (__dadd_rn / __dmul_rn / __ddiv_rn), which nvcc never contracts
+// into FMAs, and keep every per-entry sum in the reference's sequential order.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/pmgr.h"
+
+namespace pmgr {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+
+struct Error {
+    pmgr_status code;
+    std::string msg;
+    int64_t index;
+};
+
+[[noreturn]] inline void fail(pmgr_status code, const std::string &msg, int64_t index = -1) {
+    throw Error{code, msg, index};
+}
+
+[[noreturn]] inline void fail_cuda(cudaError_t e, const char *what, const char *file, int line) {
+    char buf[512];
+    snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+             cudaGetErrorString(e), file, line, what);
+    fail(e == cudaErrorMemoryAllocation ? PMGR_ERR_OOM : PMGR_ERR_CUDA, buf);
+}
+
+#define PMGR_CUDA(x)                                                        \
+    do {                                                                    \
+        cudaError_t e_ = (x);                                               \
+        if (e_ != cudaSuccess) ::pmgr::fail_cuda(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+extern std::atomic<int64_t> g_launches;
+
+// Count + check a kernel launch issued just before.
+#define PMGR_LAUNCHED()                                                                \
+    do {                                                                               \
+        ::pmgr::g_launches.fetch_add(1, std::memory_order_relaxed);                   \
+        cudaError_t e_ = cudaPeekAtLastError();                                        \
+        if (e_ != cudaSuccess) ::pmgr::fail_cuda(e_, "kernel launch", __FILE__, __LINE__); \
+    } while (0)
+
+int num_sms();
+
+inline unsigned grid_for(int64_t threads_needed, int block) {
+    int64_t g = (threads_needed + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 2147483647LL) g = 2147483647LL;
+    return (unsigned)g;
+}
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+
+// Persistent device buffer (cudaMalloc/cudaFree): owned by long-lived handles.
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    int64_t n = 0;
+    DBuf() = default;
+    explicit DBuf(int64_t count) { alloc(count); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(int64_t count) {
+        release();
+        n = count;
+        size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+        PMGR_CUDA(cudaMalloc((void **)&p, bytes));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T *get() const { return p; }
+};
+
+// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
+template <class T>
+struct TBuf {
+    T *p = nullptr;
+    int64_t n = 0;
+    cudaStream_t s = nullptr;
+    TBuf() = default;
+    TBuf(int64_t count, cudaStream_t st) { alloc(count, st); }
+    TBuf(const TBuf &) = delete;
+    TBuf &operator=(const TBuf &) = delete;
+    TBuf(TBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    TBuf &operator=(TBuf &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            s = o.s;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~TBuf() { release(); }
+    void alloc(int64_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+        PMGR_CUDA(cudaMallocAsync((void **)&p, bytes, s));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T *get() const { return p; }
+};
+
+template <class T>
+inline T read_scalar(const T *dev, cudaStream_t s) {
+    T h;
+    PMGR_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+// ---------------------------------------------------------------------------
+// device CSR
+// ---------------------------------------------------------------------------
+
+struct CsrView {
+    int64_t nrows, ncols, nnz;
+    const int64_t *ro;
+    const int32_t *ci;
+    const double *v;
+};
+
+struct Csr {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    DBuf<int64_t> ro;
+    DBuf<int32_t> ci;
+    DBuf<double> v;
+    void alloc(int64_t r, int64_t c, int64_t z) {
+        nrows = r;
+        ncols = c;
+        nnz = z;
+        ro.alloc(r + 1);
+        ci.alloc(z);
+        v.alloc(z);
+    }
+    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p}; }
+};
+
+// ---------------------------------------------------------------------------
+// warp helpers
+// ---------------------------------------------------------------------------
+
+// Sequential left-to-right sum of a chunk of up to 32 values held one per
+// lane (lane k holds element k), continued from s.  Every lane returns the
+// same, order-exact result: (((s + x0) + x1) + ...).
+__device__ __forceinline__ double warp_seq_sum(double s, double x, int cnt) {
+    for (int k = 0; k < cnt; ++k) s = __dadd_rn(s, __shfl_sync(FULL, x, k));
+    return s;
+}
+
+__device__ __forceinline__ double warp_max(double x) {
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(FULL, x, o));
+    return x;
+}
+
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t x) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// host-side primitives implemented in prims.cu (CUB based)
+// ---------------------------------------------------------------------------
+
+// out[0] = 0, out[i+1] = sum_{k<=i} in[k]; returns the total (synchronises).
+int64_t exclusive_scan_total(const int64_t *in, int64_t *out, int64_t n, cudaStream_t s);
+int64_t exclusive_scan_total_i32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
+// Sort (keys, vals) pairs within each CSR row segment by key (ascending).
+void segmented_sort_pairs(int32_t *keys, double *vals, int64_t nnz, const int64_t *ro,
+                          int64_t nrows, cudaStream_t s);
+double device_max_abs(const double *x, int64_t n, cudaStream_t s);
+
+// CSR utilities (csr.cu)
+void csr_transpose(const CsrView &A, Csr &T, cudaStream_t s);
+// mode 0: drop exact zeros (scipy product); mode 1: structural pattern kept,
+// zero sums stored as +0.0 (reference spgemm).
+void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s);
+void csr_subtract(const CsrView &A, const CsrView &B, Csr &C, cudaStream_t s);
+void csr_sparsify(const CsrView &M, const int32_t *entity, int64_t n_max, Csr &K,
+                  cudaStream_t s);
+void csr_copy(const CsrView &A, Csr &B, cudaStream_t s);
+void csr_diagonal(const CsrView &A, double *d, cudaStream_t s);
+// d = 1/diag; returns the first row whose diagonal is zero or missing (-1 if none).
+int64_t csr_diag_inverse(const CsrView &A, double *dinv, cudaStream_t s);
+void csr_validate(const CsrView &A, cudaStream_t s);
+
+// SpMV family (spmv.cu)
+void spmv(const CsrView &A, const double *x, double *y, cudaStream_t s);
+void spmv_residual(const CsrView &A, const double *x, const double *b, double *r, cudaStream_t s);
+void spmv_jacobi(const CsrView &A, const double *x, const double *b, const double *d,
+                 double *xo, cudaStream_t s);
+void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x,
+                          double *r, cudaStream_t s);
+void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s);
+void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows,
+                     double *r, cudaStream_t s);
+void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,
+                          const int64_t *findex, double *z, cudaStream_t s);
+void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,
+               const double *b, double *x, double *xpre, bool forward, cudaStream_t s);
+void dense_matvec(const double *M, int64_t n, const double *x, double *y, cudaStream_t s);
+
+// elementwise (spmv.cu)
+void vec_gather(const double *src, const int64_t *idx, int64_t n, double *dst, cudaStream_t s);
+void vec_scale_gather(const double *src, const int64_t *idx, const double *d, int64_t n,
+                      double *dst, cudaStream_t s);
+void vec_zero(double *x, int64_t n, cudaStream_t s);
+void vec_copy(const double *x, double *y, int64_t n, cudaStream_t s);
+void vec_axpy(double a, const double *x, double *y, int64_t n, cudaStream_t s);
+void vec_mul(const double *a, const double *b, double *y, int64_t n, cudaStream_t s);
+
+}  // namespace pmgr

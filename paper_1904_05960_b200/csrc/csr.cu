@@ -1,0 +1,541 @@
+// csr.cu -- setup-phase sparse kernels with the reference's exact arithmetic.
+//
+//  * csr_transpose     scipy .T.tocsr(): rows of the result in ascending
+//                      source-row order (stable counting scatter).
+//  * spgemm            scipy csr_matmat order: C_ik = seq sum over j ascending
+//                      in row i of X of X_ij*Y_jk from 0.0.
+//                      Two passes (symbolic count, numeric fill) with a hash
+//                      accumulator per warp in shared memory; rows whose
+//                      candidate set cannot fit fall back to a per-row hash
+//                      table in global memory.  Each j is processed by the
+//                      whole warp (lanes over the distinct k of row j), so
+//                      every output entry is accumulated in ascending j --
+//                      bit-identical to the sequential product.  Rows are
+//                      then key-sorted (CUB segmented sort) and, in mode 0,
+//                      compacted without exact zeros (scipy's zero drop).
+//  * csr_subtract      scipy csr_binop_csr_canonical '-', zero drop.
+//  * csr_sparsify      reference sparsify (sparse.py:439-467).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace pmgr {
+
+namespace {
+
+// ------------------------------------------------------------ validation
+__global__ void k_validate(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ro,
+                           const int32_t *ci, unsigned long long *err) {
+    // err[0]: min bad row for non-decreasing offsets; err[1]: col range; err[2]: order
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t b = ro[i], e = ro[i + 1];
+    if (e < b || b < 0 || e > nnz) {
+        atomicMin(err + 0, (unsigned long long)i);
+        return;
+    }
+    for (int64_t q = b; q < e; ++q) {
+        int32_t c = ci[q];
+        if (c < 0 || c >= ncols) atomicMin(err + 1, (unsigned long long)i);
+        if (q > b && c <= ci[q - 1]) atomicMin(err + 2, (unsigned long long)i);
+    }
+}
+
+// ------------------------------------------------------------ transpose
+__global__ void k_count_cols(const int32_t *ci, int64_t nnz, int64_t *cnt) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < nnz) atomicAdd((unsigned long long *)(cnt + ci[q]), 1ull);
+}
+
+__global__ void k_row_of_entry(int64_t nrows, const int64_t *ro, int32_t *row) {
+    // one warp per row
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= nrows) return;
+    for (int64_t q = ro[i] + lane; q < ro[i + 1]; q += 32) row[q] = (int32_t)i;
+}
+
+__global__ void k_transpose_fill(int64_t nnz, const int32_t *sorted_rows, const int32_t *perm,
+                                 const double *v, int32_t *tci, double *tv) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nnz) return;
+    tci[q] = sorted_rows[q];
+    tv[q] = v[perm[q]];
+}
+
+__global__ void k_gather_rows(int64_t nnz, const int32_t *rows, const int32_t *perm, int32_t *out) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < nnz) out[q] = rows[perm[q]];
+}
+
+__global__ void k_iota(int32_t *p, int64_t n) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < n) p[q] = (int32_t)q;
+}
+
+// ------------------------------------------------------------ spgemm
+constexpr int HS = 2048;          // hash slots per warp (shared path)
+constexpr int SP_WARPS = 4;       // warps per block (4 * 2048 * 12 B = 96 KB)
+constexpr int SMALL_LIMIT = HS / 2;
+
+__device__ __forceinline__ unsigned hash_k(int32_t k) { return (unsigned)k * 2654435761u; }
+
+// insert-or-find key k in a table of size tsz (power of two); returns slot
+// and whether this call inserted it.
+__device__ __forceinline__ int64_t table_insert(int32_t *keys, int64_t tsz, int32_t k, bool &inserted) {
+    int64_t h = hash_k(k) & (tsz - 1);
+    while (true) {
+        int32_t cur = keys[h];
+        if (cur == k) {
+            inserted = false;
+            return h;
+        }
+        if (cur == -1) {
+            int32_t prev = atomicCAS(keys + h, -1, k);
+            if (prev == -1) {
+                inserted = true;
+                return h;
+            }
+            if (prev == k) {
+                inserted = false;
+                return h;
+            }
+        }
+        h = (h + 1) & (tsz - 1);
+    }
+}
+
+// upper bound of distinct columns per row: min(sum_j nnz(Y_j), ncols)
+__global__ void k_spgemm_ub(int64_t n, const int64_t *xro, const int32_t *xci, const int64_t *yro,
+                            int64_t ycols, int64_t *ub) {
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    int64_t s = 0;
+    for (int64_t q = xro[i] + lane; q < xro[i + 1]; q += 32) {
+        int32_t j = xci[q];
+        s += yro[j + 1] - yro[j];
+    }
+    s = warp_sum_i64(s);
+    if (lane == 0) ub[i] = s < ycols ? s : ycols;
+}
+
+// global-table sizes for big rows (0 for rows on the shared path)
+__global__ void k_table_size(int64_t n, const int64_t *ub, int64_t *tsz) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t u = ub[i];
+    if (u <= SMALL_LIMIT) {
+        tsz[i] = 0;
+    } else {
+        int64_t t = 1;
+        while (t < 2 * u) t <<= 1;
+        tsz[i] = t;
+    }
+}
+
+// NUMERIC = false: count distinct columns per row into cnt[i].
+// NUMERIC = true : accumulate and dump (key, value) pairs unsorted into
+//                  C at cro[i]; structural mode stores zero sums as +0.0.
+template <bool NUMERIC>
+__global__ void __launch_bounds__(SP_WARPS * 32)
+    k_spgemm(int64_t n, const int64_t *__restrict__ xro, const int32_t *__restrict__ xci,
+             const double *__restrict__ xv, const int64_t *__restrict__ yro,
+             const int32_t *__restrict__ yci, const double *__restrict__ yv,
+             const int64_t *__restrict__ ub, const int64_t *__restrict__ toff, int32_t *gkeys,
+             double *gvals, int64_t *cnt, const int64_t *__restrict__ cro, int32_t *cci, double *cv) {
+    extern __shared__ unsigned char smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    int32_t *skeys = (int32_t *)smem + warp * HS;
+    double *svals = (double *)(smem + sizeof(int32_t) * HS * SP_WARPS) + warp * HS;
+    const int64_t nwarps = (int64_t)gridDim.x * SP_WARPS;
+    for (int64_t i = blockIdx.x * (int64_t)SP_WARPS + warp; i < n; i += nwarps) {
+        const bool big = ub[i] > SMALL_LIMIT;
+        int32_t *keys;
+        double *vals;
+        int64_t tsz;
+        if (big) {
+            keys = gkeys + toff[i];
+            vals = NUMERIC ? gvals + toff[i] : nullptr;
+            tsz = toff[i + 1] - toff[i];
+        } else {
+            keys = skeys;
+            vals = svals;
+            tsz = HS;
+        }
+        for (int64_t t = lane; t < tsz; t += 32) {
+            keys[t] = -1;
+            if (NUMERIC) vals[t] = 0.0;
+        }
+        __syncwarp();
+        int64_t local = 0;
+        for (int64_t jj = xro[i]; jj < xro[i + 1]; ++jj) {
+            const int32_t j = xci[jj];
+            const double xval = NUMERIC ? xv[jj] : 0.0;
+            for (int64_t kk = yro[j] + lane; kk < yro[j + 1]; kk += 32) {
+                const int32_t k = yci[kk];
+                bool ins;
+                int64_t slot = table_insert(keys, tsz, k, ins);
+                if (NUMERIC) {
+                    vals[slot] = __dadd_rn(vals[slot], __dmul_rn(xval, yv[kk]));
+                } else if (ins) {
+                    ++local;
+                }
+            }
+            __syncwarp();
+        }
+        if (!NUMERIC) {
+            local = warp_sum_i64(local);
+            if (lane == 0) cnt[i] = local;
+        } else {
+            // dump occupied slots (order fixed later by the segmented sort)
+            int64_t base = cro[i];
+            for (int64_t t0 = 0; t0 < tsz; t0 += 32) {
+                int64_t t = t0 + lane;
+                int32_t k = t < tsz ? keys[t] : -1;
+                unsigned m = __ballot_sync(FULL, k != -1);
+                if (k != -1) {
+                    int pos = __popc(m & ((1u << lane) - 1u));
+                    double val = vals[t];
+                    cci[base + pos] = k;
+                    cv[base + pos] = (val == 0.0) ? 0.0 : val;
+                }
+                base += __popc(m);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------ zero drop
+__global__ void k_count_nonzero(int64_t n, const int64_t *ro, const double *v, int64_t *cnt) {
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    int64_t c = 0;
+    for (int64_t q = ro[i] + lane; q < ro[i + 1]; q += 32) c += (v[q] != 0.0);
+    c = warp_sum_i64(c);
+    if (lane == 0) cnt[i] = c;
+}
+
+__global__ void k_compact_nonzero(int64_t n, const int64_t *ro, const int32_t *ci, const double *v,
+                                  const int64_t *nro, int32_t *nci, double *nv) {
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    int64_t w = nro[i];
+    for (int64_t q0 = ro[i]; q0 < ro[i + 1]; q0 += 32) {
+        int64_t q = q0 + lane;
+        bool keep = q < ro[i + 1] && v[q] != 0.0;
+        unsigned m = __ballot_sync(FULL, keep);
+        if (keep) {
+            int pos = __popc(m & ((1u << lane) - 1u));
+            nci[w + pos] = ci[q];
+            nv[w + pos] = v[q];
+        }
+        w += __popc(m);
+    }
+}
+
+// ------------------------------------------------------------ subtract
+// C = A - B over the union of two sorted rows; exact zeros dropped.
+template <bool FILL>
+__global__ void k_subtract(int64_t n, const int64_t *aro, const int32_t *aci, const double *av,
+                           const int64_t *bro, const int32_t *bci, const double *bv, int64_t *cnt,
+                           const int64_t *cro, int32_t *cci, double *cv) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t p = aro[i], pe = aro[i + 1], q = bro[i], qe = bro[i + 1];
+    int64_t w = FILL ? cro[i] : 0;
+    while (p < pe || q < qe) {
+        int64_t ca = p < pe ? aci[p] : INT64_MAX;
+        int64_t cb = q < qe ? bci[q] : INT64_MAX;
+        double r;
+        int64_t c;
+        if (ca == cb) {
+            r = __dadd_rn(av[p++], -bv[q++]);
+            c = ca;
+        } else if (ca < cb) {
+            r = __dadd_rn(av[p++], -0.0);
+            c = ca;
+        } else {
+            r = __dadd_rn(0.0, -bv[q++]);
+            c = cb;
+        }
+        if (r != 0.0) {
+            if (FILL) {
+                cci[w] = (int32_t)c;
+                cv[w] = r;
+            }
+            ++w;
+        }
+    }
+    if (!FILL) cnt[i] = w;
+}
+
+// ------------------------------------------------------------ sparsify
+// Row-wise dropping: keep same-entity entries and the n_max largest |v|
+// among the rest, ties to the smaller column; kept entries in stored order.
+template <bool FILL>
+__global__ void k_sparsify(int64_t n, const int64_t *ro, const int32_t *ci, const double *v,
+                           const int32_t *entity, int64_t nmax, int64_t *cnt, const int64_t *kro,
+                           int32_t *kci, double *kv) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t ei = entity[i];
+    int64_t w = FILL ? kro[i] : 0;
+    for (int64_t q = ro[i]; q < ro[i + 1]; ++q) {
+        bool keep = entity[ci[q]] == ei;
+        if (!keep && nmax > 0) {
+            double a = fabs(v[q]);
+            int32_t c = ci[q];
+            int64_t rank = 0;
+            for (int64_t t = ro[i]; t < ro[i + 1] && rank < nmax; ++t) {
+                if (t == q || entity[ci[t]] == ei) continue;
+                double b = fabs(v[t]);
+                if (b > a || (b == a && ci[t] < c)) ++rank;
+            }
+            keep = rank < nmax;
+        }
+        if (keep) {
+            if (FILL) {
+                kci[w] = ci[q];
+                kv[w] = v[q];
+            }
+            ++w;
+        }
+    }
+    if (!FILL) cnt[i] = w;
+}
+
+__global__ void k_diag(int64_t n, const int64_t *ro, const int32_t *ci, const double *v, double *d) {
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double dv = 0.0;
+    bool found = false;
+    for (int64_t q = ro[i] + lane; q < ro[i + 1]; q += 32)
+        if (ci[q] == i) {
+            dv = v[q];
+            found = true;
+        }
+    unsigned m = __ballot_sync(FULL, found);
+    double r = m ? __shfl_sync(FULL, dv, __ffs(m) - 1) : 0.0;
+    if (lane == 0) d[i] = r;
+}
+
+__global__ void k_diag_inverse(int64_t n, const double *d, double *dinv, unsigned long long *bad) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double x = d[i];
+    if (x == 0.0) atomicMin(bad, (unsigned long long)i);
+    dinv[i] = __ddiv_rn(1.0, x);
+}
+
+__global__ void k_fill_u64(unsigned long long *p, int64_t n, unsigned long long val) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = val;
+}
+
+}  // namespace
+
+// ===================================================================== API
+
+void csr_validate(const CsrView &A, cudaStream_t s) {
+    int64_t r0 = 0, rn = 0;
+    if (A.nrows >= 0) {
+        PMGR_CUDA(cudaMemcpyAsync(&r0, A.ro, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaMemcpyAsync(&rn, A.ro + A.nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+    if (r0 != 0 || rn != A.nnz) fail(PMGR_ERR_INVALID, "row_offsets endpoints inconsistent with nnz");
+    if (A.nrows == 0) return;
+    TBuf<unsigned long long> err(3, s);
+    k_fill_u64<<<1, 32, 0, s>>>(err.p, 3, ~0ull);
+    PMGR_LAUNCHED();
+    k_validate<<<grid_for(A.nrows, 256), 256, 0, s>>>(A.nrows, A.ncols, A.nnz, A.ro, A.ci, err.p);
+    PMGR_LAUNCHED();
+    unsigned long long h[3];
+    PMGR_CUDA(cudaMemcpyAsync(h, err.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    if (h[0] != ~0ull) fail(PMGR_ERR_INVALID, "row_offsets must be non-decreasing", (int64_t)h[0]);
+    if (h[1] != ~0ull) fail(PMGR_ERR_INVALID, "column index out of range", (int64_t)h[1]);
+    if (h[2] != ~0ull)
+        fail(PMGR_ERR_INVALID, "column indices must be strictly increasing within each row", (int64_t)h[2]);
+}
+
+void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {
+    B.alloc(A.nrows, A.ncols, A.nnz);
+    PMGR_CUDA(cudaMemcpyAsync(B.ro.p, A.ro, sizeof(int64_t) * (A.nrows + 1), cudaMemcpyDeviceToDevice, s));
+    if (A.nnz) {
+        PMGR_CUDA(cudaMemcpyAsync(B.ci.p, A.ci, sizeof(int32_t) * A.nnz, cudaMemcpyDeviceToDevice, s));
+        PMGR_CUDA(cudaMemcpyAsync(B.v.p, A.v, sizeof(double) * A.nnz, cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+void csr_transpose(const CsrView &A, Csr &T, cudaStream_t s) {
+    T.alloc(A.ncols, A.nrows, A.nnz);
+    TBuf<int64_t> cnt(A.ncols, s);
+    PMGR_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * A.ncols, s));
+    if (A.nnz) {
+        k_count_cols<<<grid_for(A.nnz, 256), 256, 0, s>>>(A.ci, A.nnz, cnt.p);
+        PMGR_LAUNCHED();
+    }
+    exclusive_scan_total(cnt.p, T.ro.p, A.ncols, s);
+    if (A.nnz == 0) return;
+    // stable radix sort of entries (row-major order) by column
+    TBuf<int32_t> rows(A.nnz, s), perm(A.nnz, s), rows_s(A.nnz, s), keys_s(A.nnz, s), perm_s(A.nnz, s);
+    k_row_of_entry<<<grid_for(A.nrows * 32, 256), 256, 0, s>>>(A.nrows, A.ro, rows.p);
+    PMGR_LAUNCHED();
+    k_iota<<<grid_for(A.nnz, 256), 256, 0, s>>>(perm.p, A.nnz);
+    PMGR_LAUNCHED();
+    int end_bit = 1;
+    while (end_bit < 31 && (1ll << end_bit) < A.ncols) ++end_bit;
+    size_t tmp = 0;
+    PMGR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, A.ci, keys_s.p, perm.p, perm_s.p, A.nnz, 0,
+                                              end_bit, s));
+    TBuf<char> t((int64_t)tmp, s);
+    PMGR_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, A.ci, keys_s.p, perm.p, perm_s.p, A.nnz, 0, end_bit, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_gather_rows<<<grid_for(A.nnz, 256), 256, 0, s>>>(A.nnz, rows.p, perm_s.p, rows_s.p);
+    PMGR_LAUNCHED();
+    k_transpose_fill<<<grid_for(A.nnz, 256), 256, 0, s>>>(A.nnz, rows_s.p, perm_s.p, A.v, T.ci.p, T.v.p);
+    PMGR_LAUNCHED();
+}
+
+void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s) {
+    if (X.ncols != Y.nrows) fail(PMGR_ERR_INVALID, "spgemm dimension mismatch");
+    const int64_t n = X.nrows;
+    TBuf<int64_t> ub(n, s), tsz(n, s), toff(n + 1, s), cnt(n, s);
+    TBuf<int64_t> cro(n + 1, s);
+    if (n == 0) {
+        C.alloc(0, Y.ncols, 0);
+        PMGR_CUDA(cudaMemsetAsync(C.ro.p, 0, sizeof(int64_t), s));
+        return;
+    }
+    k_spgemm_ub<<<grid_for(n * 32, 256), 256, 0, s>>>(n, X.ro, X.ci, Y.ro, Y.ncols, ub.p);
+    PMGR_LAUNCHED();
+    k_table_size<<<grid_for(n, 256), 256, 0, s>>>(n, ub.p, tsz.p);
+    PMGR_LAUNCHED();
+    int64_t gtotal = exclusive_scan_total(tsz.p, toff.p, n, s);
+    TBuf<int32_t> gkeys(gtotal, s);
+    TBuf<double> gvals(mode >= 0 ? gtotal : 0, s);
+
+    const size_t smem = (size_t)SP_WARPS * HS * (sizeof(int32_t) + sizeof(double));
+    static bool attr_set = false;
+    if (!attr_set) {
+        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    int64_t want = (n + SP_WARPS - 1) / SP_WARPS;
+    int64_t cap = (int64_t)num_sms() * 2 * 16;
+    unsigned grid = (unsigned)(want < cap ? want : cap);
+    if (grid < 1) grid = 1;
+
+    k_spgemm<false><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
+                                                       gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
+    PMGR_LAUNCHED();
+    int64_t total = exclusive_scan_total(cnt.p, cro.p, n, s);
+    TBuf<int32_t> tci(total, s);
+    TBuf<double> tv(total, s);
+    k_spgemm<true><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
+                                                      gkeys.p, gvals.p, nullptr, cro.p, tci.p, tv.p);
+    PMGR_LAUNCHED();
+    segmented_sort_pairs(tci.p, tv.p, total, cro.p, n, s);
+    if (mode == 1) {
+        C.nrows = n;
+        C.ncols = Y.ncols;
+        C.nnz = total;
+        C.ro.alloc(n + 1);
+        C.ci.alloc(total);
+        C.v.alloc(total);
+        PMGR_CUDA(cudaMemcpyAsync(C.ro.p, cro.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+        if (total) {
+            PMGR_CUDA(cudaMemcpyAsync(C.ci.p, tci.p, sizeof(int32_t) * total, cudaMemcpyDeviceToDevice, s));
+            PMGR_CUDA(cudaMemcpyAsync(C.v.p, tv.p, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
+        }
+        return;
+    }
+    // mode 0: drop exact zeros
+    k_count_nonzero<<<grid_for(n * 32, 256), 256, 0, s>>>(n, cro.p, tv.p, cnt.p);
+    PMGR_LAUNCHED();
+    C.ro.alloc(n + 1);
+    int64_t nz = exclusive_scan_total(cnt.p, C.ro.p, n, s);
+    C.nrows = n;
+    C.ncols = Y.ncols;
+    C.nnz = nz;
+    C.ci.alloc(nz);
+    C.v.alloc(nz);
+    k_compact_nonzero<<<grid_for(n * 32, 256), 256, 0, s>>>(n, cro.p, tci.p, tv.p, C.ro.p, C.ci.p, C.v.p);
+    PMGR_LAUNCHED();
+}
+
+void csr_subtract(const CsrView &A, const CsrView &B, Csr &C, cudaStream_t s) {
+    if (A.nrows != B.nrows || A.ncols != B.ncols) fail(PMGR_ERR_INVALID, "shape mismatch");
+    const int64_t n = A.nrows;
+    TBuf<int64_t> cnt(n, s);
+    C.ro.alloc(n + 1);
+    if (n) {
+        k_subtract<false><<<grid_for(n, 128), 128, 0, s>>>(n, A.ro, A.ci, A.v, B.ro, B.ci, B.v, cnt.p,
+                                                           nullptr, nullptr, nullptr);
+        PMGR_LAUNCHED();
+    }
+    int64_t nz = exclusive_scan_total(cnt.p, C.ro.p, n, s);
+    C.nrows = n;
+    C.ncols = A.ncols;
+    C.nnz = nz;
+    C.ci.alloc(nz);
+    C.v.alloc(nz);
+    if (n) {
+        k_subtract<true><<<grid_for(n, 128), 128, 0, s>>>(n, A.ro, A.ci, A.v, B.ro, B.ci, B.v, nullptr,
+                                                          C.ro.p, C.ci.p, C.v.p);
+        PMGR_LAUNCHED();
+    }
+}
+
+void csr_sparsify(const CsrView &M, const int32_t *entity, int64_t n_max, Csr &K, cudaStream_t s) {
+    const int64_t n = M.nrows;
+    TBuf<int64_t> cnt(n, s);
+    K.ro.alloc(n + 1);
+    if (n) {
+        k_sparsify<false><<<grid_for(n, 128), 128, 0, s>>>(n, M.ro, M.ci, M.v, entity, n_max, cnt.p,
+                                                           nullptr, nullptr, nullptr);
+        PMGR_LAUNCHED();
+    }
+    int64_t nz = exclusive_scan_total(cnt.p, K.ro.p, n, s);
+    K.nrows = n;
+    K.ncols = M.ncols;
+    K.nnz = nz;
+    K.ci.alloc(nz);
+    K.v.alloc(nz);
+    if (n) {
+        k_sparsify<true><<<grid_for(n, 128), 128, 0, s>>>(n, M.ro, M.ci, M.v, entity, n_max, nullptr,
+                                                          K.ro.p, K.ci.p, K.v.p);
+        PMGR_LAUNCHED();
+    }
+}
+
+void csr_diagonal(const CsrView &A, double *d, cudaStream_t s) {
+    int64_t n = A.nrows < A.ncols ? A.nrows : A.ncols;
+    if (n == 0) return;
+    k_diag<<<grid_for(n * 32, 256), 256, 0, s>>>(n, A.ro, A.ci, A.v, d);
+    PMGR_LAUNCHED();
+}
+
+int64_t csr_diag_inverse(const CsrView &A, double *dinv, cudaStream_t s) {
+    int64_t n = A.nrows;
+    if (n == 0) return -1;
+    TBuf<double> d(n, s);
+    csr_diagonal(A, d.p, s);
+    TBuf<unsigned long long> bad(1, s);
+    k_fill_u64<<<1, 32, 0, s>>>(bad.p, 1, ~0ull);
+    PMGR_LAUNCHED();
+    k_diag_inverse<<<grid_for(n, 256), 256, 0, s>>>(n, d.p, dinv, bad.p);
+    PMGR_LAUNCHED();
+    unsigned long long b = read_scalar(bad.p, s);
+    return b == ~0ull ? -1 : (int64_t)b;
+}
+
+}  // namespace pmgr

@@ -1,0 +1,91 @@
+// hier.cuh -- device-resident AMG and MGR hierarchies.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+struct pmgr_csr {
+    std::shared_ptr<pmgr::Csr> m;
+};
+
+namespace pmgr {
+
+// One classical-AMG level (reference amg.py:51-57).
+struct AmgLevel {
+    std::shared_ptr<const Csr> A;  // level operator (level 0 may be shared with MGR)
+    Csr P;                         // interpolation n_l x n_{l+1}
+    Csr R;                         // explicit P^T (restriction)
+    DBuf<int8_t> is_c;             // C/F split
+    DBuf<double> dtilde;           // l1 diagonal
+    DBuf<int64_t> starts;          // partition boundaries (hybrid GS only)
+    int64_t nparts = 0;
+    bool jacobi = true;            // one row per partition
+    // solve workspace
+    DBuf<double> b, x, r, xo, xpre;
+};
+
+}  // namespace pmgr
+
+struct pmgr_amg {
+    pmgr_amg_cfg cfg;
+    std::vector<pmgr::AmgLevel> levels;
+    std::shared_ptr<const pmgr::Csr> coarse;  // coarsest operator
+    pmgr::DBuf<double> coarse_inv;            // dense inverse, row-major
+    pmgr::DBuf<double> cb, cx, ctmp;          // coarsest workspace
+    int64_t flagged = 0;
+};
+
+namespace pmgr {
+
+std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A, const pmgr_amg_cfg &cfg,
+                                    cudaStream_t s);
+// out = V-cycle(h, b, x); x may be null (zero initial guess).  b/out are
+// length n_0 device vectors; out may alias neither b nor x.
+void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaStream_t s);
+
+// One MGR reduction level (reference mgr.py:300-311).
+struct MgrLevel {
+    std::shared_ptr<const Csr> A;  // level operator
+    int64_t n = 0, nc = 0, nf = 0;
+    DBuf<int8_t> is_c;
+    DBuf<int64_t> c_rows, f_rows;  // level-local row ids of C / F points
+    DBuf<int64_t> f_index;         // row -> F index or -1
+    Csr A_cf;                      // C rows x F cols (residual restriction)
+    Csr P;                         // [W_p ; I] in level order
+    DBuf<double> dinv_ff;          // 1 / diag(A_FF)
+    int32_t f_relax = PMGR_FRELAX_NONE;
+    int32_t f_relax_sweeps = 1;
+    std::shared_ptr<const Csr> A_ff;  // for Jacobi sweeps > 1
+    std::unique_ptr<pmgr_amg> amg;    // F-relaxation AMG
+    // workspace
+    DBuf<double> vf, zf, rc, zc, tmpf;
+};
+
+}  // namespace pmgr
+
+struct pmgr_mgr {
+    std::vector<pmgr::MgrLevel> levels;
+    std::shared_ptr<const pmgr::Csr> terminal_A;
+    std::unique_ptr<pmgr_amg> terminal;
+    int32_t terminal_cycles = 1;
+    int32_t f_relax_post = 0;
+    int64_t n = 0;
+    pmgr::DBuf<double> tz;  // terminal scratch
+};
+
+namespace pmgr {
+std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A, const int8_t *field_of_host,
+                                    const int32_t *entity_of_host, const pmgr_level_spec *specs,
+                                    int nlevels, const pmgr_mgr_cfg &cfg, cudaStream_t s);
+void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);
+}  // namespace pmgr
+
+namespace pmgr {
+void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, int nonzero_x0,
+                  const pmgr_gmres_cfg &cfg, pmgr_gmres_stats &stats, double *history,
+                  int32_t history_cap, cudaStream_t s);
+void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double *h, cudaStream_t s);
+void multiaxpy(const double *V, int64_t n, int32_t nvec, const double *h, double *w, cudaStream_t s);
+}  // namespace pmgr

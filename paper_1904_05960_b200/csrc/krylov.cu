@@ -1,0 +1,378 @@
+// krylov.cu -- right-preconditioned restarted GMRES on the device
+// (reference krylov.py:39-117).
+//
+// Same outer semantics as the reference: x0 = 0 unless given; convergence
+// on ||b - A x|| <= max(rtol*||r0||, atol); Givens least squares; at each
+// restart x += M^{-1}(V y), the true residual is recomputed and replaces the
+// last history entry; an Arnoldi breakdown counts as convergence in the
+// subspace.  Orthogonalisation is classical Gram-Schmidt with one
+// re-orthogonalisation (CGS2) instead of MGS: the projections become two
+// fused multi-dot / multi-axpy passes over the Krylov basis (HBM streaming,
+// deterministic block partials) -- not bitwise MGS, but at least as
+// orthogonal, which keeps iteration counts within +-1.
+// The small Hessenberg / Givens work runs in one single-thread kernel; the
+// host only reads three status words per iteration.
+#include <cmath>
+
+#include "hier.cuh"
+
+namespace pmgr {
+
+namespace {
+
+constexpr int DOT_BLOCK = 256;
+constexpr int KC = 8;  // basis vectors per register chunk
+
+int dot_grid(int64_t n) {
+    int64_t g = (n + DOT_BLOCK - 1) / DOT_BLOCK;
+    int64_t cap = 2LL * num_sms();
+    return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    return t;  // valid in thread 0
+}
+
+// partial[blk*ld + k] = sum over this block's rows of V_k[i] * w[i], k < nk
+__global__ void __launch_bounds__(DOT_BLOCK) k_multidot(const double *__restrict__ V, int64_t n, int nk,
+                                                         const double *__restrict__ w, double *partial, int ld) {
+    __shared__ double sh[DOT_BLOCK / 32];
+    for (int k0 = 0; k0 < nk; k0 += KC) {
+        double acc[KC];
+#pragma unroll
+        for (int t = 0; t < KC; ++t) acc[t] = 0.0;
+        for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
+            const double wi = w[i];
+#pragma unroll
+            for (int t = 0; t < KC; ++t)
+                if (k0 + t < nk) acc[t] = fma(V[(int64_t)(k0 + t) * n + i], wi, acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < KC; ++t) {
+            if (k0 + t >= nk) break;
+            double s = block_sum(acc[t], sh);
+            if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * ld + k0 + t] = s;
+        }
+    }
+}
+
+// w -= sum_k h[k] V_k ; then mode 1: partial dots V_k . w (k < nk),
+// mode 2: partial ||w||^2 (slot 0).  Each thread re-reads its rows of V
+// for the dots (L1-resident tile).
+__global__ void __launch_bounds__(DOT_BLOCK) k_update(const double *__restrict__ V, int64_t n, int nk,
+                                                       const double *__restrict__ h, double *w, int mode,
+                                                       double *partial, int ld) {
+    __shared__ double sh[DOT_BLOCK / 32];
+    __shared__ double hs[1024];
+    for (int k = threadIdx.x; k < nk && k < 1024; k += DOT_BLOCK) hs[k] = h[k];
+    __syncthreads();
+    double nrm = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
+        double wi = w[i];
+        for (int k = 0; k < nk; ++k) wi = fma(-hs[k], V[(int64_t)k * n + i], wi);
+        w[i] = wi;
+        nrm = fma(wi, wi, nrm);
+    }
+    if (mode == 2) {
+        double s = block_sum(nrm, sh);
+        if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * ld] = s;
+        return;
+    }
+    if (mode == 1) {
+        for (int k0 = 0; k0 < nk; k0 += KC) {
+            double acc[KC];
+#pragma unroll
+            for (int t = 0; t < KC; ++t) acc[t] = 0.0;
+            for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n;
+                 i += (int64_t)gridDim.x * DOT_BLOCK) {
+                const double wi = w[i];
+#pragma unroll
+                for (int t = 0; t < KC; ++t)
+                    if (k0 + t < nk) acc[t] = fma(V[(int64_t)(k0 + t) * n + i], wi, acc[t]);
+            }
+#pragma unroll
+            for (int t = 0; t < KC; ++t) {
+                if (k0 + t >= nk) break;
+                double s = block_sum(acc[t], sh);
+                if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * ld + k0 + t] = s;
+            }
+        }
+    }
+}
+
+// out[k] (+)= sum over blocks of partial[b*ld + k], one warp per k, fixed order
+__global__ void k_reduce_partials(const double *partial, int nblk, int nk, int ld, double *out, int accumulate) {
+    int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (k >= nk) return;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += partial[(int64_t)b * ld + k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0) out[k] = accumulate ? out[k] + s : s;
+}
+
+// u = sum_k y[k] V_k
+__global__ void k_combine(const double *__restrict__ V, int64_t n, int nk, const double *__restrict__ y,
+                          double *u) {
+    __shared__ double ys[1024];
+    for (int k = threadIdx.x; k < nk && k < 1024; k += blockDim.x) ys[k] = y[k];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nk; ++k) s = fma(ys[k], V[(int64_t)k * n + i], s);
+        u[i] = s;
+    }
+}
+
+__global__ void k_scale(const double *x, int64_t n, const double *den, double *y) {
+    const double d = *den;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] / d;
+}
+
+__global__ void k_sqrt(double *x) { *x = sqrt(*x); }
+
+struct GmresState {
+    double *H;     // (m+1) x m, row-major (i, j) at i*m + j
+    double *cs, *sn, *g;
+    double *h1, *h2;  // dot results (m+1)
+    double *hnext;    // ||w|| after orthogonalisation
+    double *y;        // triangular solve result
+    int *status;      // [0] breakdown, [1] dead column, [2] converged-by-estimate
+    double *hist;     // |g[j+1]| per iteration
+};
+
+// Arnoldi column j: h = h1 + h2, Hessenberg update, Givens (krylov.py:75-104)
+__global__ void k_arnoldi_tail(GmresState st, int m, int j, double tol) {
+    double *H = st.H;
+    const double hn = sqrt(*st.hnext);
+    double cs2 = 0.0;
+    for (int i = 0; i <= j; ++i) {
+        double hv = st.h1[i] + st.h2[i];
+        H[i * m + j] = hv;
+        cs2 += hv * hv;
+    }
+    H[(j + 1) * m + j] = hn;
+    cs2 += hn * hn;
+    const double colscale = sqrt(cs2);
+    int brk = !(hn > 1e-12 * fmax(colscale, 1e-300));
+    *st.hnext = hn;
+    for (int i = 0; i < j; ++i) {
+        double t = H[i * m + j];
+        H[i * m + j] = st.cs[i] * t + st.sn[i] * H[(i + 1) * m + j];
+        H[(i + 1) * m + j] = -st.sn[i] * t + st.cs[i] * H[(i + 1) * m + j];
+    }
+    const double a = H[j * m + j], b = H[(j + 1) * m + j];
+    const double rho = hypot(a, b);
+    if (rho == 0.0) {
+        st.status[0] = 1;
+        st.status[1] = 1;
+        return;
+    }
+    st.cs[j] = a / rho;
+    st.sn[j] = b / rho;
+    H[j * m + j] = rho;
+    H[(j + 1) * m + j] = 0.0;
+    st.g[j + 1] = -st.sn[j] * st.g[j];
+    st.g[j] = st.cs[j] * st.g[j];
+    const double est = fabs(st.g[j + 1]);
+    st.hist[j] = est;
+    st.status[0] = brk;
+    st.status[1] = 0;
+    st.status[2] = est <= tol;
+}
+
+__global__ void k_cycle_init(GmresState st, int m, const double *beta) {
+    for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) st.H[i] = 0.0;
+    for (int i = threadIdx.x; i <= m; i += blockDim.x) st.g[i] = (i == 0) ? *beta : 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) st.cs[i] = st.sn[i] = 0.0;
+    if (threadIdx.x == 0) st.status[0] = st.status[1] = st.status[2] = 0;
+}
+
+// back substitution H[:j,:j] y = g[:j]
+__global__ void k_trsv(GmresState st, int m, int j) {
+    for (int i = j - 1; i >= 0; --i) {
+        double s = st.g[i];
+        for (int k = i + 1; k < j; ++k) s -= st.H[i * m + k] * st.y[k];
+        st.y[i] = s / st.H[i * m + i];
+    }
+}
+
+struct Reducer {
+    TBuf<double> partial;
+    int nblk = 0, ld = 0;
+    void init(int64_t n, int maxk, cudaStream_t s) {
+        nblk = dot_grid(n);
+        ld = maxk > 1 ? maxk : 1;
+        partial.alloc((int64_t)nblk * ld, s);
+    }
+};
+
+void norm2(const double *x, int64_t n, Reducer &R, double *out, cudaStream_t s) {
+    // ||x||^2 via the update kernel with no basis vectors
+    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(nullptr, n, 0, nullptr, const_cast<double *>(x), 2, R.partial.p, R.ld);
+    PMGR_LAUNCHED();
+    k_reduce_partials<<<1, 32, 0, s>>>(R.partial.p, R.nblk, 1, R.ld, out, 0);
+    PMGR_LAUNCHED();
+    k_sqrt<<<1, 1, 0, s>>>(out);
+    PMGR_LAUNCHED();
+}
+
+}  // namespace
+
+void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, int nonzero_x0,
+                  const pmgr_gmres_cfg &cfg, pmgr_gmres_stats &stats, double *history, int32_t history_cap,
+                  cudaStream_t s) {
+    if (cfg.restart < 1) fail(PMGR_ERR_INVALID, "restart must be >= 1");
+    if (!(cfg.rtol > 0) || !(cfg.atol > 0)) fail(PMGR_ERR_INVALID, "tolerances must be positive");
+    const CsrView Av = A->m->view();
+    if (Av.nrows != Av.ncols) fail(PMGR_ERR_INVALID, "gmres requires a square operator");
+    if (M && M->n != Av.nrows) fail(PMGR_ERR_INVALID, "preconditioner size does not match the operator");
+    const int64_t n = Av.nrows;
+    const int m = cfg.restart;
+    TBuf<double> V((int64_t)(m + 1) * n, s), w(n, s), z(n, s), r(n, s);
+    TBuf<double> small((int64_t)(m + 1) * m + 6 * (m + 1) + 8, s);
+    TBuf<int> status(4, s);
+    TBuf<double> dhist(m + 1, s);
+    GmresState st;
+    st.H = small.p;
+    st.cs = st.H + (m + 1) * m;
+    st.sn = st.cs + (m + 1);
+    st.g = st.sn + (m + 1);
+    st.h1 = st.g + (m + 1);
+    st.h2 = st.h1 + (m + 1);
+    st.y = st.h2 + (m + 1);
+    st.hnext = st.y + (m + 1);
+    double *beta_d = st.hnext + 1;
+    st.status = status.p;
+    st.hist = dhist.p;
+    Reducer R;
+    R.init(n, m + 1, s);
+
+    std::vector<double> hist;
+    int hcount = 0;
+    auto push_hist = [&](double v) {
+        hist.push_back(v);
+        ++hcount;
+    };
+    auto apply_M = [&](const double *in, double *out) {
+        if (M) mgr_apply(*M, in, out, s);
+        else vec_copy(in, out, n, s);
+    };
+
+    if (nonzero_x0) {
+        spmv_residual(Av, x, b, r.p, s);
+    } else {
+        vec_copy(b, r.p, n, s);
+    }
+    norm2(r.p, n, R, beta_d, s);
+    double beta = read_scalar(beta_d, s);
+    push_hist(beta);
+    const double tol = std::fmax(cfg.rtol * beta, cfg.atol);
+    int total = 0;
+    int restarts = 0;
+    bool converged = beta <= tol;
+    if (!converged) {
+        while (total < cfg.max_iters) {
+            k_cycle_init<<<1, 256, 0, s>>>(st, m, beta_d);
+            PMGR_LAUNCHED();
+            k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(r.p, n, beta_d, V.p);
+            PMGR_LAUNCHED();
+            int j = 0;
+            bool brk = false;
+            while (j < m && total < cfg.max_iters) {
+                double *Vj = V.p + (int64_t)j * n;
+                apply_M(Vj, z.p);
+                spmv(Av, z.p, w.p, s);
+                const int nk = j + 1;
+                k_multidot<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, w.p, R.partial.p, R.ld);
+                PMGR_LAUNCHED();
+                k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h1, 0);
+                PMGR_LAUNCHED();
+                k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h1, w.p, 1, R.partial.p, R.ld);
+                PMGR_LAUNCHED();
+                k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h2, 0);
+                PMGR_LAUNCHED();
+                k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h2, w.p, 2, R.partial.p, R.ld);
+                PMGR_LAUNCHED();
+                k_reduce_partials<<<1, 32, 0, s>>>(R.partial.p, R.nblk, 1, R.ld, st.hnext, 0);
+                PMGR_LAUNCHED();
+                k_arnoldi_tail<<<1, 1, 0, s>>>(st, m, j, tol);
+                PMGR_LAUNCHED();
+                int flags[3];
+                PMGR_CUDA(cudaMemcpyAsync(flags, status.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
+                PMGR_CUDA(cudaStreamSynchronize(s));
+                if (flags[1]) {  // dead column: discard (krylov.py:88-91)
+                    brk = true;
+                    break;
+                }
+                if (!flags[0]) {
+                    k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(w.p, n, st.hnext, V.p + (int64_t)(j + 1) * n);
+                    PMGR_LAUNCHED();
+                } else {
+                    brk = true;
+                }
+                ++total;
+                ++j;
+                double est;
+                PMGR_CUDA(cudaMemcpyAsync(&est, dhist.p + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+                PMGR_CUDA(cudaStreamSynchronize(s));
+                push_hist(est);
+                if (flags[2] || brk) break;
+            }
+            if (j > 0) {
+                k_trsv<<<1, 1, 0, s>>>(st, m, j);
+                PMGR_LAUNCHED();
+                k_combine<<<dot_grid(n), DOT_BLOCK, 0, s>>>(V.p, n, j, st.y, w.p);
+                PMGR_LAUNCHED();
+                apply_M(w.p, z.p);
+                vec_axpy(1.0, z.p, x, n, s);
+                spmv_residual(Av, x, b, r.p, s);
+                norm2(r.p, n, R, beta_d, s);
+                beta = read_scalar(beta_d, s);
+                hist.back() = beta;
+            }
+            ++restarts;
+            if (beta <= tol) {
+                converged = true;
+                break;
+            }
+            if (brk) break;
+        }
+    }
+    stats.iterations = total;
+    stats.converged = beta <= tol;
+    stats.restarts = restarts;
+    int32_t nh = (int32_t)hist.size();
+    stats.history_len = nh < history_cap ? nh : history_cap;
+    if (history)
+        for (int32_t i = 0; i < stats.history_len; ++i) history[i] = hist[i];
+    (void)converged;
+    (void)hcount;
+}
+
+void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double *h, cudaStream_t s) {
+    Reducer R;
+    R.init(n, nvec, s);
+    k_multidot<<<R.nblk, DOT_BLOCK, 0, s>>>(V, n, nvec, w, R.partial.p, R.ld);
+    PMGR_LAUNCHED();
+    k_reduce_partials<<<(nvec * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nvec, R.ld, h, 0);
+    PMGR_LAUNCHED();
+}
+
+void multiaxpy(const double *V, int64_t n, int32_t nvec, const double *h, double *w, cudaStream_t s) {
+    Reducer R;
+    R.init(n, 1, s);
+    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V, n, nvec, h, w, 0, R.partial.p, R.ld);
+    PMGR_LAUNCHED();
+}
+
+}  // namespace pmgr

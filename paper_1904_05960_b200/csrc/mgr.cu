@@ -1,0 +1,414 @@
+// mgr.cu -- MGR setup and application on the device (reference mgr.py).
+//
+// Setup per level (mgr.py:329-371):
+//   split      is_c from the level's field tags; C/F row lists and index maps
+//   blocks     A_FF, A_FC, A_CF, A_CC with order-preserving renumbering and
+//              explicit zeros kept (extract_blocks, sparse.py:269-288)
+//   transfers  dinv = 1.0/diag(A_FF); P = [W_p; I] with W_p = A_FC*(-dinv)
+//              row-scaled; R = [0 I] is an injection and never stored
+//              (build_transfers, mgr.py:131-187, injection_jacobi/injection)
+//   F-relax    AMG on A_FF (num_functions 3 for F={U}) or Jacobi (mgr.py:374-386)
+//   coarse     T = (R A) P with the structural pattern (spgemm keeps
+//              cancellations as +0.0); with n_max the non-Galerkin
+//              A_CC - sparsify(A_CC - T) (build_coarse, mgr.py:212-231)
+// Apply per level (mgr.py:405-429), with f_relax_position "pre":
+//   z_F = M_FF^{-1} v_F ; r_C = v_C - A_CF z_F ; e_C = next level ;
+//   z = [z_F; 0] + P e_C
+// The residual is only formed on C rows (R is an injection) and only
+// against A_CF, which reads a fraction of A: the same numbers, since the
+// skipped terms multiply exact zeros of z.
+#include <set>
+
+#include "hier.cuh"
+
+namespace pmgr {
+
+namespace {
+
+__global__ void k_split(int64_t n, const int8_t *field, uint64_t cmask, int8_t *is_c, int64_t *c64,
+                        int64_t *f64) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int8_t c = (cmask >> (field[i] & 63)) & 1ull;
+    is_c[i] = c;
+    c64[i] = c;
+    f64[i] = 1 - c;
+}
+
+__global__ void k_index_maps(int64_t n, const int8_t *is_c, const int64_t *cscan, const int64_t *fscan,
+                             int64_t *c_index, int64_t *f_index, int64_t *c_rows, int64_t *f_rows) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (is_c[i]) {
+        c_index[i] = cscan[i];
+        f_index[i] = -1;
+        c_rows[cscan[i]] = i;
+    } else {
+        c_index[i] = -1;
+        f_index[i] = fscan[i];
+        f_rows[fscan[i]] = i;
+    }
+}
+
+// block extraction: rows from `rows` (k-th output row = A row rows[k]),
+// columns with colmap[j] >= 0 and is_c[j] == want_c, renumbered by colmap
+template <bool FILL>
+__global__ void k_extract(int64_t nout, const int64_t *rows, const int64_t *ro, const int32_t *ci,
+                          const double *v, const int8_t *is_c, int8_t want_c, const int64_t *colmap,
+                          int64_t *cnt, const int64_t *oro, int32_t *oci, double *ov) {
+    int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (k >= nout) return;
+    const int64_t i = rows[k];
+    int64_t w = FILL ? oro[k] : 0;
+    for (int64_t q0 = ro[i]; q0 < ro[i + 1]; q0 += 32) {
+        int64_t q = q0 + lane;
+        bool keep = false;
+        int32_t j = 0;
+        if (q < ro[i + 1]) {
+            j = ci[q];
+            keep = is_c[j] == want_c;
+        }
+        unsigned m = __ballot_sync(FULL, keep);
+        if (FILL && keep) {
+            int pos = __popc(m & ((1u << lane) - 1u));
+            oci[w + pos] = (int32_t)colmap[j];
+            ov[w + pos] = v[q];
+        }
+        w += __popc(m);
+    }
+    if (!FILL && lane == 0) cnt[k] = w;
+}
+
+// rows of A (all columns), -0.0 normalised to +0.0 (R A = 1.0*a summed from 0.0)
+template <bool FILL>
+__global__ void k_rows_of(int64_t nout, const int64_t *rows, const int64_t *ro, const int32_t *ci,
+                          const double *v, int64_t *cnt, const int64_t *oro, int32_t *oci, double *ov) {
+    int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (k >= nout) return;
+    const int64_t i = rows[k];
+    if (!FILL) {
+        if (lane == 0) cnt[k] = ro[i + 1] - ro[i];
+        return;
+    }
+    const int64_t off = oro[k] - ro[i];
+    for (int64_t q = ro[i] + lane; q < ro[i + 1]; q += 32) {
+        oci[q + off] = ci[q];
+        double a = v[q];
+        ov[q + off] = (a == 0.0) ? 0.0 : a;
+    }
+}
+
+// P = [W_p; I] in level order
+template <bool FILL>
+__global__ void k_build_p(int64_t n, const int8_t *is_c, const int64_t *c_index, const int64_t *f_index,
+                          const int64_t *fc_ro, const int32_t *fc_ci, const double *fc_v, const double *dinv,
+                          int with_wp, int64_t *cnt, const int64_t *pro, int32_t *pci, double *pv) {
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    if (is_c[i]) {
+        if (lane == 0) {
+            if (FILL) {
+                pci[pro[i]] = (int32_t)c_index[i];
+                pv[pro[i]] = 1.0;
+            } else {
+                cnt[i] = 1;
+            }
+        }
+        return;
+    }
+    const int64_t f = f_index[i];
+    if (!FILL) {
+        if (lane == 0) cnt[i] = with_wp ? fc_ro[f + 1] - fc_ro[f] : 0;
+        return;
+    }
+    if (!with_wp) return;
+    const double s = -dinv[f];
+    const int64_t off = pro[i] - fc_ro[f];
+    for (int64_t q = fc_ro[f] + lane; q < fc_ro[f + 1]; q += 32) {
+        pci[q + off] = fc_ci[q];
+        pv[q + off] = __dmul_rn(fc_v[q], s);
+    }
+}
+
+__global__ void k_scatter_add(const double *src, const int64_t *idx, int64_t n, double *dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[idx[i]] += src[i];
+}
+
+__global__ void k_jacobi_dinv(int64_t n, const int64_t *ro, const int32_t *ci, const double *v,
+                              const double *x, const double *b, const double *dinv, double *xo) {
+    // x' = x + dinv * (b - A x)  (mgr.py:249), warp per row
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int64_t q = ro[i] + lane; q < ro[i + 1]; q += 32) s = fma(v[q], x[ci[q]], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0) xo[i] = x[i] + dinv[i] * (b[i] - s);
+}
+
+// Extract one block: rows given by `rows` (count nout), columns on the
+// `want_c` side renumbered through colmap.
+void extract_block(const CsrView &A, const int64_t *rows, int64_t nout, const int8_t *is_c, bool want_c,
+                   const int64_t *colmap, int64_t ncols_out, Csr &B, cudaStream_t s) {
+    TBuf<int64_t> cnt(nout, s);
+    B.nrows = nout;
+    B.ncols = ncols_out;
+    B.ro.alloc(nout + 1);
+    if (nout) {
+        k_extract<false><<<grid_for(nout * 32, 256), 256, 0, s>>>(nout, rows, A.ro, A.ci, A.v, is_c, want_c ? 1 : 0,
+                                                                 colmap, cnt.p, nullptr, nullptr, nullptr);
+        PMGR_LAUNCHED();
+    }
+    B.nnz = exclusive_scan_total(cnt.p, B.ro.p, nout, s);
+    B.ci.alloc(B.nnz);
+    B.v.alloc(B.nnz);
+    if (nout) {
+        k_extract<true><<<grid_for(nout * 32, 256), 256, 0, s>>>(nout, rows, A.ro, A.ci, A.v, is_c, want_c ? 1 : 0,
+                                                                colmap, nullptr, B.ro.p, B.ci.p, B.v.p);
+        PMGR_LAUNCHED();
+    }
+}
+
+void rows_of(const CsrView &A, const int64_t *rows, int64_t nout, Csr &B, cudaStream_t s) {
+    TBuf<int64_t> cnt(nout, s);
+    B.nrows = nout;
+    B.ncols = A.ncols;
+    B.ro.alloc(nout + 1);
+    if (nout) {
+        k_rows_of<false><<<grid_for(nout * 32, 256), 256, 0, s>>>(nout, rows, A.ro, A.ci, A.v, cnt.p, nullptr,
+                                                                 nullptr, nullptr);
+        PMGR_LAUNCHED();
+    }
+    B.nnz = exclusive_scan_total(cnt.p, B.ro.p, nout, s);
+    B.ci.alloc(B.nnz);
+    B.v.alloc(B.nnz);
+    if (nout) {
+        k_rows_of<true><<<grid_for(nout * 32, 256), 256, 0, s>>>(nout, rows, A.ro, A.ci, A.v, nullptr, B.ro.p,
+                                                                B.ci.p, B.v.p);
+        PMGR_LAUNCHED();
+    }
+}
+
+std::string field_names(const std::set<int> &f) {
+    std::string out = "[";
+    bool first = true;
+    for (int t : f) {
+        if (!first) out += ", ";
+        first = false;
+        const char *nm = t == 0 ? "'U'" : t == 1 ? "'S'" : t == 2 ? "'P'" : nullptr;
+        out += nm ? nm : ("'F" + std::to_string(t) + "'");
+    }
+    return out + "]";
+}
+
+void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s);
+
+void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
+    if (L.f_relax == PMGR_FRELAX_AMG) {
+        amg_cycle(*L.amg, vf, nullptr, zf, s);
+        for (int c = 1; c < L.f_relax_sweeps; ++c) {
+            vec_copy(zf, L.tmpf.p, L.nf, s);
+            amg_cycle(*L.amg, vf, L.tmpf.p, zf, s);
+        }
+    } else {
+        vec_mul(L.dinv_ff.p, vf, zf, L.nf, s);
+        for (int c = 1; c < L.f_relax_sweeps; ++c) {
+            const CsrView F = L.A_ff->view();
+            k_jacobi_dinv<<<grid_for(L.nf * 32, 256), 256, 0, s>>>(L.nf, F.ro, F.ci, F.v, zf, vf, L.dinv_ff.p,
+                                                                   L.tmpf.p);
+            PMGR_LAUNCHED();
+            vec_copy(L.tmpf.p, zf, L.nf, s);
+        }
+    }
+}
+
+void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s) {
+    if (l == h.levels.size()) {
+        amg_cycle(*h.terminal, v, nullptr, z, s);
+        for (int c = 1; c < h.terminal_cycles; ++c) {
+            vec_copy(z, h.tz.p, h.terminal_A->nrows, s);
+            amg_cycle(*h.terminal, v, h.tz.p, z, s);
+        }
+        return;
+    }
+    MgrLevel &L = h.levels[l];
+    const bool pre = !h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE;
+    if (pre) {
+        vec_gather(v, L.f_rows.p, L.nf, L.vf.p, s);
+        f_relax_apply(L, L.vf.p, L.zf.p, s);
+        spmv_resid_rows(L.A_cf.view(), L.zf.p, v, L.c_rows.p, L.rc.p, s);
+    } else {
+        vec_gather(v, L.c_rows.p, L.nc, L.rc.p, s);
+    }
+    apply_level(h, l + 1, L.rc.p, L.zc.p, s);
+    spmv_prolong_combine(L.P.view(), L.zc.p, pre ? L.zf.p : nullptr, pre ? L.f_index.p : nullptr, z, s);
+    if (h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
+        // r = v - A z ; z[F] += M_FF^{-1} r[F]
+        DBuf<double> &r = L.tmpf;  // reuse: needs n, allocated as max(n, nf)
+        spmv_residual(L.A->view(), z, v, r.p, s);
+        vec_gather(r.p, L.f_rows.p, L.nf, L.vf.p, s);
+        f_relax_apply(L, L.vf.p, L.zf.p, s);
+        k_scatter_add<<<grid_for(L.nf, 256), 256, 0, s>>>(L.zf.p, L.f_rows.p, L.nf, z);
+        PMGR_LAUNCHED();
+    }
+}
+
+}  // namespace
+
+std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t *field_of_host,
+                                    const int32_t *entity_of_host, const pmgr_level_spec *specs, int nlevels,
+                                    const pmgr_mgr_cfg &cfg, cudaStream_t s) {
+    if (A0->nrows != A0->ncols) fail(PMGR_ERR_INVALID, "mgr_setup requires a square matrix");
+    auto h = std::make_unique<pmgr_mgr>();
+    h->n = A0->nrows;
+    h->terminal_cycles = cfg.terminal_cycles > 1 ? cfg.terminal_cycles : 1;
+    h->f_relax_post = cfg.f_relax_post;
+    std::vector<int8_t> fo(field_of_host, field_of_host + A0->nrows);
+    std::vector<int32_t> eo(entity_of_host, entity_of_host + A0->nrows);
+    std::shared_ptr<const Csr> cur = A0;
+    for (int li = 0; li < nlevels; ++li) {
+        const pmgr_level_spec &sp = specs[li];
+        std::set<int> present;
+        for (int8_t t : fo) present.insert((int)t);
+        std::set<int> spec_f;
+        for (int t = 0; t < 64; ++t)
+            if (((sp.f_mask | sp.c_mask) >> t) & 1ull) spec_f.insert(t);
+        if (sp.f_mask & sp.c_mask) fail(PMGR_ERR_INVALID, "f_fields and c_fields must be disjoint");
+        if (spec_f != present)
+            fail(PMGR_ERR_FIELDS, "level spec fields " + field_names(spec_f) + " do not cover the fields present " +
+                                      field_names(present));
+        if (!sp.c_mask) fail(PMGR_ERR_INVALID, "empty C set: nothing to reduce onto");
+        if (sp.global_smoother != PMGR_SMOOTHER_NONE)
+            fail(PMGR_ERR_NOT_SUPPORTED, "global smoothers (hbgs/ilu) are not on the device path yet");
+        if (sp.interp == PMGR_INTERP_IDEAL || sp.restrict_ != PMGR_RESTRICT_INJECTION)
+            fail(PMGR_ERR_NOT_SUPPORTED, "only injection restriction with injection/injection_jacobi "
+                                         "interpolation is on the device path");
+        if (sp.f_relax == PMGR_FRELAX_EXACT) fail(PMGR_ERR_NOT_SUPPORTED, "exact F-relaxation is not on the device path");
+        if (sp.quasi_impes) fail(PMGR_ERR_NOT_SUPPORTED, "quasi-IMPES is not on the device path");
+        const int64_t n = cur->nrows;
+        int64_t nc_h = 0;
+        for (int8_t t : fo) nc_h += (sp.c_mask >> (t & 63)) & 1ull;
+        if (nc_h == n) {
+            if (present.size() != 1) fail(PMGR_ERR_INVALID, "an all-C level requires a single remaining field");
+            break;  // reduction-free limit (mgr.py:347-352)
+        }
+        MgrLevel L;
+        L.A = cur;
+        L.n = n;
+        L.nc = nc_h;
+        L.nf = n - nc_h;
+        // ---- split and index maps
+        TBuf<int8_t> field(n, s);
+        PMGR_CUDA(cudaMemcpyAsync(field.p, fo.data(), n, cudaMemcpyHostToDevice, s));
+        L.is_c.alloc(n);
+        TBuf<int64_t> c64(n, s), f64(n, s), cscan(n + 1, s), fscan(n + 1, s), c_index(n, s);
+        k_split<<<grid_for(n, 256), 256, 0, s>>>(n, field.p, sp.c_mask, L.is_c.p, c64.p, f64.p);
+        PMGR_LAUNCHED();
+        exclusive_scan_total(c64.p, cscan.p, n, s);
+        exclusive_scan_total(f64.p, fscan.p, n, s);
+        L.c_rows.alloc(L.nc);
+        L.f_rows.alloc(L.nf);
+        L.f_index.alloc(n);
+        k_index_maps<<<grid_for(n, 256), 256, 0, s>>>(n, L.is_c.p, cscan.p, fscan.p, c_index.p, L.f_index.p,
+                                                     L.c_rows.p, L.f_rows.p);
+        PMGR_LAUNCHED();
+        // ---- blocks (extract_blocks, sparse.py:269-288)
+        const CsrView Av = cur->view();
+        auto A_ff = std::make_shared<Csr>();
+        Csr A_fc, A_cc;
+        extract_block(Av, L.f_rows.p, L.nf, L.is_c.p, false, L.f_index.p, L.nf, *A_ff, s);
+        extract_block(Av, L.f_rows.p, L.nf, L.is_c.p, true, c_index.p, L.nc, A_fc, s);
+        extract_block(Av, L.c_rows.p, L.nc, L.is_c.p, false, L.f_index.p, L.nf, L.A_cf, s);
+        if (sp.n_max >= 0) extract_block(Av, L.c_rows.p, L.nc, L.is_c.p, true, c_index.p, L.nc, A_cc, s);
+        // ---- transfers (build_transfers, mgr.py:131-187)
+        const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
+        if (need_dinv) {
+            L.dinv_ff.alloc(L.nf);
+            int64_t bad = csr_diag_inverse(A_ff->view(), L.dinv_ff.p, s);
+            if (bad >= 0)
+                fail(PMGR_ERR_SINGULAR_DIAG, "singular diagonal: zero or missing entry at row " + std::to_string(bad),
+                     bad);
+        }
+        const int with_wp = sp.interp == PMGR_INTERP_INJECTION_JACOBI ? 1 : 0;
+        {
+            TBuf<int64_t> cnt(n, s);
+            L.P.nrows = n;
+            L.P.ncols = L.nc;
+            L.P.ro.alloc(n + 1);
+            k_build_p<false><<<grid_for(n * 32, 256), 256, 0, s>>>(n, L.is_c.p, c_index.p, L.f_index.p, A_fc.ro.p,
+                                                                  A_fc.ci.p, A_fc.v.p, L.dinv_ff.p, with_wp, cnt.p,
+                                                                  nullptr, nullptr, nullptr);
+            PMGR_LAUNCHED();
+            L.P.nnz = exclusive_scan_total(cnt.p, L.P.ro.p, n, s);
+            L.P.ci.alloc(L.P.nnz);
+            L.P.v.alloc(L.P.nnz);
+            k_build_p<true><<<grid_for(n * 32, 256), 256, 0, s>>>(n, L.is_c.p, c_index.p, L.f_index.p, A_fc.ro.p,
+                                                                 A_fc.ci.p, A_fc.v.p, L.dinv_ff.p, with_wp, nullptr,
+                                                                 L.P.ro.p, L.P.ci.p, L.P.v.p);
+            PMGR_LAUNCHED();
+        }
+        // ---- F-relaxation (_build_f_relax, mgr.py:374-386)
+        L.f_relax = sp.f_relax;
+        L.f_relax_sweeps = sp.f_relax_sweeps > 1 ? sp.f_relax_sweeps : 1;
+        if (sp.f_relax == PMGR_FRELAX_AMG) {
+            pmgr_amg_cfg acfg = cfg.amg_f_relax;
+            acfg.num_functions = sp.amg_num_functions > 0 ? sp.amg_num_functions : 1;
+            L.amg = amg_build(A_ff, acfg, s);
+        }
+        if (sp.f_relax == PMGR_FRELAX_JACOBI && L.f_relax_sweeps > 1) L.A_ff = A_ff;
+        // ---- coarse operator (build_coarse, mgr.py:212-231)
+        auto coarse = std::make_shared<Csr>();
+        {
+            Csr RA, T;
+            rows_of(Av, L.c_rows.p, L.nc, RA, s);
+            if (sp.n_max < 0) {
+                spgemm(RA.view(), L.P.view(), 1, *coarse, s);
+            } else {
+                spgemm(RA.view(), L.P.view(), 1, T, s);
+                Csr corr, kept;
+                csr_subtract(A_cc.view(), T.view(), corr, s);
+                TBuf<int32_t> ent(L.nc, s);
+                std::vector<int32_t> ec;
+                ec.reserve(L.nc);
+                for (int64_t i = 0; i < n; ++i)
+                    if ((sp.c_mask >> (fo[i] & 63)) & 1ull) ec.push_back(eo[i]);
+                PMGR_CUDA(cudaMemcpyAsync(ent.p, ec.data(), sizeof(int32_t) * L.nc, cudaMemcpyHostToDevice, s));
+                csr_sparsify(corr.view(), ent.p, sp.n_max, kept, s);
+                csr_subtract(A_cc.view(), kept.view(), *coarse, s);
+                PMGR_CUDA(cudaStreamSynchronize(s));
+            }
+        }
+        // ---- workspace
+        L.vf.alloc(L.nf);
+        L.zf.alloc(L.nf);
+        L.rc.alloc(L.nc);
+        L.zc.alloc(L.nc);
+        L.tmpf.alloc(n > L.nf ? n : L.nf);
+        // ---- next layout
+        std::vector<int8_t> fo2;
+        std::vector<int32_t> eo2;
+        for (int64_t i = 0; i < n; ++i)
+            if ((sp.c_mask >> (fo[i] & 63)) & 1ull) {
+                fo2.push_back(fo[i]);
+                eo2.push_back(eo[i]);
+            }
+        fo.swap(fo2);
+        eo.swap(eo2);
+        h->levels.push_back(std::move(L));
+        cur = coarse;
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+    h->terminal_A = cur;
+    h->terminal = amg_build(cur, cfg.amg_terminal, s);
+    h->tz.alloc(cur->nrows);
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) { apply_level(h, 0, v, z, s); }
+
+}  // namespace pmgr

@@ -1,0 +1,92 @@
+// prims.cu -- scans, segmented sorts and reductions (CUB device primitives).
+#include <cstring>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include "common.cuh"
+
+namespace pmgr {
+
+std::atomic<int64_t> g_launches{0};
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        PMGR_CUDA(cudaGetDevice(&dev));
+        PMGR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return sms;
+}
+
+namespace {
+__global__ void k_set_zero_i64(int64_t *p) { *p = 0; }
+
+template <class T>
+__global__ void k_widen(const T *in, int64_t *out, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int64_t)in[i];
+}
+
+// max |x|: non-negative doubles order like their bit patterns
+__global__ void k_max_abs(const double *x, int64_t n, unsigned long long *out) {
+    double m = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(x[i]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+}  // namespace
+
+int64_t exclusive_scan_total(const int64_t *in, int64_t *out, int64_t n, cudaStream_t s) {
+    // out has n+1 entries: inclusive scan written at out+1, out[0] = 0.
+    k_set_zero_i64<<<1, 1, 0, s>>>(out);
+    PMGR_LAUNCHED();
+    if (n > 0) {
+        size_t tmp = 0;
+        PMGR_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out + 1, n, s));
+        TBuf<char> t((int64_t)tmp, s);
+        PMGR_CUDA(cub::DeviceScan::InclusiveSum(t.p, tmp, in, out + 1, n, s));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return read_scalar(out + n, s);
+}
+
+int64_t exclusive_scan_total_i32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s) {
+    TBuf<int64_t> w(n, s);
+    if (n > 0) {
+        k_widen<<<grid_for(n, 256), 256, 0, s>>>(in, w.p, n);
+        PMGR_LAUNCHED();
+    }
+    return exclusive_scan_total(w.p, out, n, s);
+}
+
+void segmented_sort_pairs(int32_t *keys, double *vals, int64_t nnz, const int64_t *ro,
+                          int64_t nrows, cudaStream_t s) {
+    if (nnz <= 1 || nrows == 0) return;
+    TBuf<int32_t> k2(nnz, s);
+    TBuf<double> v2(nnz, s);
+    size_t tmp = 0;
+    PMGR_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, keys, k2.p, vals, v2.p, nnz,
+                                                  nrows, ro, ro + 1, s));
+    TBuf<char> t((int64_t)tmp, s);
+    PMGR_CUDA(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, keys, k2.p, vals, v2.p, nnz, nrows,
+                                                  ro, ro + 1, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    PMGR_CUDA(cudaMemcpyAsync(keys, k2.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s));
+    PMGR_CUDA(cudaMemcpyAsync(vals, v2.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+}
+
+double device_max_abs(const double *x, int64_t n, cudaStream_t s) {
+    if (n == 0) return 0.0;
+    TBuf<unsigned long long> out(1, s);
+    PMGR_CUDA(cudaMemsetAsync(out.p, 0, sizeof(unsigned long long), s));
+    k_max_abs<<<grid_for(n, 256) < 4096 ? grid_for(n, 256) : 4096, 256, 0, s>>>(x, n, out.p);
+    PMGR_LAUNCHED();
+    unsigned long long bits = read_scalar(out.p, s);
+    double r;
+    memcpy(&r, &bits, sizeof(r));
+    return r;
+}
+
+}  // namespace pmgr

@@ -1,0 +1,252 @@
+// spmv.cu -- fp64 CSR SpMV family and the fused smoother / transfer kernels
+// of the solve phase.
+//
+// One kernel template, k_spmv<G, Op>: a group of G lanes per row walks the
+// row's (value, column) pairs with coalesced loads, gathers x through the
+// read-only path, reduces with shuffles and hands the row sum to an epilogue
+// functor.  The functors fuse what the reference does as separate numpy
+// passes around scipy's csr_matvec (sparse.py:261-266):
+//   OpY            y = A x                                  (matvec)
+//   OpResidual     r = b - A x                              (amg.py:227, mgr.py:421)
+//   OpJacobi       x' = x + (b - A x) / dtilde              (l1_gs_kernel, n partitions)
+//   OpSweep0       x = b / dtilde ; r = b - A x  (first sweep from x = 0, fused)
+//   OpAdd          x += P e                                 (amg.py:230)
+//   OpResidRows    r_C = v_C - A_CF z_F                     (mgr.py:419-422, C rows only)
+//   OpProlong      z = [z_F ; 0] + P e_C                    (mgr.py:424-425)
+// The solve phase only needs 1e-10 agreement, so these use FMA.
+#include "common.cuh"
+
+namespace pmgr {
+
+namespace {
+
+template <int G, class Op>
+__global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
+                                              const int32_t *__restrict__ ci,
+                                              const double *__restrict__ v, Op op) {
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const bool active = row < nrows;
+    int64_t b = 0, e = 0;
+    if (active) {
+        b = __ldg(ro + row);
+        e = __ldg(ro + row + 1);
+    }
+    double s = 0.0;
+    for (int64_t q = b + lane; q < e; q += G) s = fma(__ldg(v + q), op.x(__ldg(ci + q)), s);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
+    if (active && lane == 0) op.out(row, s);
+}
+
+struct OpY {
+    const double *xv;
+    double *y;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void out(int64_t i, double s) const { y[i] = s; }
+};
+struct OpResidual {
+    const double *xv, *b;
+    double *r;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void out(int64_t i, double s) const { r[i] = b[i] - s; }
+};
+struct OpJacobi {
+    const double *xv, *b, *d;
+    double *xo;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void out(int64_t i, double s) const { xo[i] = xv[i] + (b[i] - s) / d[i]; }
+};
+struct OpSweep0 {
+    const double *b, *d;
+    double *xo, *r;
+    __device__ double x(int j) const { return __ldg(b + j) / __ldg(d + j); }
+    __device__ void out(int64_t i, double s) const {
+        xo[i] = b[i] / d[i];
+        r[i] = b[i] - s;
+    }
+};
+struct OpAdd {
+    const double *e;
+    double *xio;
+    __device__ double x(int j) const { return __ldg(e + j); }
+    __device__ void out(int64_t i, double s) const { xio[i] += s; }
+};
+struct OpResidRows {
+    const double *zf, *v;
+    const int64_t *rows;
+    double *r;
+    __device__ double x(int j) const { return __ldg(zf + j); }
+    __device__ void out(int64_t k, double s) const { r[k] = v[rows[k]] - s; }
+};
+struct OpProlong {
+    const double *ec, *zf;
+    const int64_t *findex;
+    double *z;
+    __device__ double x(int j) const { return __ldg(ec + j); }
+    __device__ void out(int64_t i, double s) const {
+        int64_t f = findex ? findex[i] : -1;
+        z[i] = (f >= 0 ? zf[f] : 0.0) + s;
+    }
+};
+
+template <class Op>
+void launch(const CsrView &A, const Op &op, cudaStream_t s) {
+    if (A.nrows == 0) return;
+    double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
+    const int block = 256;
+    if (mean <= 3.0) {
+        k_spmv<2, Op><<<grid_for(A.nrows * 2, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+    } else if (mean <= 12.0) {
+        k_spmv<4, Op><<<grid_for(A.nrows * 4, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+    } else if (mean <= 48.0) {
+        k_spmv<8, Op><<<grid_for(A.nrows * 8, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+    } else if (mean <= 160.0) {
+        k_spmv<16, Op><<<grid_for(A.nrows * 16, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+    } else {
+        k_spmv<32, Op><<<grid_for(A.nrows * 32, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+    }
+    PMGR_LAUNCHED();
+}
+
+// Hybrid l1-GS over contiguous partitions (l1_gs_kernel, _kernels.py:13-44):
+// one thread per partition runs Gauss-Seidel over its rows in order, reading
+// the pre-sweep vector for columns outside the partition.
+__global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
+                            const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
+                            const double *__restrict__ v, const double *__restrict__ d,
+                            const double *__restrict__ b, double *x, const double *__restrict__ xpre,
+                            int forward) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= nparts) return;
+    int64_t lo = starts[p], hi = starts[p + 1];
+    for (int64_t t = 0; t < hi - lo; ++t) {
+        int64_t i = forward ? lo + t : hi - 1 - t;
+        double s = 0.0;
+        for (int64_t q = ro[i]; q < ro[i + 1]; ++q) {
+            int64_t j = ci[q];
+            s += v[q] * ((j >= lo && j < hi) ? x[j] : xpre[j]);
+        }
+        x[i] += (b[i] - s) / d[i];
+    }
+}
+
+__global__ void k_dense_matvec(const double *__restrict__ M, int64_t n, const double *__restrict__ x,
+                               double *__restrict__ y) {
+    // one warp per row
+    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    double s = 0.0;
+    for (int64_t j = lane; j < n; j += 32) s = fma(M[row * n + j], x[j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0) y[row] = s;
+}
+
+__global__ void k_gather(const double *__restrict__ src, const int64_t *__restrict__ idx, int64_t n,
+                         double *__restrict__ dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void k_scale_gather(const double *__restrict__ src, const int64_t *__restrict__ idx,
+                               const double *__restrict__ d, int64_t n, double *__restrict__ dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = d[i] * src[idx[i]];
+}
+__global__ void k_zero(double *x, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = 0.0;
+}
+__global__ void k_axpy(double a, const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i] += a * x[i];
+}
+__global__ void k_mul(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ y,
+                      int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i] = a[i] * b[i];
+}
+
+}  // namespace
+
+void spmv(const CsrView &A, const double *x, double *y, cudaStream_t s) { launch(A, OpY{x, y}, s); }
+
+void spmv_residual(const CsrView &A, const double *x, const double *b, double *r, cudaStream_t s) {
+    launch(A, OpResidual{x, b, r}, s);
+}
+
+void spmv_jacobi(const CsrView &A, const double *x, const double *b, const double *d, double *xo,
+                 cudaStream_t s) {
+    launch(A, OpJacobi{x, b, d, xo}, s);
+}
+
+void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x, double *r,
+                          cudaStream_t s) {
+    launch(A, OpSweep0{b, d, x, r}, s);
+}
+
+void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s) {
+    launch(A, OpAdd{e, x}, s);
+}
+
+void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows,
+                     double *r, cudaStream_t s) {
+    launch(A, OpResidRows{zf, v, rows, r}, s);
+}
+
+void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf, const int64_t *findex,
+                          double *z, cudaStream_t s) {
+    launch(P, OpProlong{ec, zf, findex, z}, s);
+}
+
+void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,
+               const double *b, double *x, double *xpre, bool forward, cudaStream_t s) {
+    PMGR_CUDA(cudaMemcpyAsync(xpre, x, sizeof(double) * A.nrows, cudaMemcpyDeviceToDevice, s));
+    k_hybrid_gs<<<grid_for(nparts, 128), 128, 0, s>>>(nparts, starts, A.ro, A.ci, A.v, d, b, x, xpre,
+                                                     forward ? 1 : 0);
+    PMGR_LAUNCHED();
+}
+
+void dense_matvec(const double *M, int64_t n, const double *x, double *y, cudaStream_t s) {
+    if (n == 0) return;
+    k_dense_matvec<<<grid_for(n * 32, 256), 256, 0, s>>>(M, n, x, y);
+    PMGR_LAUNCHED();
+}
+
+void vec_gather(const double *src, const int64_t *idx, int64_t n, double *dst, cudaStream_t s) {
+    if (n == 0) return;
+    k_gather<<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst);
+    PMGR_LAUNCHED();
+}
+
+void vec_scale_gather(const double *src, const int64_t *idx, const double *d, int64_t n, double *dst,
+                      cudaStream_t s) {
+    if (n == 0) return;
+    k_scale_gather<<<grid_for(n, 256), 256, 0, s>>>(src, idx, d, n, dst);
+    PMGR_LAUNCHED();
+}
+
+void vec_zero(double *x, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    k_zero<<<grid_for(n, 256), 256, 0, s>>>(x, n);
+    PMGR_LAUNCHED();
+}
+
+void vec_copy(const double *x, double *y, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    PMGR_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+}
+
+void vec_axpy(double a, const double *x, double *y, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    k_axpy<<<grid_for(n, 256), 256, 0, s>>>(a, x, y, n);
+    PMGR_LAUNCHED();
+}
+
+void vec_mul(const double *a, const double *b, double *y, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    k_mul<<<grid_for(n, 256), 256, 0, s>>>(a, b, y, n);
+    PMGR_LAUNCHED();
+}
+
+}  // namespace pmgr

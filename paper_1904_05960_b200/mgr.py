@@ -1,0 +1,239 @@
+"""Multigrid reduction: the reference `poromgr.mgr` surface on the device.
+
+`mgr_setup` (reference mgr.py:329-371) validates the level specs exactly
+like the reference, then builds every level in libpmgr.so: field split,
+block extraction, W_p = -D_FF^-1 A_FC, structural RAP with the optional
+N_max non-Galerkin dropping, AMG / Jacobi F-relaxation and the terminal AMG.
+`mgr_apply` / `MgrHierarchy.apply` run the reduction cycle of mgr.py:399-438.
+
+Options the reference offers but no BASELINE.json config uses (global
+HBGS/ILU smoothers, ideal transfers, exact solves, quasi-IMPES) raise
+NotImplementedError instead of silently running elsewhere.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .amg import AmgConfig, AmgHierarchy
+from .sparse import (CfSplitting, CsrMatrix, DeviceCsr, Field, FieldLayout, as_device_csr, back_like,
+                     current_stream, empty_device, ptr, to_device)
+
+__all__ = ["MgrLevelSpec", "MgrConfig", "MgrHierarchy", "mgr_setup", "mgr_apply"]
+
+logger = logging.getLogger(__name__)
+
+_INTERP_MODES = ("injection_only", "injection_jacobi", "ideal")
+_RESTRICT_MODES = ("injection", "jacobi", "ideal")
+_F_RELAX_MODES = ("none", "jacobi", "amg", "exact")
+_GLOBAL_SMOOTHERS = ("none", "hbgs", "ilu")
+
+
+@dataclass(frozen=True)
+class MgrLevelSpec:
+    """One reduction level (reference mgr.py:53-83)."""
+
+    f_fields: frozenset
+    c_fields: frozenset
+    interp: str = "injection_jacobi"
+    restrict: str = "injection"
+    f_relax: str = "jacobi"
+    f_relax_sweeps: int = 1
+    global_smoother: str = "none"
+    hbgs_sweeps: int = 3
+    ilu_fill: int = 1
+    n_max: int | None = None
+    quasi_impes: bool = False
+
+    def __post_init__(self):
+        object.__setattr__(self, "f_fields", frozenset(Field(f) for f in self.f_fields))
+        object.__setattr__(self, "c_fields", frozenset(Field(f) for f in self.c_fields))
+        if self.f_fields & self.c_fields:
+            raise ValueError("f_fields and c_fields must be disjoint")
+        if self.interp not in _INTERP_MODES:
+            raise ValueError(f"unknown interp mode {self.interp!r}")
+        if self.restrict not in _RESTRICT_MODES:
+            raise ValueError(f"unknown restrict mode {self.restrict!r}")
+        if self.f_relax not in _F_RELAX_MODES:
+            raise ValueError(f"unknown f_relax {self.f_relax!r}")
+        if self.global_smoother not in _GLOBAL_SMOOTHERS:
+            raise ValueError(f"unknown global smoother {self.global_smoother!r}")
+        if self.n_max is not None and self.n_max < 0:
+            raise ValueError("n_max must be >= 0")
+
+    def to_c(self) -> _lib.LevelSpec:
+        fm = 0
+        for f in self.f_fields:
+            fm |= 1 << int(f)
+        cm = 0
+        for f in self.c_fields:
+            cm |= 1 << int(f)
+        nfun = 3 if self.f_fields == {Field.U} else 1  # reference mgr.py:382-385
+        return _lib.LevelSpec(fm, cm, _lib.INTERP[self.interp], _lib.RESTRICT[self.restrict],
+                              _lib.FRELAX[self.f_relax], int(self.f_relax_sweeps),
+                              _lib.SMOOTHER[self.global_smoother], -1 if self.n_max is None else int(self.n_max),
+                              1 if self.quasi_impes else 0, nfun)
+
+
+@dataclass(frozen=True)
+class MgrConfig:
+    """Reference MgrConfig (mgr.py:86-123)."""
+
+    levels: tuple
+    terminal: str = "amg"
+    terminal_cycles: int = 1
+    amg_f_relax: AmgConfig = field(default_factory=lambda: AmgConfig(strength_threshold=0.5, num_functions=3))
+    amg_terminal: AmgConfig = field(default_factory=lambda: AmgConfig(strength_threshold=0.25))
+    npartitions: int = 1
+    ideal_size_cap: int = 2000
+    f_relax_position: str = "pre"
+
+    def __post_init__(self):
+        object.__setattr__(self, "levels", tuple(self.levels))
+        if self.terminal not in ("amg", "exact"):
+            raise ValueError(f"unknown terminal solver {self.terminal!r}")
+        if self.f_relax_position not in ("pre", "post"):
+            raise ValueError("f_relax_position must be 'pre' or 'post'")
+
+    @classmethod
+    def default_three_level(cls, n_max: int = 4, global_smoother: str = "ilu", hbgs_sweeps: int = 3,
+                            ilu_fill: int = 1, quasi_impes: bool = False, npartitions: int = 1,
+                            terminal_cycles: int = 1) -> "MgrConfig":
+        lvl1 = MgrLevelSpec(f_fields={Field.U}, c_fields={Field.S, Field.P}, interp="injection_jacobi",
+                            restrict="injection", f_relax="amg", global_smoother="none", n_max=n_max)
+        lvl2 = MgrLevelSpec(f_fields={Field.S}, c_fields={Field.P}, interp="injection_jacobi",
+                            restrict="injection", f_relax="jacobi", f_relax_sweeps=1,
+                            global_smoother=global_smoother, hbgs_sweeps=hbgs_sweeps, ilu_fill=ilu_fill,
+                            n_max=None, quasi_impes=quasi_impes)
+        return cls(levels=(lvl1, lvl2), terminal="amg", terminal_cycles=terminal_cycles, npartitions=npartitions)
+
+    def to_c(self) -> _lib.MgrCfg:
+        return _lib.MgrCfg(max(1, int(self.terminal_cycles)), 1 if self.f_relax_position == "post" else 0,
+                           self.amg_f_relax.to_c(), self.amg_terminal.to_c())
+
+
+@dataclass
+class MgrLevelView:
+    """Host copy of one reduction level, for inspection and parity checks."""
+
+    split: CfSplitting
+    P: CsrMatrix
+    coarse: CsrMatrix
+
+
+class MgrHierarchy:
+    """Device-resident reduction hierarchy (reference MgrHierarchy, mgr.py:313-326)."""
+
+    def __init__(self, handle, A_dev: DeviceCsr, config: MgrConfig, specs):
+        self._h = handle
+        self._A = A_dev
+        self.config = config
+        self.specs = tuple(specs)
+        n = ctypes.c_int32()
+        _lib.check(_lib.lib().pmgr_mgr_num_levels(self._h, ctypes.byref(n)))
+        self._nlev = n.value
+        self.terminal_cycles = max(1, config.terminal_cycles)
+        self.f_relax_position = config.f_relax_position
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n(self):
+        return self._A.nrows
+
+    def apply(self, v):
+        return mgr_apply(self, v)
+
+    def level_sizes(self):
+        s = np.zeros(self._nlev + 1, dtype=np.int64)
+        _lib.check(_lib.lib().pmgr_mgr_level_sizes(self._h, s.ctypes.data_as(_lib.c_i64p)))
+        return [int(v) for v in s]
+
+    def _export(self, level, what) -> CsrMatrix:
+        out = ctypes.c_void_p()
+        _lib.check(_lib.lib().pmgr_mgr_export_csr(self._h, level, what, current_stream(), ctypes.byref(out)))
+        nr, nc, nz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().pmgr_csr_info(out, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nz)))
+        return DeviceCsr(out, nr.value, nc.value, nz.value).to_host()
+
+    @property
+    def levels(self):
+        out = []
+        sizes = self.level_sizes()
+        for l in range(self._nlev):
+            isc = np.zeros(sizes[l], dtype=np.int8)
+            _lib.check(_lib.lib().pmgr_mgr_export_vec(self._h, l, 0, isc.ctypes.data, current_stream()))
+            out.append(MgrLevelView(CfSplitting(isc.astype(bool)), self._export(l, 0), self._export(l, 1)))
+        return out
+
+    def amg(self, level: int) -> AmgHierarchy | None:
+        """F-relaxation AMG of `level` (-1: terminal AMG), borrowed."""
+        out = ctypes.c_void_p()
+        _lib.check(_lib.lib().pmgr_mgr_amg(self._h, level, ctypes.byref(out)))
+        if not out.value:
+            return None
+        cfg = self.config.amg_terminal if level < 0 else self.config.amg_f_relax
+        return AmgHierarchy(out, cfg, owner=self)
+
+    @property
+    def terminal_solver(self) -> AmgHierarchy:
+        return self.amg(-1)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pmgr_mgr_destroy(self._h)
+            self._h = None
+
+
+def mgr_setup(A, layout: FieldLayout, config: MgrConfig) -> MgrHierarchy:
+    """Build the reduction hierarchy for operator A laid out by `layout`."""
+    dA = as_device_csr(A)
+    if dA.nrows != dA.ncols:
+        raise ValueError("mgr_setup requires a square matrix")
+    if layout.ndofs != dA.nrows:
+        raise ValueError("layout does not match the matrix")
+    if config.terminal != "amg":
+        raise NotImplementedError("the exact terminal solve is not on the device path (terminal='amg')")
+    # level validation mirrors mgr.py:337-352 on the host layout
+    fo = layout.field_of
+    for spec in config.levels:
+        present = {Field(v) for v in np.unique(fo)}
+        if spec.f_fields | spec.c_fields != present:
+            raise ValueError(
+                f"level spec fields {sorted(f.name for f in spec.f_fields | spec.c_fields)} "
+                f"do not cover the fields present {sorted(f.name for f in present)}")
+        if not spec.c_fields:
+            raise ValueError("empty C set: nothing to reduce onto")
+        is_c = np.isin(fo, [int(f) for f in spec.c_fields])
+        if is_c.all():
+            if len(present) != 1:
+                raise ValueError("an all-C level requires a single remaining field")
+            logger.info("all-C level: skipping reduction, solving directly with AMG")
+            break
+        fo = fo[is_c]
+    if len(set(np.unique(fo).tolist())) > 1:
+        logger.warning("terminal MGR grid carries %d fields; AMG works best on a single elliptic field",
+                       len(set(np.unique(fo).tolist())))
+    specs = (_lib.LevelSpec * max(1, len(config.levels)))(*[s.to_c() for s in config.levels])
+    cfg = config.to_c()
+    out = ctypes.c_void_p()
+    fo0 = np.ascontiguousarray(layout.field_of, dtype=np.int8)
+    eo0 = np.ascontiguousarray(layout.entity_of, dtype=np.int32)
+    _lib.check(_lib.lib().pmgr_mgr_setup(dA.handle, fo0.ctypes.data, eo0.ctypes.data, specs, len(config.levels),
+                                         ctypes.byref(cfg), current_stream(), ctypes.byref(out)))
+    return MgrHierarchy(out, dA, config, config.levels)
+
+
+def mgr_apply(h: MgrHierarchy, v):
+    """z = M^-1 v (reference mgr.py:399-429)."""
+    vd = to_device(v, h.n)
+    z = empty_device(h.n)
+    _lib.check(_lib.lib().pmgr_mgr_apply(h.handle, ptr(vd), ptr(z), current_stream()))
+    return back_like(z, v)

@@ -1,0 +1,256 @@
+"""GPU parity: libpmgr.so (sm_100a) against the reference's golden fixtures
+and the CPU oracle.
+
+Bar (BASELINE.json north_star): F/C splittings and sparsity patterns
+bit-exact; setup values bit-exact too (Appendix A contract); preconditioner
+applications within 1e-10 relative; GMRES iteration counts within +-1.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests._golden import CASES, dcsr, get_csr, load, oracle_config, oracle_levels, vec_sha
+
+pytestmark = pytest.mark.gpu
+
+JACOBI = 10 ** 9
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1904_05960_b200 import amg, krylov, mgr, sparse
+
+    return sparse, amg, mgr, krylov
+
+
+def host_csr(m):
+    return O.Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+
+
+def same_csr(gpu, ref, what=""):
+    assert (gpu.nrows, gpu.ncols) == (ref.nrows, ref.ncols), what
+    assert np.array_equal(gpu.ro, ref.ro), f"{what}: row offsets differ"
+    assert np.array_equal(gpu.ci, ref.ci), f"{what}: column pattern differs"
+    assert np.array_equal(gpu.v, ref.v), f"{what}: values differ (max {np.abs(gpu.v - ref.v).max()})"
+
+
+def mgr_config(pk, pb, n_max, four_field):
+    sparse, amg, mgr, _ = pk
+    F = sparse.Field
+    if four_field:
+        levels = (mgr.MgrLevelSpec({F.U}, {F.S, F.S2, F.P}, f_relax="amg", n_max=n_max),
+                  mgr.MgrLevelSpec({F.S2}, {F.S, F.P}, f_relax="jacobi"),
+                  mgr.MgrLevelSpec({F.S}, {F.P}, f_relax="jacobi"))
+    elif pb.cell_fields == (2,):
+        levels = (mgr.MgrLevelSpec({F.U}, {F.P}, f_relax="amg", n_max=n_max),)
+    else:
+        levels = (mgr.MgrLevelSpec({F.U}, {F.S, F.P}, f_relax="amg", n_max=n_max),
+                  mgr.MgrLevelSpec({F.S}, {F.P}, f_relax="jacobi"))
+    return mgr.MgrConfig(levels=levels,
+                         amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=JACOBI),
+                         amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=JACOBI))
+
+
+def gpu_hierarchy(pk, tag):
+    sparse, amg, mgr, _ = pk
+    gen, n_max, four = CASES[tag]
+    pb = gen()
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
+    h = mgr.mgr_setup(A, lay, mgr_config(pk, pb, n_max, four))
+    return pb, A, h
+
+
+def check_amg(d, prefix, h, full):
+    assert h.level_sizes() == list(d[prefix + "sizes"])
+    for i, lv in enumerate(h.levels):
+        k = f"{prefix}L{i}_"
+        if full:
+            assert np.array_equal(lv.split.is_c, d[k + "isc"]), f"{k} split"
+            same_csr(host_csr(lv.P), get_csr(d, k + "P"), k + "P")
+            same_csr(host_csr(lv.A), get_csr(d, k + "A"), k + "A")
+            assert np.array_equal(lv.dtilde, d[k + "dtilde"]), f"{k} dtilde"
+        else:
+            assert hashlib.sha256(lv.split.is_c.tobytes()).hexdigest() == str(d[k + "isc_sha"]), f"{k} split"
+            assert dcsr(host_csr(lv.P)) == str(d[k + "P_sha"]), f"{k} P"
+            assert dcsr(host_csr(lv.A)) == str(d[k + "A_sha"]), f"{k} A"
+            assert vec_sha(lv.dtilde) == str(d[k + "dtilde_sha"]), f"{k} dtilde"
+    if full:
+        same_csr(host_csr(h.coarse_A), get_csr(d, prefix + "coarse"), prefix + "coarse")
+    else:
+        assert dcsr(host_csr(h.coarse_A)) == str(d[prefix + "coarse_sha"]), prefix + "coarse"
+
+
+# ---------------------------------------------------------------------------
+# sparse kernels
+# ---------------------------------------------------------------------------
+
+
+def test_spmv_matches_oracle(pk):
+    sparse = pk[0]
+    from paper_1904_05960_b200 import problems
+
+    pb = problems.make_c2(seed=1, n=8)
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    x = np.random.default_rng(0).standard_normal(pb.n)
+    y = sparse.matvec(A, x)
+    yo = O.spmv(host_csr(A), x)
+    scale = np.abs(A.to_scipy()) @ np.abs(x)
+    assert np.all(np.abs(y - yo) <= 1e-14 * scale + 1e-300)
+
+
+def test_spmv_device_tensor_roundtrip(pk):
+    import torch
+
+    sparse = pk[0]
+    A = sparse.CsrMatrix.from_dense(np.array([[2.0, -1.0, 0.0], [-1.0, 2.0, -1.0], [0.0, -1.0, 2.0]]))
+    x = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64, device="cuda")
+    y = sparse.matvec(A, x)
+    assert y.is_cuda
+    assert np.allclose(y.cpu().numpy(), [0.0, 0.0, 4.0])
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        sparse.matvec(A, np.ones(4))
+
+
+def test_device_csr_upload_validates(pk):
+    sparse = pk[0]
+    with pytest.raises(ValueError, match="strictly increasing"):
+        sparse.DeviceCsr.from_arrays(2, 2, np.array([0, 2, 3]), np.array([1, 0, 1]), np.ones(3))
+    with pytest.raises(ValueError, match="out of range"):
+        sparse.DeviceCsr.from_arrays(2, 2, np.array([0, 1, 2]), np.array([0, 2]), np.ones(2))
+    d = sparse.DeviceCsr.from_arrays(2, 3, np.array([0, 2, 3]), np.array([0, 2, 1]), np.array([1.0, 2.0, 3.0]))
+    h = d.to_host()
+    assert h.shape == (2, 3) and list(h.col_indices) == [0, 2, 1]
+
+
+# ---------------------------------------------------------------------------
+# AMG on the reference's Laplacian fixtures (bitwise setup)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("t", range(3))
+@pytest.mark.parametrize("npart", [1, JACOBI])
+def test_amg_laplacian_bitwise(pk, t, npart):
+    sparse, amg, _, krylov = pk
+    d = load("units")
+    L = get_csr(d, f"lap{t}_A")
+    A = sparse.CsrMatrix(L.nrows, L.ncols, L.ro, L.ci, L.v)
+    h = amg.amg_setup(A, amg.AmgConfig(npartitions=npart))
+    tag = f"lap{t}_p{min(npart, 99)}_"
+    check_amg(d, tag, h, True)
+    b = d[tag + "b"]
+    z = amg.amg_vcycle(h, b, np.zeros(L.nrows))
+    zr = d[tag + "vcyc"]
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+    x, st = krylov.gmres(A, lambda v: amg.amg_vcycle(h, v), b,
+                         cfg=krylov.GmresConfig(restart=30, max_iters=200, rtol=1e-8))
+    assert st.converged and abs(st.iterations - int(d[tag + "its"])) <= 1
+
+
+# ---------------------------------------------------------------------------
+# MGR hierarchies on the generated poromechanics problems
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16", "c2_32"])
+def test_mgr_setup_bitwise(pk, tag):
+    d = load(tag)
+    full = "mgr0_isc" in d.files
+    pb, A, h = gpu_hierarchy(pk, tag)
+    assert h.level_sizes() == list(d["mgr_sizes"])
+    for i, lv in enumerate(h.levels):
+        k = f"mgr{i}_"
+        if full:
+            assert np.array_equal(lv.split.is_c, d[k + "isc"])
+            same_csr(host_csr(lv.P), get_csr(d, k + "P"), k + "P")
+            same_csr(host_csr(lv.coarse), get_csr(d, k + "coarse"), k + "coarse")
+        else:
+            assert hashlib.sha256(lv.split.is_c.tobytes()).hexdigest() == str(d[k + "isc_sha"])
+            assert dcsr(host_csr(lv.P)) == str(d[k + "P_sha"]), k + "P"
+            assert dcsr(host_csr(lv.coarse)) == str(d[k + "coarse_sha"]), k + "coarse"
+        a = h.amg(i)
+        if a is not None:
+            check_amg(d, k + "amg_", a, full)
+    check_amg(d, "term_", h.terminal_solver, full)
+
+
+@pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16", "c2_32"])
+def test_mgr_apply_and_gmres(pk, tag):
+    _, _, _, krylov = pk
+    d = load(tag)
+    pb, A, h = gpu_hierarchy(pk, tag)
+    z = h.apply(d["apply_v"])
+    zr = d["apply_z"]
+    rel = np.linalg.norm(z - zr) / np.linalg.norm(zr)
+    assert rel <= 1e-10, rel
+    x, st = krylov.gmres(A, h.apply, pb.rhs, cfg=krylov.GmresConfig(restart=100, max_iters=1000, rtol=1e-6))
+    assert st.converged == bool(d["gmres_conv"])
+    assert abs(st.iterations - int(d["gmres_iters"])) <= 1, (st.iterations, int(d["gmres_iters"]))
+    # the true residual meets the same tolerance as the reference's
+    r = pb.rhs - O.spmv(host_csr(A), x)
+    assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(pb.rhs) * (1 + 1e-9)
+    hr = d["gmres_hist"]
+    assert abs(len(st.residual_history) - len(hr)) <= 1
+    xr = d["gmres_x"]
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-6
+
+
+def test_gmres_device_vectors_and_generic_path(pk):
+    import torch
+
+    sparse, amg, mgr, krylov = pk
+    pb, A, h = gpu_hierarchy(pk, "c1_6")
+    b = torch.from_numpy(pb.rhs).cuda()
+    x1, s1 = krylov.gmres(A, h.apply, b, cfg=krylov.GmresConfig(restart=100))
+    assert x1.is_cuda and s1.converged
+    # reference-style lambdas go through the generic device path
+    x2, s2 = krylov.gmres(lambda v: sparse.matvec(A, v), h.apply if False else (lambda v: h.apply(v)), pb.rhs,
+                          cfg=krylov.GmresConfig(restart=100))
+    assert s2.converged and abs(s2.iterations - s1.iterations) <= 1
+    assert np.linalg.norm(x2 - x1.cpu().numpy()) <= 1e-6 * np.linalg.norm(x2)
+
+
+def test_gmres_zero_rhs_and_identity(pk):
+    sparse, _, _, krylov = pk
+    A = sparse.CsrMatrix.identity(50)
+    x, st = krylov.gmres(A, None, np.zeros(50))
+    assert st.iterations == 0 and st.converged and not np.any(x)
+    b = np.arange(50, dtype=float)
+    x, st = krylov.gmres(A, None, b)
+    assert st.iterations == 1 and np.allclose(x, b)
+
+
+def test_mgr_errors_match_reference(pk):
+    sparse, amg, mgr, _ = pk
+    F = sparse.Field
+    # zero diagonal in A_FF -> ValueError naming the F row
+    D = np.eye(4)
+    D[1, 1] = 0.0
+    D[1, 3] = 1.0
+    D[3, 1] = 1.0
+    A = sparse.CsrMatrix.from_dense(D, keep_zeros=True)
+    lay = sparse.FieldLayout(np.array([0, 0, 2, 2], dtype=np.int8), np.arange(4, dtype=np.int32))
+    cfg = mgr.MgrConfig(levels=(mgr.MgrLevelSpec({F.U}, {F.P}, f_relax="jacobi"),))
+    with pytest.raises(ValueError, match="singular diagonal: zero or missing entry at row 1"):
+        mgr.mgr_setup(A, lay, cfg)
+    cfg2 = mgr.MgrConfig(levels=(mgr.MgrLevelSpec({F.U}, {F.S}, f_relax="jacobi"),))
+    with pytest.raises(ValueError, match="fields"):
+        mgr.mgr_setup(A, lay, cfg2)
+    with pytest.raises(NotImplementedError):
+        mgr.mgr_setup(A, lay, mgr.MgrConfig(levels=(mgr.MgrLevelSpec({F.U}, {F.P}, global_smoother="ilu"),)))
+
+
+def test_launch_counter_moves(pk):
+    from paper_1904_05960_b200 import _lib
+
+    sparse = pk[0]
+    before = _lib.launch_count()
+    sparse.matvec(sparse.CsrMatrix.identity(10), np.ones(10))
+    assert _lib.launch_count() > before
