@@ -177,6 +177,14 @@ PMGR_API int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_hos
                     int nonzero_x0, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats,
                     double *history_host, int32_t history_cap, void *stream);
 
+/* ---- live kernel timing ------------------------------------------------- */
+/* Record CUDA events around selected launches (0 outer SpMV, 1 level-0
+ * F-relax first sweep + residual, 2 level-0 F-relax post-sweep, 3 MGR apply,
+ * 4 CGS2 step); enabling resets the record.  query returns the launch count,
+ * summed device milliseconds and summed algorithmic bytes of one kind. */
+PMGR_API int pmgr_prof_enable(int on);
+PMGR_API int pmgr_prof_query(int32_t kind, int64_t *count, double *ms, double *bytes);
+
 /* Device BLAS-1 helpers used by the generic (Python-callable) GMRES path:
  * h[k] = V_k . w for k < nvec (V row-major nvec x n); w -= sum_k h[k] V_k. */
 PMGR_API int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const double *w_dev,

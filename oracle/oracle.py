@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "oracle.c")
     os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+        subprocess.check_call(["gcc", "-O3", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
                                "-shared", "-o", _LIB_PATH, src, "-lm"])
     return _LIB_PATH
 

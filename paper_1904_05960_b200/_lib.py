@@ -96,6 +96,8 @@ SIGNATURES = {
                                   ctypes.POINTER(GmresStats), vp, ctypes.c_int32, vp]),
     "pmgr_gmres_host": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.POINTER(GmresCfg),
                                        ctypes.POINTER(GmresStats), vp, ctypes.c_int32, vp]),
+    "pmgr_prof_enable": (ctypes.c_int, [ctypes.c_int]),
+    "pmgr_prof_query": (ctypes.c_int, [ctypes.c_int32, c_i64p, c_dp, c_dp]),
     "pmgr_multidot": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
     "pmgr_multiaxpy": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
 }

@@ -561,7 +561,10 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s) {
     AmgLevel &L = h.levels[l];
     const CsrView A = L.A->view();
     double *bnext = (l + 1 < h.levels.size()) ? h.levels[l + 1].b.p : h.cb.p;
+    const bool tag = h.prof_tag && l == 0;
+    const double pass = csr_pass_bytes(A.nrows, A.ncols, A.nnz) + 16.0 * A.nrows;
     if (L.jacobi) {
+        ProfScope ps(tag ? PROF_FRELAX_SWEEP0 : PROF_KINDS, pass, s);
         spmv_sweep0_residual(A, L.b.p, L.dtilde.p, L.x.p, L.r.p, s);
     } else {
         vec_zero(L.x.p, A.nrows, s);
@@ -578,6 +581,7 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s) {
     }
     spmv_add(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
+        ProfScope ps(tag ? PROF_FRELAX_JACOBI : PROF_KINDS, pass, s);
         spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, L.xo.p, s);
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);

@@ -295,6 +295,17 @@ int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_host, double
     });
 }
 
+int pmgr_prof_enable(int on) {
+    return guard([&] { pmgr::prof_enable(on != 0); });
+}
+
+int pmgr_prof_query(int32_t kind, int64_t *count, double *ms, double *bytes) {
+    return guard([&] {
+        require(kind >= 0 && kind < pmgr::PROF_KINDS, "unknown profile kind");
+        pmgr::prof_query(kind, count, ms, bytes);
+    });
+}
+
 int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const double *w_dev, double *h_dev, void *stream) {
     return guard([&] { pmgr::multidot(V_dev, n, nvec, w_dev, h_dev, S(stream)); });
 }

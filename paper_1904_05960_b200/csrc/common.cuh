@@ -203,6 +203,44 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t x) {
 }
 
 // ---------------------------------------------------------------------------
+// live kernel timing (pmgr_prof_*): CUDA events around selected launches on
+// the launching stream, with the algorithmic bytes each one must move.
+// ---------------------------------------------------------------------------
+
+enum ProfKind {
+    PROF_OUTER_SPMV = 0,    // y = A z in the GMRES loop
+    PROF_FRELAX_SWEEP0 = 1, // level-0 fused first sweep + residual of the F-relax AMG
+    PROF_FRELAX_JACOBI = 2, // level-0 post-sweep of the F-relax AMG
+    PROF_MGR_APPLY = 3,     // whole preconditioner application
+    PROF_ORTHO = 4,         // CGS2 projections + normalisation of one Arnoldi step
+    PROF_KINDS = 5
+};
+
+bool prof_on();
+void prof_enable(bool on);
+void prof_query(int kind, int64_t *count, double *ms, double *bytes);
+void prof_begin(int kind, double bytes, cudaStream_t s);
+void prof_end(int kind, cudaStream_t s);
+
+struct ProfScope {
+    int kind;
+    cudaStream_t s;
+    bool on;
+    ProfScope(int k, double bytes, cudaStream_t st) : kind(k), s(st), on(k < PROF_KINDS && prof_on()) {
+        if (on) prof_begin(k, bytes, st);
+    }
+    ~ProfScope() {
+        if (on) prof_end(kind, s);
+    }
+};
+
+// algorithmic bytes of one CSR pass (int64 offsets, int32 columns, fp64
+// values; x gathered once, y written once)
+inline double csr_pass_bytes(int64_t nrows, int64_t ncols, int64_t nnz) {
+    return 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * ncols + 8.0 * nrows;
+}
+
+// ---------------------------------------------------------------------------
 // host-side primitives implemented in prims.cu (CUB based)
 // ---------------------------------------------------------------------------
 

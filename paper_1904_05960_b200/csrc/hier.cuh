@@ -35,6 +35,7 @@ struct pmgr_amg {
     pmgr::DBuf<double> coarse_inv;            // dense inverse, row-major
     pmgr::DBuf<double> cb, cx, ctmp;          // coarsest workspace
     int64_t flagged = 0;
+    bool prof_tag = false;  // time level-0 smoother kernels (F-relax AMG of MGR level 0)
 };
 
 namespace pmgr {

@@ -290,23 +290,32 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
             bool brk = false;
             while (j < m && total < cfg.max_iters) {
                 double *Vj = V.p + (int64_t)j * n;
-                apply_M(Vj, z.p);
-                spmv(Av, z.p, w.p, s);
+                {
+                    ProfScope ps(PROF_MGR_APPLY, 0.0, s);
+                    apply_M(Vj, z.p);
+                }
+                {
+                    ProfScope ps(PROF_OUTER_SPMV, csr_pass_bytes(Av.nrows, Av.ncols, Av.nnz), s);
+                    spmv(Av, z.p, w.p, s);
+                }
                 const int nk = j + 1;
-                k_multidot<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, w.p, R.partial.p, R.ld);
-                PMGR_LAUNCHED();
-                k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h1, 0);
-                PMGR_LAUNCHED();
-                k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h1, w.p, 1, R.partial.p, R.ld);
-                PMGR_LAUNCHED();
-                k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h2, 0);
-                PMGR_LAUNCHED();
-                k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h2, w.p, 2, R.partial.p, R.ld);
-                PMGR_LAUNCHED();
-                k_reduce_partials<<<1, 32, 0, s>>>(R.partial.p, R.nblk, 1, R.ld, st.hnext, 0);
-                PMGR_LAUNCHED();
-                k_arnoldi_tail<<<1, 1, 0, s>>>(st, m, j, tol);
-                PMGR_LAUNCHED();
+                {
+                    ProfScope pso(PROF_ORTHO, 8.0 * n * (3.0 * nk + 7.0), s);
+                    k_multidot<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, w.p, R.partial.p, R.ld);
+                    PMGR_LAUNCHED();
+                    k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h1, 0);
+                    PMGR_LAUNCHED();
+                    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h1, w.p, 1, R.partial.p, R.ld);
+                    PMGR_LAUNCHED();
+                    k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h2, 0);
+                    PMGR_LAUNCHED();
+                    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h2, w.p, 2, R.partial.p, R.ld);
+                    PMGR_LAUNCHED();
+                    k_reduce_partials<<<1, 32, 0, s>>>(R.partial.p, R.nblk, 1, R.ld, st.hnext, 0);
+                    PMGR_LAUNCHED();
+                    k_arnoldi_tail<<<1, 1, 0, s>>>(st, m, j, tol);
+                    PMGR_LAUNCHED();
+                }
                 int flags[3];
                 PMGR_CUDA(cudaMemcpyAsync(flags, status.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
                 PMGR_CUDA(cudaStreamSynchronize(s));

@@ -358,6 +358,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             pmgr_amg_cfg acfg = cfg.amg_f_relax;
             acfg.num_functions = sp.amg_num_functions > 0 ? sp.amg_num_functions : 1;
             L.amg = amg_build(A_ff, acfg, s);
+            L.amg->prof_tag = (li == 0);
         }
         if (sp.f_relax == PMGR_FRELAX_JACOBI && L.f_relax_sweeps > 1) L.A_ff = A_ff;
         // ---- coarse operator (build_coarse, mgr.py:212-231)

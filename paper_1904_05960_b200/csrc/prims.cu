@@ -9,6 +9,64 @@ namespace pmgr {
 
 std::atomic<int64_t> g_launches{0};
 
+namespace {
+struct ProfRec {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+};
+bool g_prof = false;
+std::vector<ProfRec> g_recs;
+size_t g_used = 0;
+std::vector<size_t> g_open[PROF_KINDS];
+}  // namespace
+
+bool prof_on() { return g_prof; }
+
+void prof_begin(int kind, double bytes, cudaStream_t s) {
+    if (g_used == g_recs.size()) {
+        ProfRec r{};
+        PMGR_CUDA(cudaEventCreate(&r.a));
+        PMGR_CUDA(cudaEventCreate(&r.b));
+        g_recs.push_back(r);
+    }
+    ProfRec &r = g_recs[g_used];
+    r.kind = kind;
+    r.bytes = bytes;
+    PMGR_CUDA(cudaEventRecord(r.a, s));
+    g_open[kind].push_back(g_used);
+    ++g_used;
+}
+
+void prof_end(int kind, cudaStream_t s) {
+    size_t i = g_open[kind].back();
+    g_open[kind].pop_back();
+    PMGR_CUDA(cudaEventRecord(g_recs[i].b, s));
+}
+
+void prof_enable(bool on) {
+    g_prof = on;
+    g_used = 0;
+    for (auto &v : g_open) v.clear();
+}
+
+void prof_query(int kind, int64_t *count, double *ms, double *bytes) {
+    int64_t c = 0;
+    double t = 0.0, by = 0.0;
+    for (size_t i = 0; i < g_used; ++i) {
+        if (g_recs[i].kind != kind) continue;
+        PMGR_CUDA(cudaEventSynchronize(g_recs[i].b));
+        float e = 0.f;
+        PMGR_CUDA(cudaEventElapsedTime(&e, g_recs[i].a, g_recs[i].b));
+        ++c;
+        t += e;
+        by += g_recs[i].bytes;
+    }
+    *count = c;
+    *ms = t;
+    *bytes = by;
+}
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {
