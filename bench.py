@@ -235,6 +235,16 @@ def run_gpu(args, rank, world, local_rank):
     for _ in range(args.warmup):
         st = solve()
     its = st.iterations
+    if args.ncu:
+        # one solve bracketed for `ncu --profile-from-start off`
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        st = solve()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        if rank == 0:
+            print(json.dumps({"ncu_solve": True, "gmres_iterations": st.iterations, "n_dofs": pb.n}))
+        return
 
     def barrier():
         if dist is not None:
@@ -352,6 +362,7 @@ def main():
     ap.add_argument("--restart", type=int, default=100)
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profile one solve between cudaProfilerStart/Stop and exit")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the roofline kernel (profiles/), echoed into the JSON")
     args = ap.parse_args()

@@ -481,11 +481,14 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
                                                             alpha.p, diag.p, lev.P.ro.p, lev.P.ci.p, lev.P.v.p);
         PMGR_LAUNCHED();
         // ---- Galerkin (P^T A) P, zero dropping after each product
+        csr_finalize(lev.P, s);
         csr_transpose(lev.P.view(), lev.R, s);
+        csr_finalize(lev.R, s);
         Csr T1;
         spgemm(lev.R.view(), Av, 0, T1, s);
         auto next = std::make_shared<Csr>();
         spgemm(T1.view(), lev.P.view(), 0, *next, s);
+        csr_finalize(*next, s);
         // ---- l1 diagonal with the contiguous partitions
         lev.jacobi = cfg.npartitions >= n;
         lev.dtilde.alloc(n);
@@ -550,42 +553,47 @@ namespace {
 
 // V(1,1) from level l with right-hand side lev.b (already in place), zero
 // initial guess; the result is left in lev.xo (or h.cx at the coarsest).
-void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s);
+void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out = nullptr);
 
 const double *coarse_solve(pmgr_amg &h, cudaStream_t s) {
     dense_matvec(h.coarse_inv.p, h.coarse->nrows, h.cb.p, h.cx.p, s);
     return h.cx.p;
 }
 
-void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s) {
+void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
+    // precondition: L.b holds the right-hand side and, on l1-Jacobi levels,
+    // L.x = L.b / dtilde (the first sweep from zero), written by the producer
     AmgLevel &L = h.levels[l];
     const CsrView A = L.A->view();
-    double *bnext = (l + 1 < h.levels.size()) ? h.levels[l + 1].b.p : h.cb.p;
+    const bool has_next = l + 1 < h.levels.size();
     const bool tag = h.prof_tag && l == 0;
     const double pass = csr_pass_bytes(A.nrows, A.ncols, A.nnz) + 16.0 * A.nrows;
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_SWEEP0 : PROF_KINDS, pass, s);
-        spmv_sweep0_residual(A, L.b.p, L.dtilde.p, L.x.p, L.r.p, s);
+        spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
     } else {
         vec_zero(L.x.p, A.nrows, s);
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, true, s);
         spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
     }
-    spmv(L.R.view(), L.r.p, bnext, s);
     const double *e;
-    if (l + 1 < h.levels.size()) {
+    if (has_next) {
+        AmgLevel &N = h.levels[l + 1];
+        if (N.jacobi) spmv_restrict_div(L.R.view(), L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
+        else spmv(L.R.view(), L.r.p, N.b.p, s);
         cycle_from_zero(h, l + 1, s);
-        e = h.levels[l + 1].xo.p;
+        e = N.xo.p;
     } else {
+        spmv(L.R.view(), L.r.p, h.cb.p, s);
         e = coarse_solve(h, s);
     }
     spmv_add(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_JACOBI : PROF_KINDS, pass, s);
-        spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, L.xo.p, s);
+        spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, out ? out : L.xo.p, s);
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);
-        vec_copy(L.x.p, L.xo.p, A.nrows, s);
+        vec_copy(L.x.p, out ? out : L.xo.p, A.nrows, s);
     }
 }
 
@@ -608,13 +616,14 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
     }
     AmgLevel &L = h.levels[0];
     const int64_t n = L.A->nrows;
-    vec_copy(b, L.b.p, n, s);
     if (!x) {
-        cycle_from_zero(h, 0, s);
-        vec_copy(L.xo.p, out, n, s);
+        if (L.jacobi) vec_copy_div(b, L.dtilde.p, n, L.b.p, L.x.p, s);
+        else vec_copy(b, L.b.p, n, s);
+        cycle_from_zero(h, 0, s, out);
         return;
     }
     // nonzero initial guess at the top level: pre-sweep from x
+    vec_copy(b, L.b.p, n, s);
     const CsrView A = L.A->view();
     if (L.jacobi) {
         spmv_jacobi(A, x, L.b.p, L.dtilde.p, L.x.p, s);
@@ -623,13 +632,15 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, true, s);
     }
     spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
-    double *bnext = h.levels.size() > 1 ? h.levels[1].b.p : h.cb.p;
-    spmv(L.R.view(), L.r.p, bnext, s);
     const double *e;
     if (h.levels.size() > 1) {
+        AmgLevel &N = h.levels[1];
+        if (N.jacobi) spmv_restrict_div(L.R.view(), L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
+        else spmv(L.R.view(), L.r.p, N.b.p, s);
         cycle_from_zero(h, 1, s);
         e = h.levels[1].xo.p;
     } else {
+        spmv(L.R.view(), L.r.p, h.cb.p, s);
         e = coarse_solve(h, s);
     }
     spmv_add(L.P.view(), e, L.x.p, s);

@@ -90,6 +90,7 @@ int pmgr_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ro
             PMGR_CUDA(cudaMemcpyAsync(m->v.p, values, sizeof(double) * nnz, k, S(stream)));
         }
         if (validate) pmgr::csr_validate(m->view(), S(stream));
+        pmgr::csr_finalize(*m, S(stream));
         PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         *out = wrap(std::move(m));
     });

@@ -162,6 +162,7 @@ struct CsrView {
     const int64_t *ro;
     const int32_t *ci;
     const double *v;
+    int64_t maxrow = -1;  // longest row (-1: unknown); picks the SpMV lane group
 };
 
 struct Csr {
@@ -177,8 +178,12 @@ struct Csr {
         ci.alloc(z);
         v.alloc(z);
     }
-    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p}; }
+    int64_t maxrow = -1;
+    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow}; }
 };
+
+// record the longest row of a finished operator (setup time, synchronises)
+void csr_finalize(Csr &A, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // warp helpers
@@ -216,7 +221,16 @@ enum ProfKind {
     PROF_KINDS = 5
 };
 
+struct ProfRec {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+};
 bool prof_on();
+void prof_capture_begin(std::vector<ProfRec> *recs);
+void prof_capture_end();
+void prof_collect(std::vector<ProfRec> &graph_recs);
+void prof_release(std::vector<ProfRec> &graph_recs);
 void prof_enable(bool on);
 void prof_query(int kind, int64_t *count, double *ms, double *bytes);
 void prof_begin(int kind, double bytes, cudaStream_t s);
@@ -274,6 +288,9 @@ void spmv_jacobi(const CsrView &A, const double *x, const double *b, const doubl
 void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x,
                           double *r, cudaStream_t s);
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s);
+void spmv_restrict_div(const CsrView &R, const double *r, const double *d, double *b, double *x,
+                       cudaStream_t s);
+void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s);
 void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows,
                      double *r, cudaStream_t s);
 void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,

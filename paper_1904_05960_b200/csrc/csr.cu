@@ -365,6 +365,34 @@ void csr_validate(const CsrView &A, cudaStream_t s) {
         fail(PMGR_ERR_INVALID, "column indices must be strictly increasing within each row", (int64_t)h[2]);
 }
 
+namespace {
+__global__ void k_maxrow(int64_t n, const int64_t *ro, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long l = (unsigned long long)(ro[i + 1] - ro[i]);
+        m = l > m ? l : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(FULL, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+}  // namespace
+
+void csr_finalize(Csr &A, cudaStream_t s) {
+    if (A.nrows == 0) {
+        A.maxrow = 0;
+        return;
+    }
+    TBuf<unsigned long long> m(1, s);
+    PMGR_CUDA(cudaMemsetAsync(m.p, 0, sizeof(unsigned long long), s));
+    unsigned g = grid_for(A.nrows, 256);
+    k_maxrow<<<g < 1024 ? g : 1024, 256, 0, s>>>(A.nrows, A.ro.p, m.p);
+    PMGR_LAUNCHED();
+    A.maxrow = (int64_t)read_scalar(m.p, s);
+}
+
 void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {
     B.alloc(A.nrows, A.ncols, A.nnz);
     PMGR_CUDA(cudaMemcpyAsync(B.ro.p, A.ro, sizeof(int64_t) * (A.nrows + 1), cudaMemcpyDeviceToDevice, s));

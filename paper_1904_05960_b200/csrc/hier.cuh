@@ -66,7 +66,26 @@ struct MgrLevel {
 
 }  // namespace pmgr
 
+namespace pmgr {
+// One instantiated CUDA graph of a full preconditioner application, keyed by
+// its input/output buffers (GMRES always uses the same pair).
+struct ApplyGraph {
+    const double *v = nullptr;
+    double *z = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool prof = false;               // captured with timing events
+    bool pending = false;            // launched, events not yet collected
+    std::vector<ProfRec> recs;
+    uint64_t last_use = 0;
+};
+}  // namespace pmgr
+
 struct pmgr_mgr {
+    ~pmgr_mgr();
+    std::vector<pmgr::ApplyGraph> graphs;
+    cudaStream_t cap_stream = nullptr;
+    bool use_graphs = true;
+    uint64_t tick = 0;
     std::vector<pmgr::MgrLevel> levels;
     std::shared_ptr<const pmgr::Csr> terminal_A;
     std::unique_ptr<pmgr_amg> terminal;
@@ -81,6 +100,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A, const int8_t *
                                     const int32_t *entity_of_host, const pmgr_level_spec *specs,
                                     int nlevels, const pmgr_mgr_cfg &cfg, cudaStream_t s);
 void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);
+void mgr_collect(pmgr_mgr &h);  // fold finished graph timing events into the totals
 }  // namespace pmgr
 
 namespace pmgr {

@@ -132,10 +132,13 @@ __global__ void k_combine(const double *__restrict__ V, int64_t n, int nk, const
     }
 }
 
-__global__ void k_scale(const double *x, int64_t n, const double *den, double *y) {
+__global__ void k_scale(const double *x, int64_t n, const double *den, double *y, double *y2) {
     const double d = *den;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = x[i] / d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = x[i] / d;
+        y[i] = t;
+        if (y2) y2[i] = t;
+    }
 }
 
 __global__ void k_sqrt(double *x) { *x = sqrt(*x); }
@@ -238,7 +241,9 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
     if (M && M->n != Av.nrows) fail(PMGR_ERR_INVALID, "preconditioner size does not match the operator");
     const int64_t n = Av.nrows;
     const int m = cfg.restart;
-    TBuf<double> V((int64_t)(m + 1) * n, s), w(n, s), z(n, s), r(n, s);
+    // vin: fixed input buffer of the preconditioner (its CUDA graph is keyed
+    // by buffer addresses); the normalisation writes V_{j+1} and vin at once
+    TBuf<double> V((int64_t)(m + 1) * n, s), w(n, s), z(n, s), r(n, s), vin(n, s);
     TBuf<double> small((int64_t)(m + 1) * m + 6 * (m + 1) + 8, s);
     TBuf<int> status(4, s);
     TBuf<double> dhist(m + 1, s);
@@ -284,7 +289,7 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
         while (total < cfg.max_iters) {
             k_cycle_init<<<1, 256, 0, s>>>(st, m, beta_d);
             PMGR_LAUNCHED();
-            k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(r.p, n, beta_d, V.p);
+            k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(r.p, n, beta_d, V.p, vin.p);
             PMGR_LAUNCHED();
             int j = 0;
             bool brk = false;
@@ -292,7 +297,7 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
                 double *Vj = V.p + (int64_t)j * n;
                 {
                     ProfScope ps(PROF_MGR_APPLY, 0.0, s);
-                    apply_M(Vj, z.p);
+                    apply_M(M ? vin.p : Vj, z.p);
                 }
                 {
                     ProfScope ps(PROF_OUTER_SPMV, csr_pass_bytes(Av.nrows, Av.ncols, Av.nnz), s);
@@ -319,12 +324,13 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
                 int flags[3];
                 PMGR_CUDA(cudaMemcpyAsync(flags, status.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
                 PMGR_CUDA(cudaStreamSynchronize(s));
+                if (M && prof_on()) mgr_collect(*M);
                 if (flags[1]) {  // dead column: discard (krylov.py:88-91)
                     brk = true;
                     break;
                 }
                 if (!flags[0]) {
-                    k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(w.p, n, st.hnext, V.p + (int64_t)(j + 1) * n);
+                    k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(w.p, n, st.hnext, V.p + (int64_t)(j + 1) * n, vin.p);
                     PMGR_LAUNCHED();
                 } else {
                     brk = true;
@@ -347,6 +353,7 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
                 spmv_residual(Av, x, b, r.p, s);
                 norm2(r.p, n, R, beta_d, s);
                 beta = read_scalar(beta_d, s);
+                if (M && prof_on()) mgr_collect(*M);
                 hist.back() = beta;
             }
             ++restarts;

@@ -17,6 +17,7 @@
 // The residual is only formed on C rows (R is an injection) and only
 // against A_CF, which reads a fraction of A: the same numbers, since the
 // skipped terms multiply exact zeros of z.
+#include <cstdlib>
 #include <set>
 
 #include "hier.cuh"
@@ -266,6 +267,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
     auto h = std::make_unique<pmgr_mgr>();
     h->n = A0->nrows;
     h->terminal_cycles = cfg.terminal_cycles > 1 ? cfg.terminal_cycles : 1;
+    if (const char *e = getenv("PMGR_NO_GRAPHS")) h->use_graphs = (e[0] == '0');
     h->f_relax_post = cfg.f_relax_post;
     std::vector<int8_t> fo(field_of_host, field_of_host + A0->nrows);
     std::vector<int32_t> eo(entity_of_host, entity_of_host + A0->nrows);
@@ -326,6 +328,8 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         if (sp.n_max >= 0) extract_block(Av, L.c_rows.p, L.nc, L.is_c.p, true, c_index.p, L.nc, A_cc, s);
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
+        csr_finalize(*A_ff, s);
+        csr_finalize(L.A_cf, s);
         if (need_dinv) {
             L.dinv_ff.alloc(L.nf);
             int64_t bad = csr_diag_inverse(A_ff->view(), L.dinv_ff.p, s);
@@ -351,6 +355,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                                                                  L.P.ro.p, L.P.ci.p, L.P.v.p);
             PMGR_LAUNCHED();
         }
+        csr_finalize(L.P, s);
         // ---- F-relaxation (_build_f_relax, mgr.py:374-386)
         L.f_relax = sp.f_relax;
         L.f_relax_sweeps = sp.f_relax_sweeps > 1 ? sp.f_relax_sweeps : 1;
@@ -383,6 +388,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                 PMGR_CUDA(cudaStreamSynchronize(s));
             }
         }
+        csr_finalize(*coarse, s);
         // ---- workspace
         L.vf.alloc(L.nf);
         L.zf.alloc(L.nf);
@@ -410,6 +416,76 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
     return h;
 }
 
-void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) { apply_level(h, 0, v, z, s); }
+void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) {
+    if (!h.use_graphs) {
+        apply_level(h, 0, v, z, s);
+        return;
+    }
+    // one CUDA graph per (v, z) pair: ~100 small launches of the multilevel
+    // cycle replay back to back instead of paying host launch latency each
+    const bool prof = prof_on();
+    ApplyGraph *g = nullptr;
+    for (auto &e : h.graphs)
+        if (e.v == v && e.z == z && e.prof == prof) g = &e;
+    if (!g) {
+        if (h.graphs.size() >= 8) {
+            auto old = h.graphs.begin();
+            for (auto it = h.graphs.begin(); it != h.graphs.end(); ++it)
+                if (it->last_use < old->last_use) old = it;
+            if (old->pending) prof_collect(old->recs);
+            prof_release(old->recs);
+            cudaGraphExecDestroy(old->exec);
+            h.graphs.erase(old);
+        }
+        if (!h.cap_stream) PMGR_CUDA(cudaStreamCreateWithFlags(&h.cap_stream, cudaStreamNonBlocking));
+        h.graphs.emplace_back();
+        g = &h.graphs.back();
+        g->v = v;
+        g->z = z;
+        g->prof = prof;
+        cudaGraph_t graph;
+        PMGR_CUDA(cudaStreamBeginCapture(h.cap_stream, cudaStreamCaptureModeThreadLocal));
+        if (prof) prof_capture_begin(&g->recs);
+        try {
+            apply_level(h, 0, v, z, h.cap_stream);
+        } catch (...) {
+            prof_capture_end();
+            cudaStreamEndCapture(h.cap_stream, &graph);
+            throw;
+        }
+        prof_capture_end();
+        PMGR_CUDA(cudaStreamEndCapture(h.cap_stream, &graph));
+        PMGR_CUDA(cudaGraphInstantiate(&g->exec, graph, 0));
+        PMGR_CUDA(cudaGraphDestroy(graph));
+    }
+    if (g->pending) {
+        prof_collect(g->recs);
+        g->pending = false;
+    }
+    g->last_use = ++h.tick;
+    PMGR_CUDA(cudaGraphLaunch(g->exec, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    g->pending = g->prof;
+}
+
+void mgr_collect(pmgr_mgr &h) {
+    for (auto &e : h.graphs)
+        if (e.pending) {
+            prof_collect(e.recs);
+            e.pending = false;
+        }
+}
+
+}  // namespace pmgr
+
+pmgr_mgr::~pmgr_mgr() {
+    for (auto &e : graphs) {
+        pmgr::prof_release(e.recs);
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+    }
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+}
+
+namespace pmgr {
 
 }  // namespace pmgr

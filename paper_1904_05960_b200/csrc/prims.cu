@@ -10,61 +10,101 @@ namespace pmgr {
 std::atomic<int64_t> g_launches{0};
 
 namespace {
-struct ProfRec {
-    int kind;
-    double bytes;
-    cudaEvent_t a, b;
-};
 bool g_prof = false;
-std::vector<ProfRec> g_recs;
+std::vector<ProfRec> g_recs;  // event pool for direct (non-graph) launches
 size_t g_used = 0;
-std::vector<size_t> g_open[PROF_KINDS];
+std::vector<std::pair<std::vector<ProfRec> *, size_t>> g_open[PROF_KINDS];
+std::vector<ProfRec> *g_capture = nullptr;  // records of the graph being captured
+int64_t g_count[PROF_KINDS];
+double g_ms[PROF_KINDS], g_bytes[PROF_KINDS];
+
+void accumulate(const ProfRec &r) {
+    PMGR_CUDA(cudaEventSynchronize(r.b));
+    float e = 0.f;
+    PMGR_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+    g_count[r.kind] += 1;
+    g_ms[r.kind] += e;
+    g_bytes[r.kind] += r.bytes;
+}
+
+void flush_direct() {
+    for (size_t i = 0; i < g_used; ++i) accumulate(g_recs[i]);
+    g_used = 0;
+}
 }  // namespace
 
 bool prof_on() { return g_prof; }
 
+void prof_capture_begin(std::vector<ProfRec> *recs) { g_capture = recs; }
+void prof_capture_end() { g_capture = nullptr; }
+
 void prof_begin(int kind, double bytes, cudaStream_t s) {
-    if (g_used == g_recs.size()) {
-        ProfRec r{};
-        PMGR_CUDA(cudaEventCreate(&r.a));
-        PMGR_CUDA(cudaEventCreate(&r.b));
-        g_recs.push_back(r);
-    }
-    ProfRec &r = g_recs[g_used];
+    ProfRec r{};
     r.kind = kind;
     r.bytes = bytes;
-    PMGR_CUDA(cudaEventRecord(r.a, s));
-    g_open[kind].push_back(g_used);
+    if (g_capture) {
+        // inside stream capture: the events become graph nodes
+        PMGR_CUDA(cudaEventCreate(&r.a));
+        PMGR_CUDA(cudaEventCreate(&r.b));
+        PMGR_CUDA(cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal));
+        g_capture->push_back(r);
+        g_open[kind].push_back({g_capture, g_capture->size() - 1});
+        return;
+    }
+    if (g_used == g_recs.size()) {
+        if (g_used >= 4096) flush_direct();
+        if (g_used == g_recs.size()) {
+            PMGR_CUDA(cudaEventCreate(&r.a));
+            PMGR_CUDA(cudaEventCreate(&r.b));
+            g_recs.push_back(r);
+        }
+    }
+    ProfRec &q = g_recs[g_used];
+    q.kind = kind;
+    q.bytes = bytes;
+    PMGR_CUDA(cudaEventRecord(q.a, s));
+    g_open[kind].push_back({&g_recs, g_used});
     ++g_used;
 }
 
 void prof_end(int kind, cudaStream_t s) {
-    size_t i = g_open[kind].back();
+    auto top = g_open[kind].back();
     g_open[kind].pop_back();
-    PMGR_CUDA(cudaEventRecord(g_recs[i].b, s));
+    ProfRec &r = (*top.first)[top.second];
+    if (top.first != &g_recs)
+        PMGR_CUDA(cudaEventRecordWithFlags(r.b, s, cudaEventRecordExternal));
+    else
+        PMGR_CUDA(cudaEventRecord(r.b, s));
+}
+
+void prof_collect(std::vector<ProfRec> &graph_recs) {
+    for (const ProfRec &r : graph_recs) accumulate(r);
+}
+
+void prof_release(std::vector<ProfRec> &graph_recs) {
+    for (ProfRec &r : graph_recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    graph_recs.clear();
 }
 
 void prof_enable(bool on) {
+    if (g_prof) flush_direct();
     g_prof = on;
     g_used = 0;
     for (auto &v : g_open) v.clear();
+    for (int k = 0; k < PROF_KINDS; ++k) {
+        g_count[k] = 0;
+        g_ms[k] = g_bytes[k] = 0.0;
+    }
 }
 
 void prof_query(int kind, int64_t *count, double *ms, double *bytes) {
-    int64_t c = 0;
-    double t = 0.0, by = 0.0;
-    for (size_t i = 0; i < g_used; ++i) {
-        if (g_recs[i].kind != kind) continue;
-        PMGR_CUDA(cudaEventSynchronize(g_recs[i].b));
-        float e = 0.f;
-        PMGR_CUDA(cudaEventElapsedTime(&e, g_recs[i].a, g_recs[i].b));
-        ++c;
-        t += e;
-        by += g_recs[i].bytes;
-    }
-    *count = c;
-    *ms = t;
-    *bytes = by;
+    flush_direct();
+    *count = g_count[kind];
+    *ms = g_ms[kind];
+    *bytes = g_bytes[kind];
 }
 
 int num_sms() {

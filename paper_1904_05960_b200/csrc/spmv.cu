@@ -66,6 +66,15 @@ struct OpSweep0 {
         r[i] = b[i] - s;
     }
 };
+struct OpRestrictDiv {  // b_c = R r, and the first smoother iterate x_c = b_c / dtilde_c
+    const double *r, *d;
+    double *b, *xo;
+    __device__ double x(int j) const { return __ldg(r + j); }
+    __device__ void out(int64_t k, double s) const {
+        b[k] = s;
+        xo[k] = s / d[k];
+    }
+};
 struct OpAdd {
     const double *e;
     double *xio;
@@ -94,6 +103,12 @@ template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
     double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
+    // skewed rows (a few dense coarse-grid rows next to short ones) get a
+    // whole warp, otherwise the longest row serialises its lane group
+    if (A.maxrow >= 0) {
+        int g = mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= 160.0 ? 16 : 32;
+        if (A.maxrow > 16 * g) mean = 1e9;
+    }
     const int block = 256;
     if (mean <= 3.0) {
         k_spmv<2, Op><<<grid_for(A.nrows * 2, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
@@ -183,6 +198,29 @@ void spmv_jacobi(const CsrView &A, const double *x, const double *b, const doubl
 void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x, double *r,
                           cudaStream_t s) {
     launch(A, OpSweep0{b, d, x, r}, s);
+}
+
+void spmv_restrict_div(const CsrView &R, const double *r, const double *d, double *b, double *x,
+                       cudaStream_t s) {
+    launch(R, OpRestrictDiv{r, d, b, x}, s);
+}
+
+namespace {
+__global__ void k_copy_div(const double *__restrict__ b, const double *__restrict__ d, int64_t n,
+                           double *__restrict__ bo, double *__restrict__ xo) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        double v = b[i];
+        bo[i] = v;
+        xo[i] = v / d[i];
+    }
+}
+}  // namespace
+
+void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s) {
+    if (n == 0) return;
+    k_copy_div<<<grid_for(n, 256), 256, 0, s>>>(b, d, n, bo, xo);
+    PMGR_LAUNCHED();
 }
 
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s) {
