@@ -143,11 +143,100 @@ __global__ void k_scale(const double *x, int64_t n, const double *den, double *y
 
 __global__ void k_sqrt(double *x) { *x = sqrt(*x); }
 
+// ---- classical Gram-Schmidt with DGKS re-orthogonalisation ---------------
+// Pass 1 (k_mdot): h_k = V_k . w for k < nk and ||w||^2, one block per
+// (row range, vector) so every block streams one contiguous slice of V.
+// Pass 2 (k_upd): w -= sum_k h_k V_k with ||w'||^2 partials.  A second
+// projection runs only when ||w'|| < ||w||/sqrt(2) (device flag; the two
+// extra launches exit at once otherwise), which keeps the basis orthogonal
+// to working precision like the reference's MGS (krylov.py:75-77).
+
+__device__ __forceinline__ double block_sum_all(double v, double *sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    return t;
+}
+
+__global__ void __launch_bounds__(DOT_BLOCK) k_mdot(const double *__restrict__ V, int64_t n, int nk,
+                                                     const double *__restrict__ w, double *partial, int nsplit,
+                                                     int64_t chunk, const int *active) {
+    if (active && !*active) return;
+    __shared__ double sh[DOT_BLOCK / 32];
+    const int k = blockIdx.y;
+    const double *x = k < nk ? V + (int64_t)k * n : w;
+    const int64_t lo = blockIdx.x * chunk;
+    const int64_t hi = lo + chunk < n ? lo + chunk : n;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t i = lo + threadIdx.x;
+    for (; i + 3 * DOT_BLOCK < hi; i += 4 * DOT_BLOCK) {
+        a0 = fma(x[i], w[i], a0);
+        a1 = fma(x[i + DOT_BLOCK], w[i + DOT_BLOCK], a1);
+        a2 = fma(x[i + 2 * DOT_BLOCK], w[i + 2 * DOT_BLOCK], a2);
+        a3 = fma(x[i + 3 * DOT_BLOCK], w[i + 3 * DOT_BLOCK], a3);
+    }
+    for (; i < hi; i += DOT_BLOCK) a0 = fma(x[i], w[i], a0);
+    double t = block_sum_all((a0 + a1) + (a2 + a3), sh);
+    if (threadIdx.x == 0) partial[(int64_t)k * nsplit + blockIdx.x] = t;
+}
+
+// out[k] = sum_s partial[k*nsplit + s], one warp per k, fixed order
+__global__ void k_preduce(const double *partial, int nsplit, int nk1, double *out, const int *active) {
+    if (active && !*active) return;
+    int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (k >= nk1) return;
+    double s = 0.0;
+    for (int b = lane; b < nsplit; b += 32) s += partial[(int64_t)k * nsplit + b];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0) out[k] = s;
+}
+
+__global__ void __launch_bounds__(DOT_BLOCK) k_upd(const double *__restrict__ V, int64_t n, int nk,
+                                                    const double *__restrict__ h, double *w, double *partial,
+                                                    const int *active) {
+    if (active && !*active) return;
+    __shared__ double sh[DOT_BLOCK / 32];
+    __shared__ double hs[1024];
+    for (int k = threadIdx.x; k < nk; k += DOT_BLOCK) hs[k] = h[k];
+    __syncthreads();
+    double nrm = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
+        double a0 = w[i], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int k = 0;
+        for (; k + 3 < nk; k += 4) {
+            a0 = fma(-hs[k], V[(int64_t)k * n + i], a0);
+            a1 = fma(-hs[k + 1], V[(int64_t)(k + 1) * n + i], a1);
+            a2 = fma(-hs[k + 2], V[(int64_t)(k + 2) * n + i], a2);
+            a3 = fma(-hs[k + 3], V[(int64_t)(k + 3) * n + i], a3);
+        }
+        for (; k < nk; ++k) a0 = fma(-hs[k], V[(int64_t)k * n + i], a0);
+        const double wi = (a0 + a1) + (a2 + a3);
+        w[i] = wi;
+        nrm = fma(wi, wi, nrm);
+    }
+    double t = block_sum_all(nrm, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// DGKS test: re-orthogonalise when ||w'||^2 < ||w||^2 / 2
+__global__ void k_reorth_flag(const double *h1, int nk, const double *nrm1, int *flag, double *h2) {
+    const int f = nrm1[0] < 0.5 * h1[nk];
+    if (threadIdx.x == 0) *flag = f;
+    for (int k = threadIdx.x; k <= nk; k += blockDim.x) h2[k] = 0.0;
+}
+
 struct GmresState {
     double *H;     // (m+1) x m, row-major (i, j) at i*m + j
     double *cs, *sn, *g;
     double *h1, *h2;  // dot results (m+1)
     double *hnext;    // ||w|| after orthogonalisation
+    double *nrm1, *nrm2;  // ||w'||^2 after the first / second projection
+    int *reorth;          // DGKS flag of the current step
     double *y;        // triangular solve result
     int *status;      // [0] breakdown, [1] dead column, [2] converged-by-estimate
     double *hist;     // |g[j+1]| per iteration
@@ -156,7 +245,7 @@ struct GmresState {
 // Arnoldi column j: h = h1 + h2, Hessenberg update, Givens (krylov.py:75-104)
 __global__ void k_arnoldi_tail(GmresState st, int m, int j, double tol) {
     double *H = st.H;
-    const double hn = sqrt(*st.hnext);
+    const double hn = sqrt(*st.reorth ? *st.nrm2 : *st.nrm1);
     double cs2 = 0.0;
     for (int i = 0; i <= j; ++i) {
         double hv = st.h1[i] + st.h2[i];
@@ -257,10 +346,35 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
     st.y = st.h2 + (m + 1);
     st.hnext = st.y + (m + 1);
     double *beta_d = st.hnext + 1;
+    st.nrm1 = beta_d + 1;
+    st.nrm2 = st.nrm1 + 1;
     st.status = status.p;
+    st.reorth = status.p + 3;
     st.hist = dhist.p;
     Reducer R;
     R.init(n, m + 1, s);
+    // projection partials: (nk+1) vectors x nsplit row slices
+    const int64_t min_chunk = 4096;
+    int nsplit_max = (int)((n + min_chunk - 1) / min_chunk);
+    if (nsplit_max < 1) nsplit_max = 1;
+    TBuf<double> mpart((int64_t)(m + 2) * (nsplit_max > 64 ? 64 : nsplit_max), s);
+    const int upd_blocks = 4 * num_sms();
+    TBuf<double> upart(upd_blocks, s);
+    auto project = [&](int nk, double *h, double *nrm, const int *active) {
+        int nsplit = (int)((4 * num_sms() + nk) / (nk + 1));
+        if (nsplit > nsplit_max) nsplit = nsplit_max;
+        if (nsplit > 64) nsplit = 64;
+        if (nsplit < 1) nsplit = 1;
+        const int64_t chunk = (n + nsplit - 1) / nsplit;
+        k_mdot<<<dim3(nsplit, nk + 1), DOT_BLOCK, 0, s>>>(V.p, n, nk, w.p, mpart.p, nsplit, chunk, active);
+        PMGR_LAUNCHED();
+        k_preduce<<<((nk + 1) * 32 + 255) / 256, 256, 0, s>>>(mpart.p, nsplit, nk + 1, h, active);
+        PMGR_LAUNCHED();
+        k_upd<<<upd_blocks, DOT_BLOCK, 0, s>>>(V.p, n, nk, h, w.p, upart.p, active);
+        PMGR_LAUNCHED();
+        k_preduce<<<1, 32, 0, s>>>(upart.p, upd_blocks, 1, nrm, active);
+        PMGR_LAUNCHED();
+    };
 
     std::vector<double> hist;
     int hcount = 0;
@@ -305,19 +419,11 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
                 }
                 const int nk = j + 1;
                 {
-                    ProfScope pso(PROF_ORTHO, 8.0 * n * (3.0 * nk + 7.0), s);
-                    k_multidot<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, w.p, R.partial.p, R.ld);
+                    ProfScope pso(PROF_ORTHO, 8.0 * n * (2.0 * nk + 6.0), s);
+                    project(nk, st.h1, st.nrm1, nullptr);
+                    k_reorth_flag<<<1, 128, 0, s>>>(st.h1, nk, st.nrm1, st.reorth, st.h2);
                     PMGR_LAUNCHED();
-                    k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h1, 0);
-                    PMGR_LAUNCHED();
-                    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h1, w.p, 1, R.partial.p, R.ld);
-                    PMGR_LAUNCHED();
-                    k_reduce_partials<<<(nk * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nk, R.ld, st.h2, 0);
-                    PMGR_LAUNCHED();
-                    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V.p, n, nk, st.h2, w.p, 2, R.partial.p, R.ld);
-                    PMGR_LAUNCHED();
-                    k_reduce_partials<<<1, 32, 0, s>>>(R.partial.p, R.nblk, 1, R.ld, st.hnext, 0);
-                    PMGR_LAUNCHED();
+                    project(nk, st.h2, st.nrm2, st.reorth);
                     k_arnoldi_tail<<<1, 1, 0, s>>>(st, m, j, tol);
                     PMGR_LAUNCHED();
                 }
