@@ -14,6 +14,8 @@
 //   OpResidRows    r_C = v_C - A_CF z_F                     (mgr.py:419-422, C rows only)
 //   OpProlong      z = [z_F ; 0] + P e_C                    (mgr.py:424-425)
 // The solve phase only needs 1e-10 agreement, so these use FMA.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pmgr {
@@ -140,7 +142,11 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     }
     // matrices far larger than L2 are streamed with evict-first loads so the
     // gathered vectors stay cached; small operators stay L2-resident
-    const bool stream = 12.0 * (double)A.nnz > 48.0 * 1024 * 1024;
+    static const double stream_mb = [] {
+        const char *e = getenv("PMGR_SPMV_STREAM_MB");
+        return e ? atof(e) : 1e30;
+    }();
+    const bool stream = 12.0 * (double)A.nnz > stream_mb * 1024 * 1024;
     if (mean <= 3.0) {
         go<2>(A, op, stream, s);
     } else if (mean <= 12.0) {
