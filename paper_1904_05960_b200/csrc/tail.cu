@@ -6,11 +6,10 @@
 // handful of CTAs, and the coarse levels of an elasticity hierarchy are
 // dozens deep.  Here one cluster of 16 CTAs (16 SMs) walks all of them:
 // phases are separated by the hardware cluster barrier (~0.2 us on
-// Blackwell) instead of kernel boundaries (several us each).  The
-// prolongation is folded into the post-smoothing sweep (x'_j = x_j + P_j e
-// recomputed per stored entry; the tail's P rows hold 1-10 entries), so a
-// level costs three barriers: residual | restriction (+ next level's first
-// sweep x = b/dtilde) | ... | prolongation-and-sweep.
+// Blackwell) instead of kernel boundaries (several us each).  A level costs
+// four barriers: residual | restriction (+ the next level's first sweep
+// x = b/dtilde) | ... | prolongation | post-sweep.  Rows are spread over all
+// 16K threads of the cluster in lane groups sized to the level's row length.
 #include <cooperative_groups.h>
 
 #include "hier.cuh"
@@ -21,90 +20,100 @@ namespace pmgr {
 
 namespace {
 
-constexpr int TAIL_THREADS = 512;
+constexpr int TAIL_THREADS = 1024;
 constexpr int TAIL_WARPS = TAIL_THREADS / 32;
 
-__device__ __forceinline__ double warp_sum_d(double s) {
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    return s;
+// lanes per row for a level: enough rows in flight for short rows, a whole
+// warp for the dense coarse rows
+__device__ __forceinline__ int group_for(int64_t nnz, int n) {
+    const int64_t mean = n ? nnz / n : 0;
+    return mean <= 3 ? 2 : mean <= 12 ? 4 : mean <= 48 ? 8 : mean <= 160 ? 16 : 32;
 }
 
-// r = b - A x
-__device__ void phase_residual(const TailLevel &L, int gw, int nw, int lane) {
-    for (int i = gw; i < L.n; i += nw) {
-        double s = 0.0;
-        for (int64_t q = L.ro[i] + lane; q < L.ro[i + 1]; q += 32) s = fma(L.v[q], L.x[L.ci[q]], s);
-        s = warp_sum_d(s);
-        if (lane == 0) L.r[i] = L.b[i] - s;
-    }
-}
-
-// b_next = R r ; x_next = b_next / dtilde_next (next level smoothed) ;
-// or cb = R r at the coarsest
-__device__ void phase_restrict(const TailLevel &L, double *bn, double *xn, const double *dn, int nn, int gw,
-                               int nw, int lane) {
-    for (int k = gw; k < nn; k += nw) {
-        double s = 0.0;
-        for (int64_t q = L.Rro[k] + lane; q < L.Rro[k + 1]; q += 32) s = fma(L.Rv[q], L.r[L.Rci[q]], s);
-        s = warp_sum_d(s);
-        if (lane == 0) {
-            bn[k] = s;
-            if (xn) xn[k] = s / dn[k];
+template <class Fx, class Fout>
+__device__ __forceinline__ void rows_spmv(int n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
+                                          const double *__restrict__ v, int G, int gt, int nt, Fx xval, Fout out) {
+    // gt / nt: global thread index / count over the cluster
+    const int lane = gt & (G - 1);
+    const int ng = nt / G;
+    const int wbase = (gt & ~31) / G;  // first row of this warp: warp-uniform trip count
+    for (int it = 0; wbase + it * ng < n; ++it) {
+        const int i = gt / G + it * ng;
+        const bool act = i < n;
+        int64_t b = 0, e = 0;
+        if (act) {
+            b = __ldg(ro + i);
+            e = __ldg(ro + i + 1);
         }
-    }
-}
-
-__device__ __forceinline__ double prolonged(const TailLevel &L, const double *e, int j) {
-    double t = L.x[j];
-    for (int64_t p = L.Pro[j]; p < L.Pro[j + 1]; ++p) t = fma(L.Pv[p], e[L.Pci[p]], t);
-    return t;
-}
-
-// out = x' + (b - A x') / dtilde with x' = x + P e
-__device__ void phase_up(const TailLevel &L, const double *e, double *out, int gw, int nw, int lane) {
-    for (int i = gw; i < L.n; i += nw) {
-        double s = 0.0;
-        for (int64_t q = L.ro[i] + lane; q < L.ro[i + 1]; q += 32) s = fma(L.v[q], prolonged(L, e, L.ci[q]), s);
-        s = warp_sum_d(s);
-        if (lane == 0) {
-            const double xi = prolonged(L, e, i);
-            out[i] = xi + (L.b[i] - s) / L.dt[i];
+        double s0 = 0.0, s1 = 0.0;
+        int64_t q = b + lane;
+        for (; q + G < e; q += 2 * G) {
+            s0 = fma(__ldg(v + q), xval(__ldg(ci + q)), s0);
+            s1 = fma(__ldg(v + q + G), xval(__ldg(ci + q + G)), s1);
         }
+        if (q < e) s0 = fma(__ldg(v + q), xval(__ldg(ci + q)), s0);
+        double s = s0 + s1;
+        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
+        if (act && lane == 0) out(i, s);
     }
 }
 
 __global__ void __launch_bounds__(TAIL_THREADS) k_tail(const TailParams *__restrict__ pp) {
     const TailParams &P = *pp;
     cg::cluster_group cl = cg::this_cluster();
-    const int lane = threadIdx.x & 31;
-    const int gw = (int)cl.block_rank() * TAIL_WARPS + (threadIdx.x >> 5);
-    const int nw = (int)cl.num_blocks() * TAIL_WARPS;
-    // down: residual, restriction
+    const int nt = (int)cl.num_blocks() * TAIL_THREADS;
+    const int gt = (int)cl.block_rank() * TAIL_THREADS + threadIdx.x;
+    // down: residual | restriction (+ first sweep of the next level)
     for (int l = 0; l < P.nlev; ++l) {
         const TailLevel &L = P.lev[l];
-        phase_residual(L, gw, nw, lane);
+        const int G = group_for(L.ro[L.n], L.n);
+        const double *x = L.x;
+        const double *b = L.b;
+        double *r = L.r;
+        rows_spmv(L.n, L.ro, L.ci, L.v, G, gt, nt, [=](int j) { return x[j]; },
+                  [=](int i, double s) { r[i] = b[i] - s; });
         cl.sync();
+        const int nn = (l + 1 < P.nlev) ? P.lev[l + 1].n : P.nc;
+        const int GR = group_for(L.Rro[nn], nn);
         if (l + 1 < P.nlev) {
             const TailLevel &N = P.lev[l + 1];
-            phase_restrict(L, N.b, N.x, N.dt, N.n, gw, nw, lane);
+            double *bn = N.b, *xn = N.x;
+            const double *dn = N.dt;
+            rows_spmv(nn, L.Rro, L.Rci, L.Rv, GR, gt, nt, [=](int j) { return r[j]; }, [=](int k, double s) {
+                bn[k] = s;
+                xn[k] = s / dn[k];
+            });
         } else {
-            phase_restrict(L, P.cb, nullptr, nullptr, P.nc, gw, nw, lane);
+            double *cb = P.cb;
+            rows_spmv(nn, L.Rro, L.Rci, L.Rv, GR, gt, nt, [=](int j) { return r[j]; },
+                      [=](int k, double s) { cb[k] = s; });
         }
         cl.sync();
     }
-    // coarsest: cx = C^{-1} cb (dense, warp per row)
-    for (int i = gw; i < P.nc; i += nw) {
-        double s = 0.0;
-        for (int j = lane; j < P.nc; j += 32) s = fma(P.cinv[(int64_t)i * P.nc + j], P.cb[j], s);
-        s = warp_sum_d(s);
-        if (lane == 0) P.cx[i] = s;
+    // coarsest: cx = C^{-1} cb (dense rows, a warp per row)
+    {
+        const int lane = threadIdx.x & 31;
+        const int gw = gt >> 5, nw = nt >> 5;
+        for (int i = gw; i < P.nc; i += nw) {
+            double s = 0.0;
+            for (int j = lane; j < P.nc; j += 32) s = fma(__ldg(P.cinv + (int64_t)i * P.nc + j), P.cb[j], s);
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+            if (lane == 0) P.cx[i] = s;
+        }
     }
     cl.sync();
-    // up: prolongation folded into the post-sweep
+    // up: prolongation | post-sweep
     for (int l = P.nlev - 1; l >= 0; --l) {
         const TailLevel &L = P.lev[l];
         const double *e = (l + 1 < P.nlev) ? P.lev[l + 1].xo : P.cx;
-        phase_up(L, e, l == 0 ? P.out : L.xo, gw, nw, lane);
+        double *x = L.x;
+        rows_spmv(L.n, L.Pro, L.Pci, L.Pv, group_for(L.Pro[L.n], L.n), gt, nt, [=](int j) { return e[j]; },
+                  [=](int i, double s) { x[i] += s; });
+        cl.sync();
+        const double *b = L.b, *dt = L.dt;
+        double *out = (l == 0) ? P.out : L.xo;
+        rows_spmv(L.n, L.ro, L.ci, L.v, group_for(L.ro[L.n], L.n), gt, nt, [=](int j) { return x[j]; },
+                  [=](int i, double s) { out[i] = x[i] + (b[i] - s) / dt[i]; });
         if (l > 0) cl.sync();
     }
 }
