@@ -21,7 +21,6 @@ namespace pmgr {
 namespace {
 
 constexpr int TAIL_THREADS = 1024;
-constexpr int TAIL_WARPS = TAIL_THREADS / 32;
 
 // lanes per row for a level: enough rows in flight for short rows, a whole
 // warp for the dense coarse rows
