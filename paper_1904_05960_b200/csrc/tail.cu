@@ -26,7 +26,10 @@ constexpr int TAIL_THREADS = 1024;
 // warp for the dense coarse rows
 __device__ __forceinline__ int group_for(int64_t nnz, int n) {
     const int64_t mean = n ? nnz / n : 0;
-    return mean <= 3 ? 2 : mean <= 12 ? 4 : mean <= 48 ? 8 : mean <= 160 ? 16 : 32;
+    int g = mean <= 3 ? 2 : mean <= 12 ? 4 : mean <= 48 ? 8 : mean <= 160 ? 16 : 32;
+    // keep every row's group resident at once (one pass of latency per phase)
+    while (g > 2 && (int64_t)n * g > 16 * 1024) g >>= 1;
+    return g;
 }
 
 template <class Fx, class Fout>
@@ -145,7 +148,7 @@ int cluster_size() {
 
 }  // namespace
 
-bool tail_qualifies(const Csr &A) { return A.nrows <= 16384 && A.nnz <= 600000; }
+bool tail_qualifies(const Csr &A) { return A.nrows <= 2048 && A.nnz <= 200000; }
 
 void tail_launch(const TailParams *dev_params, cudaStream_t s) {
     const int cs = cluster_size();
