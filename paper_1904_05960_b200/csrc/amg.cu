@@ -404,6 +404,9 @@ void setup_tail(pmgr_amg &h) {
         const AmgLevel &L = h.levels[from + l];
         TailLevel &t = p.lev[l];
         t.n = (int)L.A->nrows;
+        t.gA = tail_group(*L.A);
+        t.gR = tail_group(L.R);
+        t.gP = tail_group(L.P);
         t.ro = L.A->ro.p;
         t.ci = L.A->ci.p;
         t.v = L.A->v.p;

@@ -31,6 +31,7 @@ constexpr int MAX_TAIL = 24;
 // device-resident description of the cluster-kernel tail (tail.cu)
 struct TailLevel {
     int n;
+    int gA, gR, gP;  // lanes per row for A, R and P
     const int64_t *ro;
     const int32_t *ci;
     const double *v;
@@ -54,6 +55,7 @@ struct TailParams {
 };
 
 bool tail_qualifies(const Csr &A);
+int tail_group(const Csr &A);
 void tail_launch(const TailParams *dev_params, cudaStream_t s);
 
 }  // namespace pmgr

@@ -22,20 +22,12 @@ namespace {
 
 constexpr int TAIL_THREADS = 1024;
 
-// lanes per row for a level: enough rows in flight for short rows, a whole
-// warp for the dense coarse rows
-__device__ __forceinline__ int group_for(int64_t nnz, int n) {
-    const int64_t mean = n ? nnz / n : 0;
-    int g = mean <= 3 ? 2 : mean <= 12 ? 4 : mean <= 48 ? 8 : mean <= 160 ? 16 : 32;
-    // keep every row's group resident at once (one pass of latency per phase)
-    while (g > 2 && (int64_t)n * g > 16 * 1024) g >>= 1;
-    return g;
-}
+constexpr int TAIL_U = 8;  // entries prefetched per lane before the gathers
 
 template <class Fx, class Fout>
 __device__ __forceinline__ void rows_spmv(int n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
                                           const double *__restrict__ v, int G, int gt, int nt, Fx xval, Fout out) {
-    // gt / nt: global thread index / count over the cluster
+    // gt / nt: global thread index / count over the cluster; G lanes per row
     const int lane = gt & (G - 1);
     const int ng = nt / G;
     const int wbase = (gt & ~31) / G;  // first row of this warp: warp-uniform trip count
@@ -47,14 +39,20 @@ __device__ __forceinline__ void rows_spmv(int n, const int64_t *__restrict__ ro,
             b = __ldg(ro + i);
             e = __ldg(ro + i + 1);
         }
-        double s0 = 0.0, s1 = 0.0;
-        int64_t q = b + lane;
-        for (; q + G < e; q += 2 * G) {
-            s0 = fma(__ldg(v + q), xval(__ldg(ci + q)), s0);
-            s1 = fma(__ldg(v + q + G), xval(__ldg(ci + q + G)), s1);
+        double s = 0.0;
+        for (int64_t q = b + lane; q < e; q += TAIL_U * G) {
+            double vv[TAIL_U];
+            int cc[TAIL_U];
+#pragma unroll
+            for (int u = 0; u < TAIL_U; ++u) {
+                const int64_t k = q + (int64_t)u * G;
+                vv[u] = k < e ? __ldg(v + k) : 0.0;
+                cc[u] = k < e ? __ldg(ci + k) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < TAIL_U; ++u)
+                if (cc[u] >= 0) s = fma(vv[u], xval(cc[u]), s);
         }
-        if (q < e) s0 = fma(__ldg(v + q), xval(__ldg(ci + q)), s0);
-        double s = s0 + s1;
         for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
         if (act && lane == 0) out(i, s);
     }
@@ -68,7 +66,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(const TailParams *__restr
     // down: residual | restriction (+ first sweep of the next level)
     for (int l = 0; l < P.nlev; ++l) {
         const TailLevel &L = P.lev[l];
-        const int G = group_for(L.ro[L.n], L.n);
+        const int G = L.gA;
         const double *x = L.x;
         const double *b = L.b;
         double *r = L.r;
@@ -76,7 +74,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(const TailParams *__restr
                   [=](int i, double s) { r[i] = b[i] - s; });
         cl.sync();
         const int nn = (l + 1 < P.nlev) ? P.lev[l + 1].n : P.nc;
-        const int GR = group_for(L.Rro[nn], nn);
+        const int GR = L.gR;
         if (l + 1 < P.nlev) {
             const TailLevel &N = P.lev[l + 1];
             double *bn = N.b, *xn = N.x;
@@ -109,12 +107,12 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(const TailParams *__restr
         const TailLevel &L = P.lev[l];
         const double *e = (l + 1 < P.nlev) ? P.lev[l + 1].xo : P.cx;
         double *x = L.x;
-        rows_spmv(L.n, L.Pro, L.Pci, L.Pv, group_for(L.Pro[L.n], L.n), gt, nt, [=](int j) { return e[j]; },
+        rows_spmv(L.n, L.Pro, L.Pci, L.Pv, L.gP, gt, nt, [=](int j) { return e[j]; },
                   [=](int i, double s) { x[i] += s; });
         cl.sync();
         const double *b = L.b, *dt = L.dt;
         double *out = (l == 0) ? P.out : L.xo;
-        rows_spmv(L.n, L.ro, L.ci, L.v, group_for(L.ro[L.n], L.n), gt, nt, [=](int j) { return x[j]; },
+        rows_spmv(L.n, L.ro, L.ci, L.v, L.gA, gt, nt, [=](int j) { return x[j]; },
                   [=](int i, double s) { out[i] = x[i] + (b[i] - s) / dt[i]; });
         if (l > 0) cl.sync();
     }
@@ -149,6 +147,14 @@ int cluster_size() {
 }  // namespace
 
 bool tail_qualifies(const Csr &A) { return A.nrows <= 2048 && A.nnz <= 200000; }
+
+int tail_group(const Csr &A) {
+    const double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
+    int g = mean <= 3 ? 2 : mean <= 12 ? 4 : mean <= 48 ? 8 : mean <= 160 ? 16 : 32;
+    if (A.maxrow > (int64_t)TAIL_U * g) g = 32;  // a dense row must not serialise its group
+    while (g > 2 && A.nrows * g > 4 * 16 * 1024) g >>= 1;
+    return g;
+}
 
 void tail_launch(const TailParams *dev_params, cudaStream_t s) {
     const int cs = cluster_size();
