@@ -381,52 +381,6 @@ __global__ void __launch_bounds__(1024) k_gauss_jordan(int64_t n, double *A, dou
     }
 }
 
-// The contiguous run of small l1-Jacobi levels above the coarsest solve
-// goes to the cluster kernel of tail.cu.
-void setup_tail(pmgr_amg &h) {
-    static const bool off = getenv("PMGR_NO_TAIL") && getenv("PMGR_NO_TAIL")[0] != '0';
-    if (off || h.coarse->nrows > 4096) return;
-    int from = (int)h.levels.size();
-    while (from > 0) {
-        const AmgLevel &L = h.levels[from - 1];
-        if (!L.jacobi || !tail_qualifies(*L.A) || (int)h.levels.size() - (from - 1) > MAX_TAIL) break;
-        --from;
-    }
-    if (from == (int)h.levels.size()) return;
-    TailParams p{};
-    p.nlev = (int)h.levels.size() - from;
-    p.nc = (int)h.coarse->nrows;
-    p.cinv = h.coarse_inv.p;
-    p.cb = h.cb.p;
-    p.cx = h.cx.p;
-    p.out = h.levels[from].xo.p;
-    for (int l = 0; l < p.nlev; ++l) {
-        const AmgLevel &L = h.levels[from + l];
-        TailLevel &t = p.lev[l];
-        t.n = (int)L.A->nrows;
-        t.gA = tail_group(*L.A);
-        t.gR = tail_group(L.R);
-        t.gP = tail_group(L.P);
-        t.ro = L.A->ro.p;
-        t.ci = L.A->ci.p;
-        t.v = L.A->v.p;
-        t.dt = L.dtilde.p;
-        t.Rro = L.R.ro.p;
-        t.Rci = L.R.ci.p;
-        t.Rv = L.R.v.p;
-        t.Pro = L.P.ro.p;
-        t.Pci = L.P.ci.p;
-        t.Pv = L.P.v.p;
-        t.b = L.b.p;
-        t.x = L.x.p;
-        t.r = L.r.p;
-        t.xo = L.xo.p;
-    }
-    h.tail.alloc(1);
-    PMGR_CUDA(cudaMemcpy(h.tail.p, &p, sizeof(p), cudaMemcpyHostToDevice));
-    h.tail_from = from;
-}
-
 std::vector<int64_t> partition_starts(int64_t n, int64_t nparts) {
     // reference PartitionSet.contiguous (smoothers.py:67-75), align = 1
     int64_t np_ = nparts < n ? nparts : n;
@@ -593,7 +547,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         PMGR_LAUNCHED();
         PMGR_CUDA(cudaStreamSynchronize(s));
     }
-    setup_tail(*h);
+    collapse_tail(*h, s);
     return h;
 }
 
@@ -612,9 +566,8 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     // precondition: L.b holds the right-hand side and, on l1-Jacobi levels,
     // L.x = L.b / dtilde (the first sweep from zero), written by the producer
     AmgLevel &L = h.levels[l];
-    if ((int)l == h.tail_from) {
-        tail_launch(h.tail.p, s);
-        if (out) vec_copy(L.xo.p, out, L.A->nrows, s);
+    if ((int)l == h.collapse_from) {
+        dense_matvec(h.collapsed.p, L.A->nrows, L.b.p, out ? out : L.xo.p, s);
         return;
     }
     const CsrView A = L.A->view();

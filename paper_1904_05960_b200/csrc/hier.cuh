@@ -26,37 +26,8 @@ struct AmgLevel {
     DBuf<double> b, x, r, xo, xpre;
 };
 
-constexpr int MAX_TAIL = 24;
-
-// device-resident description of the cluster-kernel tail (tail.cu)
-struct TailLevel {
-    int n;
-    int gA, gR, gP;  // lanes per row for A, R and P
-    const int64_t *ro;
-    const int32_t *ci;
-    const double *v;
-    const double *dt;
-    const int64_t *Rro;
-    const int32_t *Rci;
-    const double *Rv;
-    const int64_t *Pro;
-    const int32_t *Pci;
-    const double *Pv;
-    double *b, *x, *r, *xo;
-};
-
-struct TailParams {
-    int nlev;
-    int nc;
-    const double *cinv;
-    double *cb, *cx;
-    double *out;
-    TailLevel lev[MAX_TAIL];
-};
-
-bool tail_qualifies(const Csr &A);
-int tail_group(const Csr &A);
-void tail_launch(const TailParams *dev_params, cudaStream_t s);
+// coarse end of the V-cycle as one dense operator (collapse.cu)
+void collapse_tail(pmgr_amg &h, cudaStream_t s);
 
 }  // namespace pmgr
 
@@ -68,8 +39,8 @@ struct pmgr_amg {
     pmgr::DBuf<double> cb, cx, ctmp;          // coarsest workspace
     int64_t flagged = 0;
     bool prof_tag = false;  // time level-0 smoother kernels (F-relax AMG of MGR level 0)
-    int tail_from = -1;     // first level run by the cluster tail kernel (-1: none)
-    pmgr::DBuf<pmgr::TailParams> tail;
+    int collapse_from = -1;          // levels >= this run as one dense operator (-1: none)
+    pmgr::DBuf<double> collapsed;    // that operator, row-major n x n
 };
 
 namespace pmgr {
