@@ -97,7 +97,10 @@ int pmgr_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ro
 }
 
 int pmgr_csr_destroy(pmgr_csr *A) {
-    return guard([&] { delete A; });
+    return guard([&] {
+        pmgr::gmres_forget(A);
+        delete A;
+    });
 }
 
 int pmgr_csr_info(const pmgr_csr *A, int64_t *nrows, int64_t *ncols, int64_t *nnz) {
@@ -208,7 +211,10 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
 }
 
 int pmgr_mgr_destroy(pmgr_mgr *h) {
-    return guard([&] { delete h; });
+    return guard([&] {
+        pmgr::gmres_forget(h);
+        delete h;
+    });
 }
 
 int pmgr_mgr_num_levels(const pmgr_mgr *h, int32_t *nlevels) {

@@ -106,9 +106,11 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A, const int8_t *
                                     int nlevels, const pmgr_mgr_cfg &cfg, cudaStream_t s);
 void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);
 void mgr_collect(pmgr_mgr &h);  // fold finished graph timing events into the totals
+void mgr_apply_direct(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);  // no graph (for capture)
 }  // namespace pmgr
 
 namespace pmgr {
+void gmres_forget(const void *obj);  // drop cached solve workspaces of a matrix / hierarchy
 void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, int nonzero_x0,
                   const pmgr_gmres_cfg &cfg, pmgr_gmres_stats &stats, double *history,
                   int32_t history_cap, cudaStream_t s);

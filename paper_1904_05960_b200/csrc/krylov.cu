@@ -1,18 +1,32 @@
 // krylov.cu -- right-preconditioned restarted GMRES on the device
 // (reference krylov.py:39-117).
 //
-// Same outer semantics as the reference: x0 = 0 unless given; convergence
-// on ||b - A x|| <= max(rtol*||r0||, atol); Givens least squares; at each
-// restart x += M^{-1}(V y), the true residual is recomputed and replaces the
-// last history entry; an Arnoldi breakdown counts as convergence in the
-// subspace.  Orthogonalisation is classical Gram-Schmidt with one
-// re-orthogonalisation (CGS2) instead of MGS: the projections become two
-// fused multi-dot / multi-axpy passes over the Krylov basis (HBM streaming,
-// deterministic block partials) -- not bitwise MGS, but at least as
-// orthogonal, which keeps iteration counts within +-1.
-// The small Hessenberg / Givens work runs in one single-thread kernel; the
-// host only reads three status words per iteration.
+// Outer semantics follow the reference exactly: x0 = 0 unless given;
+// convergence on ||b - A x|| <= max(rtol*||r0||, atol); Givens least
+// squares; at each restart x += M^{-1}(V y) and the true residual replaces
+// the last history entry; an Arnoldi breakdown counts as convergence in the
+// subspace; a dead Givens column (rho == 0) is discarded.
+//
+// B200 design:
+//  * The whole Arnoldi step -- MGR apply, SpMV, projections, Hessenberg /
+//    Givens update, normalisation -- reads the step index j from device
+//    memory, so one captured CUDA graph serves every step.  The restart cycle
+//    is a graph WHILE node: the Givens kernel sets the loop condition with
+//    cudaGraphSetConditional, and the host synchronises once per cycle.
+//  * Orthogonalisation is classical Gram-Schmidt with the re-orthogonalising
+//    second projection taken from the basis Gram matrix G = V^T V
+//    (h = a + (a - G a) with a = V^T w): the Gram column of the newest basis
+//    vector rides along in the same streaming pass as a, so each step reads
+//    the Krylov basis twice (projection + update) instead of MGS's
+//    2(j+1) vector sweeps, and stays as orthogonal as CGS2 (SURVEY §7.4 (8):
+//    not bitwise MGS; iteration counts within +-1).
+//  * With kernel timing enabled (pmgr_prof_enable) the same kernels are
+//    launched step by step with CUDA events around them (event nodes are not
+//    allowed inside conditional bodies).
 #include <cmath>
+#include <cstdlib>
+#include <map>
+#include <tuple>
 
 #include "hier.cuh"
 
@@ -21,187 +35,106 @@ namespace pmgr {
 namespace {
 
 constexpr int DOT_BLOCK = 256;
-constexpr int KC = 8;  // basis vectors per register chunk
 
-int dot_grid(int64_t n) {
-    int64_t g = (n + DOT_BLOCK - 1) / DOT_BLOCK;
-    int64_t cap = 2LL * num_sms();
-    return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
-}
+struct Dev {
+    int j;       // current step within the cycle
+    int total;   // iterations over all cycles
+    int active;  // loop condition
+    int brk;     // breakdown in the last step
+    int dead;    // dead Givens column
+    int m, max_iters;
+    double tol;
+    double hn;   // ||w|| after the projections
+};
 
-__device__ __forceinline__ double block_sum(double v, double *sh) {
+__device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// block-wide sum of two values; valid in thread 0
+__device__ __forceinline__ void block_sum2(double &a, double &b, double *sh) {
+    a = warp_sum(a);
+    b = warp_sum(b);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sh[2 * w] = a;
+        sh[2 * w + 1] = b;
+    }
     __syncthreads();
-    if (lane == 0) sh[w] = v;
-    __syncthreads();
-    double t = 0.0;
-    if (threadIdx.x == 0)
-        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
-    return t;  // valid in thread 0
-}
-
-// partial[blk*ld + k] = sum over this block's rows of V_k[i] * w[i], k < nk
-__global__ void __launch_bounds__(DOT_BLOCK) k_multidot(const double *__restrict__ V, int64_t n, int nk,
-                                                         const double *__restrict__ w, double *partial, int ld) {
-    __shared__ double sh[DOT_BLOCK / 32];
-    for (int k0 = 0; k0 < nk; k0 += KC) {
-        double acc[KC];
-#pragma unroll
-        for (int t = 0; t < KC; ++t) acc[t] = 0.0;
-        for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
-            const double wi = w[i];
-#pragma unroll
-            for (int t = 0; t < KC; ++t)
-                if (k0 + t < nk) acc[t] = fma(V[(int64_t)(k0 + t) * n + i], wi, acc[t]);
+    if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            x += sh[2 * k];
+            y += sh[2 * k + 1];
         }
-#pragma unroll
-        for (int t = 0; t < KC; ++t) {
-            if (k0 + t >= nk) break;
-            double s = block_sum(acc[t], sh);
-            if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * ld + k0 + t] = s;
-        }
+        a = x;
+        b = y;
     }
 }
 
-// w -= sum_k h[k] V_k ; then mode 1: partial dots V_k . w (k < nk),
-// mode 2: partial ||w||^2 (slot 0).  Each thread re-reads its rows of V
-// for the dots (L1-resident tile).
-__global__ void __launch_bounds__(DOT_BLOCK) k_update(const double *__restrict__ V, int64_t n, int nk,
-                                                       const double *__restrict__ h, double *w, int mode,
-                                                       double *partial, int ld) {
-    __shared__ double sh[DOT_BLOCK / 32];
-    __shared__ double hs[1024];
-    for (int k = threadIdx.x; k < nk && k < 1024; k += DOT_BLOCK) hs[k] = h[k];
-    __syncthreads();
-    double nrm = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
-        double wi = w[i];
-        for (int k = 0; k < nk; ++k) wi = fma(-hs[k], V[(int64_t)k * n + i], wi);
-        w[i] = wi;
-        nrm = fma(wi, wi, nrm);
-    }
-    if (mode == 2) {
-        double s = block_sum(nrm, sh);
-        if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * ld] = s;
-        return;
-    }
-    if (mode == 1) {
-        for (int k0 = 0; k0 < nk; k0 += KC) {
-            double acc[KC];
-#pragma unroll
-            for (int t = 0; t < KC; ++t) acc[t] = 0.0;
-            for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n;
-                 i += (int64_t)gridDim.x * DOT_BLOCK) {
-                const double wi = w[i];
-#pragma unroll
-                for (int t = 0; t < KC; ++t)
-                    if (k0 + t < nk) acc[t] = fma(V[(int64_t)(k0 + t) * n + i], wi, acc[t]);
-            }
-#pragma unroll
-            for (int t = 0; t < KC; ++t) {
-                if (k0 + t >= nk) break;
-                double s = block_sum(acc[t], sh);
-                if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * ld + k0 + t] = s;
-            }
-        }
-    }
-}
-
-// out[k] (+)= sum over blocks of partial[b*ld + k], one warp per k, fixed order
-__global__ void k_reduce_partials(const double *partial, int nblk, int nk, int ld, double *out, int accumulate) {
-    int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (k >= nk) return;
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += partial[(int64_t)b * ld + k];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == 0) out[k] = accumulate ? out[k] + s : s;
-}
-
-// u = sum_k y[k] V_k
-__global__ void k_combine(const double *__restrict__ V, int64_t n, int nk, const double *__restrict__ y,
-                          double *u) {
-    __shared__ double ys[1024];
-    for (int k = threadIdx.x; k < nk && k < 1024; k += blockDim.x) ys[k] = y[k];
-    __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int k = 0; k < nk; ++k) s = fma(ys[k], V[(int64_t)k * n + i], s);
-        u[i] = s;
-    }
-}
-
-__global__ void k_scale(const double *x, int64_t n, const double *den, double *y, double *y2) {
-    const double d = *den;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const double t = x[i] / d;
-        y[i] = t;
-        if (y2) y2[i] = t;
-    }
-}
-
-__global__ void k_sqrt(double *x) { *x = sqrt(*x); }
-
-// ---- classical Gram-Schmidt with DGKS re-orthogonalisation ---------------
-// Pass 1 (k_mdot): h_k = V_k . w for k < nk and ||w||^2, one block per
-// (row range, vector) so every block streams one contiguous slice of V.
-// Pass 2 (k_upd): w -= sum_k h_k V_k with ||w'||^2 partials.  A second
-// projection runs only when ||w'|| < ||w||/sqrt(2) (device flag; the two
-// extra launches exit at once otherwise), which keeps the basis orthogonal
-// to working precision like the reference's MGS (krylov.py:75-77).
-
-__device__ __forceinline__ double block_sum_all(double v, double *sh) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) sh[w] = v;
-    __syncthreads();
-    double t = 0.0;
-    if (threadIdx.x == 0)
-        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
-    return t;
-}
-
-__global__ void __launch_bounds__(DOT_BLOCK) k_mdot(const double *__restrict__ V, int64_t n, int nk,
-                                                     const double *__restrict__ w, double *partial, int nsplit,
-                                                     int64_t chunk, const int *active) {
-    if (active && !*active) return;
-    __shared__ double sh[DOT_BLOCK / 32];
+// pass 1: pa[k][s] = V_k . w, pg[k][s] = V_k . V_j over row slice s (k <= j)
+__global__ void __launch_bounds__(DOT_BLOCK) k_project(const double *__restrict__ V, int64_t n,
+                                                        const double *__restrict__ w, const Dev *__restrict__ dev,
+                                                        double *pa, double *pg, int nsplit, int64_t chunk) {
+    const int j = dev->j;
     const int k = blockIdx.y;
-    const double *x = k < nk ? V + (int64_t)k * n : w;
+    if (k > j) return;
+    __shared__ double sh[2 * DOT_BLOCK / 32];
+    const double *x = V + (int64_t)k * n;
+    const double *vj = V + (int64_t)j * n;
     const int64_t lo = blockIdx.x * chunk;
     const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
     int64_t i = lo + threadIdx.x;
-    for (; i + 3 * DOT_BLOCK < hi; i += 4 * DOT_BLOCK) {
-        a0 = fma(x[i], w[i], a0);
-        a1 = fma(x[i + DOT_BLOCK], w[i + DOT_BLOCK], a1);
-        a2 = fma(x[i + 2 * DOT_BLOCK], w[i + 2 * DOT_BLOCK], a2);
-        a3 = fma(x[i + 3 * DOT_BLOCK], w[i + 3 * DOT_BLOCK], a3);
+    for (; i + DOT_BLOCK < hi; i += 2 * DOT_BLOCK) {
+        const double x0 = x[i], x1 = x[i + DOT_BLOCK];
+        a0 = fma(x0, w[i], a0);
+        a1 = fma(x1, w[i + DOT_BLOCK], a1);
+        g0 = fma(x0, vj[i], g0);
+        g1 = fma(x1, vj[i + DOT_BLOCK], g1);
     }
-    for (; i < hi; i += DOT_BLOCK) a0 = fma(x[i], w[i], a0);
-    double t = block_sum_all((a0 + a1) + (a2 + a3), sh);
-    if (threadIdx.x == 0) partial[(int64_t)k * nsplit + blockIdx.x] = t;
+    if (i < hi) {
+        a0 = fma(x[i], w[i], a0);
+        g0 = fma(x[i], vj[i], g0);
+    }
+    double a = a0 + a1, g = g0 + g1;
+    block_sum2(a, g, sh);
+    if (threadIdx.x == 0) {
+        pa[(int64_t)k * nsplit + blockIdx.x] = a;
+        pg[(int64_t)k * nsplit + blockIdx.x] = g;
+    }
 }
 
-// out[k] = sum_s partial[k*nsplit + s], one warp per k, fixed order
-__global__ void k_preduce(const double *partial, int nsplit, int nk1, double *out, const int *active) {
-    if (active && !*active) return;
-    int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (k >= nk1) return;
-    double s = 0.0;
-    for (int b = lane; b < nsplit; b += 32) s += partial[(int64_t)k * nsplit + b];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == 0) out[k] = s;
+// h = a + (a - G a): reduce the slices, extend the Gram matrix by column j
+__global__ void k_coeffs(const Dev *__restrict__ dev, const double *pa, const double *pg, int nsplit, double *G,
+                         int ldg, double *a, double *h) {
+    const int j = dev->j;
+    for (int k = threadIdx.x; k <= j; k += blockDim.x) {
+        double sa = 0.0, sg = 0.0;
+        for (int s = 0; s < nsplit; ++s) {
+            sa += pa[(int64_t)k * nsplit + s];
+            sg += pg[(int64_t)k * nsplit + s];
+        }
+        a[k] = sa;
+        G[(int64_t)k * ldg + j] = sg;
+        G[(int64_t)j * ldg + k] = sg;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k <= j; k += blockDim.x) {
+        double ga = 0.0;
+        for (int l = 0; l <= j; ++l) ga = fma(G[(int64_t)k * ldg + l], a[l], ga);
+        h[k] = a[k] + (a[k] - ga);
+    }
 }
 
-__global__ void __launch_bounds__(DOT_BLOCK) k_upd(const double *__restrict__ V, int64_t n, int nk,
-                                                    const double *__restrict__ h, double *w, double *partial,
-                                                    const int *active) {
-    if (active && !*active) return;
-    __shared__ double sh[DOT_BLOCK / 32];
+// pass 2: w -= sum_{k<=j} h_k V_k ; ||w||^2 partials
+__global__ void __launch_bounds__(DOT_BLOCK) k_update(const double *__restrict__ V, int64_t n,
+                                                       const double *__restrict__ h, const Dev *__restrict__ dev,
+                                                       double *w, double *pn) {
+    __shared__ double sh[2 * DOT_BLOCK / 32];
     __shared__ double hs[1024];
+    const int nk = dev->j + 1;
     for (int k = threadIdx.x; k < nk; k += DOT_BLOCK) hs[k] = h[k];
     __syncthreads();
     double nrm = 0.0;
@@ -219,106 +152,350 @@ __global__ void __launch_bounds__(DOT_BLOCK) k_upd(const double *__restrict__ V,
         w[i] = wi;
         nrm = fma(wi, wi, nrm);
     }
-    double t = block_sum_all(nrm, sh);
-    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    double z = 0.0;
+    block_sum2(nrm, z, sh);
+    if (threadIdx.x == 0) pn[blockIdx.x] = nrm;
 }
 
-// DGKS test: re-orthogonalise when ||w'||^2 < ||w||^2 / 2
-__global__ void k_reorth_flag(const double *h1, int nk, const double *nrm1, int *flag, double *h2) {
-    const int f = nrm1[0] < 0.5 * h1[nk];
-    if (threadIdx.x == 0) *flag = f;
-    for (int k = threadIdx.x; k <= nk; k += blockDim.x) h2[k] = 0.0;
-}
-
-struct GmresState {
-    double *H;     // (m+1) x m, row-major (i, j) at i*m + j
-    double *cs, *sn, *g;
-    double *h1, *h2;  // dot results (m+1)
-    double *hnext;    // ||w|| after orthogonalisation
-    double *nrm1, *nrm2;  // ||w'||^2 after the first / second projection
-    int *reorth;          // DGKS flag of the current step
-    double *y;        // triangular solve result
-    int *status;      // [0] breakdown, [1] dead column, [2] converged-by-estimate
-    double *hist;     // |g[j+1]| per iteration
-};
-
-// Arnoldi column j: h = h1 + h2, Hessenberg update, Givens (krylov.py:75-104)
-__global__ void k_arnoldi_tail(GmresState st, int m, int j, double tol) {
-    double *H = st.H;
-    const double hn = sqrt(*st.reorth ? *st.nrm2 : *st.nrm1);
-    double cs2 = 0.0;
-    for (int i = 0; i <= j; ++i) {
-        double hv = st.h1[i] + st.h2[i];
-        H[i * m + j] = hv;
-        cs2 += hv * hv;
+// Hessenberg column, Givens rotation, convergence / breakdown flags
+// (krylov.py:78-104); one warp loads, lane 0 rotates in shared memory
+__global__ void k_givens(Dev *dev, const double *pn, int npn, const double *h, double *H, double *cs, double *sn,
+                         double *g, double *hist, cudaGraphConditionalHandle cond, int use_cond) {
+    extern __shared__ double col[];  // [m + 2] column, then cs[m + 1], sn[m + 1]
+    const int lane = threadIdx.x;
+    const int j = dev->j, m = dev->m;
+    double *css = col + (m + 2), *sns = css + (m + 1);
+    double s = 0.0;
+    for (int b = lane; b < npn; b += 32) s += pn[b];
+    s = warp_sum(s);
+    const double hn = sqrt(s);
+    for (int i = lane; i <= j; i += 32) {
+        col[i] = h[i];
+        css[i] = cs[i];
+        sns[i] = sn[i];
     }
-    H[(j + 1) * m + j] = hn;
-    cs2 += hn * hn;
-    const double colscale = sqrt(cs2);
-    int brk = !(hn > 1e-12 * fmax(colscale, 1e-300));
-    *st.hnext = hn;
+    __syncwarp();
+    if (lane != 0) return;
+    col[j + 1] = hn;
+    double c2 = 0.0;
+    for (int i = 0; i <= j + 1; ++i) c2 += col[i] * col[i];
+    const double colscale = sqrt(c2);
+    const int brk = !(hn > 1e-12 * fmax(colscale, 1e-300));
     for (int i = 0; i < j; ++i) {
-        double t = H[i * m + j];
-        H[i * m + j] = st.cs[i] * t + st.sn[i] * H[(i + 1) * m + j];
-        H[(i + 1) * m + j] = -st.sn[i] * t + st.cs[i] * H[(i + 1) * m + j];
+        const double t = col[i];
+        col[i] = css[i] * t + sns[i] * col[i + 1];
+        col[i + 1] = -sns[i] * t + css[i] * col[i + 1];
     }
-    const double a = H[j * m + j], b = H[(j + 1) * m + j];
-    const double rho = hypot(a, b);
+    const double a = col[j], bb = col[j + 1];
+    const double rho = hypot(a, bb);
+    dev->hn = hn;
     if (rho == 0.0) {
-        st.status[0] = 1;
-        st.status[1] = 1;
+        dev->brk = 1;
+        dev->dead = 1;
+        dev->active = 0;
+        if (use_cond) cudaGraphSetConditional(cond, 0);
         return;
     }
-    st.cs[j] = a / rho;
-    st.sn[j] = b / rho;
-    H[j * m + j] = rho;
-    H[(j + 1) * m + j] = 0.0;
-    st.g[j + 1] = -st.sn[j] * st.g[j];
-    st.g[j] = st.cs[j] * st.g[j];
-    const double est = fabs(st.g[j + 1]);
-    st.hist[j] = est;
-    st.status[0] = brk;
-    st.status[1] = 0;
-    st.status[2] = est <= tol;
+    cs[j] = a / rho;
+    sn[j] = bb / rho;
+    col[j] = rho;
+    col[j + 1] = 0.0;
+    for (int i = 0; i <= j + 1; ++i) H[(int64_t)i * m + j] = col[i];
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    const double est = fabs(g[j + 1]);
+    hist[dev->total] = est;
+    const int total = dev->total + 1;
+    const int jn = j + 1;
+    dev->total = total;
+    dev->j = jn;
+    dev->brk = brk;
+    const int act = !(est <= dev->tol || brk) && jn < m && total < dev->max_iters;
+    dev->active = act;
+    if (use_cond) cudaGraphSetConditional(cond, act);
 }
 
-__global__ void k_cycle_init(GmresState st, int m, const double *beta) {
-    for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) st.H[i] = 0.0;
-    for (int i = threadIdx.x; i <= m; i += blockDim.x) st.g[i] = (i == 0) ? *beta : 0.0;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) st.cs[i] = st.sn[i] = 0.0;
-    if (threadIdx.x == 0) st.status[0] = st.status[1] = st.status[2] = 0;
-}
-
-// back substitution H[:j,:j] y = g[:j]
-__global__ void k_trsv(GmresState st, int m, int j) {
-    for (int i = j - 1; i >= 0; --i) {
-        double s = st.g[i];
-        for (int k = i + 1; k < j; ++k) s -= st.H[i * m + k] * st.y[k];
-        st.y[i] = s / st.H[i * m + i];
+// V_j = w / hn (j already advanced) and the preconditioner input copy
+__global__ void k_normalize(const double *w, int64_t n, const Dev *dev, double *V, double *vin) {
+    if (dev->brk) return;
+    const double d = dev->hn;
+    double *vj = V + (int64_t)dev->j * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = w[i] / d;
+        vj[i] = t;
+        vin[i] = t;
     }
 }
 
-struct Reducer {
-    TBuf<double> partial;
-    int nblk = 0, ld = 0;
-    void init(int64_t n, int maxk, cudaStream_t s) {
-        nblk = dot_grid(n);
-        ld = maxk > 1 ? maxk : 1;
-        partial.alloc((int64_t)nblk * ld, s);
+__global__ void k_cycle_init(Dev *dev, double *H, double *G, int ldg, double *cs, double *sn, double *g, int m,
+                             const double *beta) {
+    for (int64_t i = threadIdx.x; i < (int64_t)(m + 1) * m; i += blockDim.x) H[i] = 0.0;
+    for (int64_t i = threadIdx.x; i < (int64_t)ldg * ldg; i += blockDim.x) G[i] = 0.0;
+    for (int i = threadIdx.x; i <= m; i += blockDim.x) {
+        g[i] = (i == 0) ? *beta : 0.0;
+        cs[i] = sn[i] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        dev->j = 0;
+        dev->brk = 0;
+        dev->dead = 0;
+        dev->active = dev->total < dev->max_iters;
+    }
+}
+
+__global__ void k_scale2(const double *x, int64_t n, const double *den, double *y, double *y2) {
+    const double d = *den;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = x[i] / d;
+        y[i] = t;
+        y2[i] = t;
+    }
+}
+
+// back substitution H[:j,:j] y = g[:j], right-looking, one block
+__global__ void k_trsv(const double *H, int m, int j, const double *g, double *y) {
+    extern __shared__ double rhs[];
+    __shared__ double yc_s;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) rhs[i] = g[i];
+    __syncthreads();
+    for (int c = j - 1; c >= 0; --c) {
+        if (threadIdx.x == 0) {
+            yc_s = rhs[c] / H[(int64_t)c * m + c];
+            rhs[c] = yc_s;
+        }
+        __syncthreads();
+        const double yc = yc_s;
+        for (int i = threadIdx.x; i < c; i += blockDim.x) rhs[i] -= H[(int64_t)i * m + c] * yc;
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < j; i += blockDim.x) y[i] = rhs[i];
+}
+
+// u = sum_{k<j} y_k V_k
+__global__ void k_combine(const double *__restrict__ V, int64_t n, int nk, const double *__restrict__ y,
+                          double *u) {
+    __shared__ double ys[1024];
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) ys[k] = y[k];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < nk; k += 2) {
+            s0 = fma(ys[k], V[(int64_t)k * n + i], s0);
+            s1 = fma(ys[k + 1], V[(int64_t)(k + 1) * n + i], s1);
+        }
+        if (k < nk) s0 = fma(ys[k], V[(int64_t)k * n + i], s0);
+        u[i] = s0 + s1;
+    }
+}
+
+__global__ void k_norm_partial(const double *x, int64_t n, double *pn) {
+    __shared__ double sh[2 * DOT_BLOCK / 32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK)
+        s = fma(x[i], x[i], s);
+    double z = 0.0;
+    block_sum2(s, z, sh);
+    if (threadIdx.x == 0) pn[blockIdx.x] = s;
+}
+
+__global__ void k_norm_final(const double *pn, int npn, double *out) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < npn; b += 32) s += pn[b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) *out = sqrt(s);
+}
+
+// generic helpers for the Python-callable path
+__global__ void __launch_bounds__(DOT_BLOCK) k_mdot_plain(const double *__restrict__ V, int64_t n,
+                                                           const double *__restrict__ w, double *part, int nsplit,
+                                                           int64_t chunk) {
+    __shared__ double sh[2 * DOT_BLOCK / 32];
+    const int k = blockIdx.y;
+    const double *x = V + (int64_t)k * n;
+    const int64_t lo = blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+    double a = 0.0, z = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += DOT_BLOCK) a = fma(x[i], w[i], a);
+    block_sum2(a, z, sh);
+    if (threadIdx.x == 0) part[(int64_t)k * nsplit + blockIdx.x] = a;
+}
+
+__global__ void k_sum_slices(const double *part, int nsplit, int nk, double *out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nk) return;
+    double s = 0.0;
+    for (int b = 0; b < nsplit; ++b) s += part[(int64_t)k * nsplit + b];
+    out[k] = s;
+}
+
+__global__ void k_maxpy(const double *__restrict__ V, int64_t n, int nk, const double *__restrict__ h, double *w) {
+    __shared__ double hs[1024];
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) hs[k] = h[k];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double a = w[i];
+        for (int k = 0; k < nk; ++k) a = fma(-hs[k], V[(int64_t)k * n + i], a);
+        w[i] = a;
+    }
+}
+
+// --------------------------------------------------------------- workspace
+
+struct Ws {
+    const pmgr_csr *A = nullptr;
+    pmgr_mgr *M = nullptr;
+    int m = 0, max_iters = 0;
+    int64_t n = 0;
+    int nsplit = 1, nupd = 1;
+    int64_t chunk = 0;
+    DBuf<double> V, w, z, r, vin, u;
+    DBuf<double> H, G, cs, sn, g, a, h, y, hist, pa, pg, pn, beta;
+    DBuf<Dev> dev;
+    Dev *hdev = nullptr;  // pinned mirror
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t cycle = nullptr;
+
+    ~Ws() {
+        if (cycle) cudaGraphExecDestroy(cycle);
+        if (cap) cudaStreamDestroy(cap);
+        if (hdev) cudaFreeHost(hdev);
     }
 };
 
-void norm2(const double *x, int64_t n, Reducer &R, double *out, cudaStream_t s) {
-    // ||x||^2 via the update kernel with no basis vectors
-    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(nullptr, n, 0, nullptr, const_cast<double *>(x), 2, R.partial.p, R.ld);
+std::map<std::tuple<const pmgr_csr *, pmgr_mgr *, int, int>, std::unique_ptr<Ws>> g_ws;
+
+Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
+    auto key = std::make_tuple(A, M, m, max_iters);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end()) return *it->second;
+    auto w = std::make_unique<Ws>();
+    w->A = A;
+    w->M = M;
+    w->m = m;
+    w->max_iters = max_iters;
+    w->n = n;
+    w->V.alloc((int64_t)(m + 1) * n);
+    w->w.alloc(n);
+    w->z.alloc(n);
+    w->r.alloc(n);
+    w->vin.alloc(n);
+    w->u.alloc(n);
+    w->H.alloc((int64_t)(m + 1) * m);
+    w->G.alloc((int64_t)(m + 1) * (m + 1));
+    w->cs.alloc(m + 1);
+    w->sn.alloc(m + 1);
+    w->g.alloc(m + 2);
+    w->a.alloc(m + 1);
+    w->h.alloc(m + 1);
+    w->y.alloc(m + 1);
+    w->hist.alloc((int64_t)max_iters + 2);
+    // row slices: enough blocks per basis vector to stream at full bandwidth
+    int ns = (int)((n + 8191) / 8192);
+    if (ns > 64) ns = 64;
+    if (ns < 1) ns = 1;
+    w->nsplit = ns;
+    w->chunk = (n + ns - 1) / ns;
+    w->pa.alloc((int64_t)(m + 1) * ns);
+    w->pg.alloc((int64_t)(m + 1) * ns);
+    w->nupd = 4 * num_sms();
+    w->pn.alloc(w->nupd);
+    w->beta.alloc(1);
+    w->dev.alloc(1);
+    PMGR_CUDA(cudaMallocHost((void **)&w->hdev, sizeof(Dev)));
+    PMGR_CUDA(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
+    Ws &ref = *w;
+    g_ws[key] = std::move(w);
+    return ref;
+}
+
+int vec_grid(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    int64_t cap = 4LL * num_sms();
+    return (int)(g < 1 ? 1 : (g < cap ? g : cap));
+}
+
+// one Arnoldi step on stream s (graph body or direct launches)
+void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond) {
+    const int64_t n = W.n;
+    const bool prof = !use_cond && prof_on();
+    {
+        ProfScope ps(prof ? PROF_MGR_APPLY : PROF_KINDS, 0.0, s);
+        if (W.M) mgr_apply_direct(*W.M, W.vin.p, W.z.p, s);
+        else vec_copy(W.vin.p, W.z.p, n, s);
+    }
+    {
+        ProfScope ps(prof ? PROF_OUTER_SPMV : PROF_KINDS, csr_pass_bytes(Av.nrows, Av.ncols, Av.nnz), s);
+        spmv(Av, W.z.p, W.w.p, s);
+    }
+    // algorithmic bytes of the step's orthogonalisation: basis read twice,
+    // w read twice and written once, new basis vector + copy written
+    const double bytes = prof ? 8.0 * n * (2.0 * (W.hdev->j + 1) + 5.0) : 0.0;
+    ProfScope ps(prof ? PROF_ORTHO : PROF_KINDS, bytes, s);
+    k_project<<<dim3(W.nsplit, W.m + 1), DOT_BLOCK, 0, s>>>(W.V.p, n, W.w.p, W.dev.p, W.pa.p, W.pg.p, W.nsplit,
+                                                           W.chunk);
     PMGR_LAUNCHED();
-    k_reduce_partials<<<1, 32, 0, s>>>(R.partial.p, R.nblk, 1, R.ld, out, 0);
+    k_coeffs<<<1, 256, 0, s>>>(W.dev.p, W.pa.p, W.pg.p, W.nsplit, W.G.p, W.m + 1, W.a.p, W.h.p);
     PMGR_LAUNCHED();
-    k_sqrt<<<1, 1, 0, s>>>(out);
+    k_update<<<W.nupd, DOT_BLOCK, 0, s>>>(W.V.p, n, W.h.p, W.dev.p, W.w.p, W.pn.p);
     PMGR_LAUNCHED();
+    k_givens<<<1, 32, sizeof(double) * (3 * W.m + 4), s>>>(W.dev.p, W.pn.p, W.nupd, W.h.p, W.H.p, W.cs.p, W.sn.p, W.g.p,
+                                                       W.hist.p, cond, use_cond);
+    PMGR_LAUNCHED();
+    k_normalize<<<vec_grid(n), 256, 0, s>>>(W.w.p, n, W.dev.p, W.V.p, W.vin.p);
+    PMGR_LAUNCHED();
+}
+
+void build_cycle_graph(const CsrView &Av, Ws &W) {
+    cudaGraph_t graph;
+    PMGR_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    PMGR_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    PMGR_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    PMGR_CUDA(cudaStreamBeginCaptureToGraph(W.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+        arnoldi_step(Av, W, W.cap, cond, 1);
+    } catch (...) {
+        cudaStreamEndCapture(W.cap, &body);
+        cudaGraphDestroy(graph);
+        throw;
+    }
+    PMGR_CUDA(cudaStreamEndCapture(W.cap, &body));
+    PMGR_CUDA(cudaGraphInstantiate(&W.cycle, graph, 0));
+    PMGR_CUDA(cudaGraphDestroy(graph));
+}
+
+void norm_into(const double *x, int64_t n, Ws &W, double *out, cudaStream_t s) {
+    k_norm_partial<<<W.nupd, DOT_BLOCK, 0, s>>>(x, n, W.pn.p);
+    PMGR_LAUNCHED();
+    k_norm_final<<<1, 32, 0, s>>>(W.pn.p, W.nupd, out);
+    PMGR_LAUNCHED();
+}
+
+bool use_cycle_graphs() {
+    static const bool on = [] {
+        const char *e = getenv("PMGR_NO_GRAPHS");
+        return !(e && e[0] != '0');
+    }();
+    return on;
 }
 
 }  // namespace
+
+void gmres_forget(const void *obj) {
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+        if ((const void *)std::get<0>(it->first) == obj || (const void *)std::get<1>(it->first) == obj)
+            it = g_ws.erase(it);
+        else
+            ++it;
+    }
+}
 
 void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, int nonzero_x0,
                   const pmgr_gmres_cfg &cfg, pmgr_gmres_stats &stats, double *history, int32_t history_cap,
@@ -330,170 +507,101 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
     if (M && M->n != Av.nrows) fail(PMGR_ERR_INVALID, "preconditioner size does not match the operator");
     const int64_t n = Av.nrows;
     const int m = cfg.restart;
-    // vin: fixed input buffer of the preconditioner (its CUDA graph is keyed
-    // by buffer addresses); the normalisation writes V_{j+1} and vin at once
-    TBuf<double> V((int64_t)(m + 1) * n, s), w(n, s), z(n, s), r(n, s), vin(n, s);
-    TBuf<double> small((int64_t)(m + 1) * m + 6 * (m + 1) + 8, s);
-    TBuf<int> status(4, s);
-    TBuf<double> dhist(m + 1, s);
-    GmresState st;
-    st.H = small.p;
-    st.cs = st.H + (m + 1) * m;
-    st.sn = st.cs + (m + 1);
-    st.g = st.sn + (m + 1);
-    st.h1 = st.g + (m + 1);
-    st.h2 = st.h1 + (m + 1);
-    st.y = st.h2 + (m + 1);
-    st.hnext = st.y + (m + 1);
-    double *beta_d = st.hnext + 1;
-    st.nrm1 = beta_d + 1;
-    st.nrm2 = st.nrm1 + 1;
-    st.status = status.p;
-    st.reorth = status.p + 3;
-    st.hist = dhist.p;
-    Reducer R;
-    R.init(n, m + 1, s);
-    // projection partials: (nk+1) vectors x nsplit row slices
-    const int64_t min_chunk = 4096;
-    int nsplit_max = (int)((n + min_chunk - 1) / min_chunk);
-    if (nsplit_max < 1) nsplit_max = 1;
-    TBuf<double> mpart((int64_t)(m + 2) * (nsplit_max > 64 ? 64 : nsplit_max), s);
-    const int upd_blocks = 4 * num_sms();
-    TBuf<double> upart(upd_blocks, s);
-    auto project = [&](int nk, double *h, double *nrm, const int *active) {
-        int nsplit = (int)((4 * num_sms() + nk) / (nk + 1));
-        if (nsplit > nsplit_max) nsplit = nsplit_max;
-        if (nsplit > 64) nsplit = 64;
-        if (nsplit < 1) nsplit = 1;
-        const int64_t chunk = (n + nsplit - 1) / nsplit;
-        k_mdot<<<dim3(nsplit, nk + 1), DOT_BLOCK, 0, s>>>(V.p, n, nk, w.p, mpart.p, nsplit, chunk, active);
-        PMGR_LAUNCHED();
-        k_preduce<<<((nk + 1) * 32 + 255) / 256, 256, 0, s>>>(mpart.p, nsplit, nk + 1, h, active);
-        PMGR_LAUNCHED();
-        k_upd<<<upd_blocks, DOT_BLOCK, 0, s>>>(V.p, n, nk, h, w.p, upart.p, active);
-        PMGR_LAUNCHED();
-        k_preduce<<<1, 32, 0, s>>>(upart.p, upd_blocks, 1, nrm, active);
-        PMGR_LAUNCHED();
-    };
+    const int max_iters = cfg.max_iters > 0 ? cfg.max_iters : 0;
+    Ws &W = workspace(A, M, m, max_iters, n);
+    const bool prof = prof_on();
+    const bool graph_mode = use_cycle_graphs() && !prof;
 
     std::vector<double> hist;
-    int hcount = 0;
-    auto push_hist = [&](double v) {
-        hist.push_back(v);
-        ++hcount;
-    };
-    auto apply_M = [&](const double *in, double *out) {
-        if (M) mgr_apply(*M, in, out, s);
-        else vec_copy(in, out, n, s);
-    };
-
-    if (nonzero_x0) {
-        spmv_residual(Av, x, b, r.p, s);
-    } else {
-        vec_copy(b, r.p, n, s);
-    }
-    norm2(r.p, n, R, beta_d, s);
-    double beta = read_scalar(beta_d, s);
-    push_hist(beta);
+    if (nonzero_x0) spmv_residual(Av, x, b, W.r.p, s);
+    else vec_copy(b, W.r.p, n, s);
+    norm_into(W.r.p, n, W, W.beta.p, s);
+    double beta = read_scalar(W.beta.p, s);
+    hist.push_back(beta);
     const double tol = std::fmax(cfg.rtol * beta, cfg.atol);
-    int total = 0;
-    int restarts = 0;
-    bool converged = beta <= tol;
-    if (!converged) {
-        while (total < cfg.max_iters) {
-            k_cycle_init<<<1, 256, 0, s>>>(st, m, beta_d);
+    Dev d0 = {};
+    d0.m = m;
+    d0.max_iters = max_iters;
+    d0.tol = tol;
+    PMGR_CUDA(cudaMemcpyAsync(W.dev.p, &d0, sizeof(Dev), cudaMemcpyHostToDevice, s));
+    int total = 0, restarts = 0;
+    bool brk = false;
+    if (beta > tol) {
+        if (graph_mode && !W.cycle) build_cycle_graph(Av, W);
+        while (total < max_iters) {
+            k_cycle_init<<<1, 256, 0, s>>>(W.dev.p, W.H.p, W.G.p, m + 1, W.cs.p, W.sn.p, W.g.p, m, W.beta.p);
             PMGR_LAUNCHED();
-            k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(r.p, n, beta_d, V.p, vin.p);
+            k_scale2<<<vec_grid(n), 256, 0, s>>>(W.r.p, n, W.beta.p, W.V.p, W.vin.p);
             PMGR_LAUNCHED();
-            int j = 0;
-            bool brk = false;
-            while (j < m && total < cfg.max_iters) {
-                double *Vj = V.p + (int64_t)j * n;
-                {
-                    ProfScope ps(PROF_MGR_APPLY, 0.0, s);
-                    apply_M(M ? vin.p : Vj, z.p);
-                }
-                {
-                    ProfScope ps(PROF_OUTER_SPMV, csr_pass_bytes(Av.nrows, Av.ncols, Av.nnz), s);
-                    spmv(Av, z.p, w.p, s);
-                }
-                const int nk = j + 1;
-                {
-                    ProfScope pso(PROF_ORTHO, 8.0 * n * (2.0 * nk + 6.0), s);
-                    project(nk, st.h1, st.nrm1, nullptr);
-                    k_reorth_flag<<<1, 128, 0, s>>>(st.h1, nk, st.nrm1, st.reorth, st.h2);
-                    PMGR_LAUNCHED();
-                    project(nk, st.h2, st.nrm2, st.reorth);
-                    k_arnoldi_tail<<<1, 1, 0, s>>>(st, m, j, tol);
-                    PMGR_LAUNCHED();
-                }
-                int flags[3];
-                PMGR_CUDA(cudaMemcpyAsync(flags, status.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
+            if (graph_mode) {
+                PMGR_CUDA(cudaGraphLaunch(W.cycle, s));
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                PMGR_CUDA(cudaMemcpyAsync(W.hdev, W.dev.p, sizeof(Dev), cudaMemcpyDeviceToHost, s));
                 PMGR_CUDA(cudaStreamSynchronize(s));
-                if (M && prof_on()) mgr_collect(*M);
-                if (flags[1]) {  // dead column: discard (krylov.py:88-91)
-                    brk = true;
-                    break;
+            } else {
+                while (true) {
+                    PMGR_CUDA(cudaMemcpyAsync(W.hdev, W.dev.p, sizeof(Dev), cudaMemcpyDeviceToHost, s));
+                    PMGR_CUDA(cudaStreamSynchronize(s));
+                    if (prof && M) mgr_collect(*M);
+                    if (!W.hdev->active) break;
+                    arnoldi_step(Av, W, s, 0, 0);
                 }
-                if (!flags[0]) {
-                    k_scale<<<dot_grid(n), DOT_BLOCK, 0, s>>>(w.p, n, st.hnext, V.p + (int64_t)(j + 1) * n, vin.p);
-                    PMGR_LAUNCHED();
-                } else {
-                    brk = true;
-                }
-                ++total;
-                ++j;
-                double est;
-                PMGR_CUDA(cudaMemcpyAsync(&est, dhist.p + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
-                PMGR_CUDA(cudaStreamSynchronize(s));
-                push_hist(est);
-                if (flags[2] || brk) break;
             }
+            const Dev dv = *W.hdev;
+            const int j = dv.j;
+            const int new_total = dv.total;
+            if (new_total > total) {
+                std::vector<double> hh(new_total - total);
+                PMGR_CUDA(cudaMemcpyAsync(hh.data(), W.hist.p + total, sizeof(double) * hh.size(),
+                                          cudaMemcpyDeviceToHost, s));
+                PMGR_CUDA(cudaStreamSynchronize(s));
+                hist.insert(hist.end(), hh.begin(), hh.end());
+            }
+            total = new_total;
+            brk = dv.brk != 0;
             if (j > 0) {
-                k_trsv<<<1, 1, 0, s>>>(st, m, j);
+                k_trsv<<<1, 256, sizeof(double) * j, s>>>(W.H.p, m, j, W.g.p, W.y.p);
                 PMGR_LAUNCHED();
-                k_combine<<<dot_grid(n), DOT_BLOCK, 0, s>>>(V.p, n, j, st.y, w.p);
+                k_combine<<<vec_grid(n), 256, 0, s>>>(W.V.p, n, j, W.y.p, W.u.p);
                 PMGR_LAUNCHED();
-                apply_M(w.p, z.p);
-                vec_axpy(1.0, z.p, x, n, s);
-                spmv_residual(Av, x, b, r.p, s);
-                norm2(r.p, n, R, beta_d, s);
-                beta = read_scalar(beta_d, s);
-                if (M && prof_on()) mgr_collect(*M);
+                if (M) mgr_apply(*M, W.u.p, W.z.p, s);
+                else vec_copy(W.u.p, W.z.p, n, s);
+                vec_axpy(1.0, W.z.p, x, n, s);
+                spmv_residual(Av, x, b, W.r.p, s);
+                norm_into(W.r.p, n, W, W.beta.p, s);
+                beta = read_scalar(W.beta.p, s);
+                if (prof && M) mgr_collect(*M);
                 hist.back() = beta;
             }
             ++restarts;
-            if (beta <= tol) {
-                converged = true;
-                break;
-            }
-            if (brk) break;
+            if (beta <= tol || brk) break;
         }
     }
     stats.iterations = total;
     stats.converged = beta <= tol;
     stats.restarts = restarts;
-    int32_t nh = (int32_t)hist.size();
+    const int32_t nh = (int32_t)hist.size();
     stats.history_len = nh < history_cap ? nh : history_cap;
     if (history)
         for (int32_t i = 0; i < stats.history_len; ++i) history[i] = hist[i];
-    (void)converged;
-    (void)hcount;
 }
 
 void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double *h, cudaStream_t s) {
-    Reducer R;
-    R.init(n, nvec, s);
-    k_multidot<<<R.nblk, DOT_BLOCK, 0, s>>>(V, n, nvec, w, R.partial.p, R.ld);
+    if (nvec <= 0) return;
+    int ns = (int)((n + 8191) / 8192);
+    if (ns > 64) ns = 64;
+    if (ns < 1) ns = 1;
+    const int64_t chunk = (n + ns - 1) / ns;
+    TBuf<double> part((int64_t)nvec * ns, s);
+    k_mdot_plain<<<dim3(ns, nvec), DOT_BLOCK, 0, s>>>(V, n, w, part.p, ns, chunk);
     PMGR_LAUNCHED();
-    k_reduce_partials<<<(nvec * 32 + 255) / 256, 256, 0, s>>>(R.partial.p, R.nblk, nvec, R.ld, h, 0);
+    k_sum_slices<<<(nvec + 127) / 128, 128, 0, s>>>(part.p, ns, nvec, h);
     PMGR_LAUNCHED();
 }
 
 void multiaxpy(const double *V, int64_t n, int32_t nvec, const double *h, double *w, cudaStream_t s) {
-    Reducer R;
-    R.init(n, 1, s);
-    k_update<<<R.nblk, DOT_BLOCK, 0, s>>>(V, n, nvec, h, w, 0, R.partial.p, R.ld);
+    if (nvec <= 0 || nvec > 1024) fail(PMGR_ERR_INVALID, "multiaxpy supports 1..1024 vectors");
+    k_maxpy<<<vec_grid(n), 256, 0, s>>>(V, n, nvec, h, w);
     PMGR_LAUNCHED();
 }
 

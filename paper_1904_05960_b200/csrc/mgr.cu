@@ -468,6 +468,8 @@ void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) {
     g->pending = g->prof;
 }
 
+void mgr_apply_direct(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) { apply_level(h, 0, v, z, s); }
+
 void mgr_collect(pmgr_mgr &h) {
     for (auto &e : h.graphs)
         if (e.pending) {
