@@ -50,11 +50,15 @@ struct Error {
     } while (0)
 
 extern std::atomic<int64_t> g_launches;
+// while a graph is being captured, launches are counted into the graph's
+// kernel count instead (and charged to g_launches per replay)
+extern thread_local int64_t *g_capture_count;
 
 // Count + check a kernel launch issued just before.
 #define PMGR_LAUNCHED()                                                                \
     do {                                                                               \
-        ::pmgr::g_launches.fetch_add(1, std::memory_order_relaxed);                   \
+        if (::pmgr::g_capture_count) ++*::pmgr::g_capture_count;                       \
+        else ::pmgr::g_launches.fetch_add(1, std::memory_order_relaxed);              \
         cudaError_t e_ = cudaPeekAtLastError();                                        \
         if (e_ != cudaSuccess) ::pmgr::fail_cuda(e_, "kernel launch", __FILE__, __LINE__); \
     } while (0)

@@ -82,6 +82,7 @@ struct ApplyGraph {
     bool pending = false;            // launched, events not yet collected
     std::vector<ProfRec> recs;
     uint64_t last_use = 0;
+    int64_t kernels = 0;             // kernels per replay
 };
 }  // namespace pmgr
 

@@ -354,6 +354,7 @@ struct Ws {
     Dev *hdev = nullptr;  // pinned mirror
     cudaStream_t cap = nullptr;
     cudaGraphExec_t cycle = nullptr;
+    int64_t body_kernels = 0;  // kernels per Arnoldi step in the WHILE body
 
     ~Ws() {
         if (cycle) cudaGraphExecDestroy(cycle);
@@ -459,9 +460,13 @@ void build_cycle_graph(const CsrView &Av, Ws &W) {
     PMGR_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
     cudaGraph_t body = np.conditional.phGraph_out[0];
     PMGR_CUDA(cudaStreamBeginCaptureToGraph(W.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    W.body_kernels = 0;
+    g_capture_count = &W.body_kernels;
     try {
         arnoldi_step(Av, W, W.cap, cond, 1);
+        g_capture_count = nullptr;
     } catch (...) {
+        g_capture_count = nullptr;
         cudaStreamEndCapture(W.cap, &body);
         cudaGraphDestroy(graph);
         throw;
@@ -535,9 +540,10 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
             PMGR_LAUNCHED();
             if (graph_mode) {
                 PMGR_CUDA(cudaGraphLaunch(W.cycle, s));
-                g_launches.fetch_add(1, std::memory_order_relaxed);
                 PMGR_CUDA(cudaMemcpyAsync(W.hdev, W.dev.p, sizeof(Dev), cudaMemcpyDeviceToHost, s));
                 PMGR_CUDA(cudaStreamSynchronize(s));
+                g_launches.fetch_add(W.body_kernels * (W.hdev->total - total + (W.hdev->dead ? 1 : 0)),
+                                     std::memory_order_relaxed);
             } else {
                 while (true) {
                     PMGR_CUDA(cudaMemcpyAsync(W.hdev, W.dev.p, sizeof(Dev), cudaMemcpyDeviceToHost, s));

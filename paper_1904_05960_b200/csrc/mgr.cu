@@ -446,13 +446,16 @@ void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) {
         cudaGraph_t graph;
         PMGR_CUDA(cudaStreamBeginCapture(h.cap_stream, cudaStreamCaptureModeThreadLocal));
         if (prof) prof_capture_begin(&g->recs);
+        g_capture_count = &g->kernels;
         try {
             apply_level(h, 0, v, z, h.cap_stream);
         } catch (...) {
+            g_capture_count = nullptr;
             prof_capture_end();
             cudaStreamEndCapture(h.cap_stream, &graph);
             throw;
         }
+        g_capture_count = nullptr;
         prof_capture_end();
         PMGR_CUDA(cudaStreamEndCapture(h.cap_stream, &graph));
         PMGR_CUDA(cudaGraphInstantiate(&g->exec, graph, 0));
@@ -464,7 +467,7 @@ void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) {
     }
     g->last_use = ++h.tick;
     PMGR_CUDA(cudaGraphLaunch(g->exec, s));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    g_launches.fetch_add(g->kernels, std::memory_order_relaxed);
     g->pending = g->prof;
 }
 
