@@ -65,6 +65,31 @@ extern thread_local int64_t *g_capture_count;
 
 int num_sms();
 
+// Programmatic dependent launch (Hopper+): a kernel launched with
+// launch_pdl() may start while its predecessor drains; it must call
+// pdl_wait() before touching anything the predecessor writes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess) fail_cuda(e, "cudaLaunchKernelEx", __FILE__, __LINE__);
+}
+
 inline unsigned grid_for(int64_t threads_needed, int block) {
     int64_t g = (threads_needed + block - 1) / block;
     if (g < 1) g = 1;

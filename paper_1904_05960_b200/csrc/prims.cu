@@ -1,4 +1,5 @@
 // prims.cu -- scans, segmented sorts and reductions (CUB device primitives).
+#include <cstdlib>
 #include <cstring>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -106,6 +107,14 @@ void prof_query(int kind, int64_t *count, double *ms, double *bytes) {
     *count = g_count[kind];
     *ms = g_ms[kind];
     *bytes = g_bytes[kind];
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("PMGR_NO_PDL");
+        return !(e && e[0] != '0');
+    }();
+    return on;
 }
 
 int num_sms() {

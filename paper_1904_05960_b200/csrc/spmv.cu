@@ -34,7 +34,9 @@ __device__ __forceinline__ int ldc(const int32_t *p) {
 template <int G, bool STREAM, class Op>
 __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
                                               const int32_t *__restrict__ ci,
-                                              const double *__restrict__ v, Op op) {
+                                              const double *__restrict__ v, Op op, int trigger) {
+    pdl_wait();
+    if (trigger) pdl_trigger();
     const int lane = threadIdx.x & (G - 1);
     const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const bool active = row < nrows;
@@ -124,10 +126,14 @@ struct OpProlong {
 template <int G, class Op>
 void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
     const int block = 256;
+    const unsigned grid = grid_for(A.nrows * G, block);
+    // let the next kernel's launch overlap this one only when this grid is a
+    // single wave (its early blocks must not crowd out ours)
+    const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
     if (stream)
-        k_spmv<G, true, Op><<<grid_for(A.nrows * G, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+        launch_pdl(k_spmv<G, true, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
     else
-        k_spmv<G, false, Op><<<grid_for(A.nrows * G, block), block, 0, s>>>(A.nrows, A.ro, A.ci, A.v, op);
+        launch_pdl(k_spmv<G, false, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
 }
 
 template <class Op>
@@ -185,6 +191,7 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
 
 __global__ void k_dense_matvec(const double *__restrict__ M, int64_t n, const double *__restrict__ x,
                                double *__restrict__ y) {
+    pdl_wait();
     // one warp per row
     int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
@@ -197,24 +204,29 @@ __global__ void k_dense_matvec(const double *__restrict__ M, int64_t n, const do
 
 __global__ void k_gather(const double *__restrict__ src, const int64_t *__restrict__ idx, int64_t n,
                          double *__restrict__ dst) {
+    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) dst[i] = src[idx[i]];
 }
 __global__ void k_scale_gather(const double *__restrict__ src, const int64_t *__restrict__ idx,
                                const double *__restrict__ d, int64_t n, double *__restrict__ dst) {
+    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) dst[i] = d[i] * src[idx[i]];
 }
 __global__ void k_zero(double *x, int64_t n) {
+    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = 0.0;
 }
 __global__ void k_axpy(double a, const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) y[i] += a * x[i];
 }
 __global__ void k_mul(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ y,
                       int64_t n) {
+    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) y[i] = a[i] * b[i];
 }
@@ -245,6 +257,7 @@ void spmv_restrict_div(const CsrView &R, const double *r, const double *d, doubl
 namespace {
 __global__ void k_copy_div(const double *__restrict__ b, const double *__restrict__ d, int64_t n,
                            double *__restrict__ bo, double *__restrict__ xo) {
+    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
         double v = b[i];
@@ -256,7 +269,7 @@ __global__ void k_copy_div(const double *__restrict__ b, const double *__restric
 
 void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s) {
     if (n == 0) return;
-    k_copy_div<<<grid_for(n, 256), 256, 0, s>>>(b, d, n, bo, xo);
+    launch_pdl(k_copy_div, dim3(grid_for(n, 256)), dim3(256), 0, s, b, d, n, bo, xo);
     PMGR_LAUNCHED();
 }
 
@@ -284,26 +297,26 @@ void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const do
 
 void dense_matvec(const double *M, int64_t n, const double *x, double *y, cudaStream_t s) {
     if (n == 0) return;
-    k_dense_matvec<<<grid_for(n * 32, 256), 256, 0, s>>>(M, n, x, y);
+    launch_pdl(k_dense_matvec, dim3(grid_for(n * 32, 256)), dim3(256), 0, s, M, n, x, y);
     PMGR_LAUNCHED();
 }
 
 void vec_gather(const double *src, const int64_t *idx, int64_t n, double *dst, cudaStream_t s) {
     if (n == 0) return;
-    k_gather<<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst);
+    launch_pdl(k_gather, dim3(grid_for(n, 256)), dim3(256), 0, s, src, idx, n, dst);
     PMGR_LAUNCHED();
 }
 
 void vec_scale_gather(const double *src, const int64_t *idx, const double *d, int64_t n, double *dst,
                       cudaStream_t s) {
     if (n == 0) return;
-    k_scale_gather<<<grid_for(n, 256), 256, 0, s>>>(src, idx, d, n, dst);
+    launch_pdl(k_scale_gather, dim3(grid_for(n, 256)), dim3(256), 0, s, src, idx, d, n, dst);
     PMGR_LAUNCHED();
 }
 
 void vec_zero(double *x, int64_t n, cudaStream_t s) {
     if (n == 0) return;
-    k_zero<<<grid_for(n, 256), 256, 0, s>>>(x, n);
+    launch_pdl(k_zero, dim3(grid_for(n, 256)), dim3(256), 0, s, x, n);
     PMGR_LAUNCHED();
 }
 
@@ -314,13 +327,13 @@ void vec_copy(const double *x, double *y, int64_t n, cudaStream_t s) {
 
 void vec_axpy(double a, const double *x, double *y, int64_t n, cudaStream_t s) {
     if (n == 0) return;
-    k_axpy<<<grid_for(n, 256), 256, 0, s>>>(a, x, y, n);
+    launch_pdl(k_axpy, dim3(grid_for(n, 256)), dim3(256), 0, s, a, x, y, n);
     PMGR_LAUNCHED();
 }
 
 void vec_mul(const double *a, const double *b, double *y, int64_t n, cudaStream_t s) {
     if (n == 0) return;
-    k_mul<<<grid_for(n, 256), 256, 0, s>>>(a, b, y, n);
+    launch_pdl(k_mul, dim3(grid_for(n, 256)), dim3(256), 0, s, a, b, y, n);
     PMGR_LAUNCHED();
 }
 
