@@ -85,20 +85,26 @@ __global__ void __launch_bounds__(DOT_BLOCK) k_project(const double *__restrict_
     const double *vj = V + (int64_t)j * n;
     const int64_t lo = blockIdx.x * chunk;
     const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
     int64_t i = lo + threadIdx.x;
-    for (; i + DOT_BLOCK < hi; i += 2 * DOT_BLOCK) {
-        const double x0 = x[i], x1 = x[i + DOT_BLOCK];
-        a0 = fma(x0, w[i], a0);
-        a1 = fma(x1, w[i + DOT_BLOCK], a1);
-        g0 = fma(x0, vj[i], g0);
-        g1 = fma(x1, vj[i + DOT_BLOCK], g1);
+    for (; i + 3 * DOT_BLOCK < hi; i += 4 * DOT_BLOCK) {
+        const double x0 = x[i], x1 = x[i + DOT_BLOCK], x2 = x[i + 2 * DOT_BLOCK], x3 = x[i + 3 * DOT_BLOCK];
+        const double w0 = w[i], w1 = w[i + DOT_BLOCK], w2 = w[i + 2 * DOT_BLOCK], w3 = w[i + 3 * DOT_BLOCK];
+        const double v0 = vj[i], v1 = vj[i + DOT_BLOCK], v2 = vj[i + 2 * DOT_BLOCK], v3 = vj[i + 3 * DOT_BLOCK];
+        a0 = fma(x0, w0, a0);
+        a1 = fma(x1, w1, a1);
+        a2 = fma(x2, w2, a2);
+        a3 = fma(x3, w3, a3);
+        g0 = fma(x0, v0, g0);
+        g1 = fma(x1, v1, g1);
+        g2 = fma(x2, v2, g2);
+        g3 = fma(x3, v3, g3);
     }
-    if (i < hi) {
+    for (; i < hi; i += DOT_BLOCK) {
         a0 = fma(x[i], w[i], a0);
         g0 = fma(x[i], vj[i], g0);
     }
-    double a = a0 + a1, g = g0 + g1;
+    double a = (a0 + a1) + (a2 + a3), g = (g0 + g1) + (g2 + g3);
     block_sum2(a, g, sh);
     if (threadIdx.x == 0) {
         pa[(int64_t)k * nsplit + blockIdx.x] = a;
@@ -139,16 +145,20 @@ __global__ void __launch_bounds__(DOT_BLOCK) k_update(const double *__restrict__
     __syncthreads();
     double nrm = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
-        double a0 = w[i], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        double acc[8];
+        acc[0] = w[i];
+#pragma unroll
+        for (int t = 1; t < 8; ++t) acc[t] = 0.0;
         int k = 0;
-        for (; k + 3 < nk; k += 4) {
-            a0 = fma(-hs[k], V[(int64_t)k * n + i], a0);
-            a1 = fma(-hs[k + 1], V[(int64_t)(k + 1) * n + i], a1);
-            a2 = fma(-hs[k + 2], V[(int64_t)(k + 2) * n + i], a2);
-            a3 = fma(-hs[k + 3], V[(int64_t)(k + 3) * n + i], a3);
+        for (; k + 7 < nk; k += 8) {
+            double vv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) vv[t] = V[(int64_t)(k + t) * n + i];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = fma(-hs[k + t], vv[t], acc[t]);
         }
-        for (; k < nk; ++k) a0 = fma(-hs[k], V[(int64_t)k * n + i], a0);
-        const double wi = (a0 + a1) + (a2 + a3);
+        for (; k < nk; ++k) acc[0] = fma(-hs[k], V[(int64_t)k * n + i], acc[0]);
+        const double wi = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         w[i] = wi;
         nrm = fma(wi, wi, nrm);
     }

@@ -189,17 +189,33 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
     }
 }
 
-__global__ void k_dense_matvec(const double *__restrict__ M, int64_t n, const double *__restrict__ x,
-                               double *__restrict__ y) {
+// y = M x, M dense row-major (the collapsed coarse cycle): x staged in
+// shared memory, one warp per row with four independent accumulators
+__global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t n,
+                                                      const double *__restrict__ x, double *__restrict__ y) {
     pdl_wait();
-    // one warp per row
-    int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (row >= n) return;
-    double s = 0.0;
-    for (int64_t j = lane; j < n; j += 32) s = fma(M[row * n + j], x[j], s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == 0) y[row] = s;
+    extern __shared__ double xs[];
+    const bool staged = n <= 8192;
+    if (staged)
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) xs[j] = x[j];
+    __syncthreads();
+    const double *xv = staged ? xs : x;
+    const int lane = threadIdx.x & 31;
+    for (int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5); row < n; row += (int64_t)gridDim.x * 8) {
+        const double *mr = M + row * n;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t j = lane;
+        for (; j + 96 < n; j += 128) {
+            s0 = fma(__ldg(mr + j), xv[j], s0);
+            s1 = fma(__ldg(mr + j + 32), xv[j + 32], s1);
+            s2 = fma(__ldg(mr + j + 64), xv[j + 64], s2);
+            s3 = fma(__ldg(mr + j + 96), xv[j + 96], s3);
+        }
+        for (; j < n; j += 32) s0 = fma(__ldg(mr + j), xv[j], s0);
+        double s = (s0 + s1) + (s2 + s3);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        if (lane == 0) y[row] = s;
+    }
 }
 
 __global__ void k_gather(const double *__restrict__ src, const int64_t *__restrict__ idx, int64_t n,
@@ -297,7 +313,10 @@ void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const do
 
 void dense_matvec(const double *M, int64_t n, const double *x, double *y, cudaStream_t s) {
     if (n == 0) return;
-    launch_pdl(k_dense_matvec, dim3(grid_for(n * 32, 256)), dim3(256), 0, s, M, n, x, y);
+    const int64_t blocks = (n + 7) / 8;
+    const size_t smem = n <= 8192 ? sizeof(double) * n : 0;
+    launch_pdl(k_dense_matvec, dim3((unsigned)(blocks < 4 * num_sms() ? blocks : 4 * num_sms())), dim3(256), smem, s,
+               M, n, x, y);
     PMGR_LAUNCHED();
 }
 
