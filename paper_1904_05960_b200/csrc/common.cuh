@@ -192,12 +192,6 @@ struct CsrView {
     const int32_t *ci;
     const double *v;
     int64_t maxrow = -1;  // longest row (-1: unknown); picks the SpMV lane group
-    // optional SELL-32 copy for the solve phase (sliced ELLPACK: slices of
-    // 32 rows, column-major inside a slice, padded with zero entries)
-    int64_t nslices = 0;
-    const int64_t *sptr = nullptr;  // slice offsets (entries), nslices + 1
-    const int32_t *scol = nullptr;
-    const double *sval = nullptr;
 };
 
 struct Csr {
@@ -214,13 +208,7 @@ struct Csr {
         v.alloc(z);
     }
     int64_t maxrow = -1;
-    int64_t nslices = 0;
-    DBuf<int64_t> sptr;
-    DBuf<int32_t> scol;
-    DBuf<double> sval;
-    CsrView view() const {
-        return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow, nslices, sptr.p, scol.p, sval.p};
-    }
+    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow}; }
 };
 
 // record the longest row of a finished operator (setup time, synchronises)

@@ -15,8 +15,6 @@
 //                      compacted without exact zeros (scipy's zero drop).
 //  * csr_subtract      scipy csr_binop_csr_canonical '-', zero drop.
 //  * csr_sparsify      reference sparsify (sparse.py:439-467).
-#include <cstdlib>
-
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -382,39 +380,6 @@ __global__ void k_maxrow(int64_t n, const int64_t *ro, unsigned long long *out) 
 }
 }  // namespace
 
-namespace {
-__global__ void k_slice_width(int64_t n, const int64_t *ro, int64_t *w) {
-    const int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t ns = (n + 31) / 32;
-    if (sl >= ns) return;
-    int64_t m = 0;
-    for (int64_t i = sl * 32; i < sl * 32 + 32 && i < n; ++i) {
-        const int64_t l = ro[i + 1] - ro[i];
-        m = l > m ? l : m;
-    }
-    w[sl] = 32 * m;
-}
-
-__global__ void k_sell_fill(int64_t n, const int64_t *ro, const int32_t *ci, const double *v, const int64_t *sptr,
-                            int32_t *scol, double *sval) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t sl = i / 32, lane = i % 32;
-    const int64_t base = sptr[sl], width = (sptr[sl + 1] - base) / 32;
-    const int64_t b = ro[i], len = ro[i + 1] - b;
-    for (int64_t k = 0; k < width; ++k) {
-        const int64_t o = base + k * 32 + lane;
-        if (k < len) {
-            scol[o] = ci[b + k];
-            sval[o] = v[b + k];
-        } else {
-            scol[o] = len > 0 ? ci[b + len - 1] : 0;  // a column the row already reads, zero value
-            sval[o] = 0.0;
-        }
-    }
-}
-}  // namespace
-
 void csr_finalize(Csr &A, cudaStream_t s) {
     if (A.nrows == 0) {
         A.maxrow = 0;
@@ -426,26 +391,6 @@ void csr_finalize(Csr &A, cudaStream_t s) {
     k_maxrow<<<g < 1024 ? g : 1024, 256, 0, s>>>(A.nrows, A.ro.p, m.p);
     PMGR_LAUNCHED();
     A.maxrow = (int64_t)read_scalar(m.p, s);
-    // large, evenly filled operators also get the SELL-32 solve copy
-    static const int64_t min_nnz = [] {
-        const char *e = getenv("PMGR_SELL_MIN_NNZ");
-        return e ? atoll(e) : (int64_t)262144;
-    }();
-    const double mean = (double)A.nnz / (double)A.nrows;
-    if (min_nnz > 0 && A.nnz >= min_nnz && A.ncols > 0 && (double)A.maxrow <= 1.5 * mean + 8) {
-        const int64_t ns = (A.nrows + 31) / 32;
-        TBuf<int64_t> w(ns, s);
-        k_slice_width<<<grid_for(ns, 256), 256, 0, s>>>(A.nrows, A.ro.p, w.p);
-        PMGR_LAUNCHED();
-        A.sptr.alloc(ns + 1);
-        const int64_t total = exclusive_scan_total(w.p, A.sptr.p, ns, s);
-        A.scol.alloc(total);
-        A.sval.alloc(total);
-        k_sell_fill<<<grid_for(A.nrows, 256), 256, 0, s>>>(A.nrows, A.ro.p, A.ci.p, A.v.p, A.sptr.p, A.scol.p,
-                                                          A.sval.p);
-        PMGR_LAUNCHED();
-        A.nslices = ns;
-    }
 }
 
 void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {

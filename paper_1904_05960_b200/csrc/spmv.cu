@@ -22,14 +22,6 @@ namespace pmgr {
 
 namespace {
 
-bool sell_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("PMGR_NO_SELL");
-        return !(e && e[0] != '0');
-    }();
-    return on;
-}
-
 template <bool STREAM>
 __device__ __forceinline__ double ldv(const double *p) {
     return STREAM ? __ldcs(p) : __ldg(p);
@@ -69,37 +61,6 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
     if (active && lane == 0) op.out(row, s);
-}
-
-// SELL-32: one thread per row, the warp owns one slice; every load of
-// values / columns is a contiguous 256 B / 128 B warp access and a row's
-// entries are independent loads (8 in flight per thread)
-template <class Op>
-__global__ void __launch_bounds__(256) k_sell(int64_t nrows, int64_t nslices, const int64_t *__restrict__ sptr,
-                                              const int32_t *__restrict__ scol, const double *__restrict__ sval,
-                                              Op op) {
-    pdl_wait();
-    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t sl = row >> 5;
-    if (sl >= nslices) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t base = __ldg(sptr + sl) + lane;
-    const int64_t width = (__ldg(sptr + sl + 1) - __ldg(sptr + sl)) >> 5;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int64_t k = 0;
-    for (; k + 7 < width; k += 8) {
-        double vv[8];
-        int cc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            vv[u] = __ldg(sval + base + (k + u) * 32);
-            cc[u] = __ldg(scol + base + (k + u) * 32);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u & 3] = fma(vv[u], op.x(cc[u]), acc[u & 3]);
-    }
-    for (; k < width; ++k) acc[0] = fma(__ldg(sval + base + k * 32), op.x(__ldg(scol + base + k * 32)), acc[0]);
-    if (row < nrows) op.out(row, (acc[0] + acc[1]) + (acc[2] + acc[3]));
 }
 
 struct OpY {
@@ -178,12 +139,6 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
 template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
-    if (A.nslices > 0 && sell_enabled()) {
-        launch_pdl(k_sell<Op>, dim3(grid_for(A.nslices * 32, 256)), dim3(256), 0, s, A.nrows, A.nslices, A.sptr,
-                   A.scol, A.sval, op);
-        PMGR_LAUNCHED();
-        return;
-    }
     double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
     // skewed rows (a few dense coarse-grid rows next to short ones) get a
     // whole warp, otherwise the longest row serialises its lane group
