@@ -112,25 +112,35 @@ __global__ void __launch_bounds__(DOT_BLOCK) k_project(const double *__restrict_
     }
 }
 
-// h = a + (a - G a): reduce the slices, extend the Gram matrix by column j
-__global__ void k_coeffs(const Dev *__restrict__ dev, const double *pa, const double *pg, int nsplit, double *G,
-                         int ldg, double *a, double *h) {
+// h = a + (a - G a): reduce the slices, extend the Gram matrix by column j.
+// One block of 1024 threads, a warp per coefficient (lanes over slices,
+// then over the Gram row) so no thread walks a long dependent chain.
+__global__ void __launch_bounds__(1024) k_coeffs(const Dev *__restrict__ dev, const double *pa, const double *pg,
+                                                  int nsplit, double *G, int ldg, double *a, double *h) {
+    __shared__ double as[1024];
     const int j = dev->j;
-    for (int k = threadIdx.x; k <= j; k += blockDim.x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int k = warp; k <= j; k += nw) {
         double sa = 0.0, sg = 0.0;
-        for (int s = 0; s < nsplit; ++s) {
+        for (int s = lane; s < nsplit; s += 32) {
             sa += pa[(int64_t)k * nsplit + s];
             sg += pg[(int64_t)k * nsplit + s];
         }
-        a[k] = sa;
-        G[(int64_t)k * ldg + j] = sg;
-        G[(int64_t)j * ldg + k] = sg;
+        sa = warp_sum(sa);
+        sg = warp_sum(sg);
+        if (lane == 0) {
+            as[k] = sa;
+            a[k] = sa;
+            G[(int64_t)k * ldg + j] = sg;
+            G[(int64_t)j * ldg + k] = sg;
+        }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k <= j; k += blockDim.x) {
+    for (int k = warp; k <= j; k += nw) {
         double ga = 0.0;
-        for (int l = 0; l <= j; ++l) ga = fma(G[(int64_t)k * ldg + l], a[l], ga);
-        h[k] = a[k] + (a[k] - ga);
+        for (int l = lane; l <= j; l += 32) ga = fma(G[(int64_t)k * ldg + l], as[l], ga);
+        ga = warp_sum(ga);
+        if (lane == 0) h[k] = as[k] + (as[k] - ga);
     }
 }
 
@@ -445,7 +455,7 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
     k_project<<<dim3(W.nsplit, W.m + 1), DOT_BLOCK, 0, s>>>(W.V.p, n, W.w.p, W.dev.p, W.pa.p, W.pg.p, W.nsplit,
                                                            W.chunk);
     PMGR_LAUNCHED();
-    k_coeffs<<<1, 256, 0, s>>>(W.dev.p, W.pa.p, W.pg.p, W.nsplit, W.G.p, W.m + 1, W.a.p, W.h.p);
+    k_coeffs<<<1, 1024, 0, s>>>(W.dev.p, W.pa.p, W.pg.p, W.nsplit, W.G.p, W.m + 1, W.a.p, W.h.p);
     PMGR_LAUNCHED();
     k_update<<<W.nupd, DOT_BLOCK, 0, s>>>(W.V.p, n, W.h.p, W.dev.p, W.w.p, W.pn.p);
     PMGR_LAUNCHED();
