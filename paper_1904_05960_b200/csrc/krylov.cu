@@ -28,7 +28,11 @@
 #include <map>
 #include <tuple>
 
+#include <cooperative_groups.h>
+
 #include "hier.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pmgr {
 
@@ -73,178 +77,185 @@ __device__ __forceinline__ void block_sum2(double &a, double &b, double *sh) {
     }
 }
 
-// pass 1: pa[k][s] = V_k . w, pg[k][s] = V_k . V_j over row slice s (k <= j)
-__global__ void __launch_bounds__(DOT_BLOCK) k_project(const double *__restrict__ V, int64_t n,
-                                                        const double *__restrict__ w, const Dev *__restrict__ dev,
-                                                        double *pa, double *pg, int nsplit, int64_t chunk) {
-    const int j = dev->j;
-    const int k = blockIdx.y;
-    if (k > j) return;
-    __shared__ double sh[2 * DOT_BLOCK / 32];
-    const double *x = V + (int64_t)k * n;
-    const double *vj = V + (int64_t)j * n;
-    const int64_t lo = blockIdx.x * chunk;
+// ---- one cooperative kernel per Arnoldi step --------------------------
+// Every block owns a contiguous slice of rows.  Phase 1 streams the basis
+// once (warp per basis vector, lanes over the slice's rows) for the
+// projections a_k = V_k.w and the Gram column g_k = V_k.V_j; phase 2 turns
+// the slice partials into h = a + (a - G a); phase 3 updates w on the same
+// rows (the basis slice is re-read from L2, not HBM); phase 4 normalises and
+// block 0 does the Hessenberg / Givens / convergence bookkeeping
+// (krylov.py:75-104) and sets the WHILE condition.  Three grid barriers
+// replace five launches and half of the basis traffic.
+constexpr int AO_THREADS = 512;
+constexpr int AO_WARPS = AO_THREADS / 32;
+
+struct AoParams {
+    double *V;
+    int64_t n;
+    double *w, *vin;
+    Dev *dev;
+    double *pa, *pg, *pn;  // slice partials: (m+1) x nblk, (m+1) x nblk, nblk
+    double *G;
+    int ldg;
+    double *a, *h;
+    double *H, *cs, *sn, *g, *hist;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+};
+
+__device__ __forceinline__ double block_sum1(double v, double *sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];  // every thread, same order
+    return t;
+}
+
+__global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[AO_WARPS];
+    __shared__ double hs[1024];   // h
+    __shared__ double as_[1024];  // a
+    const int nblk = gridDim.x, b = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = P.dev->j;
+    const int64_t n = P.n;
+    const int64_t chunk = (n + nblk - 1) / nblk;
+    const int64_t lo = (int64_t)b * chunk;
     const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
-    int64_t i = lo + threadIdx.x;
-    for (; i + 3 * DOT_BLOCK < hi; i += 4 * DOT_BLOCK) {
-        const double x0 = x[i], x1 = x[i + DOT_BLOCK], x2 = x[i + 2 * DOT_BLOCK], x3 = x[i + 3 * DOT_BLOCK];
-        const double w0 = w[i], w1 = w[i + DOT_BLOCK], w2 = w[i + 2 * DOT_BLOCK], w3 = w[i + 3 * DOT_BLOCK];
-        const double v0 = vj[i], v1 = vj[i + DOT_BLOCK], v2 = vj[i + 2 * DOT_BLOCK], v3 = vj[i + 3 * DOT_BLOCK];
-        a0 = fma(x0, w0, a0);
-        a1 = fma(x1, w1, a1);
-        a2 = fma(x2, w2, a2);
-        a3 = fma(x3, w3, a3);
-        g0 = fma(x0, v0, g0);
-        g1 = fma(x1, v1, g1);
-        g2 = fma(x2, v2, g2);
-        g3 = fma(x3, v3, g3);
-    }
-    for (; i < hi; i += DOT_BLOCK) {
-        a0 = fma(x[i], w[i], a0);
-        g0 = fma(x[i], vj[i], g0);
-    }
-    double a = (a0 + a1) + (a2 + a3), g = (g0 + g1) + (g2 + g3);
-    block_sum2(a, g, sh);
-    if (threadIdx.x == 0) {
-        pa[(int64_t)k * nsplit + blockIdx.x] = a;
-        pg[(int64_t)k * nsplit + blockIdx.x] = g;
-    }
-}
+    const double *vj = P.V + (int64_t)j * n;
 
-// h = a + (a - G a): reduce the slices, extend the Gram matrix by column j.
-// One block of 1024 threads, a warp per coefficient (lanes over slices,
-// then over the Gram row) so no thread walks a long dependent chain.
-__global__ void __launch_bounds__(1024) k_coeffs(const Dev *__restrict__ dev, const double *pa, const double *pg,
-                                                  int nsplit, double *G, int ldg, double *a, double *h) {
-    __shared__ double as[1024];
-    const int j = dev->j;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int k = warp; k <= j; k += nw) {
-        double sa = 0.0, sg = 0.0;
-        for (int s = lane; s < nsplit; s += 32) {
-            sa += pa[(int64_t)k * nsplit + s];
-            sg += pg[(int64_t)k * nsplit + s];
+    // phase 1: slice partials of V_k.w and V_k.V_j
+    for (int k = warp; k <= j; k += AO_WARPS) {
+        const double *x = P.V + (int64_t)k * n;
+        double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+        int64_t i = lo + lane;
+        for (; i + 32 < hi; i += 64) {
+            const double x0 = x[i], x1 = x[i + 32];
+            a0 = fma(x0, P.w[i], a0);
+            a1 = fma(x1, P.w[i + 32], a1);
+            g0 = fma(x0, vj[i], g0);
+            g1 = fma(x1, vj[i + 32], g1);
         }
-        sa = warp_sum(sa);
-        sg = warp_sum(sg);
+        if (i < hi) {
+            a0 = fma(x[i], P.w[i], a0);
+            g0 = fma(x[i], vj[i], g0);
+        }
+        const double sa = warp_sum(a0 + a1), sg = warp_sum(g0 + g1);
         if (lane == 0) {
-            as[k] = sa;
-            a[k] = sa;
-            G[(int64_t)k * ldg + j] = sg;
-            G[(int64_t)j * ldg + k] = sg;
+            P.pa[(int64_t)k * nblk + b] = sa;
+            P.pg[(int64_t)k * nblk + b] = sg;
         }
     }
-    __syncthreads();
-    for (int k = warp; k <= j; k += nw) {
-        double ga = 0.0;
-        for (int l = lane; l <= j; l += 32) ga = fma(G[(int64_t)k * ldg + l], as[l], ga);
-        ga = warp_sum(ga);
-        if (lane == 0) h[k] = as[k] + (as[k] - ga);
+    grid.sync();
+    // phase 2a: a_k and the Gram column, one block per coefficient
+    for (int k = b; k <= j; k += nblk) {
+        double sa = 0.0, sg = 0.0;
+        for (int t = threadIdx.x; t < nblk; t += AO_THREADS) {
+            sa += P.pa[(int64_t)k * nblk + t];
+            sg += P.pg[(int64_t)k * nblk + t];
+        }
+        sa = block_sum1(sa, sh);
+        sg = block_sum1(sg, sh);
+        if (threadIdx.x == 0) {
+            P.a[k] = sa;
+            P.G[(int64_t)k * P.ldg + j] = sg;
+            P.G[(int64_t)j * P.ldg + k] = sg;
+        }
     }
-}
-
-// pass 2: w -= sum_{k<=j} h_k V_k ; ||w||^2 partials
-__global__ void __launch_bounds__(DOT_BLOCK) k_update(const double *__restrict__ V, int64_t n,
-                                                       const double *__restrict__ h, const Dev *__restrict__ dev,
-                                                       double *w, double *pn) {
-    __shared__ double sh[2 * DOT_BLOCK / 32];
-    __shared__ double hs[1024];
-    const int nk = dev->j + 1;
-    for (int k = threadIdx.x; k < nk; k += DOT_BLOCK) hs[k] = h[k];
+    grid.sync();
+    // phase 2b: h = a + (a - G a), every block for itself (warp per k)
+    for (int k = threadIdx.x; k <= j; k += AO_THREADS) as_[k] = P.a[k];
     __syncthreads();
+    for (int k = warp; k <= j; k += AO_WARPS) {
+        double ga = 0.0;
+        for (int l = lane; l <= j; l += 32) ga = fma(P.G[(int64_t)k * P.ldg + l], as_[l], ga);
+        ga = warp_sum(ga);
+        if (lane == 0) hs[k] = as_[k] + (as_[k] - ga);
+    }
+    __syncthreads();
+    if (b == 0)
+        for (int k = threadIdx.x; k <= j; k += AO_THREADS) P.h[k] = hs[k];
+    // phase 3: w -= sum_k h_k V_k on this slice, ||w||^2 partial
     double nrm = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)DOT_BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * DOT_BLOCK) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
         double acc[8];
-        acc[0] = w[i];
+        acc[0] = P.w[i];
 #pragma unroll
         for (int t = 1; t < 8; ++t) acc[t] = 0.0;
         int k = 0;
-        for (; k + 7 < nk; k += 8) {
+        for (; k + 7 <= j; k += 8) {
             double vv[8];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) vv[t] = V[(int64_t)(k + t) * n + i];
+            for (int t = 0; t < 8; ++t) vv[t] = P.V[(int64_t)(k + t) * n + i];
 #pragma unroll
             for (int t = 0; t < 8; ++t) acc[t] = fma(-hs[k + t], vv[t], acc[t]);
         }
-        for (; k < nk; ++k) acc[0] = fma(-hs[k], V[(int64_t)k * n + i], acc[0]);
+        for (; k <= j; ++k) acc[0] = fma(-hs[k], P.V[(int64_t)k * n + i], acc[0]);
         const double wi = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        w[i] = wi;
+        P.w[i] = wi;
         nrm = fma(wi, wi, nrm);
     }
-    double z = 0.0;
-    block_sum2(nrm, z, sh);
-    if (threadIdx.x == 0) pn[blockIdx.x] = nrm;
-}
-
-// Hessenberg column, Givens rotation, convergence / breakdown flags
-// (krylov.py:78-104); one warp loads, lane 0 rotates in shared memory
-__global__ void k_givens(Dev *dev, const double *pn, int npn, const double *h, double *H, double *cs, double *sn,
-                         double *g, double *hist, cudaGraphConditionalHandle cond, int use_cond) {
-    extern __shared__ double col[];  // [m + 2] column, then cs[m + 1], sn[m + 1]
-    const int lane = threadIdx.x;
-    const int j = dev->j, m = dev->m;
-    double *css = col + (m + 2), *sns = css + (m + 1);
-    double s = 0.0;
-    for (int b = lane; b < npn; b += 32) s += pn[b];
-    s = warp_sum(s);
-    const double hn = sqrt(s);
-    for (int i = lane; i <= j; i += 32) {
-        col[i] = h[i];
-        css[i] = cs[i];
-        sns[i] = sn[i];
-    }
-    __syncwarp();
-    if (lane != 0) return;
-    col[j + 1] = hn;
+    nrm = block_sum1(nrm, sh);
+    if (threadIdx.x == 0) P.pn[b] = nrm;
+    grid.sync();
+    // phase 4: ||w||, breakdown test, normalisation (every block, same order)
+    double s2 = 0.0;
+    for (int t = threadIdx.x; t < nblk; t += AO_THREADS) s2 += P.pn[t];
+    s2 = block_sum1(s2, sh);
+    const double hn = sqrt(s2);
     double c2 = 0.0;
-    for (int i = 0; i <= j + 1; ++i) c2 += col[i] * col[i];
-    const double colscale = sqrt(c2);
-    const int brk = !(hn > 1e-12 * fmax(colscale, 1e-300));
-    for (int i = 0; i < j; ++i) {
-        const double t = col[i];
-        col[i] = css[i] * t + sns[i] * col[i + 1];
-        col[i + 1] = -sns[i] * t + css[i] * col[i + 1];
+    for (int k = 0; k <= j; ++k) c2 += hs[k] * hs[k];
+    c2 += hn * hn;
+    const int brk = !(hn > 1e-12 * fmax(sqrt(c2), 1e-300));
+    if (!brk && j + 1 <= P.dev->m) {
+        double *vn = P.V + (int64_t)(j + 1) * n;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
+            const double t = P.w[i] / hn;
+            vn[i] = t;
+            P.vin[i] = t;
+        }
     }
-    const double a = col[j], bb = col[j + 1];
-    const double rho = hypot(a, bb);
-    dev->hn = hn;
+    if (b != 0 || threadIdx.x != 0) return;
+    // Hessenberg column j and Givens rotation (one thread, carry in registers)
+    const int m = P.dev->m;
+    double carry = hs[0];
+    for (int i = 0; i < j; ++i) {
+        const double next = hs[i + 1];
+        const double c = P.cs[i], sn = P.sn[i];
+        P.H[(int64_t)i * m + j] = c * carry + sn * next;
+        carry = -sn * carry + c * next;
+    }
+    const double av = carry, bv = hn;
+    const double rho = hypot(av, bv);
+    Dev *dv = P.dev;
+    dv->hn = hn;
     if (rho == 0.0) {
-        dev->brk = 1;
-        dev->dead = 1;
-        dev->active = 0;
-        if (use_cond) cudaGraphSetConditional(cond, 0);
+        dv->brk = 1;
+        dv->dead = 1;
+        dv->active = 0;
+        if (P.use_cond) cudaGraphSetConditional(P.cond, 0);
         return;
     }
-    cs[j] = a / rho;
-    sn[j] = bb / rho;
-    col[j] = rho;
-    col[j + 1] = 0.0;
-    for (int i = 0; i <= j + 1; ++i) H[(int64_t)i * m + j] = col[i];
-    g[j + 1] = -sn[j] * g[j];
-    g[j] = cs[j] * g[j];
-    const double est = fabs(g[j + 1]);
-    hist[dev->total] = est;
-    const int total = dev->total + 1;
+    P.cs[j] = av / rho;
+    P.sn[j] = bv / rho;
+    P.H[(int64_t)j * m + j] = rho;
+    P.H[(int64_t)(j + 1) * m + j] = 0.0;
+    P.g[j + 1] = -P.sn[j] * P.g[j];
+    P.g[j] = P.cs[j] * P.g[j];
+    const double est = fabs(P.g[j + 1]);
+    P.hist[dv->total] = est;
+    const int total = dv->total + 1;
     const int jn = j + 1;
-    dev->total = total;
-    dev->j = jn;
-    dev->brk = brk;
-    const int act = !(est <= dev->tol || brk) && jn < m && total < dev->max_iters;
-    dev->active = act;
-    if (use_cond) cudaGraphSetConditional(cond, act);
-}
-
-// V_j = w / hn (j already advanced) and the preconditioner input copy
-__global__ void k_normalize(const double *w, int64_t n, const Dev *dev, double *V, double *vin) {
-    if (dev->brk) return;
-    const double d = dev->hn;
-    double *vj = V + (int64_t)dev->j * n;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const double t = w[i] / d;
-        vj[i] = t;
-        vin[i] = t;
-    }
+    dv->total = total;
+    dv->j = jn;
+    dv->brk = brk;
+    const int act = !(est <= dv->tol || brk) && jn < m && total < dv->max_iters;
+    dv->active = act;
+    if (P.use_cond) cudaGraphSetConditional(P.cond, act);
 }
 
 __global__ void k_cycle_init(Dev *dev, double *H, double *G, int ldg, double *cs, double *sn, double *g, int m,
@@ -366,8 +377,7 @@ struct Ws {
     pmgr_mgr *M = nullptr;
     int m = 0, max_iters = 0;
     int64_t n = 0;
-    int nsplit = 1, nupd = 1;
-    int64_t chunk = 0;
+    int nblk = 1, nupd = 1;
     DBuf<double> V, w, z, r, vin, u;
     DBuf<double> H, G, cs, sn, g, a, h, y, hist, pa, pg, pn, beta;
     DBuf<Dev> dev;
@@ -410,16 +420,15 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
     w->h.alloc(m + 1);
     w->y.alloc(m + 1);
     w->hist.alloc((int64_t)max_iters + 2);
-    // row slices: enough blocks per basis vector to stream at full bandwidth
-    int ns = (int)((n + 8191) / 8192);
-    if (ns > 64) ns = 64;
-    if (ns < 1) ns = 1;
-    w->nsplit = ns;
-    w->chunk = (n + ns - 1) / ns;
-    w->pa.alloc((int64_t)(m + 1) * ns);
-    w->pg.alloc((int64_t)(m + 1) * ns);
+    // the cooperative Arnoldi kernel: every block resident at once
+    int per_sm = 0;
+    PMGR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi, AO_THREADS, 0));
+    if (per_sm < 1) fail(PMGR_ERR_CUDA, "Arnoldi kernel cannot be resident");
+    w->nblk = (per_sm < 2 ? per_sm : 2) * num_sms();
+    w->pa.alloc((int64_t)(m + 1) * w->nblk);
+    w->pg.alloc((int64_t)(m + 1) * w->nblk);
     w->nupd = 4 * num_sms();
-    w->pn.alloc(w->nupd);
+    w->pn.alloc(w->nblk > w->nupd ? w->nblk : w->nupd);
     w->beta.alloc(1);
     w->dev.alloc(1);
     PMGR_CUDA(cudaMallocHost((void **)&w->hdev, sizeof(Dev)));
@@ -452,17 +461,36 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
     // w read twice and written once, new basis vector + copy written
     const double bytes = prof ? 8.0 * n * (2.0 * (W.hdev->j + 1) + 5.0) : 0.0;
     ProfScope ps(prof ? PROF_ORTHO : PROF_KINDS, bytes, s);
-    k_project<<<dim3(W.nsplit, W.m + 1), DOT_BLOCK, 0, s>>>(W.V.p, n, W.w.p, W.dev.p, W.pa.p, W.pg.p, W.nsplit,
-                                                           W.chunk);
-    PMGR_LAUNCHED();
-    k_coeffs<<<1, 1024, 0, s>>>(W.dev.p, W.pa.p, W.pg.p, W.nsplit, W.G.p, W.m + 1, W.a.p, W.h.p);
-    PMGR_LAUNCHED();
-    k_update<<<W.nupd, DOT_BLOCK, 0, s>>>(W.V.p, n, W.h.p, W.dev.p, W.w.p, W.pn.p);
-    PMGR_LAUNCHED();
-    k_givens<<<1, 32, sizeof(double) * (3 * W.m + 4), s>>>(W.dev.p, W.pn.p, W.nupd, W.h.p, W.H.p, W.cs.p, W.sn.p, W.g.p,
-                                                       W.hist.p, cond, use_cond);
-    PMGR_LAUNCHED();
-    k_normalize<<<vec_grid(n), 256, 0, s>>>(W.w.p, n, W.dev.p, W.V.p, W.vin.p);
+    AoParams P;
+    P.V = W.V.p;
+    P.n = n;
+    P.w = W.w.p;
+    P.vin = W.vin.p;
+    P.dev = W.dev.p;
+    P.pa = W.pa.p;
+    P.pg = W.pg.p;
+    P.pn = W.pn.p;
+    P.G = W.G.p;
+    P.ldg = W.m + 1;
+    P.a = W.a.p;
+    P.h = W.h.p;
+    P.H = W.H.p;
+    P.cs = W.cs.p;
+    P.sn = W.sn.p;
+    P.g = W.g.p;
+    P.hist = W.hist.p;
+    P.cond = cond;
+    P.use_cond = use_cond;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(W.nblk);
+    cfg.blockDim = dim3(AO_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeCooperative;
+    at.val.cooperative = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    PMGR_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi, P));
     PMGR_LAUNCHED();
 }
 
