@@ -131,20 +131,31 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     // phase 1: slice partials of V_k.w and V_k.V_j
     for (int k = warp; k <= j; k += AO_WARPS) {
         const double *x = P.V + (int64_t)k * n;
-        double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+        // 8 rows per lane per round: 24 independent loads in flight
+        double aa[8], gg[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) aa[u] = gg[u] = 0.0;
         int64_t i = lo + lane;
-        for (; i + 32 < hi; i += 64) {
-            const double x0 = x[i], x1 = x[i + 32];
-            a0 = fma(x0, P.w[i], a0);
-            a1 = fma(x1, P.w[i + 32], a1);
-            g0 = fma(x0, vj[i], g0);
-            g1 = fma(x1, vj[i + 32], g1);
+        for (; i + 7 * 32 < hi; i += 8 * 32) {
+            double xs[8], ws[8], vs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                xs[u] = x[i + 32 * u];
+                ws[u] = P.w[i + 32 * u];
+                vs[u] = vj[i + 32 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                aa[u] = fma(xs[u], ws[u], aa[u]);
+                gg[u] = fma(xs[u], vs[u], gg[u]);
+            }
         }
-        if (i < hi) {
-            a0 = fma(x[i], P.w[i], a0);
-            g0 = fma(x[i], vj[i], g0);
+        for (; i < hi; i += 32) {
+            aa[0] = fma(x[i], P.w[i], aa[0]);
+            gg[0] = fma(x[i], vj[i], gg[0]);
         }
-        const double sa = warp_sum(a0 + a1), sg = warp_sum(g0 + g1);
+        const double sa = warp_sum(((aa[0] + aa[1]) + (aa[2] + aa[3])) + ((aa[4] + aa[5]) + (aa[6] + aa[7])));
+        const double sg = warp_sum(((gg[0] + gg[1]) + (gg[2] + gg[3])) + ((gg[4] + gg[5]) + (gg[6] + gg[7])));
         if (lane == 0) {
             P.pa[(int64_t)k * nblk + b] = sa;
             P.pg[(int64_t)k * nblk + b] = sg;
