@@ -157,7 +157,7 @@ void go(const CsrView &A, const Op &op, cudaStream_t s) {
     // let the next kernel's launch overlap this one only when this grid is a
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
-    constexpr int U = G >= 16 ? 8 : 4;
+    constexpr int U = 2;
     launch_pdl(k_spmv<G, U, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
 }
 
