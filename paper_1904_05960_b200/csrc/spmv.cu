@@ -22,11 +22,16 @@ namespace pmgr {
 
 namespace {
 
-// Per row: the row bounds, then the epilogue operands (prefetched so they
-// overlap the matrix stream), then one round of U (value, column) loads per
-// lane followed by U independent gathers -- rows up to G*U entries take a
-// single memory round trip -- then a shuffle reduction and the epilogue.
-template <int G, int U, class Op>
+template <bool STREAM>
+__device__ __forceinline__ double ldv(const double *p) {
+    return STREAM ? __ldcs(p) : __ldg(p);
+}
+template <bool STREAM>
+__device__ __forceinline__ int ldc(const int32_t *p) {
+    return STREAM ? __ldcs(p) : __ldg(p);
+}
+
+template <int G, bool STREAM, class Op>
 __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
                                               const int32_t *__restrict__ ci,
                                               const double *__restrict__ v, Op op, int trigger) {
@@ -36,129 +41,99 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
     const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const bool active = row < nrows;
     int64_t b = 0, e = 0;
-    typename Op::Pre pre{};
     if (active) {
         b = __ldg(ro + row);
         e = __ldg(ro + row + 1);
-        if (lane == 0) pre = op.pre(row);
     }
-    double acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = 0.0;
-    for (int64_t q0 = b + lane; q0 < e; q0 += (int64_t)U * G) {
-        double vv[U];
-        int cc[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t q = q0 + (int64_t)u * G;
-            vv[u] = q < e ? __ldg(v + q) : 0.0;
-            cc[u] = q < e ? __ldg(ci + q) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (cc[u] >= 0) acc[u] = fma(vv[u], op.x(cc[u]), acc[u]);
+    // two independent accumulators keep two (value, column, x) load chains
+    // in flight per lane; matrix streams use evict-first loads so the
+    // gathered vector stays in L2
+    double s0 = 0.0, s1 = 0.0;
+    int64_t q = b + lane;
+    for (; q + G < e; q += 2 * G) {
+        const double v0 = ldv<STREAM>(v + q), v1 = ldv<STREAM>(v + q + G);
+        const int c0 = ldc<STREAM>(ci + q), c1 = ldc<STREAM>(ci + q + G);
+        s0 = fma(v0, op.x(c0), s0);
+        s1 = fma(v1, op.x(c1), s1);
     }
-    double s = 0.0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) s += acc[u];
+    if (q < e) s0 = fma(ldv<STREAM>(v + q), op.x(ldc<STREAM>(ci + q)), s0);
+    double s = s0 + s1;
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
-    if (active && lane == 0) op.out(row, s, pre);
+    if (active && lane == 0) op.out(row, s);
 }
 
-struct Pre0 {};
-struct Pre1 {
-    double a;
-};
-struct Pre3 {
-    double a, b, c;
-};
-
 struct OpY {
-    using Pre = Pre0;
     const double *xv;
     double *y;
-    __device__ Pre pre(int64_t) const { return {}; }
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void out(int64_t i, double s, const Pre &) const { y[i] = s; }
+    __device__ void out(int64_t i, double s) const { y[i] = s; }
 };
 struct OpResidual {
-    using Pre = Pre1;
     const double *xv, *b;
     double *r;
-    __device__ Pre pre(int64_t i) const { return {b[i]}; }
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void out(int64_t i, double s, const Pre &p) const { r[i] = p.a - s; }
+    __device__ void out(int64_t i, double s) const { r[i] = b[i] - s; }
 };
 struct OpJacobi {
-    using Pre = Pre3;
     const double *xv, *b, *d;
     double *xo;
-    __device__ Pre pre(int64_t i) const { return {xv[i], b[i], d[i]}; }
     __device__ double x(int j) const { return __ldg(xv + j); }
-    __device__ void out(int64_t i, double s, const Pre &p) const { xo[i] = p.a + (p.b - s) / p.c; }
+    __device__ void out(int64_t i, double s) const { xo[i] = xv[i] + (b[i] - s) / d[i]; }
 };
 struct OpSweep0 {
-    using Pre = Pre3;
     const double *b, *d;
     double *xo, *r;
-    __device__ Pre pre(int64_t i) const { return {b[i], d[i], 0.0}; }
     __device__ double x(int j) const { return __ldg(b + j) / __ldg(d + j); }
-    __device__ void out(int64_t i, double s, const Pre &p) const {
-        xo[i] = p.a / p.b;
-        r[i] = p.a - s;
+    __device__ void out(int64_t i, double s) const {
+        xo[i] = b[i] / d[i];
+        r[i] = b[i] - s;
     }
 };
 struct OpRestrictDiv {  // b_c = R r, and the first smoother iterate x_c = b_c / dtilde_c
-    using Pre = Pre1;
     const double *r, *d;
     double *b, *xo;
-    __device__ Pre pre(int64_t k) const { return {d[k]}; }
     __device__ double x(int j) const { return __ldg(r + j); }
-    __device__ void out(int64_t k, double s, const Pre &p) const {
+    __device__ void out(int64_t k, double s) const {
         b[k] = s;
-        xo[k] = s / p.a;
+        xo[k] = s / d[k];
     }
 };
 struct OpAdd {
-    using Pre = Pre1;
     const double *e;
     double *xio;
-    __device__ Pre pre(int64_t i) const { return {xio[i]}; }
     __device__ double x(int j) const { return __ldg(e + j); }
-    __device__ void out(int64_t i, double s, const Pre &p) const { xio[i] = p.a + s; }
+    __device__ void out(int64_t i, double s) const { xio[i] += s; }
 };
 struct OpResidRows {
-    using Pre = Pre1;
     const double *zf, *v;
     const int64_t *rows;
     double *r;
-    __device__ Pre pre(int64_t k) const { return {v[rows[k]]}; }
     __device__ double x(int j) const { return __ldg(zf + j); }
-    __device__ void out(int64_t k, double s, const Pre &p) const { r[k] = p.a - s; }
+    __device__ void out(int64_t k, double s) const { r[k] = v[rows[k]] - s; }
 };
 struct OpProlong {
-    using Pre = Pre1;
     const double *ec, *zf;
     const int64_t *findex;
     double *z;
-    __device__ Pre pre(int64_t i) const {
-        const int64_t f = findex ? findex[i] : -1;
-        return {f >= 0 ? zf[f] : 0.0};
-    }
     __device__ double x(int j) const { return __ldg(ec + j); }
-    __device__ void out(int64_t i, double s, const Pre &p) const { z[i] = p.a + s; }
+    __device__ void out(int64_t i, double s) const {
+        int64_t f = findex ? findex[i] : -1;
+        z[i] = (f >= 0 ? zf[f] : 0.0) + s;
+    }
 };
 
 template <int G, class Op>
-void go(const CsrView &A, const Op &op, cudaStream_t s) {
+void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
     const int block = 256;
     const unsigned grid = grid_for(A.nrows * G, block);
     // let the next kernel's launch overlap this one only when this grid is a
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
-    constexpr int U = 2;
-    launch_pdl(k_spmv<G, U, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
+    if (stream)
+        launch_pdl(k_spmv<G, true, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
+    else
+        launch_pdl(k_spmv<G, false, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
 }
 
 template <class Op>
@@ -171,16 +146,23 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
         int g = mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= 160.0 ? 16 : 32;
         if (A.maxrow > 16 * g) mean = 1e9;
     }
+    // matrices far larger than L2 are streamed with evict-first loads so the
+    // gathered vectors stay cached; small operators stay L2-resident
+    static const double stream_mb = [] {
+        const char *e = getenv("PMGR_SPMV_STREAM_MB");
+        return e ? atof(e) : 1e30;
+    }();
+    const bool stream = 12.0 * (double)A.nnz > stream_mb * 1024 * 1024;
     if (mean <= 3.0) {
-        go<2>(A, op, s);
+        go<2>(A, op, stream, s);
     } else if (mean <= 12.0) {
-        go<4>(A, op, s);
+        go<4>(A, op, stream, s);
     } else if (mean <= 48.0) {
-        go<8>(A, op, s);
+        go<8>(A, op, stream, s);
     } else if (mean <= 160.0) {
-        go<16>(A, op, s);
+        go<16>(A, op, stream, s);
     } else {
-        go<32>(A, op, s);
+        go<32>(A, op, stream, s);
     }
     PMGR_LAUNCHED();
 }
