@@ -468,9 +468,9 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
         ProfScope ps(prof ? PROF_OUTER_SPMV : PROF_KINDS, csr_pass_bytes(Av.nrows, Av.ncols, Av.nnz), s);
         spmv(Av, W.z.p, W.w.p, s);
     }
-    // algorithmic bytes of the step's orthogonalisation: basis read twice,
-    // w read twice and written once, new basis vector + copy written
-    const double bytes = prof ? 8.0 * n * (2.0 * (W.hdev->j + 1) + 5.0) : 0.0;
+    // compulsory bytes of the step's orthogonalisation: the basis V_0..V_j
+    // read once, w read and written, V_{j+1} and the preconditioner copy written
+    const double bytes = prof ? 8.0 * n * ((W.hdev->j + 1) + 4.0) : 0.0;
     ProfScope ps(prof ? PROF_ORTHO : PROF_KINDS, bytes, s);
     AoParams P;
     P.V = W.V.p;

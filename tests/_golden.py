@@ -48,6 +48,8 @@ CASES = {
     "c4_4": (lambda: problems.make_c4(seed=9, n=4), 4, True),
     "c1_16": (lambda: problems.make_c1(seed=0, n=16), None, False),
     "c2_32": (lambda: problems.make_c2(seed=0, n=32), 4, False),
+    "c4_16": (lambda: problems.make_c4(seed=0, n=16), 4, True),
+    "c3_64": (lambda: problems.make_c3(seed=0, n=64), 4, False),
 }
 
 
