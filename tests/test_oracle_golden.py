@@ -2,6 +2,8 @@
 oracle/make_golden.py (running poromgr itself) must be reproduced bitwise for
 patterns/setup values, and to 1e-12 for applies and solves."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -85,8 +87,12 @@ def test_amg_laplacian(units, t, npart):
     assert np.allclose(hist, units[tag + "hist"], rtol=1e-8)
 
 
-@pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16",
-                                 pytest.param("c2_32", marks=pytest.mark.slow)])
+SLOW = pytest.mark.skipif(not os.environ.get("PMGR_SLOW"), reason="set PMGR_SLOW=1 for the large oracle cases")
+
+
+@pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16", "c4_16",
+                                 pytest.param("c2_32", marks=pytest.mark.slow),
+                                 pytest.param("c3_64", marks=[pytest.mark.slow, SLOW])])
 def test_mgr_problem(tag):
     d = load(tag)
     full = "mgr0_isc" in d.files
