@@ -53,13 +53,10 @@ void prof_begin(int kind, double bytes, cudaStream_t s) {
         g_open[kind].push_back({g_capture, g_capture->size() - 1});
         return;
     }
-    if (g_used == g_recs.size()) {
-        if (g_used >= 4096) flush_direct();
-        if (g_used == g_recs.size()) {
-            PMGR_CUDA(cudaEventCreate(&r.a));
-            PMGR_CUDA(cudaEventCreate(&r.b));
-            g_recs.push_back(r);
-        }
+    if (g_used == g_recs.size()) {  // the pool only grows; scopes may still be open
+        PMGR_CUDA(cudaEventCreate(&r.a));
+        PMGR_CUDA(cudaEventCreate(&r.b));
+        g_recs.push_back(r);
     }
     ProfRec &q = g_recs[g_used];
     q.kind = kind;
