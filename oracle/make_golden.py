@@ -254,8 +254,8 @@ def main():
         dump_problem("c2_32", problems.make_c2(seed=0, n=32), 4, False)
     if "c4_16" in which:
         dump_problem("c4_16", problems.make_c4(seed=0, n=16), 4, False, four_field=True)
-    if "c3_64" in which:
-        dump_problem("c3_64", problems.make_c3(seed=0, n=64), 4, False, restart=100)
+    if "c3_16" in which:
+        dump_problem("c3_16", problems.make_c3(seed=0, n=16), 4, False, restart=100)
 
 
 if __name__ == "__main__":

@@ -49,7 +49,7 @@ CASES = {
     "c1_16": (lambda: problems.make_c1(seed=0, n=16), None, False),
     "c2_32": (lambda: problems.make_c2(seed=0, n=32), 4, False),
     "c4_16": (lambda: problems.make_c4(seed=0, n=16), 4, True),
-    "c3_64": (lambda: problems.make_c3(seed=0, n=64), 4, False),
+    "c3_16": (lambda: problems.make_c3(seed=0, n=16), 4, False),
 }
 
 

@@ -145,7 +145,7 @@ def test_amg_laplacian_bitwise(pk, t, npart):
 # MGR hierarchies on the generated poromechanics problems
 # ---------------------------------------------------------------------------
 
-ALL_TAGS = ["c1_6", "c2_6", "c4_4", "c1_16", "c4_16", "c2_32", "c3_64"]
+ALL_TAGS = ["c1_6", "c2_6", "c4_4", "c1_16", "c4_16", "c2_32", "c3_16"]
 
 def available(tags):
     import os

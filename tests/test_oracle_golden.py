@@ -92,7 +92,7 @@ SLOW = pytest.mark.skipif(not os.environ.get("PMGR_SLOW"), reason="set PMGR_SLOW
 
 @pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16", "c4_16",
                                  pytest.param("c2_32", marks=pytest.mark.slow),
-                                 pytest.param("c3_64", marks=[pytest.mark.slow, SLOW])])
+                                 pytest.param("c3_16", marks=[pytest.mark.slow, SLOW])])
 def test_mgr_problem(tag):
     d = load(tag)
     full = "mgr0_isc" in d.files
