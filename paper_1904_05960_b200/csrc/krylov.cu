@@ -230,13 +230,22 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
             P.vin[i] = t;
         }
     }
-    if (b != 0 || threadIdx.x != 0) return;
-    // Hessenberg column j and Givens rotation (one thread, carry in registers)
+    if (b != 0) return;
+    // Hessenberg column j and Givens rotation: block 0 stages the previous
+    // rotations in shared memory, one thread applies them (carry in registers)
+    double *css = as_;  // a is no longer needed
+    __shared__ double sns[1024];
+    for (int i = threadIdx.x; i < j; i += AO_THREADS) {
+        css[i] = P.cs[i];
+        sns[i] = P.sn[i];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     const int m = P.dev->m;
     double carry = hs[0];
     for (int i = 0; i < j; ++i) {
         const double next = hs[i + 1];
-        const double c = P.cs[i], sn = P.sn[i];
+        const double c = css[i], sn = sns[i];
         P.H[(int64_t)i * m + j] = c * carry + sn * next;
         carry = -sn * carry + c * next;
     }
