@@ -605,6 +605,14 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
 
 }  // namespace
 
+bool amg_cycle_rows(pmgr_amg &h, const double *v, const int64_t *rows, double *out, cudaStream_t s) {
+    if (h.levels.empty() || !h.levels[0].jacobi) return false;
+    AmgLevel &L = h.levels[0];
+    vec_gather_div(v, rows, L.dtilde.p, L.A->nrows, L.b.p, L.x.p, s);
+    cycle_from_zero(h, 0, s, out);
+    return true;
+}
+
 void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaStream_t s) {
     if (h.levels.empty()) {
         const int64_t n = h.coarse->nrows;

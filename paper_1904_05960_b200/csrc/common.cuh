@@ -320,6 +320,9 @@ void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s);
 void spmv_restrict_div(const CsrView &R, const double *r, const double *d, double *b, double *x,
                        cudaStream_t s);
 void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s);
+// bo = v[rows], xo = bo / d (gathered right-hand side + first l1-Jacobi sweep)
+void vec_gather_div(const double *v, const int64_t *rows, const double *d, int64_t n, double *bo, double *xo,
+                    cudaStream_t s);
 void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows,
                      double *r, cudaStream_t s);
 void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,

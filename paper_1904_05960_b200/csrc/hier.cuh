@@ -50,6 +50,9 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A, const pmgr_amg
 // out = V-cycle(h, b, x); x may be null (zero initial guess).  b/out are
 // length n_0 device vectors; out may alias neither b nor x.
 void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaStream_t s);
+// zero-guess cycle on the right-hand side v[rows] (gather fused into the
+// first sweep); false when the hierarchy cannot take that path
+bool amg_cycle_rows(pmgr_amg &h, const double *v, const int64_t *rows, double *out, cudaStream_t s);
 
 // One MGR reduction level (reference mgr.py:300-311).
 struct MgrLevel {

@@ -239,8 +239,20 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
     MgrLevel &L = h.levels[l];
     const bool pre = !h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE;
     if (pre) {
-        vec_gather(v, L.f_rows.p, L.nf, L.vf.p, s);
-        f_relax_apply(L, L.vf.p, L.zf.p, s);
+        // single sweep: the F gather is fused into the relaxation's first kernel
+        bool done = false;
+        if (L.f_relax_sweeps == 1) {
+            if (L.f_relax == PMGR_FRELAX_AMG) {
+                done = amg_cycle_rows(*L.amg, v, L.f_rows.p, L.zf.p, s);
+            } else {
+                vec_scale_gather(v, L.f_rows.p, L.dinv_ff.p, L.nf, L.zf.p, s);
+                done = true;
+            }
+        }
+        if (!done) {
+            vec_gather(v, L.f_rows.p, L.nf, L.vf.p, s);
+            f_relax_apply(L, L.vf.p, L.zf.p, s);
+        }
         spmv_resid_rows(L.A_cf.view(), L.zf.p, v, L.c_rows.p, L.rc.p, s);
     } else {
         vec_gather(v, L.c_rows.p, L.nc, L.rc.p, s);

@@ -283,6 +283,27 @@ __global__ void k_copy_div(const double *__restrict__ b, const double *__restric
 }
 }  // namespace
 
+namespace {
+__global__ void k_gather_div(const double *__restrict__ v, const int64_t *__restrict__ rows,
+                             const double *__restrict__ d, int64_t n, double *__restrict__ bo,
+                             double *__restrict__ xo) {
+    pdl_wait();
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double t = v[rows[i]];
+        bo[i] = t;
+        xo[i] = t / d[i];
+    }
+}
+}  // namespace
+
+void vec_gather_div(const double *v, const int64_t *rows, const double *d, int64_t n, double *bo, double *xo,
+                    cudaStream_t s) {
+    if (n == 0) return;
+    launch_pdl(k_gather_div, dim3(grid_for(n, 256)), dim3(256), 0, s, v, rows, d, n, bo, xo);
+    PMGR_LAUNCHED();
+}
+
 void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s) {
     if (n == 0) return;
     launch_pdl(k_copy_div, dim3(grid_for(n, 256)), dim3(256), 0, s, b, d, n, bo, xo);
