@@ -321,12 +321,23 @@ def run_gpu(args, rank, world, local_rank):
                                                      "cgs2_step") and v["gbs"]}
     dom = max(cands, key=lambda k: cands[k]["ms_total"]) if cands else None
     roof = None
+    traffic = args.traffic
+    tfile = os.path.join(REPO, "profiles", "roofline_traffic.json")
+    if traffic is None and os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                tj = json.load(f)
+            if tj.get("kernel") == dom and tj.get("config") == args.config:
+                traffic = float(tj["dram_bytes_per_launch"])
+        except Exception:
+            traffic = None
     if dom:
         d = prof[dom]
         roof = {"kernel": dom, "bound": "hbm", "achieved": d["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": d["gbs"] / peak, "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
                 "bytes_per_launch": d["bytes_total"] / d["launches"], "avg_launch_us": d["avg_us"],
-                "traffic": args.traffic}
+                "traffic": traffic, "traffic_source": "profiles/roofline_traffic.json (ncu --set full, "
+                                                       "dram__bytes_read.sum + dram__bytes_write.sum)"}
 
     if rank != 0:
         if dist is not None:
