@@ -425,6 +425,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         TBuf<int32_t> sci(snnz, s);
         k_mask_compact<<<grid_for(n * 32, 256), 256, 0, s>>>(n, Av.ro, Av.ci, mask.p, sro.p, sci.p);
         PMGR_LAUNCHED();
+        setup_trace("amg strength", (int64_t)h->levels.size(), s);
         // ---- measures and S^T
         TBuf<int32_t> meas(n, s);
         PMGR_CUDA(cudaMemsetAsync(meas.p, 0, sizeof(int32_t) * n, s));
@@ -438,6 +439,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         TBuf<int32_t> tci(snnz, s);
         k_transpose_pattern<<<grid_for(n, 256), 256, 0, s>>>(n, sro.p, sci.p, cursor.p, tci.p);
         PMGR_LAUNCHED();
+        setup_trace("amg measure+transpose", (int64_t)h->levels.size(), s);
         // ---- lexicographically-first MIS rounds
         TBuf<int8_t> status(n, s);
         TBuf<int> undec(1, s);
@@ -459,6 +461,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         if (nc == n) break;  // coarsening stagnated (amg.py:196-198)
         k_cindex<<<grid_for(n, 256), 256, 0, s>>>(n, lev.is_c.p, cscan.p, cidx.p);
         PMGR_LAUNCHED();
+        setup_trace("amg MIS", (int64_t)h->levels.size(), s);
         // ---- direct interpolation
         TBuf<double> alpha(n, s), diag(n, s);
         TBuf<int64_t> pcnt(n, s);
@@ -481,6 +484,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         k_interp_fill<<<grid_for(n * 32, 256), 256, 0, s>>>(n, Av.ro, Av.ci, Av.v, mask.p, lev.is_c.p, cidx.p,
                                                             alpha.p, diag.p, lev.P.ro.p, lev.P.ci.p, lev.P.v.p);
         PMGR_LAUNCHED();
+        setup_trace("amg interpolation", (int64_t)h->levels.size(), s);
         // ---- Galerkin (P^T A) P, zero dropping after each product
         csr_finalize(lev.P, s);
         csr_transpose(lev.P.view(), lev.R, s);
@@ -490,6 +494,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         auto next = std::make_shared<Csr>();
         spgemm(T1.view(), lev.P.view(), 0, *next, s);
         csr_finalize(*next, s);
+        setup_trace("amg Galerkin", (int64_t)h->levels.size(), s);
         // ---- l1 diagonal with the contiguous partitions
         lev.jacobi = cfg.npartitions >= n;
         lev.dtilde.alloc(n);
@@ -511,6 +516,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         PMGR_LAUNCHED();
         unsigned long long b = read_scalar(bad.p, s);
         if (b != ~0ull) fail(PMGR_ERR_L1_VANISHES, "l1 diagonal vanishes at row " + std::to_string(b), (int64_t)b);
+        setup_trace("amg l1 diagonal", (int64_t)h->levels.size(), s);
         // ---- next level functions
         TBuf<int32_t> nfuncs(nc, s);
         k_gather_i32<<<grid_for(n, 256), 256, 0, s>>>(funcs.p, cidx.p, n, nfuncs.p);
@@ -547,7 +553,9 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         PMGR_LAUNCHED();
         PMGR_CUDA(cudaStreamSynchronize(s));
     }
+    setup_trace("amg coarsest inverse", (int64_t)h->levels.size(), s);
     collapse_tail(*h, s);
+    setup_trace("amg collapse", h->collapse_from, s);
     return h;
 }
 

@@ -73,6 +73,10 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();
 
+// PMGR_SETUP_TRACE=1: synchronise and print the wall time of each setup
+// phase to stderr (diagnostics only; off by default)
+void setup_trace(const char *what, int64_t level, cudaStream_t s);
+
 template <class... KArgs, class... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args... args) {

@@ -330,6 +330,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         k_index_maps<<<grid_for(n, 256), 256, 0, s>>>(n, L.is_c.p, cscan.p, fscan.p, c_index.p, L.f_index.p,
                                                      L.c_rows.p, L.f_rows.p);
         PMGR_LAUNCHED();
+        setup_trace("mgr split", li, s);
         // ---- blocks (extract_blocks, sparse.py:269-288)
         const CsrView Av = cur->view();
         auto A_ff = std::make_shared<Csr>();
@@ -338,6 +339,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         extract_block(Av, L.f_rows.p, L.nf, L.is_c.p, true, c_index.p, L.nc, A_fc, s);
         extract_block(Av, L.c_rows.p, L.nc, L.is_c.p, false, L.f_index.p, L.nf, L.A_cf, s);
         if (sp.n_max >= 0) extract_block(Av, L.c_rows.p, L.nc, L.is_c.p, true, c_index.p, L.nc, A_cc, s);
+        setup_trace("mgr blocks", li, s);
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
         csr_finalize(*A_ff, s);
@@ -368,6 +370,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             PMGR_LAUNCHED();
         }
         csr_finalize(L.P, s);
+        setup_trace("mgr transfers", li, s);
         // ---- F-relaxation (_build_f_relax, mgr.py:374-386)
         L.f_relax = sp.f_relax;
         L.f_relax_sweeps = sp.f_relax_sweeps > 1 ? sp.f_relax_sweeps : 1;
@@ -378,6 +381,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             L.amg->prof_tag = (li == 0);
         }
         if (sp.f_relax == PMGR_FRELAX_JACOBI && L.f_relax_sweeps > 1) L.A_ff = A_ff;
+        setup_trace("mgr F-relax AMG", li, s);
         // ---- coarse operator (build_coarse, mgr.py:212-231)
         auto coarse = std::make_shared<Csr>();
         {
@@ -401,6 +405,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             }
         }
         csr_finalize(*coarse, s);
+        setup_trace("mgr coarse RAP", li, s);
         // ---- workspace
         L.vf.alloc(L.nf);
         L.zf.alloc(L.nf);

@@ -1,4 +1,5 @@
 // prims.cu -- scans, segmented sorts and reductions (CUB device primitives).
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <cub/device/device_scan.cuh>
@@ -104,6 +105,20 @@ void prof_query(int kind, int64_t *count, double *ms, double *bytes) {
     *count = g_count[kind];
     *ms = g_ms[kind];
     *bytes = g_bytes[kind];
+}
+
+void setup_trace(const char *what, int64_t level, cudaStream_t s) {
+    static const bool on = [] {
+        const char *e = getenv("PMGR_SETUP_TRACE");
+        return e && e[0] != '0';
+    }();
+    if (!on) return;
+    static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pmgr setup] %-28s level %3lld  %9.3f ms\n", what, (long long)level,
+            std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
 }
 
 bool pdl_enabled() {
