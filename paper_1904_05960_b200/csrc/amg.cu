@@ -381,6 +381,80 @@ __global__ void __launch_bounds__(1024) k_gauss_jordan(int64_t n, double *A, dou
     }
 }
 
+// Gauss-Jordan for larger coarsest grids: five small launches per pivot
+__global__ void k_gj_pivot(int64_t n, int64_t k, const double *A, int64_t *piv, int *singular) {
+    __shared__ double sval[32];
+    __shared__ int64_t sidx[32];
+    double best = -1.0;
+    int64_t bi = n;
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) {
+        double a = fabs(A[i * n + k]);
+        if (a > best) {
+            best = a;
+            bi = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(FULL, best, o);
+        int64_t oi = __shfl_xor_sync(FULL, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sval[threadIdx.x >> 5] = best;
+        sidx[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = -1.0;
+        int64_t p = n;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            if (sval[w] > b || (sval[w] == b && sidx[w] < p)) {
+                b = sval[w];
+                p = sidx[w];
+            }
+        *piv = p;
+        if (b == 0.0) *singular = 1;
+    }
+}
+
+__global__ void k_gj_swap(int64_t n, int64_t k, const int64_t *piv, double *A, double *X) {
+    const int64_t p = *piv;
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p == k || j >= n) return;
+    double t = A[k * n + j];
+    A[k * n + j] = A[p * n + j];
+    A[p * n + j] = t;
+    t = X[k * n + j];
+    X[k * n + j] = X[p * n + j];
+    X[p * n + j] = t;
+}
+
+__global__ void k_gj_col(int64_t n, int64_t k, const double *A, double *colk) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) colk[i] = A[i * n + k];
+}
+
+__global__ void k_gj_scale(int64_t n, int64_t k, const double *colk, double *A, double *X) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const double inv = 1.0 / colk[k];
+    A[k * n + j] *= inv;
+    X[k * n + j] *= inv;
+}
+
+__global__ void k_gj_elim(int64_t n, int64_t k, const double *colk, double *A, double *X) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i = blockIdx.y;
+    if (j >= n || i == k) return;
+    const double f = colk[i];
+    if (f == 0.0) return;
+    A[i * n + j] -= f * A[k * n + j];
+    X[i * n + j] -= f * X[k * n + j];
+}
+
 std::vector<int64_t> partition_starts(int64_t n, int64_t nparts) {
     // reference PartitionSet.contiguous (smoothers.py:67-75), align = 1
     int64_t np_ = nparts < n ? nparts : n;
@@ -549,8 +623,22 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         PMGR_LAUNCHED();
         k_identity<<<grid_for(nc * nc, 256), 256, 0, s>>>(nc, h->coarse_inv.p);
         PMGR_LAUNCHED();
-        k_gauss_jordan<<<1, 1024, 0, s>>>(nc, M.p, h->coarse_inv.p, colk.p, sing.p);
-        PMGR_LAUNCHED();
+        if (nc <= 512) {
+            k_gauss_jordan<<<1, 1024, 0, s>>>(nc, M.p, h->coarse_inv.p, colk.p, sing.p);
+            PMGR_LAUNCHED();
+        } else {
+            TBuf<int64_t> piv(1, s);
+            const unsigned gx = grid_for(nc, 256);
+            for (int64_t k = 0; k < nc; ++k) {
+                k_gj_pivot<<<1, 1024, 0, s>>>(nc, k, M.p, piv.p, sing.p);
+                k_gj_swap<<<gx, 256, 0, s>>>(nc, k, piv.p, M.p, h->coarse_inv.p);
+                k_gj_col<<<gx, 256, 0, s>>>(nc, k, M.p, colk.p);
+                k_gj_scale<<<gx, 256, 0, s>>>(nc, k, colk.p, M.p, h->coarse_inv.p);
+                k_gj_elim<<<dim3(gx, (unsigned)nc), 256, 0, s>>>(nc, k, colk.p, M.p, h->coarse_inv.p);
+                g_launches.fetch_add(5, std::memory_order_relaxed);
+            }
+            PMGR_CUDA(cudaPeekAtLastError());
+        }
         PMGR_CUDA(cudaStreamSynchronize(s));
     }
     setup_trace("amg coarsest inverse", (int64_t)h->levels.size(), s);

@@ -447,6 +447,7 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
     k_table_size<<<grid_for(n, 256), 256, 0, s>>>(n, ub.p, tsz.p);
     PMGR_LAUNCHED();
     int64_t gtotal = exclusive_scan_total(tsz.p, toff.p, n, s);
+    setup_trace("  spgemm bounds", gtotal, s);
     TBuf<int32_t> gkeys(gtotal, s);
     TBuf<double> gvals(mode >= 0 ? gtotal : 0, s);
 
@@ -466,12 +467,15 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
                                                        gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
     PMGR_LAUNCHED();
     int64_t total = exclusive_scan_total(cnt.p, cro.p, n, s);
+    setup_trace("  spgemm symbolic", total, s);
     TBuf<int32_t> tci(total, s);
     TBuf<double> tv(total, s);
     k_spgemm<true><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
                                                       gkeys.p, gvals.p, nullptr, cro.p, tci.p, tv.p);
     PMGR_LAUNCHED();
+    setup_trace("  spgemm numeric", total, s);
     segmented_sort_pairs(tci.p, tv.p, total, cro.p, n, s);
+    setup_trace("  spgemm sort", total, s);
     if (mode == 1) {
         C.nrows = n;
         C.ncols = Y.ncols;

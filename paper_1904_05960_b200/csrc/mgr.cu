@@ -287,7 +287,12 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
     for (int li = 0; li < nlevels; ++li) {
         const pmgr_level_spec &sp = specs[li];
         std::set<int> present;
-        for (int8_t t : fo) present.insert((int)t);
+        {
+            bool seen[256] = {};
+            for (int8_t t : fo) seen[(uint8_t)t] = true;
+            for (int t = 0; t < 256; ++t)
+                if (seen[t]) present.insert((int)(int8_t)t);
+        }
         std::set<int> spec_f;
         for (int t = 0; t < 64; ++t)
             if (((sp.f_mask | sp.c_mask) >> t) & 1ull) spec_f.insert(t);
