@@ -1,0 +1,237 @@
+"""z-slab domain decomposition: ownership, halo plans and the distributed
+Krylov plumbing.
+
+One process per GPU.  Rank r owns the node planes and cell layers
+z in [z0_r, z1_r) of the structured poromechanics grid (the last rank also
+owns the top node plane) and every dof living on them.  Rows stay in the
+global ordering's relative order, columns keep their global stored order
+inside each row, so a row's products are summed in the same order on any
+number of ranks.  Communication happens only where the path has a real
+exchange step:
+
+* halo exchange of x before every SpMV / smoother / transfer (point-to-point
+  with the z-neighbours; NCCL over NVLink on the GPU, gloo in CPU tests);
+* all-reduce of the Arnoldi projections and norms.
+
+The local compute is pluggable (`local_matvec`): libpmgr's SpMV on the GPU,
+the oracle in the CPU tests.  Round 1 ships this layer with its tests; the
+distributed MGR hierarchy (ghost rows for strength/interpolation, a status
+halo per MIS round, P_ext for the RAP products) is the next step, so
+`bench.py --gpus N` still runs replicas.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def slab_bounds(nz: int, nranks: int):
+    """Cell-layer ranges [z0, z1) per rank (near-equal, contiguous)."""
+    if nranks < 1 or nranks > nz:
+        raise ValueError(f"cannot split {nz} cell layers over {nranks} ranks")
+    b = [(r * nz) // nranks for r in range(nranks + 1)]
+    return [(b[r], b[r + 1]) for r in range(nranks)]
+
+
+def dof_owner(pb, nranks: int) -> np.ndarray:
+    """Owning rank of every dof of a generated problem (problems.Problem)."""
+    bounds = slab_bounds(pb.nz, nranks)
+    zcell_owner = np.empty(pb.nz, dtype=np.int32)
+    for r, (z0, z1) in enumerate(bounds):
+        zcell_owner[z0:z1] = r
+    # node plane k belongs to the rank owning cell layer k (top plane -> last rank)
+    znode_owner = np.empty(pb.nz + 1, dtype=np.int32)
+    znode_owner[:pb.nz] = zcell_owner
+    znode_owner[pb.nz] = nranks - 1
+    n_u = pb.n_u
+    owner = np.empty(pb.n, dtype=np.int32)
+    node = pb.entity_of[:n_u].astype(np.int64)
+    owner[:n_u] = znode_owner[node // ((pb.nx + 1) * (pb.ny + 1))]
+    cell = pb.entity_of[n_u:].astype(np.int64)
+    owner[n_u:] = zcell_owner[cell // (pb.nx * pb.ny)]
+    return owner
+
+
+@dataclass
+class HaloPlan:
+    """What rank `rank` owns, what it must receive, and what it must send."""
+
+    rank: int
+    nranks: int
+    owned: np.ndarray                    # global ids, ascending
+    ghosts: np.ndarray                   # global ids needed but not owned, ascending
+    recv_from: dict = field(default_factory=dict)   # peer -> positions in ghosts (ascending global id)
+    send_to: dict = field(default_factory=dict)     # peer -> local owned indices to send
+    # local CSR over owned rows; columns index [owned | ghosts]
+    ro: np.ndarray = None
+    ci: np.ndarray = None
+    v: np.ndarray = None
+
+    @property
+    def n_own(self) -> int:
+        return len(self.owned)
+
+    @property
+    def n_ext(self) -> int:
+        return len(self.owned) + len(self.ghosts)
+
+
+def build_halo_plan(ro, ci, v, owner: np.ndarray, rank: int, nranks: int) -> HaloPlan:
+    """Local rows, ghost columns and the send/recv lists of one rank.
+
+    The send lists are derived symmetrically (every rank computes what each
+    peer needs from it), so no communication is needed to build the plan.
+    """
+    ro = np.asarray(ro, dtype=np.int64)
+    ci = np.asarray(ci, dtype=np.int64)
+    owned = np.flatnonzero(owner == rank)
+    gl2own = np.full(len(owner), -1, dtype=np.int64)
+    gl2own[owned] = np.arange(len(owned))
+    starts, ends = ro[owned], ro[owned + 1]
+    cnt = ends - starts
+    take = np.repeat(starts - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt) + np.arange(cnt.sum())
+    cols = ci[take]
+    ghosts = np.unique(cols[owner[cols] != rank])
+    plan = HaloPlan(rank, nranks, owned, ghosts)
+    gpos = np.searchsorted(ghosts, cols)
+    local = np.where(owner[cols] == rank, gl2own[cols], len(owned) + gpos)
+    plan.ro = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+    plan.ci = local.astype(np.int32)
+    plan.v = np.asarray(v)[take] if v is not None else None
+    for peer in range(nranks):
+        if peer == rank:
+            continue
+        mine = np.flatnonzero(owner[ghosts] == peer)
+        if len(mine):
+            plan.recv_from[peer] = mine
+        # what `peer` needs from me: ghosts of peer that I own, ascending
+        p_owned = np.flatnonzero(owner == peer)
+        p_cnt = ro[p_owned + 1] - ro[p_owned]
+        p_take = np.repeat(ro[p_owned] - np.concatenate([[0], np.cumsum(p_cnt)[:-1]]), p_cnt) + np.arange(p_cnt.sum())
+        p_cols = np.unique(ci[p_take])
+        need = p_cols[owner[p_cols] == rank]
+        if len(need):
+            plan.send_to[peer] = gl2own[need]
+    return plan
+
+
+def halo_exchange(x_ext, plan: HaloPlan, dist, group=None):
+    """Fill the ghost part of x_ext (torch tensor of length n_ext) from the
+    owning ranks: one isend/irecv pair per neighbour."""
+    import torch
+
+    n = plan.n_own
+    reqs, bufs = [], []
+    for peer, idx in plan.recv_from.items():
+        buf = torch.empty(len(idx), dtype=x_ext.dtype, device=x_ext.device)
+        bufs.append((peer, idx, buf))
+        reqs.append(dist.irecv(buf, src=peer, group=group))
+    for peer, idx in plan.send_to.items():
+        sidx = torch.as_tensor(idx, device=x_ext.device)
+        reqs.append(dist.isend(x_ext[:n].index_select(0, sidx).contiguous(), dst=peer, group=group))
+    for r in reqs:
+        r.wait()
+    for peer, idx, buf in bufs:
+        x_ext[n + torch.as_tensor(idx, device=x_ext.device)] = buf
+    return x_ext
+
+
+def dist_dots(V_rows, w, dist, group=None):
+    """Global dot products of the rows of V with w (one all-reduce)."""
+    import torch
+
+    local = V_rows @ w
+    dist.all_reduce(local, group=group)
+    return local
+
+
+def dist_norm(w, dist, group=None) -> float:
+    import torch
+
+    s = torch.dot(w, w).reshape(1)
+    dist.all_reduce(s, group=group)
+    return float(torch.sqrt(s))
+
+
+class DistOperator:
+    """v (owned part) -> A v (owned rows) with a halo exchange first."""
+
+    def __init__(self, plan: HaloPlan, local_matvec, dist, group=None):
+        self.plan, self.local_matvec, self.dist, self.group = plan, local_matvec, dist, group
+
+    def __call__(self, v_own):
+        import torch
+
+        x_ext = torch.zeros(self.plan.n_ext, dtype=v_own.dtype, device=v_own.device)
+        x_ext[:self.plan.n_own] = v_own
+        halo_exchange(x_ext, self.plan, self.dist, self.group)
+        return self.local_matvec(x_ext)
+
+
+def dist_gmres(apply_A, apply_M_inv, b, dist, group=None, restart=50, max_iters=500, rtol=1e-6, atol=1e-12):
+    """Right-preconditioned restarted GMRES (reference krylov.py:39-117) on
+    row-distributed vectors: classical Gram-Schmidt with one
+    re-orthogonalisation, one all-reduce per projection; the small
+    Hessenberg algebra is replicated on every rank."""
+    import torch
+    from scipy.linalg import solve_triangular
+
+    n = b.numel()
+    M = (lambda v: v) if apply_M_inv is None else apply_M_inv
+    x = torch.zeros_like(b)
+    r = b.clone()
+    beta = dist_norm(r, dist, group)
+    hist = [beta]
+    tol = max(rtol * beta, atol)
+    total = 0
+    brk = False
+    while beta > tol and total < max_iters:
+        m = restart
+        V = torch.zeros((m + 1, n), dtype=b.dtype, device=b.device)
+        H = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        V[0] = r / beta
+        g[0] = beta
+        j = 0
+        while j < m and total < max_iters:
+            w = apply_A(M(V[j]))
+            h = np.zeros(j + 1)
+            for _ in range(2):
+                c = dist_dots(V[:j + 1], w, dist, group)
+                w = w - c @ V[:j + 1]
+                h += c.cpu().numpy()
+            H[:j + 1, j] = h
+            hn = dist_norm(w, dist, group)
+            H[j + 1, j] = hn
+            if hn > 1e-12 * max(float(np.linalg.norm(H[:j + 2, j])), 1e-300):
+                V[j + 1] = w / hn
+            else:
+                brk = True
+            for i in range(j):
+                t = H[i, j]
+                H[i, j] = cs[i] * t + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * t + cs[i] * H[i + 1, j]
+            rho = float(np.hypot(H[j, j], H[j + 1, j]))
+            if rho == 0.0:
+                brk = True
+                break
+            cs[j], sn[j] = H[j, j] / rho, H[j + 1, j] / rho
+            H[j, j], H[j + 1, j] = rho, 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            j += 1
+            hist.append(abs(float(g[j])))
+            if abs(g[j]) <= tol or brk:
+                break
+        if j > 0:
+            y = solve_triangular(H[:j, :j], g[:j], lower=False)
+            x = x + M(torch.as_tensor(y, dtype=b.dtype, device=b.device) @ V[:j])
+            r = b - apply_A(x)
+            beta = dist_norm(r, dist, group)
+            hist[-1] = beta
+        if brk:
+            break
+    return x, total, np.array(hist), bool(beta <= tol)
