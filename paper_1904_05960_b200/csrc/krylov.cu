@@ -114,8 +114,13 @@ __device__ __forceinline__ double block_sum1(double v, double *sh) {
     return t;
 }
 
+// SM = true: the block's slices of w and V_j live in shared memory, so the
+// basis stream is the only per-vector L2/HBM traffic and w never returns to
+// global memory (small and medium n); SM = false streams them from L2.
+template <bool SM>
 __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     cg::grid_group grid = cg::this_grid();
+    extern __shared__ double slice[];  // SM: w slice, then V_j slice
     __shared__ double sh[AO_WARPS];
     __shared__ double hs[1024];   // h
     __shared__ double as_[1024];  // a
@@ -126,7 +131,19 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     const int64_t chunk = (n + nblk - 1) / nblk;
     const int64_t lo = (int64_t)b * chunk;
     const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    const double *vj = P.V + (int64_t)j * n;
+    const double *vjg = P.V + (int64_t)j * n;
+    double *wsl = slice;
+    double *vsl = slice + chunk;
+    if (SM) {
+        for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
+            wsl[i - lo] = P.w[i];
+            vsl[i - lo] = vjg[i];
+        }
+        __syncthreads();
+    }
+    // row-indexed accessors for the w / V_j slices (shared or global)
+    auto wv = [&](int64_t i) { return SM ? wsl[i - lo] : P.w[i]; };
+    auto vj = [&](int64_t i) { return SM ? vsl[i - lo] : vjg[i]; };
 
     // phase 1: slice partials of V_k.w and V_k.V_j
     for (int k = warp; k <= j; k += AO_WARPS) {
@@ -141,8 +158,8 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 xs[u] = x[i + 32 * u];
-                ws[u] = P.w[i + 32 * u];
-                vs[u] = vj[i + 32 * u];
+                ws[u] = wv(i + 32 * u);
+                vs[u] = vj(i + 32 * u);
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -151,8 +168,8 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
             }
         }
         for (; i < hi; i += 32) {
-            aa[0] = fma(x[i], P.w[i], aa[0]);
-            gg[0] = fma(x[i], vj[i], gg[0]);
+            aa[0] = fma(x[i], wv(i), aa[0]);
+            gg[0] = fma(x[i], vj(i), gg[0]);
         }
         const double sa = warp_sum(((aa[0] + aa[1]) + (aa[2] + aa[3])) + ((aa[4] + aa[5]) + (aa[6] + aa[7])));
         const double sg = warp_sum(((gg[0] + gg[1]) + (gg[2] + gg[3])) + ((gg[4] + gg[5]) + (gg[6] + gg[7])));
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     double nrm = 0.0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
         double acc[8];
-        acc[0] = P.w[i];
+        acc[0] = wv(i);
 #pragma unroll
         for (int t = 1; t < 8; ++t) acc[t] = 0.0;
         int k = 0;
@@ -207,7 +224,8 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
         }
         for (; k <= j; ++k) acc[0] = fma(-hs[k], P.V[(int64_t)k * n + i], acc[0]);
         const double wi = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        P.w[i] = wi;
+        if (SM) wsl[i - lo] = wi;  // same thread reads it back in phase 4
+        else P.w[i] = wi;
         nrm = fma(wi, wi, nrm);
     }
     nrm = block_sum1(nrm, sh);
@@ -225,7 +243,7 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     if (!brk && j + 1 <= P.dev->m) {
         double *vn = P.V + (int64_t)(j + 1) * n;
         for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
-            const double t = P.w[i] / hn;
+            const double t = (SM ? wsl[i - lo] : P.w[i]) / hn;
             vn[i] = t;
             P.vin[i] = t;
         }
@@ -398,6 +416,8 @@ struct Ws {
     int m = 0, max_iters = 0;
     int64_t n = 0;
     int nblk = 1, nupd = 1;
+    bool use_smem = false;
+    size_t smem = 0;
     DBuf<double> V, w, z, r, vin, u;
     DBuf<double> H, G, cs, sn, g, a, h, y, hist, pa, pg, pn, beta;
     DBuf<Dev> dev;
@@ -442,9 +462,24 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
     w->hist.alloc((int64_t)max_iters + 2);
     // the cooperative Arnoldi kernel: every block resident at once
     int per_sm = 0;
-    PMGR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi, AO_THREADS, 0));
+    PMGR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi<false>, AO_THREADS, 0));
     if (per_sm < 1) fail(PMGR_ERR_CUDA, "Arnoldi kernel cannot be resident");
     w->nblk = (per_sm < 2 ? per_sm : 2) * num_sms();
+    {
+        const int64_t chunk = (n + w->nblk - 1) / w->nblk;
+        int per_sm_sm = 0;
+        w->smem = (size_t)(16 * chunk);
+        if (chunk <= 3072 &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sm, k_arnoldi<true>, AO_THREADS, w->smem) ==
+                cudaSuccess &&
+            per_sm_sm * num_sms() >= w->nblk) {
+            w->use_smem = true;
+        } else {
+            cudaGetLastError();
+            w->use_smem = false;
+            w->smem = 0;
+        }
+    }
     w->pa.alloc((int64_t)(m + 1) * w->nblk);
     w->pg.alloc((int64_t)(m + 1) * w->nblk);
     w->nupd = 4 * num_sms();
@@ -504,13 +539,15 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(W.nblk);
     cfg.blockDim = dim3(AO_THREADS);
+    cfg.dynamicSmemBytes = W.smem;
     cfg.stream = s;
     cudaLaunchAttribute at;
     at.id = cudaLaunchAttributeCooperative;
     at.val.cooperative = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    PMGR_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi, P));
+    if (W.use_smem) PMGR_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi<true>, P));
+    else PMGR_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi<false>, P));
     PMGR_LAUNCHED();
 }
 
