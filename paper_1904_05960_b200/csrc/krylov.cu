@@ -464,7 +464,9 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
     int per_sm = 0;
     PMGR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi<false>, AO_THREADS, 0));
     if (per_sm < 1) fail(PMGR_ERR_CUDA, "Arnoldi kernel cannot be resident");
-    w->nblk = (per_sm < 2 ? per_sm : 2) * num_sms();
+    int bps = 2;
+    if (const char *e = getenv("PMGR_ARNOLDI_BPS")) bps = atoi(e) > 0 ? atoi(e) : 2;
+    w->nblk = (per_sm < bps ? per_sm : bps) * num_sms();
     {
         const int64_t chunk = (n + w->nblk - 1) / w->nblk;
         int per_sm_sm = 0;
