@@ -101,7 +101,16 @@ struct AoParams {
     double *H, *cs, *sn, *g, *hist;
     cudaGraphConditionalHandle cond;
     int use_cond;
+    unsigned long long *stamps;  // PMGR_ARNOLDI_STAMPS: phase timestamps of block 0 (diagnostics)
 };
+
+__device__ __forceinline__ void stamp(const AoParams &P, int slot) {
+    if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicAdd(P.stamps + slot, t);
+    }
+}
 
 __device__ __forceinline__ double block_sum1(double v, double *sh) {
     v = warp_sum(v);
@@ -131,6 +140,7 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     const int64_t chunk = (n + nblk - 1) / nblk;
     const int64_t lo = (int64_t)b * chunk;
     const int64_t hi = lo + chunk < n ? lo + chunk : n;
+    stamp(P, 0);
     const double *vjg = P.V + (int64_t)j * n;
     double *wsl = slice;
     double *vsl = slice + chunk;
@@ -178,7 +188,9 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
             P.pg[(int64_t)k * nblk + b] = sg;
         }
     }
+    stamp(P, 1);
     grid.sync();
+    stamp(P, 2);
     // phase 2a: a_k and the Gram column, one block per coefficient
     for (int k = b; k <= j; k += nblk) {
         double sa = 0.0, sg = 0.0;
@@ -194,7 +206,9 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
             P.G[(int64_t)j * P.ldg + k] = sg;
         }
     }
+    stamp(P, 3);
     grid.sync();
+    stamp(P, 4);
     // phase 2b: h = a + (a - G a), every block for itself (warp per k)
     for (int k = threadIdx.x; k <= j; k += AO_THREADS) as_[k] = P.a[k];
     __syncthreads();
@@ -207,6 +221,7 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     __syncthreads();
     if (b == 0)
         for (int k = threadIdx.x; k <= j; k += AO_THREADS) P.h[k] = hs[k];
+    stamp(P, 7);
     // phase 3: w -= sum_k h_k V_k on this slice, ||w||^2 partial
     double nrm = 0.0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
@@ -230,7 +245,9 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     }
     nrm = block_sum1(nrm, sh);
     if (threadIdx.x == 0) P.pn[b] = nrm;
+    stamp(P, 5);
     grid.sync();
+    stamp(P, 6);
     // phase 4: ||w||, breakdown test, normalisation (every block, same order)
     double s2 = 0.0;
     for (int t = threadIdx.x; t < nblk; t += AO_THREADS) s2 += P.pn[t];
@@ -248,6 +265,7 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
             P.vin[i] = t;
         }
     }
+    stamp(P, 8);
     if (b != 0) return;
     // Hessenberg column j and Givens rotation: block 0 stages the previous
     // rotations in shared memory, one thread applies them (carry in registers)
@@ -421,6 +439,7 @@ struct Ws {
     DBuf<double> V, w, z, r, vin, u;
     DBuf<double> H, G, cs, sn, g, a, h, y, hist, pa, pg, pn, beta;
     DBuf<Dev> dev;
+    DBuf<unsigned long long> stamps;  // diagnostics (null unless PMGR_ARNOLDI_STAMPS)
     Dev *hdev = nullptr;  // pinned mirror
     cudaStream_t cap = nullptr;
     cudaGraphExec_t cycle = nullptr;
@@ -488,6 +507,10 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
     w->pn.alloc(w->nblk > w->nupd ? w->nblk : w->nupd);
     w->beta.alloc(1);
     w->dev.alloc(1);
+    if (getenv("PMGR_ARNOLDI_STAMPS")) {
+        w->stamps.alloc(16);
+        PMGR_CUDA(cudaMemset(w->stamps.p, 0, 16 * sizeof(unsigned long long)));
+    }
     PMGR_CUDA(cudaMallocHost((void **)&w->hdev, sizeof(Dev)));
     PMGR_CUDA(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
     Ws &ref = *w;
@@ -538,6 +561,7 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
     P.hist = W.hist.p;
     P.cond = cond;
     P.use_cond = use_cond;
+    P.stamps = W.stamps.p;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(W.nblk);
     cfg.blockDim = dim3(AO_THREADS);
@@ -689,6 +713,20 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
             ++restarts;
             if (beta <= tol || brk) break;
         }
+    }
+    if (W.stamps.p && total > 0) {
+        unsigned long long st[16];
+        PMGR_CUDA(cudaMemcpy(st, W.stamps.p, sizeof(st), cudaMemcpyDeviceToHost));
+        static const char *names[] = {"phase1", "sync1", "phase2a", "sync2", "phase2b", "phase3", "sync3",
+                                      "phase4"};
+        const int order[] = {0, 1, 2, 3, 4, 7, 5, 6, 8};
+        fprintf(stderr, "[k_arnoldi stamps, mean over %d steps, block 0]", total);
+        for (int q = 0; q + 1 < 9; ++q) {
+            const int a = order[q], b2 = order[q + 1];
+            fprintf(stderr, " %s=%.2fus", names[q], (double)(st[b2] - st[a]) / total / 1e3);
+        }
+        fprintf(stderr, "\n");
+        PMGR_CUDA(cudaMemset(W.stamps.p, 0, sizeof(st)));
     }
     stats.iterations = total;
     stats.converged = beta <= tol;
