@@ -127,7 +127,7 @@ __device__ __forceinline__ double block_sum1(double v, double *sh) {
 // basis stream is the only per-vector L2/HBM traffic and w never returns to
 // global memory (small and medium n); SM = false streams them from L2.
 template <bool SM>
-__global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
+__global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double slice[];  // SM: w slice, then V_j slice
     __shared__ double sh[AO_WARPS];
@@ -155,46 +155,38 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     auto wv = [&](int64_t i) { return SM ? wsl[i - lo] : P.w[i]; };
     auto vj = [&](int64_t i) { return SM ? vsl[i - lo] : vjg[i]; };
 
-    // phase 1: slice partials of V_k.w and V_k.V_j.  Threads own rows, the
-    // basis is walked in chunks of 8 vectors with 8 independent loads in
-    // flight per thread; per chunk one warp reduction of 16 partials and one
-    // pass over the warps.
-    __shared__ double red[AO_WARPS][16];
-    for (int k0 = 0; k0 <= j; k0 += 8) {
-        double pa_[8], pg_[8];
+    // phase 1: slice partials of V_k.w and V_k.V_j
+    for (int k = warp; k <= j; k += AO_WARPS) {
+        const double *x = P.V + (int64_t)k * n;
+        // 8 rows per lane per round: 24 independent loads in flight
+        double aa[8], gg[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) pa_[u] = pg_[u] = 0.0;
-        for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
-            const double wi = wv(i), vi = vj(i);
-            double xs[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) xs[u] = (k0 + u <= j) ? P.V[(int64_t)(k0 + u) * n + i] : 0.0;
+        for (int u = 0; u < 8; ++u) aa[u] = gg[u] = 0.0;
+        int64_t i = lo + lane;
+        for (; i + 7 * 32 < hi; i += 8 * 32) {
+            double xs[8], ws[8], vs[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                pa_[u] = fma(xs[u], wi, pa_[u]);
-                pg_[u] = fma(xs[u], vi, pg_[u]);
+                xs[u] = x[i + 32 * u];
+                ws[u] = wv(i + 32 * u);
+                vs[u] = vj(i + 32 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                aa[u] = fma(xs[u], ws[u], aa[u]);
+                gg[u] = fma(xs[u], vs[u], gg[u]);
             }
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            pa_[u] = warp_sum(pa_[u]);
-            pg_[u] = warp_sum(pg_[u]);
+        for (; i < hi; i += 32) {
+            aa[0] = fma(x[i], wv(i), aa[0]);
+            gg[0] = fma(x[i], vj(i), gg[0]);
         }
+        const double sa = warp_sum(((aa[0] + aa[1]) + (aa[2] + aa[3])) + ((aa[4] + aa[5]) + (aa[6] + aa[7])));
+        const double sg = warp_sum(((gg[0] + gg[1]) + (gg[2] + gg[3])) + ((gg[4] + gg[5]) + (gg[6] + gg[7])));
         if (lane == 0) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                red[warp][2 * u] = pa_[u];
-                red[warp][2 * u + 1] = pg_[u];
-            }
+            P.pa[(int64_t)k * nblk + b] = sa;
+            P.pg[(int64_t)k * nblk + b] = sg;
         }
-        __syncthreads();
-        if (threadIdx.x < 16) {
-            const int u = threadIdx.x >> 1, k = k0 + u;
-            double t = 0.0;
-            for (int w2 = 0; w2 < AO_WARPS; ++w2) t += red[w2][threadIdx.x];
-            if (k <= j) ((threadIdx.x & 1) ? P.pg : P.pa)[(int64_t)k * nblk + b] = t;
-        }
-        __syncthreads();
     }
     stamp(P, 1);
     grid.sync();
