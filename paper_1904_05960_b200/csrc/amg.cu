@@ -670,26 +670,6 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     const bool has_next = l + 1 < h.levels.size();
     const bool tag = h.prof_tag && l == 0;
     const double pass = csr_pass_bytes(A.nrows, A.ncols, A.nnz) + 16.0 * A.nrows;
-    static const int64_t fuse_rows = [] {
-        const char *e = getenv("PMGR_FUSE_ROWS");
-        return e ? atoll(e) : (int64_t)16384;
-    }();
-    if (L.jacobi && A.nrows <= fuse_rows) {
-        // small level: two fused kernels instead of four
-        const double *e;
-        if (has_next) {
-            AmgLevel &N = h.levels[l + 1];
-            const bool nj = N.jacobi;
-            resid_restrict(A, L.R.view(), L.x.p, L.b.p, nj ? N.dtilde.p : nullptr, N.b.p, nj ? N.x.p : nullptr, s);
-            cycle_from_zero(h, l + 1, s);
-            e = N.xo.p;
-        } else {
-            resid_restrict(A, L.R.view(), L.x.p, L.b.p, nullptr, h.cb.p, nullptr, s);
-            e = coarse_solve(h, s);
-        }
-        prolong_jacobi(A, L.P.view(), e, L.x.p, L.b.p, L.dtilde.p, out ? out : L.xo.p, s);
-        return;
-    }
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_SWEEP0 : PROF_KINDS, pass, s);
         spmv_residual(A, L.x.p, L.b.p, L.r.p, s);

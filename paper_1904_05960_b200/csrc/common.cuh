@@ -321,12 +321,6 @@ void spmv_jacobi(const CsrView &A, const double *x, const double *b, const doubl
 void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x,
                           double *r, cudaStream_t s);
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s);
-// small-level fusions (see spmv.cu): b_n = R (b - A x) [, x_n = b_n / d_n];
-// out = x' + (b - A x') / d with x' = x + P e
-void resid_restrict(const CsrView &A, const CsrView &R, const double *x, const double *b, const double *dn,
-                    double *bn, double *xn, cudaStream_t s);
-void prolong_jacobi(const CsrView &A, const CsrView &P, const double *e, const double *x, const double *b,
-                    const double *d, double *out, cudaStream_t s);
 void spmv_restrict_div(const CsrView &R, const double *r, const double *d, double *b, double *x,
                        cudaStream_t s);
 void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s);

@@ -310,89 +310,6 @@ void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, doubl
     PMGR_LAUNCHED();
 }
 
-namespace {
-// Small levels: residual and restriction in one pass.  Warp per coarse row
-// k: for each fine row q of R row k the warp forms r_q = b_q - A_q x with a
-// shuffle reduction and accumulates R_kq r_q (A rows are re-read ~|P row|
-// times, cheap below a few thousand rows, and one launch disappears).
-__global__ void __launch_bounds__(256) k_resid_restrict(int64_t nc, const int64_t *__restrict__ rro,
-                                                        const int32_t *__restrict__ rci,
-                                                        const double *__restrict__ rv,
-                                                        const int64_t *__restrict__ aro,
-                                                        const int32_t *__restrict__ aci,
-                                                        const double *__restrict__ av, const double *__restrict__ x,
-                                                        const double *__restrict__ b, const double *__restrict__ dn,
-                                                        double *bn, double *xn) {
-    pdl_wait();
-    const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (k >= nc) return;
-    double acc = 0.0;
-    for (int64_t t = rro[k]; t < rro[k + 1]; ++t) {
-        const int32_t q = rci[t];
-        double s0 = 0.0, s1 = 0.0;
-        int64_t p = aro[q] + lane;
-        const int64_t e = aro[q + 1];
-        for (; p + 32 < e; p += 64) {
-            s0 = fma(av[p], x[aci[p]], s0);
-            s1 = fma(av[p + 32], x[aci[p + 32]], s1);
-        }
-        if (p < e) s0 = fma(av[p], x[aci[p]], s0);
-        double s = s0 + s1;
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-        acc = fma(rv[t], b[q] - s, acc);
-    }
-    if (lane == 0) {
-        bn[k] = acc;
-        if (xn) xn[k] = acc / dn[k];
-    }
-}
-
-// Small levels: prolongation folded into the post-smoothing sweep,
-// out_i = x'_i + (b_i - A_i x') / dtilde_i with x'_p = x_p + P_p e.
-__global__ void __launch_bounds__(256) k_prolong_jacobi(int64_t n, const int64_t *__restrict__ aro,
-                                                        const int32_t *__restrict__ aci,
-                                                        const double *__restrict__ av,
-                                                        const int64_t *__restrict__ pro,
-                                                        const int32_t *__restrict__ pci,
-                                                        const double *__restrict__ pv, const double *__restrict__ e,
-                                                        const double *__restrict__ x, const double *__restrict__ b,
-                                                        const double *__restrict__ d, double *out) {
-    pdl_wait();
-    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    auto xp = [&](int32_t p) {
-        double t = x[p];
-        for (int64_t c = pro[p]; c < pro[p + 1]; ++c) t = fma(pv[c], e[pci[c]], t);
-        return t;
-    };
-    double s = 0.0;
-    for (int64_t q = aro[i] + lane; q < aro[i + 1]; q += 32) s = fma(av[q], xp(aci[q]), s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == 0) {
-        const double xi = xp((int32_t)i);
-        out[i] = xi + (b[i] - s) / d[i];
-    }
-}
-}  // namespace
-
-void resid_restrict(const CsrView &A, const CsrView &R, const double *x, const double *b, const double *dn,
-                    double *bn, double *xn, cudaStream_t s) {
-    if (R.nrows == 0) return;
-    launch_pdl(k_resid_restrict, dim3(grid_for(R.nrows * 32, 256)), dim3(256), 0, s, R.nrows, R.ro, R.ci, R.v, A.ro,
-               A.ci, A.v, x, b, dn, bn, xn);
-    PMGR_LAUNCHED();
-}
-
-void prolong_jacobi(const CsrView &A, const CsrView &P, const double *e, const double *x, const double *b,
-                    const double *d, double *out, cudaStream_t s) {
-    if (A.nrows == 0) return;
-    launch_pdl(k_prolong_jacobi, dim3(grid_for(A.nrows * 32, 256)), dim3(256), 0, s, A.nrows, A.ro, A.ci, A.v, P.ro,
-               P.ci, P.v, e, x, b, d, out);
-    PMGR_LAUNCHED();
-}
-
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s) {
     launch(A, OpAdd{e, x}, s);
 }
