@@ -78,39 +78,20 @@ bool pdl_enabled();
 void setup_trace(const char *what, int64_t level, cudaStream_t s);
 
 template <class... KArgs, class... Args>
-inline void launch_pdl_l2(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                          const void *l2_base, size_t l2_bytes, float l2_hit, Args... args) {
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    int na = 0;
-    if (pdl_enabled()) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    if (l2_base) {
-        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
-        at[na].val.accessPolicyWindow.base_ptr = const_cast<void *>(l2_base);
-        at[na].val.accessPolicyWindow.num_bytes = l2_bytes;
-        at[na].val.accessPolicyWindow.hitRatio = l2_hit;
-        at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        ++na;
-    }
-    cfg.attrs = at;
-    cfg.numAttrs = na;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
     if (e != cudaSuccess) fail_cuda(e, "cudaLaunchKernelEx", __FILE__, __LINE__);
-}
-
-template <class... KArgs, class... Args>
-inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args... args) {
-    launch_pdl_l2(kernel, grid, block, smem, s, nullptr, 0, 0.f, args...);
 }
 
 inline unsigned grid_for(int64_t threads_needed, int block) {
@@ -215,10 +196,6 @@ struct CsrView {
     const int32_t *ci;
     const double *v;
     int64_t maxrow = -1;  // longest row (-1: unknown); picks the SpMV lane group
-    // optional L2 persistence window over the value array (hot operators)
-    const void *l2_base = nullptr;
-    size_t l2_bytes = 0;
-    float l2_hit = 0.f;
 };
 
 struct Csr {
@@ -235,15 +212,8 @@ struct Csr {
         v.alloc(z);
     }
     int64_t maxrow = -1;
-    const void *l2_base = nullptr;
-    size_t l2_bytes = 0;
-    float l2_hit = 0.f;
-    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow, l2_base, l2_bytes, l2_hit}; }
+    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow}; }
 };
-
-// mark an operator's values as L2-persisting (best effort; no-op when the
-// device or PMGR_NO_L2PERSIST says no)
-void l2_persist(Csr &A);
 
 // record the longest row of a finished operator (setup time, synchronises)
 void csr_finalize(Csr &A, cudaStream_t s);

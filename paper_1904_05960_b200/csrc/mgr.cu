@@ -348,7 +348,6 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
         csr_finalize(*A_ff, s);
-        if (li == 0 && sp.f_relax == PMGR_FRELAX_AMG) l2_persist(*A_ff);  // read twice per V-cycle
         csr_finalize(L.A_cf, s);
         if (need_dinv) {
             L.dinv_ff.alloc(L.nf);

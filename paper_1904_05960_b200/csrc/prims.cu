@@ -121,40 +121,6 @@ void setup_trace(const char *what, int64_t level, cudaStream_t s) {
     last = now;
 }
 
-void l2_persist(Csr &A) {
-    static const size_t max_persist = [] {
-        const char *e = getenv("PMGR_NO_L2PERSIST");
-        if (e && e[0] != '0') return (size_t)0;
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return (size_t)0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || v <= 0) {
-            cudaGetLastError();
-            return (size_t)0;
-        }
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v) != cudaSuccess) {
-            cudaGetLastError();
-            return (size_t)0;
-        }
-        return (size_t)v;
-    }();
-    static const size_t max_window = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess) {
-            cudaGetLastError();
-            return (size_t)0;
-        }
-        return (size_t)v;
-    }();
-    if (!max_persist || !max_window || A.nnz == 0) return;
-    size_t bytes = sizeof(double) * (size_t)A.nnz;
-    if (bytes > max_window) bytes = max_window;
-    A.l2_base = A.v.p;
-    A.l2_bytes = bytes;
-    const double hit = (double)max_persist / (double)bytes;
-    A.l2_hit = (float)(hit < 1.0 ? hit : 1.0);
-}
-
 bool pdl_enabled() {
     static const bool on = [] {
         const char *e = getenv("PMGR_NO_PDL");

@@ -131,11 +131,9 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
     if (stream)
-        launch_pdl_l2(k_spmv<G, true, Op>, dim3(grid), dim3(block), 0, s, A.l2_base, A.l2_bytes, A.l2_hit, A.nrows,
-                      A.ro, A.ci, A.v, op, trigger);
+        launch_pdl(k_spmv<G, true, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
     else
-        launch_pdl_l2(k_spmv<G, false, Op>, dim3(grid), dim3(block), 0, s, A.l2_base, A.l2_bytes, A.l2_hit, A.nrows,
-                      A.ro, A.ci, A.v, op, trigger);
+        launch_pdl(k_spmv<G, false, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
 }
 
 template <class Op>
