@@ -135,10 +135,33 @@ def dump_amg(d, prefix, h, full):
         d[prefix + "coarse_sha"] = dcsr(h.coarse_A)
 
 
-def dump_problem(tag, pb, n_max, full, restart=100, four_field=False):
+# option variants of the reference API exercised on a small two-phase problem
+VARIANTS = {
+    "v1": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", f_relax_sweeps=2,
+                            interp="injection_only", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi")),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre")),
+    "v3": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="none")),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre")),
+    "v2": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg"),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi", f_relax_sweeps=2)),
+               cfg=dict(terminal_cycles=2, f_relax_position="post")),
+}
+
+
+def dump_problem(tag, pb, n_max, full, restart=100, four_field=False, variant=None):
     A = CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
     lay = FieldLayout(pb.field_of, pb.entity_of)
-    if four_field:
+    if variant is not None:
+        V = VARIANTS[variant]
+        levels = tuple(pmgr.MgrLevelSpec(lv["f"], lv["c"], **{k: x for k, x in lv.items() if k not in ("f", "c")})
+                       for lv in V["levels"])
+        base = parity_config(levels)
+        cfg = pmgr.MgrConfig(levels=levels, amg_f_relax=base.amg_f_relax, amg_terminal=base.amg_terminal,
+                             **V["cfg"])
+        h = pmgr.mgr_setup(A, lay, cfg)
+    elif four_field:
         cfg = parity_config(())
         h = setup_4field(A, lay, n_max, cfg)
     else:
@@ -254,6 +277,12 @@ def main():
         dump_problem("c2_32", problems.make_c2(seed=0, n=32), 4, False)
     if "c4_16" in which:
         dump_problem("c4_16", problems.make_c4(seed=0, n=16), 4, False, four_field=True)
+    if "c2_6_v1" in which:
+        dump_problem("c2_6_v1", problems.make_c2(seed=5, n=6), None, True, variant="v1")
+    if "c2_6_v2" in which:
+        dump_problem("c2_6_v2", problems.make_c2(seed=5, n=6), None, True, variant="v2")
+    if "c2_6_v3" in which:
+        dump_problem("c2_6_v3", problems.make_c2(seed=5, n=6), None, True, variant="v3")
     if "c3_16" in which:
         dump_problem("c3_16", problems.make_c3(seed=0, n=16), 4, False, restart=100)
 

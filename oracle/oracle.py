@@ -351,6 +351,7 @@ class MgrLevelSpec:
     f_relax: str = "jacobi"         # "jacobi" | "amg" | "none"
     f_relax_sweeps: int = 1
     n_max: int | None = None
+    interp: str = "injection_jacobi"  # | "injection_only" (mgr.py:151-152)
 
 
 @dataclass(frozen=True)
@@ -419,10 +420,13 @@ def diag_inverse(A: Csr) -> np.ndarray:
     return 1.0 / d
 
 
-def build_interp(blocks, is_c: np.ndarray, dinv: np.ndarray) -> Csr:
+def build_interp(blocks, is_c: np.ndarray, dinv, interp="injection_jacobi") -> Csr:
     """P = [W_p; I] in level order, W_p = A_FC * (-dinv_F) row-scaled
-    (reference mgr.py:150-176, injection_jacobi)."""
+    (reference mgr.py:150-176, injection_jacobi); injection_only has no W_p."""
     a_ff, a_fc, _, _ = blocks
+    if interp == "injection_only":
+        a_fc = Csr(a_fc.nrows, a_fc.ncols, np.zeros(a_fc.nrows + 1, dtype=np.int64), [], [])
+        dinv = np.zeros(a_fc.nrows)
     n = len(is_c)
     nc = int(is_c.sum())
     f_rows = np.flatnonzero(~is_c)
@@ -478,8 +482,11 @@ def mgr_setup(A: Csr, field_of: np.ndarray, entity_of: np.ndarray, cfg: MgrConfi
         if is_c.all():
             break
         blocks = extract_blocks(cur, is_c)
-        dinv = diag_inverse(blocks[0])
-        P = build_interp(blocks, is_c, dinv)
+        # diag_inverse runs for injection_jacobi interpolation and for the
+        # Jacobi F-relaxation (build_transfers mgr.py:153-155, _JacobiFRelax :241)
+        need = spec.interp == "injection_jacobi" or spec.f_relax == "jacobi"
+        dinv = diag_inverse(blocks[0]) if need else None
+        P = build_interp(blocks, is_c, dinv, spec.interp)
         if spec.f_relax == "amg":
             acfg = cfg.amg_f_relax
             nf = 3 if set(spec.f_fields) == {0} else 1

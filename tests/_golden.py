@@ -65,6 +65,30 @@ def oracle_levels(pb, n_max, four_field):
             O.MgrLevelSpec(frozenset({S}), frozenset({P}), "jacobi", 1, None))
 
 
+# option variants (oracle/make_golden.py VARIANTS): (levels, terminal_cycles, position)
+U_, S_, P_ = problems.FIELD_U, problems.FIELD_S, problems.FIELD_P
+VARIANT_SPECS = {
+    "c2_6_v1": ([dict(f={U_}, c={S_, P_}, f_relax="amg", f_relax_sweeps=2, interp="injection_only", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi")], 1, "pre"),
+    "c2_6_v2": ([dict(f={U_}, c={S_, P_}, f_relax="amg"),
+                 dict(f={S_}, c={P_}, f_relax="jacobi", f_relax_sweeps=2)], 2, "post"),
+    "c2_6_v3": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="none")], 1, "pre"),
+}
+
+
+def oracle_variant_hierarchy(tag):
+    levels, tc, pos = VARIANT_SPECS[tag]
+    pb = problems.make_c2(seed=5, n=6)
+    specs = tuple(O.MgrLevelSpec(frozenset(lv["f"]), frozenset(lv["c"]), lv.get("f_relax", "jacobi"),
+                                 lv.get("f_relax_sweeps", 1), lv.get("n_max"), lv.get("interp", "injection_jacobi"))
+                  for lv in levels)
+    base = oracle_config(specs)
+    cfg = O.MgrConfig(levels=specs, terminal_cycles=tc, amg_f_relax=base.amg_f_relax, amg_terminal=base.amg_terminal,
+                      f_relax_position=pos)
+    return pb, O.mgr_setup(problem_csr(pb), pb.field_of, pb.entity_of, cfg)
+
+
 def oracle_config(levels, parts=JACOBI):
     return O.MgrConfig(levels=levels,
                        amg_f_relax=O.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=parts),

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests._golden import CASES, dcsr, get_csr, load, oracle_config, oracle_levels, vec_sha
+from tests._golden import CASES, VARIANT_SPECS, dcsr, get_csr, load, oracle_config, oracle_levels, vec_sha
 
 pytestmark = pytest.mark.gpu
 
@@ -308,3 +308,42 @@ def test_empty_and_tiny_systems(pk):
     h = amg.amg_setup(sparse.CsrMatrix.identity(5), amg.AmgConfig(npartitions=JACOBI))
     assert h.level_sizes() == [5]
     assert np.allclose(amg.amg_vcycle(h, np.arange(5.0)), np.arange(5.0))
+
+
+# ---------------------------------------------------------------------------
+# option variants of the reference API (injection_only, multi-sweep F-relax,
+# f_relax none, post position, several terminal cycles) against goldens
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("tag", sorted(VARIANT_SPECS))
+def test_mgr_option_variants(pk, tag):
+    sparse, amg, mgr, krylov = pk
+    from paper_1904_05960_b200 import problems
+
+    levels, tc, pos = VARIANT_SPECS[tag]
+    pb = problems.make_c2(seed=5, n=6)
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    specs = tuple(mgr.MgrLevelSpec({sparse.Field(t) for t in lv["f"]}, {sparse.Field(t) for t in lv["c"]},
+                                   **{k: v for k, v in lv.items() if k not in ("f", "c")}) for lv in levels)
+    cfg = mgr.MgrConfig(levels=specs, terminal_cycles=tc, f_relax_position=pos,
+                        amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=JACOBI),
+                        amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=JACOBI))
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of), cfg)
+    d = load(tag)
+    assert h.level_sizes() == list(d["mgr_sizes"])
+    for i, lv in enumerate(h.levels):
+        k = f"mgr{i}_"
+        assert np.array_equal(lv.split.is_c, d[k + "isc"])
+        same_csr(host_csr(lv.P), get_csr(d, k + "P"), k + "P")
+        same_csr(host_csr(lv.coarse), get_csr(d, k + "coarse"), k + "coarse")
+    z = h.apply(d["apply_v"])
+    zr = d["apply_z"]
+    assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
+    x, st = krylov.gmres(A, h.apply, pb.rhs, cfg=krylov.GmresConfig(restart=100, max_iters=1000, rtol=1e-6))
+    assert st.converged == bool(d["gmres_conv"])
+    if st.converged:
+        assert abs(st.iterations - int(d["gmres_iters"])) <= 1
+    else:
+        assert st.iterations == int(d["gmres_iters"])
+        assert np.allclose(st.residual_history[:20], d["gmres_hist"][:20], rtol=1e-6)
