@@ -208,6 +208,73 @@ __global__ void __launch_bounds__(SP_WARPS * 32)
     }
 }
 
+// Coarse products (few output columns): a dense accumulator per row in
+// shared memory, block per row.  The middle index is walked in ascending
+// order with a block barrier between j's, so every entry is summed exactly
+// like csr_matmat; the flag bitmap yields the row already sorted.
+constexpr int DENSE_COLS = 12288;
+constexpr int DENSE_THREADS = 256;
+
+template <bool NUMERIC>
+__global__ void __launch_bounds__(DENSE_THREADS)
+    k_spgemm_dense(int64_t n, int64_t ncols, const int64_t *__restrict__ xro, const int32_t *__restrict__ xci,
+                   const double *__restrict__ xv, const int64_t *__restrict__ yro, const int32_t *__restrict__ yci,
+                   const double *__restrict__ yv, int64_t *cnt, const int64_t *__restrict__ cro, int32_t *cci,
+                   double *cv) {
+    extern __shared__ unsigned char smem[];
+    const int W = (int)((ncols + 31) / 32);
+    unsigned *flags = (unsigned *)smem;
+    double *acc = (double *)(smem + sizeof(unsigned) * ((W + 1) & ~1));
+    __shared__ int64_t wbase[DENSE_THREADS + 1];
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        for (int t = threadIdx.x; t < W; t += DENSE_THREADS) flags[t] = 0u;
+        if (NUMERIC)
+            for (int64_t t = threadIdx.x; t < ncols; t += DENSE_THREADS) acc[t] = 0.0;
+        __syncthreads();
+        for (int64_t jj = xro[i]; jj < xro[i + 1]; ++jj) {
+            const int32_t j = xci[jj];
+            const double xval = NUMERIC ? xv[jj] : 0.0;
+            for (int64_t kk = yro[j] + threadIdx.x; kk < yro[j + 1]; kk += DENSE_THREADS) {
+                const int32_t k = yci[kk];
+                atomicOr(flags + (k >> 5), 1u << (k & 31));
+                if (NUMERIC) acc[k] = __dadd_rn(acc[k], __dmul_rn(xval, yv[kk]));
+            }
+            if (NUMERIC) __syncthreads();
+        }
+        __syncthreads();
+        // words [w0, w1) of this thread, in order
+        const int per = (W + DENSE_THREADS - 1) / DENSE_THREADS;
+        const int w0 = threadIdx.x * per, w1 = (w0 + per < W) ? w0 + per : W;
+        int64_t mine = 0;
+        for (int w = w0; w < w1; ++w) mine += __popc(flags[w]);
+        wbase[threadIdx.x + 1] = mine;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            wbase[0] = 0;
+            for (int t = 1; t <= DENSE_THREADS; ++t) wbase[t] += wbase[t - 1];
+        }
+        __syncthreads();
+        if (!NUMERIC) {
+            if (threadIdx.x == 0) cnt[i] = wbase[DENSE_THREADS];
+        } else {
+            int64_t o = cro[i] + wbase[threadIdx.x];
+            for (int w = w0; w < w1; ++w) {
+                unsigned f = flags[w];
+                while (f) {
+                    const int bit = __ffs(f) - 1;
+                    f &= f - 1;
+                    const int k = w * 32 + bit;
+                    const double val = acc[k];
+                    cci[o] = k;
+                    cv[o] = (val == 0.0) ? 0.0 : val;
+                    ++o;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------ zero drop
 __global__ void k_count_nonzero(int64_t n, const int64_t *ro, const double *v, int64_t *cnt) {
     int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -442,6 +509,32 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
         PMGR_CUDA(cudaMemsetAsync(C.ro.p, 0, sizeof(int64_t), s));
         return;
     }
+    int64_t total = 0;
+    TBuf<int32_t> tci;
+    TBuf<double> tv;
+    if (Y.ncols <= DENSE_COLS) {
+        const int W = (int)((Y.ncols + 31) / 32);
+        const size_t fbytes = sizeof(unsigned) * (size_t)((W + 1) & ~1);
+        const size_t smem_num = fbytes + sizeof(double) * (size_t)Y.ncols;
+        static bool dense_attr = false;
+        if (!dense_attr) {
+            const int maxs = (int)(sizeof(unsigned) * DENSE_COLS / 32 + 8 + sizeof(double) * DENSE_COLS);
+            PMGR_CUDA(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
+            dense_attr = true;
+        }
+        const int64_t gcap = (int64_t)num_sms() * 4;
+        const unsigned g = (unsigned)(n < gcap ? n : gcap);
+        k_spgemm_dense<false><<<g, DENSE_THREADS, fbytes, s>>>(n, Y.ncols, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, cnt.p,
+                                                               nullptr, nullptr, nullptr);
+        PMGR_LAUNCHED();
+        total = exclusive_scan_total(cnt.p, cro.p, n, s);
+        tci.alloc(total, s);
+        tv.alloc(total, s);
+        k_spgemm_dense<true><<<g, DENSE_THREADS, smem_num, s>>>(n, Y.ncols, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v,
+                                                                nullptr, cro.p, tci.p, tv.p);
+        PMGR_LAUNCHED();
+        setup_trace("  spgemm dense", total, s);
+    } else {
     k_spgemm_ub<<<grid_for(n * 32, 256), 256, 0, s>>>(n, X.ro, X.ci, Y.ro, Y.ncols, ub.p);
     PMGR_LAUNCHED();
     k_table_size<<<grid_for(n, 256), 256, 0, s>>>(n, ub.p, tsz.p);
@@ -466,16 +559,17 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
     k_spgemm<false><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
                                                        gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
     PMGR_LAUNCHED();
-    int64_t total = exclusive_scan_total(cnt.p, cro.p, n, s);
+    total = exclusive_scan_total(cnt.p, cro.p, n, s);
     setup_trace("  spgemm symbolic", total, s);
-    TBuf<int32_t> tci(total, s);
-    TBuf<double> tv(total, s);
+    tci.alloc(total, s);
+    tv.alloc(total, s);
     k_spgemm<true><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
                                                       gkeys.p, gvals.p, nullptr, cro.p, tci.p, tv.p);
     PMGR_LAUNCHED();
     setup_trace("  spgemm numeric", total, s);
     segmented_sort_pairs(tci.p, tv.p, total, cro.p, n, s);
     setup_trace("  spgemm sort", total, s);
+    }
     if (mode == 1) {
         C.nrows = n;
         C.ncols = Y.ncols;
