@@ -669,7 +669,7 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     const CsrView A = L.A->view();
     const bool has_next = l + 1 < h.levels.size();
     const bool tag = h.prof_tag && l == 0;
-    const double pass = csr_pass_bytes(A.nrows, A.ncols, A.nnz) + 16.0 * A.nrows;
+    const double pass = csr_pass_bytes(A) + 16.0 * A.nrows;
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_SWEEP0 : PROF_KINDS, pass, s);
         spmv_residual(A, L.x.p, L.b.p, L.r.p, s);

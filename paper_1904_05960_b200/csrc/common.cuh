@@ -196,6 +196,12 @@ struct CsrView {
     const int32_t *ci;
     const double *v;
     int64_t maxrow = -1;  // longest row (-1: unknown); picks the SpMV lane group
+    // optional 3x3 block copy for the solve phase (node-blocked elasticity):
+    // block rows of 3 scalar rows, blocks column-major, zeros where the CSR has none
+    int64_t nbrows = 0, nblocks = 0;
+    const int64_t *bro = nullptr;
+    const int32_t *bci = nullptr;
+    const double *bval = nullptr;
 };
 
 struct Csr {
@@ -212,8 +218,17 @@ struct Csr {
         v.alloc(z);
     }
     int64_t maxrow = -1;
-    CsrView view() const { return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow}; }
+    int64_t nbrows = 0, nblocks = 0;
+    DBuf<int64_t> bro;
+    DBuf<int32_t> bci;
+    DBuf<double> bval;
+    CsrView view() const {
+        return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow, nbrows, nblocks, bro.p, bci.p, bval.p};
+    }
 };
+
+// build the 3x3 block (BSR3) solve copy of a node-blocked square operator
+void csr_make_bsr3(Csr &A, cudaStream_t s);
 
 // record the longest row of a finished operator (setup time, synchronises)
 void csr_finalize(Csr &A, cudaStream_t s);
@@ -285,6 +300,11 @@ struct ProfScope {
 // values; x gathered once, y written once)
 inline double csr_pass_bytes(int64_t nrows, int64_t ncols, int64_t nnz) {
     return 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * ncols + 8.0 * nrows;
+}
+// one pass over the format the solve actually streams (BSR3 copy if present)
+inline double csr_pass_bytes(const CsrView &A) {
+    if (A.nbrows > 0) return 76.0 * A.nblocks + 8.0 * (A.nbrows + 1) + 8.0 * A.ncols + 8.0 * A.nrows;
+    return csr_pass_bytes(A.nrows, A.ncols, A.nnz);
 }
 
 // ---------------------------------------------------------------------------

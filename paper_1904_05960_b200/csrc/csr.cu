@@ -460,6 +460,84 @@ void csr_finalize(Csr &A, cudaStream_t s) {
     A.maxrow = (int64_t)read_scalar(m.p, s);
 }
 
+namespace {
+// number of distinct block columns of node row I (union over its 3 rows)
+__global__ void k_bsr_count(int64_t nb, const int64_t *ro, const int32_t *ci, int64_t *cnt) {
+    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (I >= nb) return;
+    // merge the three sorted rows by block column
+    int64_t p[3], e[3];
+    for (int r = 0; r < 3; ++r) {
+        p[r] = ro[3 * I + r];
+        e[r] = ro[3 * I + r + 1];
+    }
+    int64_t c = 0;
+    int32_t last = -1;
+    while (true) {
+        int32_t best = INT32_MAX;
+        for (int r = 0; r < 3; ++r)
+            if (p[r] < e[r]) best = min(best, ci[p[r]] / 3);
+        if (best == INT32_MAX) break;
+        for (int r = 0; r < 3; ++r)
+            while (p[r] < e[r] && ci[p[r]] / 3 == best) ++p[r];
+        if (best != last) {
+            ++c;
+            last = best;
+        }
+    }
+    cnt[I] = c;
+}
+
+__global__ void k_bsr_fill(int64_t nb, const int64_t *ro, const int32_t *ci, const double *v, const int64_t *bro,
+                           int32_t *bci, double *bval) {
+    const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (I >= nb) return;
+    int64_t p[3], e[3];
+    for (int r = 0; r < 3; ++r) {
+        p[r] = ro[3 * I + r];
+        e[r] = ro[3 * I + r + 1];
+    }
+    int64_t w = bro[I];
+    while (true) {
+        int32_t best = INT32_MAX;
+        for (int r = 0; r < 3; ++r)
+            if (p[r] < e[r]) best = min(best, ci[p[r]] / 3);
+        if (best == INT32_MAX) break;
+        bci[w] = best;
+        double *blk = bval + 9 * w;
+        for (int t = 0; t < 9; ++t) blk[t] = 0.0;
+        for (int r = 0; r < 3; ++r)
+            while (p[r] < e[r] && ci[p[r]] / 3 == best) {
+                blk[r + 3 * (ci[p[r]] - 3 * best)] = v[p[r]];  // column-major
+                ++p[r];
+            }
+        ++w;
+    }
+}
+}  // namespace
+
+void csr_make_bsr3(Csr &A, cudaStream_t s) {
+    static const bool off = getenv("PMGR_NO_BSR") && getenv("PMGR_NO_BSR")[0] != '0';
+    if (off || A.nrows != A.ncols || A.nrows % 3 != 0 || A.nrows == 0) return;
+    const int64_t nb = A.nrows / 3;
+    TBuf<int64_t> cnt(nb, s);
+    k_bsr_count<<<grid_for(nb, 128), 128, 0, s>>>(nb, A.ro.p, A.ci.p, cnt.p);
+    PMGR_LAUNCHED();
+    A.bro.alloc(nb + 1);
+    const int64_t nblk = exclusive_scan_total(cnt.p, A.bro.p, nb, s);
+    // only worth it when the blocks are (nearly) full
+    if (9.0 * (double)nblk > 1.25 * (double)A.nnz) {
+        A.bro.release();
+        return;
+    }
+    A.bci.alloc(nblk);
+    A.bval.alloc(9 * nblk);
+    k_bsr_fill<<<grid_for(nb, 128), 128, 0, s>>>(nb, A.ro.p, A.ci.p, A.v.p, A.bro.p, A.bci.p, A.bval.p);
+    PMGR_LAUNCHED();
+    A.nbrows = nb;
+    A.nblocks = nblk;
+}
+
 void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {
     B.alloc(A.nrows, A.ncols, A.nnz);
     PMGR_CUDA(cudaMemcpyAsync(B.ro.p, A.ro, sizeof(int64_t) * (A.nrows + 1), cudaMemcpyDeviceToDevice, s));

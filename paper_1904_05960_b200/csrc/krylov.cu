@@ -534,7 +534,7 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
         else vec_copy(W.vin.p, W.z.p, n, s);
     }
     {
-        ProfScope ps(prof ? PROF_OUTER_SPMV : PROF_KINDS, csr_pass_bytes(Av.nrows, Av.ncols, Av.nnz), s);
+        ProfScope ps(prof ? PROF_OUTER_SPMV : PROF_KINDS, csr_pass_bytes(Av), s);
         spmv(Av, W.z.p, W.w.p, s);
     }
     // compulsory bytes of the step's orthogonalisation: the basis V_0..V_j

@@ -348,6 +348,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
         csr_finalize(*A_ff, s);
+        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3) csr_make_bsr3(*A_ff, s);
         csr_finalize(L.A_cf, s);
         if (need_dinv) {
             L.dinv_ff.alloc(L.nf);

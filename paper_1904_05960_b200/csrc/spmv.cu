@@ -63,6 +63,45 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
     if (active && lane == 0) op.out(row, s);
 }
 
+// BSR3: a warp per block row (3 scalar rows), blocks stored column-major.
+// Lane 3k+c (k < 10) owns column c of every 10th block: one column index,
+// one x load and three contiguous values feeding the three row sums, so x
+// is gathered once per block column instead of once per entry and the
+// matrix stream is 76 B per 9 entries instead of CSR's 108 B.
+template <class Op>
+__global__ void __launch_bounds__(256) k_bsr3(int64_t nb, const int64_t *__restrict__ bro,
+                                              const int32_t *__restrict__ bci, const double *__restrict__ bval,
+                                              Op op, int trigger) {
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const bool active = I < nb;
+    int64_t k0 = 0, k1 = 0;
+    if (active) {
+        k0 = __ldg(bro + I);
+        k1 = __ldg(bro + I + 1);
+    }
+    const int kk = lane / 3, c = lane - 3 * kk;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (lane < 30) {
+        for (int64_t k = k0 + kk; k < k1; k += 10) {
+            const double xv = op.x(3 * __ldg(bci + k) + c);
+            const double *p = bval + 9 * k + 3 * c;
+            a0 = fma(__ldg(p), xv, a0);
+            a1 = fma(__ldg(p + 1), xv, a1);
+            a2 = fma(__ldg(p + 2), xv, a2);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(FULL, a0, o);
+        a1 += __shfl_xor_sync(FULL, a1, o);
+        a2 += __shfl_xor_sync(FULL, a2, o);
+    }
+    if (active && lane < 3) op.out(3 * I + lane, lane == 0 ? a0 : lane == 1 ? a1 : a2);
+}
+
 struct OpY {
     const double *xv;
     double *y;
@@ -139,6 +178,13 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
 template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
+    if (A.nbrows > 0) {
+        const unsigned grid = grid_for(A.nbrows * 32, 256);
+        const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
+        launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, A.nbrows, A.bro, A.bci, A.bval, op, trigger);
+        PMGR_LAUNCHED();
+        return;
+    }
     double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
     // skewed rows (a few dense coarse-grid rows next to short ones) get a
     // whole warp, otherwise the longest row serialises its lane group
