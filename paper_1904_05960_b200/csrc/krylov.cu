@@ -86,12 +86,13 @@ __device__ __forceinline__ void block_sum2(double &a, double &b, double *sh) {
 // block 0 does the Hessenberg / Givens / convergence bookkeeping
 // (krylov.py:75-104) and sets the WHILE condition.  Three grid barriers
 // replace five launches and half of the basis traffic.
-constexpr int AO_THREADS = 512;
+constexpr int AO_THREADS = 256;
+constexpr int AO_UM = 10;  // phase 1: double2 loads per lane per basis vector batch
 constexpr int AO_WARPS = AO_THREADS / 32;
 
 struct AoParams {
     double *V;
-    int64_t n;
+    int64_t n, ldv, chunk;  // basis leading dimension and rows per block (multiples of 32)
     double *w, *vin;
     Dev *dev;
     double *pa, *pg, *pn;  // slice partials: (m+1) x nblk, (m+1) x nblk, nblk
@@ -127,21 +128,22 @@ __device__ __forceinline__ double block_sum1(double v, double *sh) {
 // basis stream is the only per-vector L2/HBM traffic and w never returns to
 // global memory (small and medium n); SM = false streams them from L2.
 template <bool SM>
-__global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
+__global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double slice[];  // SM: w slice, then V_j slice
     __shared__ double sh[AO_WARPS];
     __shared__ double hs[1024];   // h
     __shared__ double as_[1024];  // a
+    __shared__ double red[AO_WARPS][128];
     const int nblk = gridDim.x, b = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = P.dev->j;
     const int64_t n = P.n;
-    const int64_t chunk = (n + nblk - 1) / nblk;
+    const int64_t ldv = P.ldv, chunk = P.chunk;
     const int64_t lo = (int64_t)b * chunk;
-    const int64_t hi = lo + chunk < n ? lo + chunk : n;
+    const int64_t hi = lo + chunk < n ? lo + chunk : (n > lo ? n : lo);
     stamp(P, 0);
-    const double *vjg = P.V + (int64_t)j * n;
+    const double *vjg = P.V + (int64_t)j * ldv;
     double *wsl = slice;
     double *vsl = slice + chunk;
     if (SM) {
@@ -155,37 +157,56 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     auto wv = [&](int64_t i) { return SM ? wsl[i - lo] : P.w[i]; };
     auto vj = [&](int64_t i) { return SM ? vsl[i - lo] : vjg[i]; };
 
-    // phase 1: slice partials of V_k.w and V_k.V_j
-    for (int k = warp; k <= j; k += AO_WARPS) {
-        const double *x = P.V + (int64_t)k * n;
-        // 8 rows per lane per round: 24 independent loads in flight
-        double aa[8], gg[8];
+    // phase 1: slice partials of V_k.w and V_k.V_j.  A warp takes two basis
+    // vectors at a time and issues every 16-byte load of both slices before
+    // consuming them (one memory latency per pair for slices up to 640 rows);
+    // slices are 256-byte aligned (ldv, chunk multiples of 32).
+    {
+        const int len = (int)(hi - lo), len2 = len >> 1;
+        const double2 *w2 = reinterpret_cast<const double2 *>(SM ? wsl : P.w + lo);
+        const double2 *v2 = reinterpret_cast<const double2 *>(SM ? vsl : vjg + lo);
+        for (int k = 2 * warp; k <= j; k += 2 * AO_WARPS) {
+            double a0[2] = {0.0, 0.0}, a1[2] = {0.0, 0.0}, g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+            for (int base = 0; base < len2; base += 32 * AO_UM) {
+                double2 xs[2][AO_UM];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) aa[u] = gg[u] = 0.0;
-        int64_t i = lo + lane;
-        for (; i + 7 * 32 < hi; i += 8 * 32) {
-            double xs[8], ws[8], vs[8];
+                for (int q = 0; q < 2; ++q) {
+                    const double2 *x2 = reinterpret_cast<const double2 *>(P.V + (int64_t)(k + q) * ldv + lo);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                xs[u] = x[i + 32 * u];
-                ws[u] = wv(i + 32 * u);
-                vs[u] = vj(i + 32 * u);
+                    for (int u = 0; u < AO_UM; ++u) {
+                        const int p = base + lane + 32 * u;
+                        xs[q][u] = (k + q <= j && p < len2) ? x2[p] : make_double2(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < AO_UM; ++u) {
+                    const int p = base + lane + 32 * u;
+                    if (p < len2) {
+                        const double2 ww = w2[p], vv = v2[p];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            a0[q] = fma(xs[q][u].x, ww.x, a0[q]);
+                            a1[q] = fma(xs[q][u].y, ww.y, a1[q]);
+                            g0[q] = fma(xs[q][u].x, vv.x, g0[q]);
+                            g1[q] = fma(xs[q][u].y, vv.y, g1[q]);
+                        }
+                    }
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                aa[u] = fma(xs[u], ws[u], aa[u]);
-                gg[u] = fma(xs[u], vs[u], gg[u]);
+            for (int q = 0; q < 2; ++q) {
+                if ((len & 1) && lane == 0 && k + q <= j) {  // odd last slice: its final row
+                    const double xl = P.V[(int64_t)(k + q) * ldv + hi - 1];
+                    a0[q] = fma(xl, wv(hi - 1), a0[q]);
+                    g0[q] = fma(xl, vj(hi - 1), g0[q]);
+                }
+                const double sa = warp_sum(a0[q] + a1[q]);
+                const double sg = warp_sum(g0[q] + g1[q]);
+                if (lane == 0 && k + q <= j) {
+                    P.pa[(int64_t)(k + q) * nblk + b] = sa;
+                    P.pg[(int64_t)(k + q) * nblk + b] = sg;
+                }
             }
-        }
-        for (; i < hi; i += 32) {
-            aa[0] = fma(x[i], wv(i), aa[0]);
-            gg[0] = fma(x[i], vj(i), gg[0]);
-        }
-        const double sa = warp_sum(((aa[0] + aa[1]) + (aa[2] + aa[3])) + ((aa[4] + aa[5]) + (aa[6] + aa[7])));
-        const double sg = warp_sum(((gg[0] + gg[1]) + (gg[2] + gg[3])) + ((gg[4] + gg[5]) + (gg[6] + gg[7])));
-        if (lane == 0) {
-            P.pa[(int64_t)k * nblk + b] = sa;
-            P.pg[(int64_t)k * nblk + b] = sg;
         }
     }
     stamp(P, 1);
@@ -209,39 +230,80 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     stamp(P, 3);
     grid.sync();
     stamp(P, 4);
-    // phase 2b: h = a + (a - G a), every block for itself (warp per k)
+    // phase 2b: h = a + (a - G a), every block for itself.  G is symmetric,
+    // so (G a)_k = sum_l G[l][k] a_l: warps split l, lanes take k (coalesced
+    // rows of G, every load of a lane independent), then a fixed-order sum
+    // over the warps.
     for (int k = threadIdx.x; k <= j; k += AO_THREADS) as_[k] = P.a[k];
     __syncthreads();
-    for (int k = warp; k <= j; k += AO_WARPS) {
-        double ga = 0.0;
-        for (int l = lane; l <= j; l += 32) ga = fma(P.G[(int64_t)k * P.ldg + l], as_[l], ga);
-        ga = warp_sum(ga);
-        if (lane == 0) hs[k] = as_[k] + (as_[k] - ga);
+    for (int c0 = 0; c0 <= j; c0 += 128) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int l = warp; l <= j; l += AO_WARPS) {
+            const double al = as_[l];
+            const double *row = P.G + (int64_t)l * P.ldg;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int k = c0 + 32 * c + lane;
+                if (k <= j) acc[c] = fma(row[k], al, acc[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) red[warp][32 * c + lane] = acc[c];
+        __syncthreads();
+        if (threadIdx.x < 128 && c0 + (int)threadIdx.x <= j) {
+            const int k = c0 + threadIdx.x;
+            double ga = 0.0;
+            for (int w = 0; w < AO_WARPS; ++w) ga += red[w][threadIdx.x];
+            hs[k] = as_[k] + (as_[k] - ga);
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (b == 0)
         for (int k = threadIdx.x; k <= j; k += AO_THREADS) P.h[k] = hs[k];
     stamp(P, 7);
-    // phase 3: w -= sum_k h_k V_k on this slice, ||w||^2 partial
+    // phase 3: w -= sum_k h_k V_k on this slice (row pairs, 16 basis vectors
+    // per batch: 32 independent L2 loads in flight per thread), ||w||^2 partial
     double nrm = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
-        double acc[8];
-        acc[0] = wv(i);
+    {
+        const int len = (int)(hi - lo), len2 = len >> 1;
+        double2 *wo2 = reinterpret_cast<double2 *>(SM ? wsl : P.w + lo);
+        const double2 *Vb = reinterpret_cast<const double2 *>(P.V + lo);
+        const int64_t ld2 = ldv >> 1;
+        for (int p = threadIdx.x; p < len2; p += AO_THREADS) {
+            double2 acc[4];
+            acc[0] = wo2[p];
+            acc[1] = acc[2] = acc[3] = make_double2(0.0, 0.0);
+            for (int k = 0; k <= j; k += 16) {
+                double2 vv[16];
+                double hc[16];
 #pragma unroll
-        for (int t = 1; t < 8; ++t) acc[t] = 0.0;
-        int k = 0;
-        for (; k + 7 <= j; k += 8) {
-            double vv[8];
+                for (int t = 0; t < 16; ++t) {
+                    const bool ok = k + t <= j;
+                    vv[t] = ok ? Vb[(int64_t)(k + t) * ld2 + p] : make_double2(0.0, 0.0);
+                    hc[t] = ok ? -hs[k + t] : 0.0;
+                }
 #pragma unroll
-            for (int t = 0; t < 8; ++t) vv[t] = P.V[(int64_t)(k + t) * n + i];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc[t] = fma(-hs[k + t], vv[t], acc[t]);
+                for (int t = 0; t < 16; ++t) {
+                    acc[t & 3].x = fma(hc[t], vv[t].x, acc[t & 3].x);
+                    acc[t & 3].y = fma(hc[t], vv[t].y, acc[t & 3].y);
+                }
+            }
+            double2 wi;
+            wi.x = (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x);
+            wi.y = (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y);
+            wo2[p] = wi;
+            nrm = fma(wi.x, wi.x, nrm);
+            nrm = fma(wi.y, wi.y, nrm);
         }
-        for (; k <= j; ++k) acc[0] = fma(-hs[k], P.V[(int64_t)k * n + i], acc[0]);
-        const double wi = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        if (SM) wsl[i - lo] = wi;  // same thread reads it back in phase 4
-        else P.w[i] = wi;
-        nrm = fma(wi, wi, nrm);
+        if ((len & 1) && threadIdx.x == 0) {  // odd last slice: its final row
+            const int64_t i = hi - 1;
+            double acc = wv(i);
+            for (int k = 0; k <= j; ++k) acc = fma(-hs[k], P.V[(int64_t)k * ldv + i], acc);
+            if (SM) wsl[i - lo] = acc;
+            else P.w[i] = acc;
+            nrm = fma(acc, acc, nrm);
+        }
     }
     nrm = block_sum1(nrm, sh);
     if (threadIdx.x == 0) P.pn[b] = nrm;
@@ -258,7 +320,7 @@ __global__ void __launch_bounds__(AO_THREADS) k_arnoldi(AoParams P) {
     c2 += hn * hn;
     const int brk = !(hn > 1e-12 * fmax(sqrt(c2), 1e-300));
     if (!brk && j + 1 <= P.dev->m) {
-        double *vn = P.V + (int64_t)(j + 1) * n;
+        double *vn = P.V + (int64_t)(j + 1) * ldv;
         for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) {
             const double t = (SM ? wsl[i - lo] : P.w[i]) / hn;
             vn[i] = t;
@@ -359,7 +421,7 @@ __global__ void k_trsv(const double *H, int m, int j, const double *g, double *y
 }
 
 // u = sum_{k<j} y_k V_k
-__global__ void k_combine(const double *__restrict__ V, int64_t n, int nk, const double *__restrict__ y,
+__global__ void k_combine(const double *__restrict__ V, int64_t n, int64_t ldv, int nk, const double *__restrict__ y,
                           double *u) {
     __shared__ double ys[1024];
     for (int k = threadIdx.x; k < nk; k += blockDim.x) ys[k] = y[k];
@@ -368,10 +430,10 @@ __global__ void k_combine(const double *__restrict__ V, int64_t n, int nk, const
         double s0 = 0.0, s1 = 0.0;
         int k = 0;
         for (; k + 1 < nk; k += 2) {
-            s0 = fma(ys[k], V[(int64_t)k * n + i], s0);
-            s1 = fma(ys[k + 1], V[(int64_t)(k + 1) * n + i], s1);
+            s0 = fma(ys[k], V[(int64_t)k * ldv + i], s0);
+            s1 = fma(ys[k + 1], V[(int64_t)(k + 1) * ldv + i], s1);
         }
-        if (k < nk) s0 = fma(ys[k], V[(int64_t)k * n + i], s0);
+        if (k < nk) s0 = fma(ys[k], V[(int64_t)k * ldv + i], s0);
         u[i] = s0 + s1;
     }
 }
@@ -434,6 +496,7 @@ struct Ws {
     int m = 0, max_iters = 0;
     int64_t n = 0;
     int nblk = 1, nupd = 1;
+    int64_t ldv = 0, chunk = 0;
     bool use_smem = false;
     size_t smem = 0;
     DBuf<double> V, w, z, r, vin, u;
@@ -464,7 +527,8 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
     w->m = m;
     w->max_iters = max_iters;
     w->n = n;
-    w->V.alloc((int64_t)(m + 1) * n);
+    w->ldv = (n + 31) / 32 * 32;
+    w->V.alloc((int64_t)(m + 1) * w->ldv);
     w->w.alloc(n);
     w->z.alloc(n);
     w->r.alloc(n);
@@ -487,7 +551,8 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
     if (const char *e = getenv("PMGR_ARNOLDI_BPS")) bps = atoi(e) > 0 ? atoi(e) : 2;
     w->nblk = (per_sm < bps ? per_sm : bps) * num_sms();
     {
-        const int64_t chunk = (n + w->nblk - 1) / w->nblk;
+        const int64_t chunk = ((n + w->nblk - 1) / w->nblk + 31) / 32 * 32;
+        w->chunk = chunk;
         int per_sm_sm = 0;
         w->smem = (size_t)(16 * chunk);
         if (chunk <= 3072 &&
@@ -544,6 +609,8 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
     AoParams P;
     P.V = W.V.p;
     P.n = n;
+    P.ldv = W.ldv;
+    P.chunk = W.chunk;
     P.w = W.w.p;
     P.vin = W.vin.p;
     P.dev = W.dev.p;
@@ -699,7 +766,7 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
             if (j > 0) {
                 k_trsv<<<1, 256, sizeof(double) * j, s>>>(W.H.p, m, j, W.g.p, W.y.p);
                 PMGR_LAUNCHED();
-                k_combine<<<vec_grid(n), 256, 0, s>>>(W.V.p, n, j, W.y.p, W.u.p);
+                k_combine<<<vec_grid(n), 256, 0, s>>>(W.V.p, n, W.ldv, j, W.y.p, W.u.p);
                 PMGR_LAUNCHED();
                 if (M) mgr_apply(*M, W.u.p, W.z.p, s);
                 else vec_copy(W.u.p, W.z.p, n, s);
