@@ -84,13 +84,28 @@ __global__ void __launch_bounds__(256) k_bsr3(int64_t nb, const int64_t *__restr
     }
     const int kk = lane / 3, c = lane - 3 * kk;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (lane < 30) {
-        for (int64_t k = k0 + kk; k < k1; k += 10) {
-            const double xv = op.x(3 * __ldg(bci + k) + c);
+    // batches of 30 blocks: every column index and value load of a lane's
+    // three blocks is issued before the dependent x gathers
+    for (int64_t kb = k0; kb < k1; kb += 30) {
+        int cc[3];
+        double vv[3][3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int64_t k = kb + kk + 10 * t;
+            const bool ok = lane < 30 && k < k1;
+            cc[t] = ok ? __ldg(bci + k) : -1;
             const double *p = bval + 9 * k + 3 * c;
-            a0 = fma(__ldg(p), xv, a0);
-            a1 = fma(__ldg(p + 1), xv, a1);
-            a2 = fma(__ldg(p + 2), xv, a2);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) vv[t][r] = ok ? __ldg(p + r) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            if (cc[t] >= 0) {
+                const double xv = op.x(3 * cc[t] + c);
+                a0 = fma(vv[t][0], xv, a0);
+                a1 = fma(vv[t][1], xv, a1);
+                a2 = fma(vv[t][2], xv, a2);
+            }
         }
     }
 #pragma unroll
