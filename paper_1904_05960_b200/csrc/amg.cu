@@ -654,7 +654,7 @@ namespace {
 void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out = nullptr);
 
 const double *coarse_solve(pmgr_amg &h, cudaStream_t s) {
-    dense_matvec(h.coarse_inv.p, h.coarse->nrows, h.cb.p, h.cx.p, s);
+    dense_matvec(h.coarse_inv.p, h.coarse->nrows, h.coarse->nrows, h.cb.p, h.cx.p, s);
     return h.cx.p;
 }
 
@@ -663,7 +663,7 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     // L.x = L.b / dtilde (the first sweep from zero), written by the producer
     AmgLevel &L = h.levels[l];
     if ((int)l == h.collapse_from) {
-        dense_matvec(h.collapsed.p, L.A->nrows, L.b.p, out ? out : L.xo.p, s);
+        dense_matvec(h.collapsed.p, L.A->nrows, h.collapsed_ld, L.b.p, out ? out : L.xo.p, s);
         return;
     }
     const CsrView A = L.A->view();
@@ -715,12 +715,12 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
         if (x) {
             // x + inv * (b - A x)
             spmv_residual(h.coarse->view(), x, b, h.cb.p, s);
-            dense_matvec(h.coarse_inv.p, n, h.cb.p, h.cx.p, s);
+            dense_matvec(h.coarse_inv.p, n, n, h.cb.p, h.cx.p, s);
             vec_copy(x, out, n, s);
             vec_axpy(1.0, h.cx.p, out, n, s);
         } else {
             vec_copy(b, h.cb.p, n, s);
-            dense_matvec(h.coarse_inv.p, n, h.cb.p, out, s);
+            dense_matvec(h.coarse_inv.p, n, n, h.cb.p, out, s);
         }
         return;
     }

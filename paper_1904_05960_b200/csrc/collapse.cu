@@ -116,8 +116,13 @@ void collapse_tail(pmgr_amg &h, cudaStream_t s) {
     TBuf<double> B(k * k, s);
     k_eye<<<grid_for(k * k, 256), 256, 0, s>>>(k, B.p);
     PMGR_LAUNCHED();
-    h.collapsed.alloc(k * k);
-    cycle_block(h, (size_t)from, k, B.p, h.collapsed.p, s);
+    TBuf<double> Mt(k * k, s);
+    cycle_block(h, (size_t)from, k, B.p, Mt.p, s);
+    // rows padded to 256 bytes for the paired loads of the solve-phase matvec
+    h.collapsed_ld = (k + 31) / 32 * 32;
+    h.collapsed.alloc(k * h.collapsed_ld);
+    PMGR_CUDA(cudaMemcpy2DAsync(h.collapsed.p, sizeof(double) * h.collapsed_ld, Mt.p, sizeof(double) * k,
+                                sizeof(double) * k, k, cudaMemcpyDeviceToDevice, s));
     PMGR_CUDA(cudaStreamSynchronize(s));
     h.collapse_from = from;
 }

@@ -353,7 +353,7 @@ void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,
                           const int64_t *findex, double *z, cudaStream_t s);
 void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,
                const double *b, double *x, double *xpre, bool forward, cudaStream_t s);
-void dense_matvec(const double *M, int64_t n, const double *x, double *y, cudaStream_t s);
+void dense_matvec(const double *M, int64_t n, int64_t ld, const double *x, double *y, cudaStream_t s);
 
 // elementwise (spmv.cu)
 void vec_gather(const double *src, const int64_t *idx, int64_t n, double *dst, cudaStream_t s);

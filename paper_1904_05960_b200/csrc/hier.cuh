@@ -40,7 +40,8 @@ struct pmgr_amg {
     int64_t flagged = 0;
     bool prof_tag = false;  // time level-0 smoother kernels (F-relax AMG of MGR level 0)
     int collapse_from = -1;          // levels >= this run as one dense operator (-1: none)
-    pmgr::DBuf<double> collapsed;    // that operator, row-major n x n
+    pmgr::DBuf<double> collapsed;    // that operator, row-major n x collapsed_ld
+    int64_t collapsed_ld = 0;
 };
 
 namespace pmgr {

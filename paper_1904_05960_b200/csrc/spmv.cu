@@ -250,32 +250,64 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
     }
 }
 
-// y = M x, M dense row-major (the collapsed coarse cycle): x staged in
-// shared memory, one warp per row with four independent accumulators
-__global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t n,
+// y = M x, M dense row-major with leading dimension ld (the collapsed coarse
+// cycle, the coarsest inverse).  A block owns 8 rows; its warps split the
+// columns, so a lane's x element is loaded once and reused for the 8 rows
+// whose 8 independent matrix loads are in flight together.  PAIR: ld even,
+// 16-byte loads of column pairs.
+template <bool PAIR>
+__global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t n, int64_t ld,
                                                       const double *__restrict__ x, double *__restrict__ y) {
     pdl_wait();
-    extern __shared__ double xs[];
-    const bool staged = n <= 8192;
-    if (staged)
-        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) xs[j] = x[j];
-    __syncthreads();
-    const double *xv = staged ? xs : x;
-    const int lane = threadIdx.x & 31;
-    for (int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5); row < n; row += (int64_t)gridDim.x * 8) {
-        const double *mr = M + row * n;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int64_t j = lane;
-        for (; j + 96 < n; j += 128) {
-            s0 = fma(__ldg(mr + j), xv[j], s0);
-            s1 = fma(__ldg(mr + j + 32), xv[j + 32], s1);
-            s2 = fma(__ldg(mr + j + 64), xv[j + 64], s2);
-            s3 = fma(__ldg(mr + j + 96), xv[j + 96], s3);
+    constexpr int RB = 8, W = 8;
+    __shared__ double red[W][RB];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * RB;
+    const int nr = (int)(n - r0 < RB ? n - r0 : RB);
+    double acc[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+    if (PAIR) {
+        const int64_t np = n >> 1;
+        for (int64_t p = warp * 32 + lane; p < np; p += W * 32) {
+            const double2 xv = make_double2(__ldg(x + 2 * p), __ldg(x + 2 * p + 1));
+            double2 m[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                m[r] = r < nr ? __ldg(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + p)
+                              : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) acc[r] = fma(m[r].y, xv.y, fma(m[r].x, xv.x, acc[r]));
         }
-        for (; j < n; j += 32) s0 = fma(__ldg(mr + j), xv[j], s0);
-        double s = (s0 + s1) + (s2 + s3);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-        if (lane == 0) y[row] = s;
+        if ((n & 1) && warp == 0 && lane == 0) {
+            const double xl = __ldg(x + n - 1);
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                if (r < nr) acc[r] = fma(__ldg(M + (r0 + r) * ld + n - 1), xl, acc[r]);
+        }
+    } else {
+        for (int64_t c = warp * 32 + lane; c < n; c += W * 32) {
+            const double xv = __ldg(x + c);
+            double m[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) m[r] = r < nr ? __ldg(M + (r0 + r) * ld + c) : 0.0;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) acc[r] = fma(m[r], xv, acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        double t = acc[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+        if (lane == 0) red[warp][r] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) t += red[w][threadIdx.x];
+        y[r0 + threadIdx.x] = t;
     }
 }
 
@@ -393,12 +425,13 @@ void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const do
     PMGR_LAUNCHED();
 }
 
-void dense_matvec(const double *M, int64_t n, const double *x, double *y, cudaStream_t s) {
+void dense_matvec(const double *M, int64_t n, int64_t ld, const double *x, double *y, cudaStream_t s) {
     if (n == 0) return;
-    const int64_t blocks = (n + 7) / 8;
-    const size_t smem = n <= 8192 ? sizeof(double) * n : 0;
-    launch_pdl(k_dense_matvec, dim3((unsigned)(blocks < 4 * num_sms() ? blocks : 4 * num_sms())), dim3(256), smem, s,
-               M, n, x, y);
+    const unsigned blocks = (unsigned)((n + 7) / 8);
+    if (ld % 2 == 0)
+        launch_pdl(k_dense_matvec<true>, dim3(blocks), dim3(256), 0, s, M, n, ld, x, y);
+    else
+        launch_pdl(k_dense_matvec<false>, dim3(blocks), dim3(256), 0, s, M, n, ld, x, y);
     PMGR_LAUNCHED();
 }
 
