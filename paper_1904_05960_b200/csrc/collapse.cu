@@ -100,7 +100,7 @@ void cycle_block(pmgr_amg &h, size_t l, int64_t k, const double *B, double *XO, 
 void collapse_tail(pmgr_amg &h, cudaStream_t s) {
     static const int64_t limit = [] {
         const char *e = getenv("PMGR_COLLAPSE_ROWS");
-        const int64_t v = e ? atoll(e) : (int64_t)2560;
+        const int64_t v = e ? atoll(e) : (int64_t)3584;  // <= ~100 MB dense, read once per cycle
         return v < 65535 ? v : (int64_t)65535;
     }();
     if (limit <= 0 || h.levels.empty()) return;

@@ -214,13 +214,17 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
         return e ? atof(e) : 1e30;
     }();
     const bool stream = 12.0 * (double)A.nnz > stream_mb * 1024 * 1024;
+    static const double g32_mean = [] {
+        const char *e = getenv("PMGR_SPMV_G32_MEAN");
+        return e ? atof(e) : 100.0;
+    }();
     if (mean <= 3.0) {
         go<2>(A, op, stream, s);
     } else if (mean <= 12.0) {
         go<4>(A, op, stream, s);
     } else if (mean <= 48.0) {
         go<8>(A, op, stream, s);
-    } else if (mean <= 160.0) {
+    } else if (mean <= g32_mean) {
         go<16>(A, op, stream, s);
     } else {
         go<32>(A, op, stream, s);
