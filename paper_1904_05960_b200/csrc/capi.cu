@@ -206,6 +206,11 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
         require(nlevels >= 0 && (nlevels == 0 || levels), "bad level list");
         init_pool();
         auto h = pmgr::mgr_build(A->m, field_of, entity_of, levels, nlevels, *cfg, S(stream));
+        // solve-phase block copy of A0 for the Krylov SpMV (node-blocked F prefix)
+        if (h->block_prefix > 0 && A->m->nbrows == 0) {
+            pmgr::csr_make_bsr3(*A->m, h->block_prefix, S(stream));
+            PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        }
         *out = h.release();
     });
 }

@@ -196,12 +196,16 @@ struct CsrView {
     const int32_t *ci;
     const double *v;
     int64_t maxrow = -1;  // longest row (-1: unknown); picks the SpMV lane group
-    // optional 3x3 block copy for the solve phase (node-blocked elasticity):
-    // block rows of 3 scalar rows, blocks column-major, zeros where the CSR has none
-    int64_t nbrows = 0, nblocks = 0;
+    // optional solve-phase copy: the leading 3*nbrows rows/columns as 3x3
+    // blocks (node-blocked displacement; blocks column-major, zero-filled),
+    // every other entry as a remainder CSR over all rows (rro null: none)
+    int64_t nbrows = 0, nblocks = 0, nrem = 0;
     const int64_t *bro = nullptr;
     const int32_t *bci = nullptr;
     const double *bval = nullptr;
+    const int64_t *rro = nullptr;
+    const int32_t *rci = nullptr;
+    const double *rv = nullptr;
 };
 
 struct Csr {
@@ -218,17 +222,20 @@ struct Csr {
         v.alloc(z);
     }
     int64_t maxrow = -1;
-    int64_t nbrows = 0, nblocks = 0;
-    DBuf<int64_t> bro;
-    DBuf<int32_t> bci;
-    DBuf<double> bval;
+    int64_t nbrows = 0, nblocks = 0, nrem = 0;
+    DBuf<int64_t> bro, rro;
+    DBuf<int32_t> bci, rci;
+    DBuf<double> bval, rv;
     CsrView view() const {
-        return CsrView{nrows, ncols, nnz, ro.p, ci.p, v.p, maxrow, nbrows, nblocks, bro.p, bci.p, bval.p};
+        return CsrView{nrows, ncols,  nnz,   ro.p,   ci.p,  v.p,   maxrow, nbrows,
+                       nblocks, nrem, bro.p, bci.p, bval.p, rro.p, rci.p, rv.p};
     }
 };
 
-// build the 3x3 block (BSR3) solve copy of a node-blocked square operator
-void csr_make_bsr3(Csr &A, cudaStream_t s);
+// build the block-prefix solve copy of a square operator whose leading
+// `prefix` rows/columns are node-blocked by 3 (prefix = nrows: pure BSR3);
+// keeps the plain CSR when the blocks would be too sparse
+void csr_make_bsr3(Csr &A, int64_t prefix, cudaStream_t s);
 
 // record the longest row of a finished operator (setup time, synchronises)
 void csr_finalize(Csr &A, cudaStream_t s);
@@ -303,7 +310,9 @@ inline double csr_pass_bytes(int64_t nrows, int64_t ncols, int64_t nnz) {
 }
 // one pass over the format the solve actually streams (BSR3 copy if present)
 inline double csr_pass_bytes(const CsrView &A) {
-    if (A.nbrows > 0) return 76.0 * A.nblocks + 8.0 * (A.nbrows + 1) + 8.0 * A.ncols + 8.0 * A.nrows;
+    if (A.nbrows > 0)
+        return 76.0 * A.nblocks + 8.0 * (A.nbrows + 1) + 12.0 * A.nrem + (A.rro ? 8.0 * (A.nrows + 1) : 0.0) +
+               8.0 * A.ncols + 8.0 * A.nrows;
     return csr_pass_bytes(A.nrows, A.ncols, A.nnz);
 }
 

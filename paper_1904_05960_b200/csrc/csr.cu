@@ -461,8 +461,8 @@ void csr_finalize(Csr &A, cudaStream_t s) {
 }
 
 namespace {
-// number of distinct block columns of node row I (union over its 3 rows)
-__global__ void k_bsr_count(int64_t nb, const int64_t *ro, const int32_t *ci, int64_t *cnt) {
+// block columns (< prefix) of node row I: union over its 3 rows
+__global__ void k_bsr_count(int64_t nb, int32_t prefix, const int64_t *ro, const int32_t *ci, int64_t *cnt) {
     const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (I >= nb) return;
     // merge the three sorted rows by block column
@@ -472,24 +472,20 @@ __global__ void k_bsr_count(int64_t nb, const int64_t *ro, const int32_t *ci, in
         e[r] = ro[3 * I + r + 1];
     }
     int64_t c = 0;
-    int32_t last = -1;
     while (true) {
         int32_t best = INT32_MAX;
         for (int r = 0; r < 3; ++r)
-            if (p[r] < e[r]) best = min(best, ci[p[r]] / 3);
+            if (p[r] < e[r] && ci[p[r]] < prefix) best = min(best, ci[p[r]] / 3);
         if (best == INT32_MAX) break;
         for (int r = 0; r < 3; ++r)
-            while (p[r] < e[r] && ci[p[r]] / 3 == best) ++p[r];
-        if (best != last) {
-            ++c;
-            last = best;
-        }
+            while (p[r] < e[r] && ci[p[r]] < prefix && ci[p[r]] / 3 == best) ++p[r];
+        ++c;
     }
     cnt[I] = c;
 }
 
-__global__ void k_bsr_fill(int64_t nb, const int64_t *ro, const int32_t *ci, const double *v, const int64_t *bro,
-                           int32_t *bci, double *bval) {
+__global__ void k_bsr_fill(int64_t nb, int32_t prefix, const int64_t *ro, const int32_t *ci, const double *v,
+                           const int64_t *bro, int32_t *bci, double *bval) {
     const int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (I >= nb) return;
     int64_t p[3], e[3];
@@ -501,41 +497,81 @@ __global__ void k_bsr_fill(int64_t nb, const int64_t *ro, const int32_t *ci, con
     while (true) {
         int32_t best = INT32_MAX;
         for (int r = 0; r < 3; ++r)
-            if (p[r] < e[r]) best = min(best, ci[p[r]] / 3);
+            if (p[r] < e[r] && ci[p[r]] < prefix) best = min(best, ci[p[r]] / 3);
         if (best == INT32_MAX) break;
         bci[w] = best;
         double *blk = bval + 9 * w;
         for (int t = 0; t < 9; ++t) blk[t] = 0.0;
         for (int r = 0; r < 3; ++r)
-            while (p[r] < e[r] && ci[p[r]] / 3 == best) {
+            while (p[r] < e[r] && ci[p[r]] < prefix && ci[p[r]] / 3 == best) {
                 blk[r + 3 * (ci[p[r]] - 3 * best)] = v[p[r]];  // column-major
                 ++p[r];
             }
         ++w;
     }
 }
+
+// remainder entries: columns >= prefix of the prefix rows, all of the others
+__global__ void k_rem_count(int64_t n, int32_t prefix, const int64_t *ro, const int32_t *ci, int64_t *cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t c = 0;
+    for (int64_t q = ro[i]; q < ro[i + 1]; ++q) c += (i >= prefix || ci[q] >= prefix);
+    cnt[i] = c;
+}
+
+__global__ void k_rem_fill(int64_t n, int32_t prefix, const int64_t *ro, const int32_t *ci, const double *v,
+                           const int64_t *rro, int32_t *rci, double *rv) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t w = rro[i];
+    for (int64_t q = ro[i]; q < ro[i + 1]; ++q)
+        if (i >= prefix || ci[q] >= prefix) {
+            rci[w] = ci[q];
+            rv[w] = v[q];
+            ++w;
+        }
+}
 }  // namespace
 
-void csr_make_bsr3(Csr &A, cudaStream_t s) {
+void csr_make_bsr3(Csr &A, int64_t prefix, cudaStream_t s) {
     static const bool off = getenv("PMGR_NO_BSR") && getenv("PMGR_NO_BSR")[0] != '0';
-    if (off || A.nrows != A.ncols || A.nrows % 3 != 0 || A.nrows == 0) return;
-    const int64_t nb = A.nrows / 3;
+    if (off || A.nrows != A.ncols || prefix % 3 != 0 || prefix <= 0 || prefix > A.nrows) return;
+    const int64_t nb = prefix / 3, n = A.nrows;
     TBuf<int64_t> cnt(nb, s);
-    k_bsr_count<<<grid_for(nb, 128), 128, 0, s>>>(nb, A.ro.p, A.ci.p, cnt.p);
+    k_bsr_count<<<grid_for(nb, 128), 128, 0, s>>>(nb, (int32_t)prefix, A.ro.p, A.ci.p, cnt.p);
     PMGR_LAUNCHED();
     A.bro.alloc(nb + 1);
     const int64_t nblk = exclusive_scan_total(cnt.p, A.bro.p, nb, s);
+    int64_t nrem = 0;
+    if (prefix < n) {
+        TBuf<int64_t> rc(n, s);
+        k_rem_count<<<grid_for(n, 128), 128, 0, s>>>(n, (int32_t)prefix, A.ro.p, A.ci.p, rc.p);
+        PMGR_LAUNCHED();
+        A.rro.alloc(n + 1);
+        nrem = exclusive_scan_total(rc.p, A.rro.p, n, s);
+    }
     // only worth it when the blocks are (nearly) full
-    if (9.0 * (double)nblk > 1.25 * (double)A.nnz) {
+    if (9.0 * (double)nblk > 1.25 * (double)(A.nnz - nrem)) {
         A.bro.release();
+        A.rro.release();
         return;
     }
     A.bci.alloc(nblk);
     A.bval.alloc(9 * nblk);
-    k_bsr_fill<<<grid_for(nb, 128), 128, 0, s>>>(nb, A.ro.p, A.ci.p, A.v.p, A.bro.p, A.bci.p, A.bval.p);
+    k_bsr_fill<<<grid_for(nb, 128), 128, 0, s>>>(nb, (int32_t)prefix, A.ro.p, A.ci.p, A.v.p, A.bro.p, A.bci.p,
+                                                 A.bval.p);
     PMGR_LAUNCHED();
+    if (prefix < n) {
+        A.rci.alloc(nrem);
+        A.rv.alloc(nrem);
+        k_rem_fill<<<grid_for(n, 128), 128, 0, s>>>(n, (int32_t)prefix, A.ro.p, A.ci.p, A.v.p, A.rro.p, A.rci.p,
+                                                    A.rv.p);
+        PMGR_LAUNCHED();
+    }
     A.nbrows = nb;
     A.nblocks = nblk;
+    A.nrem = nrem;
 }
 
 void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {

@@ -102,6 +102,7 @@ struct pmgr_mgr {
     int32_t terminal_cycles = 1;
     int32_t f_relax_post = 0;
     int64_t n = 0;
+    int64_t block_prefix = 0;  // level-0 F rows: a node-blocked prefix of A0 (0: none)
     pmgr::DBuf<double> tz;  // terminal scratch
 };
 

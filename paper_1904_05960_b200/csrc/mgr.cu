@@ -348,7 +348,13 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
         csr_finalize(*A_ff, s);
-        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3) csr_make_bsr3(*A_ff, s);
+        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3) csr_make_bsr3(*A_ff, A_ff->nrows, s);
+        if (li == 0 && A_ff->nbrows > 0) {
+            // F rows first, then C rows: the same blocks lead A0 itself
+            bool prefix = true;
+            for (int64_t i = 0; i < n && prefix; ++i) prefix = (((sp.c_mask >> (fo[i] & 63)) & 1ull) != 0) == (i >= L.nf);
+            if (prefix) h->block_prefix = L.nf;
+        }
         csr_finalize(L.A_cf, s);
         if (need_dinv) {
             L.dinv_ff.alloc(L.nf);

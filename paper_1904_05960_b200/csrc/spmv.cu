@@ -63,49 +63,68 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
     if (active && lane == 0) op.out(row, s);
 }
 
-// BSR3: a warp per block row (3 scalar rows), blocks stored column-major.
-// Lane 3k+c (k < 10) owns column c of every 10th block: one column index,
-// one x load and three contiguous values feeding the three row sums, so x
-// is gathered once per block column instead of once per entry and the
-// matrix stream is 76 B per 9 entries instead of CSR's 108 B.
+// Block-prefix SpMV: a warp per row triple.  Triples inside the node-blocked
+// prefix stream their 3x3 blocks (column-major): lane 3k+c (k < 10) owns
+// column c of every 10th block -- one column index, one x gather and three
+// contiguous values feeding the three row sums, 76 B per 9 entries instead
+// of CSR's 108 B.  Remainder entries (coupling columns, rows past the
+// prefix) are read as CSR by three 10-lane groups, one per row.
 template <class Op>
-__global__ void __launch_bounds__(256) k_bsr3(int64_t nb, const int64_t *__restrict__ bro,
+__global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
                                               const int32_t *__restrict__ bci, const double *__restrict__ bval,
-                                              Op op, int trigger) {
+                                              const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
+                                              const double *__restrict__ rv, Op op, int trigger) {
     pdl_wait();
     if (trigger) pdl_trigger();
     const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    const bool active = I < nb;
-    int64_t k0 = 0, k1 = 0;
-    if (active) {
-        k0 = __ldg(bro + I);
-        k1 = __ldg(bro + I + 1);
-    }
     const int kk = lane / 3, c = lane - 3 * kk;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    // batches of 30 blocks: every column index and value load of a lane's
-    // three blocks is issued before the dependent x gathers
-    for (int64_t kb = k0; kb < k1; kb += 30) {
-        int cc[3];
-        double vv[3][3];
+    if (I < nb) {
+        const int64_t k0 = __ldg(bro + I), k1 = __ldg(bro + I + 1);
+        // batches of 30 blocks: every column index and value load of a lane's
+        // three blocks is issued before the dependent x gathers
+        for (int64_t kb = k0; kb < k1; kb += 30) {
+            int cc[3];
+            double vv[3][3];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            const int64_t k = kb + kk + 10 * t;
-            const bool ok = lane < 30 && k < k1;
-            cc[t] = ok ? __ldg(bci + k) : -1;
-            const double *p = bval + 9 * k + 3 * c;
+            for (int t = 0; t < 3; ++t) {
+                const int64_t k = kb + kk + 10 * t;
+                const bool ok = lane < 30 && k < k1;
+                cc[t] = ok ? __ldg(bci + k) : -1;
+                const double *p = bval + 9 * k + 3 * c;
 #pragma unroll
-            for (int r = 0; r < 3; ++r) vv[t][r] = ok ? __ldg(p + r) : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            if (cc[t] >= 0) {
-                const double xv = op.x(3 * cc[t] + c);
-                a0 = fma(vv[t][0], xv, a0);
-                a1 = fma(vv[t][1], xv, a1);
-                a2 = fma(vv[t][2], xv, a2);
+                for (int r = 0; r < 3; ++r) vv[t][r] = ok ? __ldg(p + r) : 0.0;
             }
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                if (cc[t] >= 0) {
+                    const double xv = op.x(3 * cc[t] + c);
+                    a0 = fma(vv[t][0], xv, a0);
+                    a1 = fma(vv[t][1], xv, a1);
+                    a2 = fma(vv[t][2], xv, a2);
+                }
+            }
+        }
+    }
+    if (rro != nullptr && I < ntrip) {
+        const int g = lane / 10, gl = lane - 10 * g;
+        const int64_t row = 3 * I + g;
+        if (g < 3 && row < n) {
+            const int64_t q1 = __ldg(rro + row + 1);
+            double t0 = 0.0, t1 = 0.0;
+            int64_t q = __ldg(rro + row) + gl;
+            for (; q + 10 < q1; q += 20) {
+                const double v0 = __ldg(rv + q), v1 = __ldg(rv + q + 10);
+                const int c0 = __ldg(rci + q), c1 = __ldg(rci + q + 10);
+                t0 = fma(v0, op.x(c0), t0);
+                t1 = fma(v1, op.x(c1), t1);
+            }
+            if (q < q1) t0 = fma(__ldg(rv + q), op.x(__ldg(rci + q)), t0);
+            const double t = t0 + t1;
+            if (g == 0) a0 += t;
+            else if (g == 1) a1 += t;
+            else a2 += t;
         }
     }
 #pragma unroll
@@ -114,7 +133,7 @@ __global__ void __launch_bounds__(256) k_bsr3(int64_t nb, const int64_t *__restr
         a1 += __shfl_xor_sync(FULL, a1, o);
         a2 += __shfl_xor_sync(FULL, a2, o);
     }
-    if (active && lane < 3) op.out(3 * I + lane, lane == 0 ? a0 : lane == 1 ? a1 : a2);
+    if (I < ntrip && lane < 3 && 3 * I + lane < n) op.out(3 * I + lane, lane == 0 ? a0 : lane == 1 ? a1 : a2);
 }
 
 struct OpY {
@@ -194,9 +213,11 @@ template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
     if (A.nbrows > 0) {
-        const unsigned grid = grid_for(A.nbrows * 32, 256);
+        const int64_t ntrip = A.rro ? (A.nrows + 2) / 3 : A.nbrows;
+        const unsigned grid = grid_for(ntrip * 32, 256);
         const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
-        launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, A.nbrows, A.bro, A.bci, A.bval, op, trigger);
+        launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval, A.rro,
+                   A.rci, A.rv, op, trigger);
         PMGR_LAUNCHED();
         return;
     }
