@@ -709,6 +709,17 @@ bool amg_cycle_rows(pmgr_amg &h, const double *v, const int64_t *rows, double *o
     return true;
 }
 
+bool amg_entry(pmgr_amg &h, double **b, double **x, const double **dtilde) {
+    if (h.levels.empty() || !h.levels[0].jacobi) return false;
+    AmgLevel &L = h.levels[0];
+    *b = L.b.p;
+    *x = L.x.p;
+    *dtilde = L.dtilde.p;
+    return true;
+}
+
+void amg_cycle_prefilled(pmgr_amg &h, double *out, cudaStream_t s) { cycle_from_zero(h, 0, s, out); }
+
 void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaStream_t s) {
     if (h.levels.empty()) {
         const int64_t n = h.coarse->nrows;

@@ -356,8 +356,16 @@ void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, doubl
 // bo = v[rows], xo = bo / d (gathered right-hand side + first l1-Jacobi sweep)
 void vec_gather_div(const double *v, const int64_t *rows, const double *d, int64_t n, double *bo, double *xo,
                     cudaStream_t s);
-void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows,
-                     double *r, cudaStream_t s);
+// optional fused first step of the level consuming a C residual
+struct ResidNext {
+    const double *d2 = nullptr;  // l1-Jacobi entry of an AMG: x2 = r / d2
+    double *x2 = nullptr;
+    const int64_t *sidx = nullptr;  // Jacobi F-relaxation of an MGR level: sz[sidx[k]] = sd[..] r[k]
+    const double *sd = nullptr;
+    double *sz = nullptr;
+};
+void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows, double *r,
+                     const ResidNext &nx, cudaStream_t s);
 void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,
                           const int64_t *findex, double *z, cudaStream_t s);
 void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,

@@ -54,6 +54,11 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
 // zero-guess cycle on the right-hand side v[rows] (gather fused into the
 // first sweep); false when the hierarchy cannot take that path
 bool amg_cycle_rows(pmgr_amg &h, const double *v, const int64_t *rows, double *out, cudaStream_t s);
+// l1-Jacobi entry of a hierarchy whose first step a producer fuses: the
+// right-hand side goes to *b, b / dtilde to *x (false: not such a hierarchy)
+bool amg_entry(pmgr_amg &h, double **b, double **x, const double **dtilde);
+// V-cycle from zero once amg_entry's buffers are filled
+void amg_cycle_prefilled(pmgr_amg &h, double *out, cudaStream_t s);
 
 // One MGR reduction level (reference mgr.py:300-311).
 struct MgrLevel {

@@ -206,7 +206,7 @@ std::string field_names(const std::set<int> &f) {
     return out + "]";
 }
 
-void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s);
+void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s, bool prefilled = false);
 
 void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
     if (L.f_relax == PMGR_FRELAX_AMG) {
@@ -227,8 +227,14 @@ void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
     }
 }
 
-void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s) {
+// prefilled: the producer of v already ran this level's first step (the
+// terminal AMG's l1-Jacobi entry, or a single Jacobi F-relaxation)
+void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s, bool prefilled) {
     if (l == h.levels.size()) {
+        if (prefilled) {
+            amg_cycle_prefilled(*h.terminal, z, s);
+            return;
+        }
         amg_cycle(*h.terminal, v, nullptr, z, s);
         for (int c = 1; c < h.terminal_cycles; ++c) {
             vec_copy(z, h.tz.p, h.terminal_A->nrows, s);
@@ -238,10 +244,12 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
     }
     MgrLevel &L = h.levels[l];
     const bool pre = !h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE;
+    double *rc = L.rc.p;
+    bool next_prefilled = false;
     if (pre) {
         // single sweep: the F gather is fused into the relaxation's first kernel
-        bool done = false;
-        if (L.f_relax_sweeps == 1) {
+        bool done = prefilled;
+        if (!done && L.f_relax_sweeps == 1) {
             if (L.f_relax == PMGR_FRELAX_AMG) {
                 done = amg_cycle_rows(*L.amg, v, L.f_rows.p, L.zf.p, s);
             } else {
@@ -253,11 +261,31 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
             vec_gather(v, L.f_rows.p, L.nf, L.vf.p, s);
             f_relax_apply(L, L.vf.p, L.zf.p, s);
         }
-        spmv_resid_rows(L.A_cf.view(), L.zf.p, v, L.c_rows.p, L.rc.p, s);
+        // the consumer's first step rides on the residual kernel
+        ResidNext nx;
+        if (l + 1 == h.levels.size()) {
+            const double *d = nullptr;
+            double *b = nullptr, *x = nullptr;
+            if (h.terminal_cycles == 1 && amg_entry(*h.terminal, &b, &x, &d)) {
+                rc = b;
+                nx.x2 = x;
+                nx.d2 = d;
+                next_prefilled = true;
+            }
+        } else {
+            MgrLevel &N = h.levels[l + 1];
+            if (N.f_relax == PMGR_FRELAX_JACOBI && N.f_relax_sweeps == 1) {
+                nx.sidx = N.f_index.p;
+                nx.sd = N.dinv_ff.p;
+                nx.sz = N.zf.p;
+                next_prefilled = true;
+            }
+        }
+        spmv_resid_rows(L.A_cf.view(), L.zf.p, v, L.c_rows.p, rc, nx, s);
     } else {
         vec_gather(v, L.c_rows.p, L.nc, L.rc.p, s);
     }
-    apply_level(h, l + 1, L.rc.p, L.zc.p, s);
+    apply_level(h, l + 1, rc, L.zc.p, s, next_prefilled);
     spmv_prolong_combine(L.P.view(), L.zc.p, pre ? L.zf.p : nullptr, pre ? L.f_index.p : nullptr, z, s);
     if (h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
         // r = v - A z ; z[F] += M_FF^{-1} r[F]

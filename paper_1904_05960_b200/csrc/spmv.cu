@@ -182,8 +182,23 @@ struct OpResidRows {
     const double *zf, *v;
     const int64_t *rows;
     double *r;
+    // the next level's first step, fused: its l1-Jacobi entry x2 = r / d2,
+    // or its Jacobi F-relaxation sz[f] = sd[f] r for its F rows f = sidx[k]
+    const double *d2;
+    double *x2;
+    const int64_t *sidx;
+    const double *sd;
+    double *sz;
     __device__ double x(int j) const { return __ldg(zf + j); }
-    __device__ void out(int64_t k, double s) const { r[k] = v[rows[k]] - s; }
+    __device__ void out(int64_t k, double s) const {
+        const double t = v[rows[k]] - s;
+        r[k] = t;
+        if (x2) x2[k] = t / d2[k];
+        if (sidx) {
+            const int64_t f = sidx[k];
+            if (f >= 0) sz[f] = sd[f] * t;
+        }
+    }
 };
 struct OpProlong {
     const double *ec, *zf;
@@ -432,9 +447,9 @@ void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s) {
     launch(A, OpAdd{e, x}, s);
 }
 
-void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows,
-                     double *r, cudaStream_t s) {
-    launch(A, OpResidRows{zf, v, rows, r}, s);
+void spmv_resid_rows(const CsrView &A, const double *zf, const double *v, const int64_t *rows, double *r,
+                     const ResidNext &nx, cudaStream_t s) {
+    launch(A, OpResidRows{zf, v, rows, r, nx.d2, nx.x2, nx.sidx, nx.sd, nx.sz}, s);
 }
 
 void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf, const int64_t *findex,
