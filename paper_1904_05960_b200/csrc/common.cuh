@@ -199,6 +199,7 @@ struct CsrView {
     // optional solve-phase copy: the leading 3*nbrows rows/columns as 3x3
     // blocks (node-blocked displacement; blocks column-major, zero-filled),
     // every other entry as a remainder CSR over all rows (rro null: none)
+    const uint16_t *ci16 = nullptr;  // 16-bit copy of ci (ncols <= 65536), solve phase
     int64_t nbrows = 0, nblocks = 0, nrem = 0;
     const int64_t *bro = nullptr;
     const int32_t *bci = nullptr;
@@ -222,13 +223,14 @@ struct Csr {
         v.alloc(z);
     }
     int64_t maxrow = -1;
+    DBuf<uint16_t> ci16;
     int64_t nbrows = 0, nblocks = 0, nrem = 0;
     DBuf<int64_t> bro, rro;
     DBuf<int32_t> bci, rci;
     DBuf<double> bval, rv;
     CsrView view() const {
-        return CsrView{nrows, ncols,  nnz,   ro.p,   ci.p,  v.p,   maxrow, nbrows,
-                       nblocks, nrem, bro.p, bci.p, bval.p, rro.p, rci.p, rv.p};
+        return CsrView{nrows,   ncols, nnz,    ro.p,  ci.p,  v.p,  maxrow, ci16.p,
+                       nbrows, nblocks, nrem, bro.p, bci.p, bval.p, rro.p, rci.p, rv.p};
     }
 };
 
@@ -313,7 +315,7 @@ inline double csr_pass_bytes(const CsrView &A) {
     if (A.nbrows > 0)
         return 76.0 * A.nblocks + 8.0 * (A.nbrows + 1) + 12.0 * A.nrem + (A.rro ? 8.0 * (A.nrows + 1) : 0.0) +
                8.0 * A.ncols + 8.0 * A.nrows;
-    return csr_pass_bytes(A.nrows, A.ncols, A.nnz);
+    return csr_pass_bytes(A.nrows, A.ncols, A.nnz) - (A.ci16 ? 2.0 * A.nnz : 0.0);
 }
 
 // ---------------------------------------------------------------------------

@@ -30,10 +30,15 @@ template <bool STREAM>
 __device__ __forceinline__ int ldc(const int32_t *p) {
     return STREAM ? __ldcs(p) : __ldg(p);
 }
+template <bool STREAM>
+__device__ __forceinline__ int ldc(const uint16_t *p) {
+    return (int)(STREAM ? __ldcs(reinterpret_cast<const unsigned short *>(p))
+                        : __ldg(reinterpret_cast<const unsigned short *>(p)));
+}
 
-template <int G, bool STREAM, class Op>
+template <int G, bool STREAM, class Op, class IT>
 __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
-                                              const int32_t *__restrict__ ci,
+                                              const IT *__restrict__ ci,
                                               const double *__restrict__ v, Op op, int trigger) {
     pdl_wait();
     if (trigger) pdl_trigger();
@@ -211,17 +216,23 @@ struct OpProlong {
     }
 };
 
-template <int G, class Op>
-void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
+template <int G, class Op, class IT>
+void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_t s) {
     const int block = 256;
     const unsigned grid = grid_for(A.nrows * G, block);
     // let the next kernel's launch overlap this one only when this grid is a
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
     if (stream)
-        launch_pdl(k_spmv<G, true, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
+        launch_pdl(k_spmv<G, true, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, trigger);
     else
-        launch_pdl(k_spmv<G, false, Op>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, A.ci, A.v, op, trigger);
+        launch_pdl(k_spmv<G, false, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, trigger);
+}
+
+template <int G, class Op>
+void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
+    if (A.ci16) go_t<G>(A, A.ci16, op, stream, s);
+    else go_t<G>(A, A.ci, op, stream, s);
 }
 
 template <class Op>
