@@ -192,6 +192,41 @@ PMGR_API int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const d
 PMGR_API int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h_dev,
                    double *w_dev, void *stream);
 
+/* ---- row distribution (the reference is single-process) ---
+ * Every rank builds the global A / MGR hierarchy on its own GPU (replicated
+ * setup), then pmgr_dist_create keeps its rows of every operator.  `bounds`
+ * (nranks + 1 entries) are the ranks' contiguous row ranges of a rank-major
+ * numbered A (problems.rank_major); all coarser spaces inherit contiguous
+ * ranges.  Exchange steps: halo exchange before each operator that reads
+ * other ranks' entries, an all-gather of the collapsed coarse right-hand
+ * side, all-reduces of the Krylov projections.  A distributed application is
+ * bitwise identical to the single-GPU one. */
+typedef struct { char internal[128]; } pmgr_nccl_id;   /* ncclUniqueId */
+typedef struct pmgr_transport pmgr_transport;
+typedef struct pmgr_dist pmgr_dist;
+PMGR_API int pmgr_nccl_get_id(pmgr_nccl_id *out);
+/* NCCL communicator over the process's libnccl (one GPU per rank). */
+PMGR_API int pmgr_transport_nccl_create(const pmgr_nccl_id *id, int32_t rank, int32_t nranks,
+                                        pmgr_transport **out);
+PMGR_API int pmgr_transport_destroy(pmgr_transport *t);
+PMGR_API int pmgr_dist_create(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t rank,
+                              int32_t nranks, pmgr_transport *t, void *stream, pmgr_dist **out);
+/* global index of the first owned row and the number of owned rows */
+PMGR_API int pmgr_dist_info(const pmgr_dist *d, int64_t *lo, int64_t *n_own);
+/* owned slices (n_own doubles) in and out */
+PMGR_API int pmgr_dist_apply(pmgr_dist *d, const double *v_own_dev, double *z_own_dev, void *stream);
+PMGR_API int pmgr_dist_spmv(pmgr_dist *d, const double *x_own_dev, double *y_own_dev, void *stream);
+PMGR_API int pmgr_dist_gmres(pmgr_dist *d, const double *b_own_dev, double *x_own_dev, int nonzero_x0,
+                             const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, double *history_host,
+                             int32_t history_cap, void *stream);
+PMGR_API int pmgr_dist_destroy(pmgr_dist *d);
+/* Test harness: nranks ranks emulated on this GPU (in-process loopback
+ * transport, one host thread per rank).  what = 0: z = M v; what = 1: GMRES
+ * from x0 = 0 (stats filled).  in / out are global device vectors. */
+PMGR_API int pmgr_dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t nranks,
+                               int32_t what, const double *in_dev, double *out_dev,
+                               const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

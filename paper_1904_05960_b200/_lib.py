@@ -58,6 +58,10 @@ class GmresCfg(ctypes.Structure):
                 ("atol", ctypes.c_double)]
 
 
+class NcclId(ctypes.Structure):
+    _fields_ = [("internal", ctypes.c_char * 128)]
+
+
 class GmresStats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32), ("history_len", ctypes.c_int32),
                 ("restarts", ctypes.c_int32)]
@@ -100,6 +104,19 @@ SIGNATURES = {
     "pmgr_prof_query": (ctypes.c_int, [ctypes.c_int32, c_i64p, c_dp, c_dp]),
     "pmgr_multidot": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
     "pmgr_multiaxpy": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
+    "pmgr_nccl_get_id": (ctypes.c_int, [ctypes.POINTER(NcclId)]),
+    "pmgr_transport_nccl_create": (ctypes.c_int, [ctypes.POINTER(NcclId), ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.POINTER(vp)]),
+    "pmgr_transport_destroy": (ctypes.c_int, [vp]),
+    "pmgr_dist_create": (ctypes.c_int, [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, vp, vp, ctypes.POINTER(vp)]),
+    "pmgr_dist_info": (ctypes.c_int, [vp, c_i64p, c_i64p]),
+    "pmgr_dist_apply": (ctypes.c_int, [vp, vp, vp, vp]),
+    "pmgr_dist_spmv": (ctypes.c_int, [vp, vp, vp, vp]),
+    "pmgr_dist_gmres": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.POINTER(GmresCfg),
+                                       ctypes.POINTER(GmresStats), vp, ctypes.c_int32, vp]),
+    "pmgr_dist_destroy": (ctypes.c_int, [vp]),
+    "pmgr_dist_emulate": (ctypes.c_int, [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, vp, vp,
+                                         ctypes.POINTER(GmresCfg), ctypes.POINTER(GmresStats), vp]),
 }
 
 _lib = None

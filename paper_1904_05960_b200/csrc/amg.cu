@@ -660,10 +660,18 @@ const double *coarse_solve(pmgr_amg &h, cudaStream_t s) {
 
 void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     // precondition: L.b holds the right-hand side and, on l1-Jacobi levels,
-    // L.x = L.b / dtilde (the first sweep from zero), written by the producer
+    // L.x = L.b / dtilde (the first sweep from zero), written by the producer.
+    // Row-distributed hierarchies: owned rows only, ghosts exchanged before
+    // every operator that reads them (halo_exchange is a no-op otherwise).
     AmgLevel &L = h.levels[l];
+    double *y = out ? out : L.xo.p;
     if ((int)l == h.collapse_from) {
-        dense_matvec(h.collapsed.p, L.A->nrows, h.collapsed_ld, L.b.p, out ? out : L.xo.p, s);
+        if (h.gather) {
+            gather_full(h.gather.get(), L.b.p + L.off, h.full.p, s);
+            dense_matvec_rows(h.collapsed.p, L.A->nrows, h.gather->n_full, h.collapsed_ld, h.full.p, y + L.off, s);
+        } else {
+            dense_matvec(h.collapsed.p, L.A->nrows, h.collapsed_ld, L.b.p, y, s);
+        }
         return;
     }
     const CsrView A = L.A->view();
@@ -672,18 +680,21 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     const double pass = csr_pass_bytes(A) + 16.0 * A.nrows;
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_SWEEP0 : PROF_KINDS, pass, s);
+        halo_exchange(L.halo.get(), L.x.p, s);
         spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
     } else {
         vec_zero(L.x.p, A.nrows, s);
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, true, s);
         spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
     }
+    halo_exchange(L.halo.get(), L.r.p, s);
     const double *e;
     if (has_next) {
         AmgLevel &N = h.levels[l + 1];
         if (N.jacobi) spmv_restrict_div(L.R.view(), L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
         else spmv(L.R.view(), L.r.p, N.b.p, s);
         cycle_from_zero(h, l + 1, s);
+        halo_exchange(N.halo.get(), N.xo.p, s);
         e = N.xo.p;
     } else {
         spmv(L.R.view(), L.r.p, h.cb.p, s);
@@ -692,10 +703,11 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     spmv_add(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_JACOBI : PROF_KINDS, pass, s);
-        spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, out ? out : L.xo.p, s);
+        halo_exchange(L.halo.get(), L.x.p, s);
+        spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, y, s);
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);
-        vec_copy(L.x.p, out ? out : L.xo.p, A.nrows, s);
+        vec_copy(L.x.p, y, A.nrows, s);
     }
 }
 
@@ -704,7 +716,8 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
 bool amg_cycle_rows(pmgr_amg &h, const double *v, const int64_t *rows, double *out, cudaStream_t s) {
     if (h.levels.empty() || !h.levels[0].jacobi) return false;
     AmgLevel &L = h.levels[0];
-    vec_gather_div(v, rows, L.dtilde.p, L.A->nrows, L.b.p, L.x.p, s);
+    const int64_t o = L.off;
+    vec_gather_div(v, rows + o, L.dtilde.p + o, L.A->nrows, L.b.p + o, L.x.p + o, s);
     cycle_from_zero(h, 0, s, out);
     return true;
 }
@@ -738,7 +751,8 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
     AmgLevel &L = h.levels[0];
     const int64_t n = L.A->nrows;
     if (!x) {
-        if (L.jacobi) vec_copy_div(b, L.dtilde.p, n, L.b.p, L.x.p, s);
+        const int64_t o = L.off;
+        if (L.jacobi) vec_copy_div(b + o, L.dtilde.p + o, n, L.b.p + o, L.x.p + o, s);
         else vec_copy(b, L.b.p, n, s);
         cycle_from_zero(h, 0, s, out);
         return;

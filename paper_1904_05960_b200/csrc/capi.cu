@@ -6,7 +6,7 @@
 #include <cstring>
 #include <string>
 
-#include "hier.cuh"
+#include "dist.cuh"
 
 namespace {
 thread_local std::string g_msg;
@@ -208,7 +208,7 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
         auto h = pmgr::mgr_build(A->m, field_of, entity_of, levels, nlevels, *cfg, S(stream));
         // solve-phase block copy of A0 for the Krylov SpMV (node-blocked F prefix)
         if (h->block_prefix > 0 && A->m->nbrows == 0) {
-            pmgr::csr_make_bsr3(*A->m, h->block_prefix, S(stream));
+            pmgr::csr_make_bsr3(*A->m, h->block_prefix, h->block_prefix, S(stream));
             PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         }
         *out = h.release();
@@ -328,3 +328,108 @@ int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- distribution
+
+struct pmgr_transport {
+    std::unique_ptr<pmgr::Transport> t;
+};
+struct pmgr_dist {
+    std::unique_ptr<pmgr::DistSolver> d;
+};
+
+int pmgr_nccl_get_id(pmgr_nccl_id *out) {
+    return guard([&] {
+        require(out, "NULL argument");
+        pmgr::nccl_unique_id(out);
+    });
+}
+
+int pmgr_transport_nccl_create(const pmgr_nccl_id *id, int32_t rank, int32_t nranks, pmgr_transport **out) {
+    return guard([&] {
+        require(id && out, "NULL argument");
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+        auto *t = new pmgr_transport;
+        t->t = pmgr::make_nccl_transport(*id, rank, nranks);
+        *out = t;
+    });
+}
+
+int pmgr_transport_destroy(pmgr_transport *t) {
+    return guard([&] { delete t; });
+}
+
+int pmgr_dist_create(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t rank, int32_t nranks,
+                     pmgr_transport *t, void *stream, pmgr_dist **out) {
+    return guard([&] {
+        require(A && M && bounds && out, "NULL argument");
+        require(nranks == 1 || t, "a transport is required for more than one rank");
+        init_pool();
+        auto *d = new pmgr_dist;
+        try {
+            d->d = pmgr::dist_build(A, M, bounds, rank, nranks, t ? t->t.get() : nullptr, S(stream));
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
+int pmgr_dist_info(const pmgr_dist *d, int64_t *lo, int64_t *n_own) {
+    return guard([&] {
+        require(d && lo && n_own, "NULL argument");
+        *lo = d->d->lo;
+        *n_own = d->d->n_own;
+    });
+}
+
+int pmgr_dist_apply(pmgr_dist *d, const double *v_own_dev, double *z_own_dev, void *stream) {
+    return guard([&] {
+        require(d && (d->d->n_own == 0 || (v_own_dev && z_own_dev)), "NULL argument");
+        pmgr::dist_apply(*d->d, v_own_dev, z_own_dev, S(stream));
+    });
+}
+
+int pmgr_dist_spmv(pmgr_dist *d, const double *x_own_dev, double *y_own_dev, void *stream) {
+    return guard([&] {
+        require(d && (d->d->n_own == 0 || (x_own_dev && y_own_dev)), "NULL argument");
+        pmgr::DistSolver &D = *d->d;
+        D.ensure_work();
+        if (D.n_own > 0)
+            PMGR_CUDA(cudaMemcpyAsync(D.ze.p + D.off, x_own_dev, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice,
+                                      S(stream)));
+        pmgr::halo_exchange(D.halo0.get(), D.ze.p, S(stream));
+        pmgr::spmv(D.A.view(), D.ze.p, D.we.p, S(stream));
+        if (D.n_own > 0)
+            PMGR_CUDA(cudaMemcpyAsync(y_own_dev, D.we.p + D.off, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice,
+                                      S(stream)));
+    });
+}
+
+int pmgr_dist_gmres(pmgr_dist *d, const double *b_own_dev, double *x_own_dev, int nonzero_x0,
+                    const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, double *history_host, int32_t history_cap,
+                    void *stream) {
+    return guard([&] {
+        require(d && cfg && stats, "NULL argument");
+        require(d->d->n_own == 0 || (b_own_dev && x_own_dev), "NULL argument");
+        pmgr::dist_gmres(*d->d, b_own_dev, x_own_dev, nonzero_x0, *cfg, *stats, history_host, history_cap,
+                         S(stream));
+    });
+}
+
+int pmgr_dist_destroy(pmgr_dist *d) {
+    return guard([&] { delete d; });
+}
+
+int pmgr_dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t nranks, int32_t what,
+                      const double *in_dev, double *out_dev, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats,
+                      void *stream) {
+    return guard([&] {
+        require(A && M && bounds && in_dev && out_dev, "NULL argument");
+        require(what == 0 || (cfg && stats), "NULL argument");
+        require(nranks >= 1, "nranks must be positive");
+        init_pool();
+        pmgr::dist_emulate(A, M, bounds, nranks, what, in_dev, out_dev, cfg, stats, S(stream));
+    });
+}

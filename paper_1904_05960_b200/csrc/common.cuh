@@ -196,10 +196,14 @@ struct CsrView {
     const int32_t *ci;
     const double *v;
     int64_t maxrow = -1;  // longest row (-1: unknown); picks the SpMV lane group
+    // row-distributed operators (dist.cu): output row i is written at i + row_off
+    // of the output vector; lanes force the global operator's lane group
+    int64_t row_off = 0;
+    int lanes = 0;
+    const uint16_t *ci16 = nullptr;  // 16-bit copy of ci (ncols <= 65536), solve phase
     // optional solve-phase copy: the leading 3*nbrows rows/columns as 3x3
     // blocks (node-blocked displacement; blocks column-major, zero-filled),
     // every other entry as a remainder CSR over all rows (rro null: none)
-    const uint16_t *ci16 = nullptr;  // 16-bit copy of ci (ncols <= 65536), solve phase
     int64_t nbrows = 0, nblocks = 0, nrem = 0;
     const int64_t *bro = nullptr;
     const int32_t *bci = nullptr;
@@ -223,21 +227,23 @@ struct Csr {
         v.alloc(z);
     }
     int64_t maxrow = -1;
+    int64_t row_off = 0;
+    int lanes = 0;
     DBuf<uint16_t> ci16;
     int64_t nbrows = 0, nblocks = 0, nrem = 0;
     DBuf<int64_t> bro, rro;
     DBuf<int32_t> bci, rci;
     DBuf<double> bval, rv;
     CsrView view() const {
-        return CsrView{nrows,   ncols, nnz,    ro.p,  ci.p,  v.p,  maxrow, ci16.p,
-                       nbrows, nblocks, nrem, bro.p, bci.p, bval.p, rro.p, rci.p, rv.p};
+        return CsrView{nrows,  ncols,   nnz,  ro.p,  ci.p,  v.p,    maxrow, row_off, lanes,
+                       ci16.p, nbrows, nblocks, nrem, bro.p, bci.p, bval.p, rro.p, rci.p, rv.p};
     }
 };
 
-// build the block-prefix solve copy of a square operator whose leading
-// `prefix` rows/columns are node-blocked by 3 (prefix = nrows: pure BSR3);
-// keeps the plain CSR when the blocks would be too sparse
-void csr_make_bsr3(Csr &A, int64_t prefix, cudaStream_t s);
+// build the block-prefix solve copy of an operator whose leading prow rows
+// and pcol columns are node-blocked by 3 (prow = nrows, pcol = ncols: pure
+// BSR3); keeps the plain CSR when the blocks would be too sparse (unless force)
+void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force = false);
 
 // record the longest row of a finished operator (setup time, synchronises)
 void csr_finalize(Csr &A, cudaStream_t s);
@@ -372,6 +378,10 @@ void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,
                           const int64_t *findex, double *z, cudaStream_t s);
 void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,
                const double *b, double *x, double *xpre, bool forward, cudaStream_t s);
+int spmv_lanes(const CsrView &A);
+// y[0:nrows) = M[0:nrows, 0:ncols) x (row-distributed collapsed operators)
+void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld, const double *x, double *y,
+                       cudaStream_t s);
 void dense_matvec(const double *M, int64_t n, int64_t ld, const double *x, double *y, cudaStream_t s);
 
 // elementwise (spmv.cu)

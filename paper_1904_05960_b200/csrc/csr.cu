@@ -526,21 +526,22 @@ __global__ void k_bsr_fill(int64_t nb, int32_t prefix, const int64_t *ro, const 
 }
 
 // remainder entries: columns >= prefix of the prefix rows, all of the others
-__global__ void k_rem_count(int64_t n, int32_t prefix, const int64_t *ro, const int32_t *ci, int64_t *cnt) {
+__global__ void k_rem_count(int64_t n, int64_t prow, int32_t prefix, const int64_t *ro, const int32_t *ci,
+                            int64_t *cnt) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int64_t c = 0;
-    for (int64_t q = ro[i]; q < ro[i + 1]; ++q) c += (i >= prefix || ci[q] >= prefix);
+    for (int64_t q = ro[i]; q < ro[i + 1]; ++q) c += (i >= prow || ci[q] >= prefix);
     cnt[i] = c;
 }
 
-__global__ void k_rem_fill(int64_t n, int32_t prefix, const int64_t *ro, const int32_t *ci, const double *v,
-                           const int64_t *rro, int32_t *rci, double *rv) {
+__global__ void k_rem_fill(int64_t n, int64_t prow, int32_t prefix, const int64_t *ro, const int32_t *ci,
+                           const double *v, const int64_t *rro, int32_t *rci, double *rv) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int64_t w = rro[i];
     for (int64_t q = ro[i]; q < ro[i + 1]; ++q)
-        if (i >= prefix || ci[q] >= prefix) {
+        if (i >= prow || ci[q] >= prefix) {
             rci[w] = ci[q];
             rv[w] = v[q];
             ++w;
@@ -548,38 +549,37 @@ __global__ void k_rem_fill(int64_t n, int32_t prefix, const int64_t *ro, const i
 }
 }  // namespace
 
-void csr_make_bsr3(Csr &A, int64_t prefix, cudaStream_t s) {
+void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force) {
     static const bool off = getenv("PMGR_NO_BSR") && getenv("PMGR_NO_BSR")[0] != '0';
-    if (off || A.nrows != A.ncols || prefix % 3 != 0 || prefix <= 0 || prefix > A.nrows) return;
-    const int64_t nb = prefix / 3, n = A.nrows;
+    if (off || prow % 3 != 0 || pcol % 3 != 0 || prow <= 0 || prow > A.nrows || pcol > A.ncols) return;
+    const int64_t nb = prow / 3, n = A.nrows;
+    const int32_t prefix = (int32_t)pcol;
     TBuf<int64_t> cnt(nb, s);
-    k_bsr_count<<<grid_for(nb, 128), 128, 0, s>>>(nb, (int32_t)prefix, A.ro.p, A.ci.p, cnt.p);
+    k_bsr_count<<<grid_for(nb, 128), 128, 0, s>>>(nb, prefix, A.ro.p, A.ci.p, cnt.p);
     PMGR_LAUNCHED();
     A.bro.alloc(nb + 1);
     const int64_t nblk = exclusive_scan_total(cnt.p, A.bro.p, nb, s);
     int64_t nrem = 0;
-    if (prefix < n) {
-        TBuf<int64_t> rc(n, s);
-        k_rem_count<<<grid_for(n, 128), 128, 0, s>>>(n, (int32_t)prefix, A.ro.p, A.ci.p, rc.p);
-        PMGR_LAUNCHED();
-        A.rro.alloc(n + 1);
-        nrem = exclusive_scan_total(rc.p, A.rro.p, n, s);
-    }
+    TBuf<int64_t> rc(n, s);
+    k_rem_count<<<grid_for(n, 128), 128, 0, s>>>(n, prow, prefix, A.ro.p, A.ci.p, rc.p);
+    PMGR_LAUNCHED();
+    A.rro.alloc(n + 1);
+    nrem = exclusive_scan_total(rc.p, A.rro.p, n, s);
+    if (nrem == 0) A.rro.release();
     // only worth it when the blocks are (nearly) full
-    if (9.0 * (double)nblk > 1.25 * (double)(A.nnz - nrem)) {
+    if (!force && 9.0 * (double)nblk > 1.25 * (double)(A.nnz - nrem)) {
         A.bro.release();
         A.rro.release();
         return;
     }
     A.bci.alloc(nblk);
     A.bval.alloc(9 * nblk);
-    k_bsr_fill<<<grid_for(nb, 128), 128, 0, s>>>(nb, (int32_t)prefix, A.ro.p, A.ci.p, A.v.p, A.bro.p, A.bci.p,
-                                                 A.bval.p);
+    k_bsr_fill<<<grid_for(nb, 128), 128, 0, s>>>(nb, prefix, A.ro.p, A.ci.p, A.v.p, A.bro.p, A.bci.p, A.bval.p);
     PMGR_LAUNCHED();
-    if (prefix < n) {
+    if (nrem > 0) {
         A.rci.alloc(nrem);
         A.rv.alloc(nrem);
-        k_rem_fill<<<grid_for(n, 128), 128, 0, s>>>(n, (int32_t)prefix, A.ro.p, A.ci.p, A.v.p, A.rro.p, A.rci.p,
+        k_rem_fill<<<grid_for(n, 128), 128, 0, s>>>(n, prow, prefix, A.ro.p, A.ci.p, A.v.p, A.rro.p, A.rci.p,
                                                     A.rv.p);
         PMGR_LAUNCHED();
     }

@@ -1,0 +1,999 @@
+// dist.cu -- row-distributed solve phase.
+//
+// One process per GPU.  Every rank builds the global hierarchy (replicated
+// setup: same kernels, same bits), then keeps only its rows of every operator:
+//
+// * numbering: level 0 is rank-major (problems.rank_major), so each rank owns
+//   one contiguous global range of every space -- F/C splits and AMG C points
+//   keep their relative order, so the ranges survive coarsening;
+// * a rank stores a space as an "ext" vector: owned range plus the ghost
+//   entries its local operators read, in global order.  Local rows therefore
+//   sum their columns in the global stored order with the global operator's
+//   lane group (and block layout), so a distributed application is bitwise
+//   identical to the single-GPU one;
+// * exchange steps: a halo exchange before every operator that reads ghosts
+//   (point-to-point, only the neighbours that share entries), an all-gather
+//   of the collapsed coarse right-hand side (a few thousand doubles), and the
+//   all-reduces of the Krylov projections and norms.
+//
+// Transports: NCCL (loaded at run time, one GPU per rank) and an in-process
+// loopback hub that emulates N ranks on one GPU for the parity tests (host
+// threads meet at every exchange; the copies are ordinary stream-ordered
+// kernels, no kernel ever waits on another rank).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
+
+#include <thrust/copy.h>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
+
+#include "dist.cuh"
+
+namespace pmgr {
+
+// =========================================================== transports
+
+namespace {
+
+__global__ void k_pull(double *__restrict__ dst, const double *__restrict__ src, const int64_t *__restrict__ idx,
+                       int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n) dst[t] = src[idx[t]];
+}
+
+constexpr int MAX_RANKS = 64;
+struct PtrPack {
+    double *p[MAX_RANKS];
+};
+
+__global__ void k_sum_ranks(PtrPack bufs, int nranks, int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += bufs.p[r][t];  // rank order on every rank
+    for (int r = 0; r < nranks; ++r) bufs.p[r][t] = s;
+}
+
+}  // namespace
+
+// ---- loopback: N ranks of one process on one GPU and one stream ---------
+struct LoopbackHub {
+    int n;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool failed = false;
+    std::string why;
+    enum Kind { EXCHANGE, GATHER, ALLREDUCE };
+    struct Post {
+        Kind kind;
+        Halo *h = nullptr;
+        Gather *g = nullptr;
+        double *p = nullptr;
+        const double *cp = nullptr;
+        int64_t cnt = 0;
+    };
+    std::vector<Post> posts;
+    explicit LoopbackHub(int nr) : n(nr), posts(nr) {}
+
+    void execute(cudaStream_t s) {
+        const Kind k = posts[0].kind;
+        for (auto &p : posts)
+            if (p.kind != k) fail(PMGR_ERR_INVALID, "loopback ranks diverged (different collective order)");
+        if (k == EXCHANGE) {
+            for (int r = 0; r < n; ++r) {
+                Halo &hr = *posts[r].h;
+                for (size_t i = 0; i < hr.rpeer.size(); ++i) {
+                    const int p = hr.rpeer[i];
+                    Halo &hp = *posts[p].h;
+                    auto it = std::find(hp.speer.begin(), hp.speer.end(), r);
+                    if (it == hp.speer.end()) fail(PMGR_ERR_INVALID, "halo plans disagree");
+                    const size_t j = (size_t)(it - hp.speer.begin());
+                    if (hp.scnt[j] != hr.rcnt[i]) fail(PMGR_ERR_INVALID, "halo segment sizes disagree");
+                    if (hr.rcnt[i] == 0) continue;
+                    k_pull<<<grid_for(hr.rcnt[i], 256), 256, 0, s>>>(posts[r].p + hr.roff[i], posts[p].p + hp.off,
+                                                                      hp.send_idx.p + hp.soff[j], hr.rcnt[i]);
+                    PMGR_LAUNCHED();
+                }
+            }
+        } else if (k == GATHER) {
+            for (int r = 0; r < n; ++r) {
+                Gather &g = *posts[r].g;
+                for (int p = 0; p < n; ++p) {
+                    const int64_t c = g.start[p + 1] - g.start[p];
+                    if (c > 0)
+                        PMGR_CUDA(cudaMemcpyAsync(posts[r].p + g.start[p], posts[p].cp, sizeof(double) * c,
+                                                  cudaMemcpyDeviceToDevice, s));
+                }
+            }
+        } else {
+            if (n > MAX_RANKS) fail(PMGR_ERR_NOT_SUPPORTED, "loopback all-reduce: too many ranks");
+            PtrPack pk;
+            for (int r = 0; r < n; ++r) pk.p[r] = posts[r].p;
+            const int64_t cnt = posts[0].cnt;
+            if (cnt > 0) {
+                k_sum_ranks<<<grid_for(cnt, 128), 128, 0, s>>>(pk, n, cnt);
+                PMGR_LAUNCHED();
+            }
+        }
+    }
+
+    void arrive(int rank, const Post &p, cudaStream_t s) {
+        std::unique_lock<std::mutex> lk(m);
+        if (failed) fail(PMGR_ERR_CUDA, "loopback peer failed: " + why);
+        posts[rank] = p;
+        const uint64_t my = gen;
+        if (++arrived == n) {
+            try {
+                execute(s);
+            } catch (const Error &e) {
+                failed = true;
+                why = e.msg;
+            }
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != my || failed; });
+        }
+        if (failed) fail(PMGR_ERR_CUDA, "loopback exchange failed: " + why);
+    }
+
+    void abort(const std::string &w) {
+        std::lock_guard<std::mutex> lk(m);
+        if (!failed) {
+            failed = true;
+            why = w;
+        }
+        cv.notify_all();
+    }
+};
+
+struct LoopbackTransport : Transport {
+    LoopbackHub *hub;
+    LoopbackTransport(LoopbackHub *h, int r) : hub(h) {
+        rank = r;
+        nranks = h->n;
+    }
+    void exchange(Halo &h, double *ext, cudaStream_t s) override {
+        LoopbackHub::Post p;
+        p.kind = LoopbackHub::EXCHANGE;
+        p.h = &h;
+        p.p = ext;
+        hub->arrive(rank, p, s);
+    }
+    void gather(Gather &g, const double *own, double *full, cudaStream_t s) override {
+        LoopbackHub::Post p;
+        p.kind = LoopbackHub::GATHER;
+        p.g = &g;
+        p.cp = own;
+        p.p = full;
+        hub->arrive(rank, p, s);
+    }
+    void allreduce(double *buf, int64_t n, cudaStream_t s) override {
+        LoopbackHub::Post p;
+        p.kind = LoopbackHub::ALLREDUCE;
+        p.p = buf;
+        p.cnt = n;
+        hub->arrive(rank, p, s);
+    }
+};
+
+// ---- NCCL, resolved at run time (the process's libnccl, e.g. torch's) ----
+namespace {
+typedef int nres_t;  // ncclResult_t
+struct NcclApi {
+    void *h = nullptr;
+    nres_t (*GetUniqueId)(void *) = nullptr;
+    nres_t (*CommInitRank)(void **, int, pmgr_nccl_id, int) = nullptr;
+    nres_t (*CommDestroy)(void *) = nullptr;
+    nres_t (*GroupStart)() = nullptr;
+    nres_t (*GroupEnd)() = nullptr;
+    nres_t (*Send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    nres_t (*Recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    nres_t (*AllReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(nres_t) = nullptr;
+};
+constexpr int NCCL_FLOAT64 = 8;  // ncclFloat64 / ncclDouble
+constexpr int NCCL_SUM = 0;      // ncclSum
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *nm : names) {
+            api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+            if (!api.h) api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (api.h) break;
+        }
+        if (!api.h) return;
+        api.GetUniqueId = (nres_t(*)(void *))dlsym(api.h, "ncclGetUniqueId");
+        api.CommInitRank = (nres_t(*)(void **, int, pmgr_nccl_id, int))dlsym(api.h, "ncclCommInitRank");
+        api.CommDestroy = (nres_t(*)(void *))dlsym(api.h, "ncclCommDestroy");
+        api.GroupStart = (nres_t(*)())dlsym(api.h, "ncclGroupStart");
+        api.GroupEnd = (nres_t(*)())dlsym(api.h, "ncclGroupEnd");
+        api.Send = (nres_t(*)(const void *, size_t, int, int, void *, cudaStream_t))dlsym(api.h, "ncclSend");
+        api.Recv = (nres_t(*)(void *, size_t, int, int, void *, cudaStream_t))dlsym(api.h, "ncclRecv");
+        api.AllReduce =
+            (nres_t(*)(const void *, void *, size_t, int, int, void *, cudaStream_t))dlsym(api.h, "ncclAllReduce");
+        api.GetErrorString = (const char *(*)(nres_t))dlsym(api.h, "ncclGetErrorString");
+    });
+    if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.AllReduce)
+        fail(PMGR_ERR_NOT_SUPPORTED, "NCCL is not loadable in this process (libnccl.so.2)");
+    return api;
+}
+
+void nccl_check(nres_t r, const char *what) {
+    if (r != 0) {
+        const char *msg = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+        fail(PMGR_ERR_CUDA, std::string(what) + ": " + msg);
+    }
+}
+
+__global__ void k_pack(double *__restrict__ dst, const double *__restrict__ src, const int64_t *__restrict__ idx,
+                       int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n) dst[t] = src[idx[t]];
+}
+}  // namespace
+
+void nccl_unique_id(pmgr_nccl_id *out) { nccl_check(nccl().GetUniqueId(out), "ncclGetUniqueId"); }
+
+struct NcclTransport : Transport {
+    void *comm = nullptr;
+    NcclTransport(const pmgr_nccl_id &id, int r, int nr) {
+        rank = r;
+        nranks = nr;
+        nccl_check(nccl().CommInitRank(&comm, nr, id, r), "ncclCommInitRank");
+    }
+    ~NcclTransport() override {
+        if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
+    }
+    void exchange(Halo &h, double *ext, cudaStream_t s) override {
+        const int64_t ns = h.send_idx.n;
+        if (ns > 0) {
+            k_pack<<<grid_for(ns, 256), 256, 0, s>>>(h.sbuf.p, ext + h.off, h.send_idx.p, ns);
+            PMGR_LAUNCHED();
+        }
+        NcclApi &a = nccl();
+        nccl_check(a.GroupStart(), "ncclGroupStart");
+        for (size_t i = 0; i < h.speer.size(); ++i)
+            if (h.scnt[i] > 0)
+                nccl_check(a.Send(h.sbuf.p + h.soff[i], (size_t)h.scnt[i], NCCL_FLOAT64, h.speer[i], comm, s),
+                           "ncclSend");
+        for (size_t i = 0; i < h.rpeer.size(); ++i)
+            if (h.rcnt[i] > 0)
+                nccl_check(a.Recv(ext + h.roff[i], (size_t)h.rcnt[i], NCCL_FLOAT64, h.rpeer[i], comm, s),
+                           "ncclRecv");
+        nccl_check(a.GroupEnd(), "ncclGroupEnd");
+    }
+    void gather(Gather &g, const double *own, double *full, cudaStream_t s) override {
+        const int64_t mine = g.start[rank + 1] - g.start[rank];
+        if (mine > 0)
+            PMGR_CUDA(cudaMemcpyAsync(full + g.start[rank], own, sizeof(double) * mine, cudaMemcpyDeviceToDevice, s));
+        NcclApi &a = nccl();
+        nccl_check(a.GroupStart(), "ncclGroupStart");
+        for (int p = 0; p < nranks; ++p) {
+            if (p == rank) continue;
+            const int64_t c = g.start[p + 1] - g.start[p];
+            if (mine > 0) nccl_check(a.Send(own, (size_t)mine, NCCL_FLOAT64, p, comm, s), "ncclSend");
+            if (c > 0) nccl_check(a.Recv(full + g.start[p], (size_t)c, NCCL_FLOAT64, p, comm, s), "ncclRecv");
+        }
+        nccl_check(a.GroupEnd(), "ncclGroupEnd");
+    }
+    void allreduce(double *buf, int64_t n, cudaStream_t s) override {
+        if (n <= 0) return;
+        nccl_check(nccl().AllReduce(buf, buf, (size_t)n, NCCL_FLOAT64, NCCL_SUM, comm, s), "ncclAllReduce");
+    }
+};
+
+std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank, int nranks) {
+    return std::unique_ptr<Transport>(new NcclTransport(id, rank, nranks));
+}
+
+void halo_exchange(Halo *h, double *ext, cudaStream_t s) {
+    if (h && h->tr && h->tr->nranks > 1) h->tr->exchange(*h, ext, s);
+}
+
+void gather_full(Gather *g, const double *own, double *full, cudaStream_t s) {
+    if (g->tr && g->tr->nranks > 1) {
+        g->tr->gather(*g, own, full, s);
+    } else {
+        const int64_t c = g->n_full;
+        if (c > 0) PMGR_CUDA(cudaMemcpyAsync(full, own, sizeof(double) * c, cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// ===================================================== local hierarchy
+
+namespace {
+
+// a vector space of the global hierarchy as seen by one rank
+struct Space {
+    int id = -1;
+    int64_t n = 0;                 // global size
+    std::vector<int64_t> start;    // nranks + 1 global range starts
+    std::vector<std::vector<int64_t>> ghosts;  // per rank, sorted global ids
+    bool triples = false;          // close ghost sets under node triples (BSR operators)
+    DBuf<int64_t> gdev;            // my ghosts on the device
+    int64_t lo = 0, hi = 0, nlow = 0;
+    std::shared_ptr<Halo> halo;
+    int64_t n_own() const { return hi - lo; }
+    int64_t n_ext() const { return (int64_t)ghosts_me->size() + n_own(); }
+    const std::vector<int64_t> *ghosts_me = nullptr;
+};
+
+struct Reader {
+    const Csr *Y;
+    Space *rows;
+};
+
+__global__ void k_mark_outside(int64_t n, const int64_t *ro, int64_t r0, const int32_t *ci, int64_t c0, int64_t c1,
+                               int64_t *out, int64_t *cnt) {
+    // collect columns outside [c0, c1) of rows [r0, r0 + n)
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int64_t q = ro[r0 + i]; q < ro[r0 + i + 1]; ++q) {
+        const int64_t c = ci[q];
+        if (c < c0 || c >= c1) out[atomicAdd((unsigned long long *)cnt, 1ull)] = c;
+    }
+}
+
+__global__ void k_localize(int64_t n, const int64_t *ro, int64_t r0, const int32_t *ci, const double *v, int64_t c0,
+                           int64_t c1, int64_t nlow, const int64_t *ghosts, int64_t ng, int64_t *lro, int32_t *lci,
+                           double *lv) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int64_t base = ro[r0];
+    lro[i] = ro[r0 + i] - base;
+    if (i == n) return;
+    for (int64_t q = ro[r0 + i]; q < ro[r0 + i + 1]; ++q) {
+        const int64_t c = ci[q];
+        int64_t pos;
+        if (c >= c0 && c < c1) {
+            pos = nlow + (c - c0);
+        } else {
+            int64_t a = 0, b = ng;  // lower_bound in the sorted ghost list
+            while (a < b) {
+                const int64_t m = (a + b) >> 1;
+                if (ghosts[m] < c) a = m + 1;
+                else b = m;
+            }
+            pos = a < nlow ? a : a + (c1 - c0);
+        }
+        lci[q - base] = (int32_t)pos;
+        lv[q - base] = v[q];
+    }
+}
+
+// level-local index maps: out[off_o + t] = map(in[g_lo + t]) for the owned entries
+__global__ void k_map_owned(int64_t n, const int64_t *in, int64_t g_lo, int64_t in_lo, int64_t in_off, int64_t *out,
+                            int64_t off_o, int keep_negative) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int64_t g = in[g_lo + t];
+    out[off_o + t] = (keep_negative && g < 0) ? -1 : in_off + (g - in_lo);
+}
+
+__global__ void k_count_sel(int64_t n, const int8_t *is_c, int want, int64_t *o) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) o[i] = (is_c[i] != 0) == (want != 0) ? 1 : 0;
+}
+
+}  // namespace
+
+struct Builder {
+    int rank, nranks;
+    Transport *tr;
+    cudaStream_t s;
+    std::vector<std::unique_ptr<Space>> spaces;
+    std::vector<std::vector<Reader>> readers;  // per space id
+
+    Builder(int r, int nr, Transport *t, cudaStream_t st) : rank(r), nranks(nr), tr(t), s(st) {}
+
+    Space *root(int64_t n, const int64_t *bounds) {
+        auto sp = std::make_unique<Space>();
+        sp->id = (int)spaces.size();
+        sp->n = n;
+        sp->start.assign(bounds, bounds + nranks + 1);
+        if (sp->start[0] != 0 || sp->start[nranks] != n)
+            fail(PMGR_ERR_INVALID, "rank bounds must cover [0, n)");
+        for (int r = 0; r < nranks; ++r)
+            if (sp->start[r + 1] < sp->start[r]) fail(PMGR_ERR_INVALID, "rank bounds must be non-decreasing");
+        spaces.push_back(std::move(sp));
+        readers.emplace_back();
+        return spaces.back().get();
+    }
+
+    // entries of `parent` with (is_c != 0) == want, in order
+    Space *derive(const Space *parent, const int8_t *is_c, bool want) {
+        const int64_t n = parent->n;
+        TBuf<int64_t> sel(n > 0 ? n : 1, s), sc(n + 1, s);
+        if (n > 0) {
+            k_count_sel<<<grid_for(n, 256), 256, 0, s>>>(n, is_c, want ? 1 : 0, sel.p);
+            PMGR_LAUNCHED();
+        }
+        const int64_t tot = exclusive_scan_total(sel.p, sc.p, n, s);
+        std::vector<int64_t> hsc(n + 1);
+        PMGR_CUDA(cudaMemcpyAsync(hsc.data(), sc.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        hsc[n] = tot;
+        auto sp = std::make_unique<Space>();
+        sp->id = (int)spaces.size();
+        sp->n = tot;
+        sp->start.resize(nranks + 1);
+        for (int r = 0; r <= nranks; ++r) sp->start[r] = hsc[parent->start[r]];
+        spaces.push_back(std::move(sp));
+        readers.emplace_back();
+        return spaces.back().get();
+    }
+
+    void read(Space *cols, const Csr *Y, Space *rows) { readers[cols->id].push_back({Y, rows}); }
+
+    // ghost sets of every rank, my halo plan
+    void finalize(Space *sp) {
+        sp->ghosts.assign(nranks, {});
+        for (int q = 0; q < nranks; ++q) {
+            std::vector<int64_t> all;
+            for (const Reader &rd : readers[sp->id]) {
+                const int64_t r0 = rd.rows->start[q], r1 = rd.rows->start[q + 1];
+                if (r1 <= r0) continue;
+                int64_t e0, e1;
+                PMGR_CUDA(cudaMemcpyAsync(&e0, rd.Y->ro.p + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                PMGR_CUDA(cudaMemcpyAsync(&e1, rd.Y->ro.p + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                PMGR_CUDA(cudaStreamSynchronize(s));
+                if (e1 <= e0) continue;
+                TBuf<int64_t> buf(e1 - e0, s), cnt(1, s);
+                PMGR_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t), s));
+                k_mark_outside<<<grid_for(r1 - r0, 128), 128, 0, s>>>(r1 - r0, rd.Y->ro.p, r0, rd.Y->ci.p,
+                                                                      sp->start[q], sp->start[q + 1], buf.p, cnt.p);
+                PMGR_LAUNCHED();
+                const int64_t c = read_scalar(cnt.p, s);
+                if (c == 0) continue;
+                thrust::device_ptr<int64_t> b(buf.p);
+                thrust::sort(thrust::cuda::par.on(s), b, b + c);
+                const int64_t u = thrust::unique(thrust::cuda::par.on(s), b, b + c) - b;
+                const size_t old = all.size();
+                all.resize(old + u);
+                PMGR_CUDA(cudaMemcpyAsync(all.data() + old, buf.p, sizeof(int64_t) * u, cudaMemcpyDeviceToHost, s));
+                PMGR_CUDA(cudaStreamSynchronize(s));
+            }
+            if (sp->triples) {
+                const size_t m = all.size();
+                for (size_t i = 0; i < m; ++i)
+                    for (int c = 0; c < 3; ++c) all.push_back(3 * (all[i] / 3) + c);
+            }
+            std::sort(all.begin(), all.end());
+            all.erase(std::unique(all.begin(), all.end()), all.end());
+            // closure may pull in owned entries: drop them
+            all.erase(std::remove_if(all.begin(), all.end(),
+                                     [&](int64_t g) { return g >= sp->start[q] && g < sp->start[q + 1]; }),
+                      all.end());
+            sp->ghosts[q] = std::move(all);
+        }
+        sp->lo = sp->start[rank];
+        sp->hi = sp->start[rank + 1];
+        sp->ghosts_me = &sp->ghosts[rank];
+        const auto &gm = sp->ghosts[rank];
+        sp->nlow = std::lower_bound(gm.begin(), gm.end(), sp->lo) - gm.begin();
+        sp->gdev.alloc((int64_t)gm.size());
+        if (!gm.empty())
+            PMGR_CUDA(cudaMemcpyAsync(sp->gdev.p, gm.data(), sizeof(int64_t) * gm.size(), cudaMemcpyHostToDevice, s));
+        // halo plan
+        auto h = std::make_shared<Halo>();
+        h->tr = tr;
+        h->id = sp->id;
+        h->n_own = sp->n_own();
+        h->off = sp->nlow;
+        h->n_ext = sp->n_ext();
+        for (int p = 0; p < nranks; ++p) {
+            if (p == rank) continue;
+            const int64_t a = std::lower_bound(gm.begin(), gm.end(), sp->start[p]) - gm.begin();
+            const int64_t b = std::lower_bound(gm.begin(), gm.end(), sp->start[p + 1]) - gm.begin();
+            if (b > a) {
+                h->rpeer.push_back(p);
+                h->roff.push_back(a < sp->nlow ? a : a + sp->n_own());
+                h->rcnt.push_back(b - a);
+            }
+        }
+        std::vector<int64_t> sidx;
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank) continue;
+            const auto &gq = sp->ghosts[q];
+            const int64_t a = std::lower_bound(gq.begin(), gq.end(), sp->lo) - gq.begin();
+            const int64_t b = std::lower_bound(gq.begin(), gq.end(), sp->hi) - gq.begin();
+            if (b > a) {
+                h->speer.push_back(q);
+                h->soff.push_back((int64_t)sidx.size());
+                h->scnt.push_back(b - a);
+                for (int64_t t = a; t < b; ++t) sidx.push_back(gq[t] - sp->lo);
+            }
+        }
+        h->send_idx.alloc((int64_t)sidx.size());
+        h->sbuf.alloc((int64_t)sidx.size());
+        if (!sidx.empty())
+            PMGR_CUDA(cudaMemcpyAsync(h->send_idx.p, sidx.data(), sizeof(int64_t) * sidx.size(),
+                                      cudaMemcpyHostToDevice, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        sp->halo = h;
+    }
+
+    // my rows of Y (rows space R) with columns at their ext positions in C
+    void localize(const Csr &Y, const Space *R, const Space *C, Csr &out) {
+        const int64_t r0 = R->lo, n = R->n_own();
+        int64_t e0 = 0, e1 = 0;
+        PMGR_CUDA(cudaMemcpyAsync(&e0, Y.ro.p + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaMemcpyAsync(&e1, Y.ro.p + r0 + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        out.nrows = n;
+        out.ncols = C->n_ext();
+        out.nnz = e1 - e0;
+        out.ro.alloc(n + 1);
+        out.ci.alloc(out.nnz);
+        out.v.alloc(out.nnz);
+        k_localize<<<grid_for(n + 1, 128), 128, 0, s>>>(n, Y.ro.p, r0, Y.ci.p, Y.v.p, C->lo, C->hi, C->nlow,
+                                                        C->gdev.p, (int64_t)C->ghosts_me->size(), out.ro.p,
+                                                        out.ci.p, out.v.p);
+        PMGR_LAUNCHED();
+        csr_finalize(out, s);
+        out.row_off = R->nlow;
+        out.lanes = spmv_lanes(Y.view());
+        // a pure block operator keeps its blocks (same blocks, same order as the
+        // global copy); a block-prefix operator (A0 on the original layout)
+        // is sliced as CSR
+        if (Y.nbrows > 0 && Y.nbrows * 3 == Y.nrows && !Y.rro.p) {
+            csr_make_bsr3(out, out.nrows, out.ncols, s, true);
+            if (out.nbrows * 3 != out.nrows) fail(PMGR_ERR_INVALID, "local block copy failed");
+        }
+    }
+
+    // owned values of a global per-entry array into an ext-length buffer
+    void own_values(const double *glob, const Space *sp, DBuf<double> &ext) {
+        ext.alloc(sp->n_ext());
+        PMGR_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(double) * (size_t)(ext.n > 0 ? ext.n : 1), s));
+        if (sp->n_own() > 0)
+            PMGR_CUDA(cudaMemcpyAsync(ext.p + sp->nlow, glob + sp->lo, sizeof(double) * sp->n_own(),
+                                      cudaMemcpyDeviceToDevice, s));
+    }
+    void ext_buffer(const Space *sp, DBuf<double> &ext) {
+        ext.alloc(sp->n_ext());
+        PMGR_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(double) * (size_t)(ext.n > 0 ? ext.n : 1), s));
+    }
+    // index map over the owned entries of `over`: global ids in space `to`
+    // (owned by this rank as well) -> ext positions of `to`
+    void own_map(const int64_t *glob, const Space *over, const Space *to, DBuf<int64_t> &ext, bool keep_negative) {
+        ext.alloc(over->n_ext());
+        PMGR_CUDA(cudaMemsetAsync(ext.p, 0xff, sizeof(int64_t) * (size_t)(ext.n > 0 ? ext.n : 1), s));
+        if (over->n_own() > 0) {
+            k_map_owned<<<grid_for(over->n_own(), 256), 256, 0, s>>>(over->n_own(), glob, over->lo, to->lo, to->nlow,
+                                                                      ext.p, over->nlow, keep_negative ? 1 : 0);
+            PMGR_LAUNCHED();
+        }
+    }
+};
+
+namespace {
+
+// AMG hierarchy over space S0: register spaces and readers (phase 1)
+struct AmgPlan {
+    const pmgr_amg *G;
+    std::vector<Space *> sp;  // per level (up to collapse_from inclusive)
+};
+
+void plan_amg(Builder &B, const pmgr_amg &G, Space *S0, AmgPlan &P) {
+    P.G = &G;
+    if (G.levels.empty() || G.collapse_from < 0)
+        fail(PMGR_ERR_NOT_SUPPORTED,
+             "row distribution needs the collapsed coarse cycle (PMGR_COLLAPSE_ROWS > 0, at least one AMG level)");
+    for (const AmgLevel &L : G.levels)
+        if (!L.jacobi) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution needs l1-Jacobi AMG levels (npartitions >= n)");
+    P.sp.push_back(S0);
+    for (int l = 0; l < G.collapse_from; ++l) P.sp.push_back(B.derive(P.sp[l], G.levels[l].is_c.p, true));
+    for (int l = 0; l < G.collapse_from; ++l) {
+        const AmgLevel &L = G.levels[l];
+        B.read(P.sp[l], L.A.get(), P.sp[l]);
+        B.read(P.sp[l], &L.R, P.sp[l + 1]);
+        B.read(P.sp[l + 1], &L.P, P.sp[l]);
+    }
+    if (G.levels[0].A->nbrows > 0) S0->triples = true;
+}
+
+std::unique_ptr<pmgr_amg> build_amg(Builder &B, const AmgPlan &P) {
+    const pmgr_amg &G = *P.G;
+    auto h = std::make_unique<pmgr_amg>();
+    h->cfg = G.cfg;
+    h->collapse_from = G.collapse_from;
+    h->levels.resize(G.collapse_from + 1);
+    for (int l = 0; l <= G.collapse_from; ++l) {
+        const AmgLevel &GL = G.levels[l];
+        AmgLevel &L = h->levels[l];
+        Space *S = P.sp[l];
+        L.jacobi = true;
+        L.off = S->nlow;
+        L.halo = S->halo;
+        auto A = std::make_shared<Csr>();
+        if (l < G.collapse_from) {
+            B.localize(*GL.A, S, S, *A);
+            B.localize(GL.P, S, P.sp[l + 1], L.P);
+            B.localize(GL.R, P.sp[l + 1], S, L.R);
+        } else {
+            A->nrows = S->n_own();  // the collapsed level only needs its row count
+            A->ncols = S->n_ext();
+        }
+        L.A = A;
+        B.own_values(GL.dtilde.p, S, L.dtilde);
+        B.ext_buffer(S, L.b);
+        B.ext_buffer(S, L.x);
+        B.ext_buffer(S, L.r);
+        B.ext_buffer(S, L.xo);
+    }
+    // collapsed operator: my rows, full width
+    Space *Sc = P.sp[G.collapse_from];
+    h->collapsed_ld = G.collapsed_ld;
+    h->collapsed.alloc(Sc->n_own() * G.collapsed_ld);
+    if (Sc->n_own() > 0)
+        PMGR_CUDA(cudaMemcpyAsync(h->collapsed.p, G.collapsed.p + Sc->lo * G.collapsed_ld,
+                                  sizeof(double) * Sc->n_own() * G.collapsed_ld, cudaMemcpyDeviceToDevice, B.s));
+    h->gather = std::make_shared<Gather>();
+    h->gather->tr = B.tr;
+    h->gather->n_full = Sc->n;
+    h->gather->start = Sc->start;
+    h->gather->id = Sc->id;
+    h->full.alloc(Sc->n > 0 ? Sc->n : 1);
+    return h;
+}
+
+}  // namespace
+
+std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int rank, int nranks,
+                                       Transport *tr, cudaStream_t s) {
+    if (!M || M->dist) fail(PMGR_ERR_INVALID, "row distribution needs a global hierarchy");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(PMGR_ERR_INVALID, "bad rank / nranks");
+    if (tr && (tr->rank != rank || tr->nranks != nranks)) fail(PMGR_ERR_INVALID, "transport rank mismatch");
+    const Csr &A0 = *A->m;
+    if (A0.nrows != M->n) fail(PMGR_ERR_INVALID, "matrix and hierarchy sizes differ");
+    if (M->f_relax_post || M->terminal_cycles != 1)
+        fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports pre F-relaxation and one terminal cycle");
+    for (const MgrLevel &L : M->levels) {
+        if (L.f_relax == PMGR_FRELAX_NONE || L.f_relax_sweeps != 1)
+            fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports single-sweep AMG / Jacobi F-relaxation");
+    }
+    if (!M->terminal) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution needs a terminal AMG");
+    Builder B(rank, nranks, tr, s);
+    // ---- phase 1: spaces and who reads them
+    Space *M0 = B.root(A0.nrows, bounds);
+    B.read(M0, &A0, M0);
+    const size_t nl = M->levels.size();
+    std::vector<Space *> Ms{M0}, Fs;
+    std::vector<AmgPlan> fplans(nl);
+    for (size_t l = 0; l < nl; ++l) {
+        const MgrLevel &L = M->levels[l];
+        Space *F = B.derive(Ms[l], L.is_c.p, false);
+        Space *C = B.derive(Ms[l], L.is_c.p, true);
+        Fs.push_back(F);
+        Ms.push_back(C);
+        B.read(F, &L.A_cf, C);
+        B.read(C, &L.P, Ms[l]);
+        if (L.f_relax == PMGR_FRELAX_AMG) plan_amg(B, *L.amg, F, fplans[l]);
+    }
+    AmgPlan tplan;
+    plan_amg(B, *M->terminal, Ms[nl], tplan);
+    for (auto &sp : B.spaces) B.finalize(sp.get());
+    // ---- phase 2: local operators and workspaces
+    auto D = std::make_unique<DistSolver>();
+    D->rank = rank;
+    D->nranks = nranks;
+    D->tr = tr;
+    D->n_global = A0.nrows;
+    D->lo = M0->lo;
+    D->n_own = M0->n_own();
+    D->off = M0->nlow;
+    D->n_ext = M0->n_ext();
+    D->halo0 = M0->halo;
+    B.localize(A0, M0, M0, D->A);
+    auto h = std::make_unique<pmgr_mgr>();
+    h->dist = true;
+    h->use_graphs = false;
+    h->terminal_cycles = 1;
+    h->f_relax_post = 0;
+    h->n = M0->n_own();
+    h->levels.resize(nl);
+    for (size_t l = 0; l < nl; ++l) {
+        const MgrLevel &G = M->levels[l];
+        MgrLevel &L = h->levels[l];
+        Space *Mi = Ms[l], *F = Fs[l], *C = Ms[l + 1];
+        L.n = Mi->n_own();
+        L.nf = F->n_own();
+        L.nc = C->n_own();
+        L.off = Mi->nlow;
+        L.off_f = F->nlow;
+        L.off_c = C->nlow;
+        L.halo_f = F->halo;
+        L.halo_c = C->halo;
+        L.f_relax = G.f_relax;
+        L.f_relax_sweeps = 1;
+        B.localize(G.A_cf, C, F, L.A_cf);
+        B.localize(G.P, Mi, C, L.P);
+        B.own_map(G.f_rows.p, F, Mi, L.f_rows, false);
+        B.own_map(G.c_rows.p, C, Mi, L.c_rows, false);
+        B.own_map(G.f_index.p, Mi, F, L.f_index, true);
+        if (G.dinv_ff.p) B.own_values(G.dinv_ff.p, F, L.dinv_ff);
+        B.ext_buffer(F, L.zf);
+        B.ext_buffer(C, L.rc);
+        B.ext_buffer(C, L.zc);
+        if (G.f_relax == PMGR_FRELAX_AMG) L.amg = build_amg(B, fplans[l]);
+    }
+    h->terminal = build_amg(B, tplan);
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    D->M = std::move(h);
+    D->spaces.reserve(B.spaces.size());
+    for (auto &sp : B.spaces) D->halos.push_back(sp->halo);
+    return D;
+}
+
+// ========================================================= apply, GMRES
+
+void dist_apply(DistSolver &D, const double *v_own, double *z_own, cudaStream_t s) {
+    D.ensure_work();
+    if (D.n_own > 0)
+        PMGR_CUDA(cudaMemcpyAsync(D.ve.p + D.off, v_own, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice, s));
+    mgr_apply_direct(*D.M, D.ve.p, D.ze.p, s);
+    if (D.n_own > 0)
+        PMGR_CUDA(cudaMemcpyAsync(z_own, D.ze.p + D.off, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice, s));
+}
+
+void DistSolver::ensure_work() {
+    if (ve.p) return;
+    ve.alloc(n_ext > 0 ? n_ext : 1);
+    ze.alloc(n_ext > 0 ? n_ext : 1);
+    we.alloc(n_ext > 0 ? n_ext : 1);
+    PMGR_CUDA(cudaMemset(ve.p, 0, sizeof(double) * ve.n));
+    PMGR_CUDA(cudaMemset(ze.p, 0, sizeof(double) * ze.n));
+    PMGR_CUDA(cudaMemset(we.p, 0, sizeof(double) * we.n));
+}
+
+namespace {
+__global__ void k_dot_partial(const double *a, const double *b, int64_t n, double *part) {
+    __shared__ double sh[8];
+    double t = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        t = fma(a[i], b[i], t);
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) u += sh[w];
+        part[blockIdx.x] = u;
+    }
+}
+__global__ void k_sum_part(const double *part, int n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += part[i];
+        *out = s;
+    }
+}
+__global__ void k_scale_to(const double *x, double a, int64_t n, double *y) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i] = x[i] * a;
+}
+__global__ void k_resid_own(const double *b, const double *ax, int64_t n, double *r) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) r[i] = b[i] - ax[i];
+}
+}  // namespace
+
+// global dot of two owned vectors into *out (device), all ranks equal
+static void gdot(DistSolver &D, const double *a, const double *b, double *out, cudaStream_t s) {
+    const int nb = 148;
+    TBuf<double> part(nb, s);
+    k_dot_partial<<<nb, 256, 0, s>>>(a, b, D.n_own, part.p);
+    PMGR_LAUNCHED();
+    k_sum_part<<<1, 32, 0, s>>>(part.p, nb, out);
+    PMGR_LAUNCHED();
+    if (D.tr && D.nranks > 1) D.tr->allreduce(out, 1, s);
+}
+
+// y = A x for an owned x (halo exchange into the ext buffer first)
+static void dist_spmv(DistSolver &D, const double *x_own, double *y_own, cudaStream_t s) {
+    D.ensure_work();
+    if (D.n_own > 0)
+        PMGR_CUDA(cudaMemcpyAsync(D.ze.p + D.off, x_own, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice, s));
+    halo_exchange(D.halo0.get(), D.ze.p, s);
+    spmv(D.A.view(), D.ze.p, D.we.p, s);
+    if (D.n_own > 0)
+        PMGR_CUDA(cudaMemcpyAsync(y_own, D.we.p + D.off, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice, s));
+}
+
+// Right-preconditioned restarted GMRES (krylov.py:39-117) on row-distributed
+// vectors: CGS with one re-orthogonalisation (one all-reduce per pass), the
+// small Hessenberg / Givens algebra replicated on every rank (identical
+// all-reduced inputs => identical control flow everywhere).
+void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const pmgr_gmres_cfg &cfg,
+                pmgr_gmres_stats &st, double *history, int32_t history_cap, cudaStream_t s) {
+    const int64_t n = D.n_own;
+    const int m = cfg.restart > 0 ? cfg.restart : 50;
+    if (m > 1000) fail(PMGR_ERR_INVALID, "restart too large for the distributed solver");
+    const int maxit = cfg.max_iters;
+    DBuf<double> V((int64_t)(m + 1) * (n > 0 ? n : 1)), w(n > 0 ? n : 1), z(n > 0 ? n : 1), r(n > 0 ? n : 1),
+        u(n > 0 ? n : 1), h((int64_t)m + 2), sc(2);
+    if (!nonzero_x0 && n > 0) PMGR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    auto to_host = [&](const double *dv, double *hv, int cnt) {
+        PMGR_CUDA(cudaMemcpyAsync(hv, dv, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    };
+    auto norm = [&](const double *a) {
+        gdot(D, a, a, sc.p, s);
+        double v;
+        to_host(sc.p, &v, 1);
+        return std::sqrt(v);
+    };
+    // r = b - A x
+    auto residual = [&]() {
+        dist_spmv(D, x, w.p, s);
+        if (n > 0) {
+            k_resid_own<<<grid_for(n, 256), 256, 0, s>>>(b, w.p, n, r.p);
+            PMGR_LAUNCHED();
+        }
+    };
+    residual();
+    double beta = norm(r.p);
+    const double bnorm = nonzero_x0 ? norm(b) : beta;
+    const double tol = std::max(cfg.rtol * bnorm, cfg.atol);
+    std::vector<double> hist{beta};
+    int total = 0, restarts = 0;
+    bool brk = false;
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hc(m + 2);
+    while (beta > tol && total < maxit) {
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        if (n > 0) {
+            k_scale_to<<<grid_for(n, 256), 256, 0, s>>>(r.p, 1.0 / beta, n, V.p);
+            PMGR_LAUNCHED();
+        }
+        int j = 0;
+        while (j < m && total < maxit) {
+            double *vj = V.p + (int64_t)j * n;
+            dist_apply(D, vj, z.p, s);
+            dist_spmv(D, z.p, w.p, s);
+            std::fill(hc.begin(), hc.end(), 0.0);
+            for (int pass = 0; pass < 2; ++pass) {
+                if (n > 0) multidot(V.p, n, j + 1, w.p, h.p, s);
+                else PMGR_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * (j + 1), s));
+                if (D.tr && D.nranks > 1) D.tr->allreduce(h.p, j + 1, s);
+                if (n > 0) multiaxpy(V.p, n, j + 1, h.p, w.p, s);
+                std::vector<double> hp(j + 1);
+                to_host(h.p, hp.data(), j + 1);
+                for (int i = 0; i <= j; ++i) hc[i] += hp[i];
+            }
+            const double hn = norm(w.p);
+            double cn = 0.0;
+            for (int i = 0; i <= j; ++i) cn += hc[i] * hc[i];
+            cn = std::sqrt(cn + hn * hn);
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hc[i];
+            H[(size_t)(j + 1) * m + j] = hn;
+            if (hn > 1e-12 * std::max(cn, 1e-300)) {
+                if (n > 0) {
+                    k_scale_to<<<grid_for(n, 256), 256, 0, s>>>(w.p, 1.0 / hn, n, V.p + (int64_t)(j + 1) * n);
+                    PMGR_LAUNCHED();
+                }
+            } else {
+                brk = true;
+            }
+            for (int i = 0; i < j; ++i) {
+                const double t = H[(size_t)i * m + j];
+                H[(size_t)i * m + j] = cs[i] * t + sn[i] * H[(size_t)(i + 1) * m + j];
+                H[(size_t)(i + 1) * m + j] = -sn[i] * t + cs[i] * H[(size_t)(i + 1) * m + j];
+            }
+            const double rho = std::hypot(H[(size_t)j * m + j], H[(size_t)(j + 1) * m + j]);
+            if (rho == 0.0) {
+                brk = true;
+                break;
+            }
+            cs[j] = H[(size_t)j * m + j] / rho;
+            sn[j] = H[(size_t)(j + 1) * m + j] / rho;
+            H[(size_t)j * m + j] = rho;
+            H[(size_t)(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++total;
+            ++j;
+            hist.push_back(std::fabs(g[j]));
+            if (std::fabs(g[j]) <= tol || brk) break;
+        }
+        if (j > 0) {
+            std::vector<double> y(j);
+            for (int i = j - 1; i >= 0; --i) {
+                double t = g[i];
+                for (int k = i + 1; k < j; ++k) t -= H[(size_t)i * m + k] * y[k];
+                y[i] = t / H[(size_t)i * m + i];
+            }
+            // u = V y ; x += M u
+            if (n > 0) {
+                PMGR_CUDA(cudaMemsetAsync(u.p, 0, sizeof(double) * n, s));
+                std::vector<double> ny(j);
+                for (int i = 0; i < j; ++i) ny[i] = -y[i];
+                PMGR_CUDA(cudaMemcpyAsync(h.p, ny.data(), sizeof(double) * j, cudaMemcpyHostToDevice, s));
+                multiaxpy(V.p, n, j, h.p, u.p, s);  // u -= V (-y)
+                PMGR_CUDA(cudaStreamSynchronize(s));  // ny is a host temporary
+            }
+            dist_apply(D, u.p, z.p, s);
+            if (n > 0) vec_axpy(1.0, z.p, x, n, s);
+            residual();
+            beta = norm(r.p);
+            hist.back() = beta;
+        }
+        if (brk) break;
+        if (beta > tol && total < maxit) ++restarts;
+    }
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    st.iterations = total;
+    st.converged = beta <= tol ? 1 : 0;
+    st.restarts = restarts;
+    st.history_len = (int32_t)std::min<size_t>(hist.size(), history ? (size_t)history_cap : 0);
+    if (history)
+        for (int i = 0; i < (int)hist.size() && i < history_cap; ++i) history[i] = hist[i];
+}
+
+// ====================================================== one-GPU emulation
+
+void dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int nranks, int what, const double *in,
+                  double *out, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, cudaStream_t s) {
+    LoopbackHub hub(nranks);
+    std::vector<std::unique_ptr<LoopbackTransport>> trs;
+    std::vector<std::unique_ptr<DistSolver>> ds;
+    for (int r = 0; r < nranks; ++r) {
+        trs.emplace_back(new LoopbackTransport(&hub, r));
+        ds.push_back(dist_build(A, M, bounds, r, nranks, trs.back().get(), s));
+    }
+    int dev = 0;
+    PMGR_CUDA(cudaGetDevice(&dev));
+    std::vector<std::string> errs(nranks);
+    std::vector<pmgr_gmres_stats> st(nranks);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r) {
+        th.emplace_back([&, r] {
+            try {
+                PMGR_CUDA(cudaSetDevice(dev));
+                DistSolver &D = *ds[r];
+                if (what == 0) {
+                    dist_apply(D, in + D.lo, out + D.lo, s);
+                } else {
+                    pmgr_gmres_stats z = {};
+                    dist_gmres(D, in + D.lo, out + D.lo, 0, *cfg, z, nullptr, 0, s);
+                    st[r] = z;
+                }
+            } catch (const Error &e) {
+                errs[r] = e.msg.empty() ? "error" : e.msg;
+                hub.abort(errs[r]);
+            } catch (const std::exception &e) {
+                errs[r] = e.what();
+                hub.abort(e.what());
+            }
+        });
+    }
+    for (auto &t : th) t.join();
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < nranks; ++r)
+        if (!errs[r].empty()) fail(PMGR_ERR_CUDA, "rank " + std::to_string(r) + ": " + errs[r]);
+    if (stats && what == 1) {
+        *stats = st[0];
+        for (int r = 1; r < nranks; ++r)
+            if (st[r].iterations != st[0].iterations)
+                fail(PMGR_ERR_INVALID, "emulated ranks disagree on the iteration count");
+    }
+}
+
+}  // namespace pmgr

@@ -12,6 +12,32 @@ struct pmgr_csr {
 
 namespace pmgr {
 
+// ---- row distribution (dist.cu) --------------------------------
+// Every vector space of a row-distributed hierarchy is owned in contiguous
+// global ranges, rank after rank (the level-0 numbering is rank-major and C
+// points keep their order).  A rank stores a space as an "ext" vector: its
+// owned range plus the ghost entries its operators read, in global order, so
+// local rows sum their columns in the global stored order.
+struct Transport;
+struct Halo {  // ghost exchange of one space on one rank
+    Transport *tr = nullptr;
+    int64_t n_ext = 0, off = 0, n_own = 0;  // owned entries sit at [off, off + n_own)
+    std::vector<int> rpeer, speer;          // peers I receive from / send to
+    std::vector<int64_t> roff, rcnt;        // per receive peer: its contiguous ghost segment
+    std::vector<int64_t> soff, scnt;        // per send peer: its segment of send_idx
+    DBuf<int64_t> send_idx;                 // owned-local indices, peer after peer
+    DBuf<double> sbuf;                      // packed send values
+    int id = -1;                            // space id (matches across ranks)
+};
+struct Gather {  // all-gather of one space into its full global-order vector
+    Transport *tr = nullptr;
+    int64_t n_full = 0;
+    std::vector<int64_t> start;  // per rank global range start (nranks + 1)
+    int id = -1;
+};
+void halo_exchange(Halo *h, double *ext, cudaStream_t s);
+void gather_full(Gather *g, const double *own, double *full, cudaStream_t s);
+
 // One classical-AMG level (reference amg.py:51-57).
 struct AmgLevel {
     std::shared_ptr<const Csr> A;  // level operator (level 0 may be shared with MGR)
@@ -24,6 +50,9 @@ struct AmgLevel {
     bool jacobi = true;            // one row per partition
     // solve workspace
     DBuf<double> b, x, r, xo, xpre;
+    // row distribution: owned rows start at ext position off; halo of this space
+    int64_t off = 0;
+    std::shared_ptr<Halo> halo;
 };
 
 // coarse end of the V-cycle as one dense operator (collapse.cu)
@@ -42,6 +71,10 @@ struct pmgr_amg {
     int collapse_from = -1;          // levels >= this run as one dense operator (-1: none)
     pmgr::DBuf<double> collapsed;    // that operator, row-major n x collapsed_ld
     int64_t collapsed_ld = 0;
+    // row distribution: the collapsed operator holds the owned rows only and
+    // reads the full right-hand side gathered from every rank
+    std::shared_ptr<pmgr::Gather> gather;
+    pmgr::DBuf<double> full;
 };
 
 namespace pmgr {
@@ -76,6 +109,10 @@ struct MgrLevel {
     std::unique_ptr<pmgr_amg> amg;    // F-relaxation AMG
     // workspace
     DBuf<double> vf, zf, rc, zc, tmpf;
+    // row distribution: owned offsets of the level (M), F and C spaces; halos
+    // of the F space (read by A_CF) and of the C space (read by P)
+    int64_t off = 0, off_f = 0, off_c = 0;
+    std::shared_ptr<Halo> halo_f, halo_c;
 };
 
 }  // namespace pmgr
@@ -108,6 +145,7 @@ struct pmgr_mgr {
     int32_t f_relax_post = 0;
     int64_t n = 0;
     int64_t block_prefix = 0;  // level-0 F rows: a node-blocked prefix of A0 (0: none)
+    bool dist = false;         // a rank's row slice of a hierarchy (dist.cu)
     pmgr::DBuf<double> tz;  // terminal scratch
 };
 

@@ -253,7 +253,8 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
             if (L.f_relax == PMGR_FRELAX_AMG) {
                 done = amg_cycle_rows(*L.amg, v, L.f_rows.p, L.zf.p, s);
             } else {
-                vec_scale_gather(v, L.f_rows.p, L.dinv_ff.p, L.nf, L.zf.p, s);
+                const int64_t o = L.off_f;
+                vec_scale_gather(v, L.f_rows.p + o, L.dinv_ff.p + o, L.nf, L.zf.p + o, s);
                 done = true;
             }
         }
@@ -281,11 +282,13 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
                 next_prefilled = true;
             }
         }
+        halo_exchange(L.halo_f.get(), L.zf.p, s);
         spmv_resid_rows(L.A_cf.view(), L.zf.p, v, L.c_rows.p, rc, nx, s);
     } else {
-        vec_gather(v, L.c_rows.p, L.nc, L.rc.p, s);
+        vec_gather(v, L.c_rows.p + L.off_c, L.nc, L.rc.p + L.off_c, s);
     }
     apply_level(h, l + 1, rc, L.zc.p, s, next_prefilled);
+    halo_exchange(L.halo_c.get(), L.zc.p, s);
     spmv_prolong_combine(L.P.view(), L.zc.p, pre ? L.zf.p : nullptr, pre ? L.f_index.p : nullptr, z, s);
     if (h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
         // r = v - A z ; z[F] += M_FF^{-1} r[F]
@@ -376,7 +379,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
         csr_finalize(*A_ff, s);
-        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3) csr_make_bsr3(*A_ff, A_ff->nrows, s);
+        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3) csr_make_bsr3(*A_ff, A_ff->nrows, A_ff->ncols, s);
         if (li == 0 && A_ff->nbrows > 0) {
             // F rows first, then C rows: the same blocks lead A0 itself
             bool prefix = true;

@@ -39,7 +39,7 @@ __device__ __forceinline__ int ldc(const uint16_t *p) {
 template <int G, bool STREAM, class Op, class IT>
 __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
                                               const IT *__restrict__ ci,
-                                              const double *__restrict__ v, Op op, int trigger) {
+                                              const double *__restrict__ v, Op op, int64_t row_off, int trigger) {
     pdl_wait();
     if (trigger) pdl_trigger();
     const int lane = threadIdx.x & (G - 1);
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
     double s = s0 + s1;
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
-    if (active && lane == 0) op.out(row, s);
+    if (active && lane == 0) op.out(row + row_off, s);
 }
 
 // Block-prefix SpMV: a warp per row triple.  Triples inside the node-blocked
@@ -78,7 +78,7 @@ template <class Op>
 __global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
                                               const int32_t *__restrict__ bci, const double *__restrict__ bval,
                                               const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
-                                              const double *__restrict__ rv, Op op, int trigger) {
+                                              const double *__restrict__ rv, Op op, int64_t row_off, int trigger) {
     pdl_wait();
     if (trigger) pdl_trigger();
     const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t
         a1 += __shfl_xor_sync(FULL, a1, o);
         a2 += __shfl_xor_sync(FULL, a2, o);
     }
-    if (I < ntrip && lane < 3 && 3 * I + lane < n) op.out(3 * I + lane, lane == 0 ? a0 : lane == 1 ? a1 : a2);
+    if (I < ntrip && lane < 3 && 3 * I + lane < n)
+        op.out(3 * I + lane + row_off, lane == 0 ? a0 : lane == 1 ? a1 : a2);
 }
 
 struct OpY {
@@ -224,9 +225,11 @@ void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
     if (stream)
-        launch_pdl(k_spmv<G, true, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, trigger);
+        launch_pdl(k_spmv<G, true, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
+                   trigger);
     else
-        launch_pdl(k_spmv<G, false, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, trigger);
+        launch_pdl(k_spmv<G, false, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
+                   trigger);
 }
 
 template <int G, class Op>
@@ -234,6 +237,27 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
     if (A.ci16) go_t<G>(A, A.ci16, op, stream, s);
     else go_t<G>(A, A.ci, op, stream, s);
 }
+
+}  // namespace
+
+// lane group per row the CSR kernel picks for A (row-distributed copies of an
+// operator reuse the global choice so their per-row sums are bitwise equal)
+int spmv_lanes(const CsrView &A) {
+    double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
+    // skewed rows (a few dense coarse-grid rows next to short ones) get a
+    // whole warp, otherwise the longest row serialises its lane group
+    if (A.maxrow >= 0) {
+        int g = mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= 160.0 ? 16 : 32;
+        if (A.maxrow > 16 * g) mean = 1e9;
+    }
+    static const double g32_mean = [] {
+        const char *e = getenv("PMGR_SPMV_G32_MEAN");
+        return e ? atof(e) : 100.0;
+    }();
+    return mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= g32_mean ? 16 : 32;
+}
+
+namespace {
 
 template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
@@ -243,16 +267,9 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
         const unsigned grid = grid_for(ntrip * 32, 256);
         const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
         launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval, A.rro,
-                   A.rci, A.rv, op, trigger);
+                   A.rci, A.rv, op, A.row_off, trigger);
         PMGR_LAUNCHED();
         return;
-    }
-    double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
-    // skewed rows (a few dense coarse-grid rows next to short ones) get a
-    // whole warp, otherwise the longest row serialises its lane group
-    if (A.maxrow >= 0) {
-        int g = mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= 160.0 ? 16 : 32;
-        if (A.maxrow > 16 * g) mean = 1e9;
     }
     // matrices far larger than L2 are streamed with evict-first loads so the
     // gathered vectors stay cached; small operators stay L2-resident
@@ -261,20 +278,12 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
         return e ? atof(e) : 1e30;
     }();
     const bool stream = 12.0 * (double)A.nnz > stream_mb * 1024 * 1024;
-    static const double g32_mean = [] {
-        const char *e = getenv("PMGR_SPMV_G32_MEAN");
-        return e ? atof(e) : 100.0;
-    }();
-    if (mean <= 3.0) {
-        go<2>(A, op, stream, s);
-    } else if (mean <= 12.0) {
-        go<4>(A, op, stream, s);
-    } else if (mean <= 48.0) {
-        go<8>(A, op, stream, s);
-    } else if (mean <= g32_mean) {
-        go<16>(A, op, stream, s);
-    } else {
-        go<32>(A, op, stream, s);
+    switch (A.lanes > 0 ? A.lanes : spmv_lanes(A)) {
+        case 2: go<2>(A, op, stream, s); break;
+        case 4: go<4>(A, op, stream, s); break;
+        case 8: go<8>(A, op, stream, s); break;
+        case 16: go<16>(A, op, stream, s); break;
+        default: go<32>(A, op, stream, s); break;
     }
     PMGR_LAUNCHED();
 }
@@ -307,14 +316,14 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
 // whose 8 independent matrix loads are in flight together.  PAIR: ld even,
 // 16-byte loads of column pairs.
 template <bool PAIR>
-__global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t n, int64_t ld,
+__global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t nrows, int64_t n, int64_t ld,
                                                       const double *__restrict__ x, double *__restrict__ y) {
     pdl_wait();
     constexpr int RB = 8, W = 8;
     __shared__ double red[W][RB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = (int64_t)blockIdx.x * RB;
-    const int nr = (int)(n - r0 < RB ? n - r0 : RB);
+    const int nr = (int)(nrows - r0 < RB ? nrows - r0 : RB);
     double acc[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) acc[r] = 0.0;
@@ -477,12 +486,17 @@ void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const do
 }
 
 void dense_matvec(const double *M, int64_t n, int64_t ld, const double *x, double *y, cudaStream_t s) {
-    if (n == 0) return;
-    const unsigned blocks = (unsigned)((n + 7) / 8);
+    dense_matvec_rows(M, n, n, ld, x, y, s);
+}
+
+void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld, const double *x, double *y,
+                       cudaStream_t s) {
+    if (nrows == 0) return;
+    const unsigned blocks = (unsigned)((nrows + 7) / 8);
     if (ld % 2 == 0)
-        launch_pdl(k_dense_matvec<true>, dim3(blocks), dim3(256), 0, s, M, n, ld, x, y);
+        launch_pdl(k_dense_matvec<true>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
     else
-        launch_pdl(k_dense_matvec<false>, dim3(blocks), dim3(256), 0, s, M, n, ld, x, y);
+        launch_pdl(k_dense_matvec<false>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
     PMGR_LAUNCHED();
 }
 

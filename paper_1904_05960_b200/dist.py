@@ -13,15 +13,17 @@ exchange step:
   with the z-neighbours; NCCL over NVLink on the GPU, gloo in CPU tests);
 * all-reduce of the Arnoldi projections and norms.
 
-The local compute is pluggable (`local_matvec`): libpmgr's SpMV on the GPU,
-the oracle in the CPU tests.  Round 1 ships this layer with its tests; the
-distributed MGR hierarchy (ghost rows for strength/interpolation, a status
-halo per MIS round, P_ext for the RAP products) is the next step, so
-`bench.py --gpus N` still runs replicas.
+The local compute is pluggable (`local_matvec`): the oracle in the CPU
+tests (gloo, world_size 2).  The device path (`DeviceDistSolver`, bottom of
+this file) is libpmgr's row distribution: replicated setup of a rank-major
+problem, every operator sliced to the rank's rows, halo exchanges over NCCL
+inside libpmgr; `emulate_apply` / `emulate_gmres` run N ranks on one GPU
+(loopback transport) for the parity tests.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -235,3 +237,136 @@ def dist_gmres(apply_A, apply_M_inv, b, dist, group=None, restart=50, max_iters=
         if brk:
             break
     return x, total, np.array(hist), bool(beta <= tol)
+
+
+# ---------------------------------------------------------------------------
+# device path: libpmgr's row distribution (include/pmgr.h, csrc/dist.cu)
+# ---------------------------------------------------------------------------
+#
+# Every rank builds the global hierarchy of a rank-major numbered problem
+# (problems.rank_major) on its own GPU, then keeps its rows of every
+# operator.  Vectors are the rank's owned slices (float64 CUDA tensors).
+
+
+def nccl_transport(rank: int, nranks: int, dist):
+    """NCCL communicator inside libpmgr; the unique id travels through the
+    caller's torch.distributed process group (any backend)."""
+    from . import _lib
+
+    L = _lib.lib()
+    nid = _lib.NcclId()
+    if rank == 0:
+        _lib.check(L.pmgr_nccl_get_id(ctypes.byref(nid)))
+    box = [bytes(nid.internal) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    raw = box[0].ljust(128, b"\0")
+    ctypes.memmove(ctypes.addressof(nid), raw, 128)
+    out = ctypes.c_void_p()
+    _lib.check(L.pmgr_transport_nccl_create(ctypes.byref(nid), rank, nranks, ctypes.byref(out)))
+    return _Handle(out, "pmgr_transport_destroy")
+
+
+class _Handle:
+    def __init__(self, h, destroy):
+        self.h, self._destroy = h, destroy
+
+    def __del__(self):
+        from . import _lib
+
+        if getattr(self, "h", None) and _lib._lib is not None:
+            getattr(_lib._lib, self._destroy)(self.h)
+            self.h = None
+
+
+class DeviceDistSolver:
+    """Rank `rank`'s slice of an MgrHierarchy (and its matrix) for the
+    distributed solve: `apply` / `spmv` / `gmres` on owned slices."""
+
+    def __init__(self, h, bounds, rank: int, nranks: int, transport=None):
+        from . import _lib
+        from .sparse import current_stream
+
+        self.h, self.rank, self.nranks = h, rank, nranks
+        self.transport = transport
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        if len(self.bounds) != nranks + 1:
+            raise ValueError("bounds must have nranks + 1 entries")
+        out = ctypes.c_void_p()
+        th = transport.h if transport is not None else None
+        _lib.check(_lib.lib().pmgr_dist_create(h._A.handle, h.handle, self.bounds.ctypes.data, rank, nranks, th,
+                                               current_stream(), ctypes.byref(out)))
+        self._d = _Handle(out, "pmgr_dist_destroy")
+        lo, no = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().pmgr_dist_info(self._d.h, ctypes.byref(lo), ctypes.byref(no)))
+        self.lo, self.n_own = lo.value, no.value
+
+    def _vec(self, v):
+        from .sparse import to_device
+
+        return to_device(v, self.n_own).contiguous()
+
+    def apply(self, v_own):
+        from . import _lib
+        from .sparse import current_stream, empty_device, ptr
+
+        v = self._vec(v_own)
+        z = empty_device(self.n_own)
+        _lib.check(_lib.lib().pmgr_dist_apply(self._d.h, ptr(v), ptr(z), current_stream()))
+        return z
+
+    def spmv(self, x_own):
+        from . import _lib
+        from .sparse import current_stream, empty_device, ptr
+
+        x = self._vec(x_own)
+        y = empty_device(self.n_own)
+        _lib.check(_lib.lib().pmgr_dist_spmv(self._d.h, ptr(x), ptr(y), current_stream()))
+        return y
+
+    def gmres(self, b_own, cfg=None):
+        from . import _lib
+        from .krylov import GmresConfig, SolveStats
+        from .sparse import current_stream, empty_device, ptr
+
+        cfg = cfg or GmresConfig()
+        b = self._vec(b_own)
+        x = empty_device(self.n_own).zero_()
+        c = _lib.GmresCfg(int(cfg.restart), int(cfg.max_iters), float(cfg.rtol), float(cfg.atol))
+        st = _lib.GmresStats()
+        cap = int(cfg.max_iters) + 2
+        hist = np.zeros(cap)
+        _lib.check(_lib.lib().pmgr_dist_gmres(self._d.h, ptr(b), ptr(x), 0, ctypes.byref(c), ctypes.byref(st),
+                                              hist.ctypes.data, cap, current_stream()))
+        return x, SolveStats(int(st.iterations), hist[:st.history_len].copy(), bool(st.converged))
+
+
+def emulate_apply(h, bounds, v):
+    """z = M v with the hierarchy row-distributed over len(bounds)-1 ranks
+    emulated on this GPU (loopback transport): the parity harness of §8e."""
+    from . import _lib
+    from .sparse import current_stream, empty_device, ptr, to_device
+
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    vd = to_device(v, h.n).contiguous()
+    z = empty_device(h.n)
+    _lib.check(_lib.lib().pmgr_dist_emulate(h._A.handle, h.handle, b.ctypes.data, len(b) - 1, 0, ptr(vd), ptr(z),
+                                            None, None, current_stream()))
+    return z
+
+
+def emulate_gmres(h, bounds, rhs, cfg=None):
+    """Distributed GMRES(MGR) from x0 = 0 over emulated ranks; returns the
+    gathered solution and the iteration count / convergence flag."""
+    from . import _lib
+    from .krylov import GmresConfig
+    from .sparse import current_stream, empty_device, ptr, to_device
+
+    cfg = cfg or GmresConfig()
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    bd = to_device(rhs, h.n).contiguous()
+    x = empty_device(h.n).zero_()
+    c = _lib.GmresCfg(int(cfg.restart), int(cfg.max_iters), float(cfg.rtol), float(cfg.atol))
+    st = _lib.GmresStats()
+    _lib.check(_lib.lib().pmgr_dist_emulate(h._A.handle, h.handle, b.ctypes.data, len(b) - 1, 1, ptr(bd), ptr(x),
+                                            ctypes.byref(c), ctypes.byref(st), current_stream()))
+    return x, int(st.iterations), bool(st.converged)

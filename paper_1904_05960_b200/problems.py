@@ -482,6 +482,53 @@ def make_c5(seed=0, nxy=128, nz_per_gpu=128, gpus=1):
                     name=f"C5-{nxy}x{nxy}x{nz}")
 
 
+def rank_major(pb: Problem, nranks: int):
+    """Renumber a problem so that each rank's z-slab is one contiguous range.
+
+    Rank r owns the node planes and cell layers z in [z0_r, z1_r) of
+    `dist.slab_bounds` (the last rank also owns the top node plane).  The new
+    order is rank after rank; inside a rank: its displacement dofs
+    (node-blocked, nodes in their original order) then its flow dofs (cells
+    in their original order, fields interleaved).  For nranks == 1 this is the
+    original layout.  Row and column numbering change together (P A P^T) and
+    each row's columns are re-sorted, so the result is again a valid
+    reference CsrMatrix.  Returns (problem, bounds) with bounds[r] the first
+    row of rank r (bounds[nranks] = n): the row ranges libpmgr's row
+    distribution takes.
+    """
+    from .dist import slab_bounds
+
+    slabs = slab_bounds(pb.nz, nranks)
+    plane = (pb.nx + 1) * (pb.ny + 1)
+    layer = pb.nx * pb.ny
+    nf = len(pb.cell_fields)
+    n_u = pb.n_u
+    parts, bounds = [], [0]
+    for r, (z0, z1) in enumerate(slabs):
+        zn1 = z1 + 1 if r == nranks - 1 else z1
+        parts.append(np.arange(3 * plane * z0, 3 * plane * zn1, dtype=np.int64))
+        parts.append(n_u + np.arange(nf * layer * z0, nf * layer * z1, dtype=np.int64))
+        bounds.append(bounds[-1] + len(parts[-2]) + len(parts[-1]))
+    perm = np.concatenate(parts)  # new -> old
+    n = pb.n
+    if len(perm) != n:
+        raise AssertionError("rank-major permutation does not cover the dofs")
+    inv = np.empty(n, dtype=np.int64)
+    inv[perm] = np.arange(n)
+    ro = pb.row_offsets
+    cnt = np.diff(ro)[perm]
+    new_ro = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(cnt, out=new_ro[1:])
+    take = np.repeat(ro[perm] - new_ro[:-1], cnt) + np.arange(new_ro[-1])
+    rows = np.repeat(np.arange(n, dtype=np.int64), cnt)
+    cols = inv[pb.col_indices[take]]
+    order = np.lexsort((cols, rows))
+    new = Problem(pb.name + f"-rm{nranks}", pb.nx, pb.ny, pb.nz, new_ro, cols[order].astype(np.int32),
+                  pb.values[take][order], pb.field_of[perm], pb.entity_of[perm], pb.rhs[perm], pb.cell_fields,
+                  dict(pb.meta, rank_bounds=list(bounds), perm=perm))
+    return new, np.array(bounds, dtype=np.int64)
+
+
 CONFIGS = {"C1": make_c1, "C2": make_c2, "C3": make_c3, "C4": make_c4, "C5": make_c5}
 
 

@@ -1,0 +1,107 @@
+"""Row-distributed solve on one GPU: N ranks emulated inside
+libpmgr (loopback transport, one host thread per rank, every exchange an
+ordinary stream-ordered copy).  Bar: a distributed MGR application is
+BITWISE equal to the single-GPU one (each local row sums its columns in the
+global stored order with the global lane group / block layout), and the
+distributed GMRES converges in the single-GPU iteration count +-1 to the same
+solution."""
+
+import numpy as np
+import pytest
+
+from tests.test_gpu_parity import mgr_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1904_05960_b200 import amg, dist, krylov, mgr, problems, sparse
+
+    return sparse, amg, mgr, krylov, dist, problems
+
+
+def build(pk, pb, n_max=4, four=False):
+    sparse, amg, mgr, krylov, dist, problems = pk
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of), mgr_config(pk[:4], pb, n_max, four))
+    return A, h
+
+
+CASES = [("C2", dict(n=8), 4, False), ("C1", dict(n=8), None, False), ("C4", dict(n=6), 4, True)]
+
+
+@pytest.mark.parametrize("name,kw,n_max,four", CASES)
+@pytest.mark.parametrize("nranks", [1, 2, 3])
+def test_distributed_apply_is_bitwise(pk, name, kw, n_max, four, nranks):
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make(name, seed=3, **kw), nranks)
+    A, h = build(pk, pb, n_max, four)
+    v = np.random.default_rng(7).standard_normal(pb.n)
+    z = h.apply(v)
+    zd = dist.emulate_apply(h, bounds, v).cpu().numpy()
+    assert np.array_equal(zd, z), f"max diff {np.abs(zd - z).max()}"
+
+
+def test_distributed_apply_uneven_and_empty_ranks(pk):
+    """More ranks than some coarse spaces have rows: empty owned ranges."""
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make("C2", seed=5, n=6), 6)
+    A, h = build(pk, pb)
+    v = np.random.default_rng(1).standard_normal(pb.n)
+    assert np.array_equal(dist.emulate_apply(h, bounds, v).cpu().numpy(), h.apply(v))
+
+
+def test_distributed_apply_original_layout_one_rank(pk):
+    """One rank on the original (block-prefix) layout: the outer operator's
+    block copy is sliced as CSR, the application stays bitwise."""
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb = problems.make("C2", seed=2, n=8)
+    A, h = build(pk, pb)
+    v = np.random.default_rng(3).standard_normal(pb.n)
+    assert np.array_equal(dist.emulate_apply(h, [0, pb.n], v).cpu().numpy(), h.apply(v))
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_distributed_gmres_matches_single_gpu(pk, nranks):
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make("C2", seed=4, n=12), nranks)
+    A, h = build(pk, pb)
+    cfg = krylov.GmresConfig(restart=100, max_iters=400, rtol=1e-6)
+    x1, st = krylov.gmres(A, h.apply, pb.rhs, cfg=cfg)
+    xd, its, conv = dist.emulate_gmres(h, bounds, pb.rhs, cfg)
+    xd = xd.cpu().numpy()
+    assert conv and st.converged
+    assert abs(its - st.iterations) <= 1
+    r = pb.rhs - sparse.matvec(A, xd)
+    assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(pb.rhs) * (1 + 1e-9)
+    assert np.linalg.norm(xd - x1) <= 1e-5 * np.linalg.norm(x1)
+
+
+def test_single_rank_solver_api(pk):
+    """The per-rank API (what a torchrun job calls) with one rank."""
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make("C2", seed=6, n=8), 1)
+    A, h = build(pk, pb)
+    d = dist.DeviceDistSolver(h, bounds, 0, 1)
+    assert (d.lo, d.n_own) == (0, pb.n)
+    v = np.random.default_rng(2).standard_normal(pb.n)
+    assert np.array_equal(d.apply(v).cpu().numpy(), h.apply(v))
+    y = d.spmv(v).cpu().numpy()
+    assert np.allclose(y, sparse.matvec(A, v), rtol=1e-13, atol=1e-13 * np.abs(y).max())
+    x, st = d.gmres(pb.rhs, krylov.GmresConfig(restart=100, max_iters=300))
+    assert st.converged
+    r = pb.rhs - sparse.matvec(A, x.cpu().numpy())
+    assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(pb.rhs) * (1 + 1e-9)
+
+
+def test_distribution_rejects_unsupported(pk):
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make("C2", seed=1, n=6), 2)
+    A, h = build(pk, pb)
+    with pytest.raises(ValueError):
+        dist.emulate_apply(h, [0, 5, pb.n - 1], np.zeros(pb.n))  # bounds do not cover [0, n)
