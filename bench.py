@@ -15,9 +15,13 @@ timed region.  `value` = dofs solved per second over all ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pmgr|reference]
 
-N > 1 (torchrun): replicas only -- every rank solves its own copy of the
-workload (the z-slab decomposition is future work); timing is
-the max over ranks.  `--impl reference` times the CPU oracle (the reference
+N > 1 (torchrun): weak scaling of the row-distributed solve -- the global
+problem is the C2 slab stacked N times in z (32 x 32 x 32N, the C5 generator,
+identical to C2 at N = 1), numbered rank-major; every rank builds the global
+hierarchy (replicated setup) and solves on its z-slab rows with halo
+exchanges / all-reduces over NCCL inside libpmgr.  Timing is the max over
+ranks; `value` = global dofs / time.  `--replicas` runs N independent C2
+solves instead.  `--impl reference` times the CPU oracle (the reference
 algorithm restated in C, oracle/) on the host cores, rank 0 only.
 """
 
@@ -184,6 +188,123 @@ class Clocks:
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_gpu_dist(args, rank, world, local_rank):
+    """Row-distributed weak-scaling solve, NCCL transport."""
+    import ctypes
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1904_05960_b200 import _lib, amg, dist as D, krylov, mgr, problems, sparse
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    base = problems.make_c5(seed=args.seed, nxy=32, nz_per_gpu=32, gpus=world)
+    pb, bounds = problems.rank_major(base, world)
+    del base
+    _, levels = workload("C2", args.seed)
+    F = sparse.Field
+    specs = tuple(mgr.MgrLevelSpec({F(t) for t in f}, {F(t) for t in c}, f_relax=relax, n_max=nm)
+                  for relax, f, c, nm in levels)
+    cfg = mgr.MgrConfig(levels=specs,
+                        amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=10 ** 9),
+                        amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=10 ** 9))
+    stream = torch.cuda.current_stream()
+    A = sparse.DeviceCsr.from_arrays(pb.n, pb.n, torch.from_numpy(pb.row_offsets).cuda(),
+                                     torch.from_numpy(pb.col_indices).cuda(), torch.from_numpy(pb.values).cuda())
+    lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h = mgr.mgr_setup(A, lay, cfg)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    setup_s = e0.elapsed_time(e1) / 1e3
+    tr = D.nccl_transport(rank, world, tdist)
+    t0 = time.perf_counter()
+    solver = D.DeviceDistSolver(h, bounds, rank, world, tr)
+    torch.cuda.synchronize()
+    dist_setup_s = time.perf_counter() - t0
+    lo, no = solver.lo, solver.n_own
+    b_own = torch.from_numpy(pb.rhs[lo:lo + no].copy()).cuda()
+    gcfg = krylov.GmresConfig(restart=args.restart, max_iters=1000, rtol=args.rtol)
+    flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        x, st = solver.gmres(b_own, gcfg)
+    clocks = Clocks(local_rank)
+    launches0 = _lib.launch_count()
+    times = []
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        x, st = solver.gmres(b_own, gcfg)
+        s1.record(stream)
+        s1.synchronize()
+        times.append(s0.elapsed_time(s1) / 1e3)
+    barrier()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+
+    def tmax(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        if world > 1:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t)
+
+    t_max = tmax(statistics.mean(times))
+    # e2e: host b slice in, host x slice out, inside the timed region
+    e2e_times = []
+    bh = pb.rhs[lo:lo + no].copy()
+    for k in range(max(1, args.steps)):
+        flush.fill_(float(k))
+        barrier()
+        t0 = time.perf_counter()
+        xd, st2 = solver.gmres(torch.from_numpy(bh).cuda(), gcfg)
+        xh = xd.cpu().numpy()
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_mean = tmax(statistics.mean(e2e_times))
+    # true residual of the gathered solution on rank 0
+    r_own = b_own - solver.spmv(x)
+    rr = torch.tensor([float(torch.dot(r_own, r_own)), float(torch.dot(b_own, b_own))], dtype=torch.float64,
+                      device="cuda")
+    if world > 1:
+        tdist.all_reduce(rr)
+    rel = float(torch.sqrt(rr[0] / rr[1]))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": pb.n / t_max / 1e6, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, paper_1904_05960_b200/problems.py)",
+            "config": {"workload": f"C2 slab x{world}: two-phase poromechanics 32x32x{32 * world} (C5 generator, "
+                                   "rank-major z-slabs), 3-level MGR (U AMG, N_max=4 -> S Jacobi -> P AMG)",
+                       "n_dofs": pb.n, "n_dofs_per_gpu": int(np.diff(bounds).max()), "nnz": pb.nnz,
+                       "restart": args.restart, "rtol": args.rtol, "gmres_iterations": st.iterations,
+                       "true_relative_residual": rel, "mgr_levels": h.level_sizes(),
+                       "l2": "flushed between steps (512 MiB write, untimed)",
+                       "parallelism": f"row-distributed z-slabs over {world} GPU(s): replicated setup, "
+                                      "NCCL halo exchange / all-gather / all-reduce inside libpmgr"},
+            "setup_s": setup_s, "dist_setup_s": dist_setup_s,
+            "e2e": {"value": pb.n / e2e_mean / 1e6, "unit": UNIT, "h2d_bytes_per_step": 8 * no,
+                    "d2h_bytes_per_step": 8 * no, "ms_per_step": e2e_mean * 1e3, "note": "per-rank slices"},
+            "gpu_launches": launches, "clocks": clk, "roofline": None, "cpu_baseline": None,
+            "kernel_timing": "not instrumented on the distributed path (see the N = 1 line)",
+        }
+        print(json.dumps(line), flush=True)
+    del solver, tr
+    if world > 1:
+        tdist.destroy_process_group()
 
 
 def run_gpu(args, rank, world, local_rank):
@@ -384,6 +505,9 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profile one solve between cudaProfilerStart/Stop and exit")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent C2 solves instead of the "
+                                                                "row-distributed slab stack")
+    ap.add_argument("--dist", action="store_true", help="use the row-distributed path even at N = 1")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the roofline kernel (profiles/), echoed into the JSON")
     args = ap.parse_args()
@@ -392,6 +516,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if args.dist or (world > 1 and not args.replicas and not args.ncu):
+        run_gpu_dist(args, rank, world, local_rank)
         return
     run_gpu(args, rank, world, local_rank)
 

@@ -302,11 +302,11 @@ std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank,
 }
 
 void halo_exchange(Halo *h, double *ext, cudaStream_t s) {
-    if (h && h->tr && h->tr->nranks > 1) h->tr->exchange(*h, ext, s);
+    if (h && h->tr) h->tr->exchange(*h, ext, s);
 }
 
 void gather_full(Gather *g, const double *own, double *full, cudaStream_t s) {
-    if (g->tr && g->tr->nranks > 1) {
+    if (g->tr) {
         g->tr->gather(*g, own, full, s);
     } else {
         const int64_t c = g->n_full;
@@ -802,7 +802,7 @@ static void gdot(DistSolver &D, const double *a, const double *b, double *out, c
     PMGR_LAUNCHED();
     k_sum_part<<<1, 32, 0, s>>>(part.p, nb, out);
     PMGR_LAUNCHED();
-    if (D.tr && D.nranks > 1) D.tr->allreduce(out, 1, s);
+    if (D.tr) D.tr->allreduce(out, 1, s);
 }
 
 // y = A x for an owned x (halo exchange into the ext buffer first)
@@ -872,7 +872,7 @@ void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const
             for (int pass = 0; pass < 2; ++pass) {
                 if (n > 0) multidot(V.p, n, j + 1, w.p, h.p, s);
                 else PMGR_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * (j + 1), s));
-                if (D.tr && D.nranks > 1) D.tr->allreduce(h.p, j + 1, s);
+                if (D.tr) D.tr->allreduce(h.p, j + 1, s);
                 if (n > 0) multiaxpy(V.p, n, j + 1, h.p, w.p, s);
                 std::vector<double> hp(j + 1);
                 to_host(h.p, hp.data(), j + 1);

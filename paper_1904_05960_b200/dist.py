@@ -257,10 +257,10 @@ def nccl_transport(rank: int, nranks: int, dist):
     nid = _lib.NcclId()
     if rank == 0:
         _lib.check(L.pmgr_nccl_get_id(ctypes.byref(nid)))
-    box = [bytes(nid.internal) if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0)
-    raw = box[0].ljust(128, b"\0")
-    ctypes.memmove(ctypes.addressof(nid), raw, 128)
+    if nranks > 1:
+        box = [ctypes.string_at(ctypes.addressof(nid), 128) if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        ctypes.memmove(ctypes.addressof(nid), box[0], 128)
     out = ctypes.c_void_p()
     _lib.check(L.pmgr_transport_nccl_create(ctypes.byref(nid), rank, nranks, ctypes.byref(out)))
     return _Handle(out, "pmgr_transport_destroy")

@@ -105,3 +105,18 @@ def test_distribution_rejects_unsupported(pk):
     A, h = build(pk, pb)
     with pytest.raises(ValueError):
         dist.emulate_apply(h, [0, 5, pb.n - 1], np.zeros(pb.n))  # bounds do not cover [0, n)
+
+
+def test_nccl_transport_single_rank(pk):
+    """The NCCL transport (libnccl resolved at run time) on a one-rank
+    communicator: id, communicator, grouped send/recv, all-reduce."""
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make("C2", seed=8, n=8), 1)
+    A, h = build(pk, pb)
+    tr = dist.nccl_transport(0, 1, None)
+    d = dist.DeviceDistSolver(h, bounds, 0, 1, tr)
+    v = np.random.default_rng(4).standard_normal(pb.n)
+    assert np.array_equal(d.apply(v).cpu().numpy(), h.apply(v))
+    x, st = d.gmres(pb.rhs, krylov.GmresConfig(restart=100, max_iters=300))
+    x1, st1 = krylov.gmres(A, h.apply, pb.rhs, cfg=krylov.GmresConfig(restart=100, max_iters=300))
+    assert st.converged and abs(st.iterations - st1.iterations) <= 1
