@@ -125,3 +125,33 @@ def test_distributed_gmres_matches_global(run2):
         x[res["owned"]] = res["x"]
     assert np.linalg.norm(x - xg) <= 1e-6 * np.linalg.norm(xg)
     assert bool(run2[0]["conv"]) == conv
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 5])
+def test_rank_major_numbering(nranks):
+    """problems.rank_major: a symmetric renumbering P A P^T whose rank ranges
+    are exactly the z-slab ownership of `dof_owner`, valid CSR (sorted
+    columns), identity for one rank (the layout libpmgr's row distribution
+    slices)."""
+    import scipy.sparse as sp
+
+    from paper_1904_05960_b200 import dist as D
+    from paper_1904_05960_b200 import problems
+
+    pb = problems.make_c2(seed=2, n=5)
+    q, bounds = problems.rank_major(pb, nranks)
+    perm = q.meta["perm"]
+    assert bounds[0] == 0 and bounds[-1] == pb.n and np.all(np.diff(bounds) > 0)
+    owner = D.dof_owner(pb, nranks)
+    for r in range(nranks):
+        assert np.all(owner[perm[bounds[r]:bounds[r + 1]]] == r)
+    A = sp.csr_matrix((pb.values, pb.col_indices, pb.row_offsets), shape=(pb.n, pb.n))
+    B = sp.csr_matrix((q.values, q.col_indices, q.row_offsets), shape=(q.n, q.n))
+    assert abs(A[perm][:, perm] - B).max() == 0.0
+    for i in range(0, q.n, 97):
+        cols = q.col_indices[q.row_offsets[i]:q.row_offsets[i + 1]]
+        assert np.all(np.diff(cols) > 0)
+    assert np.array_equal(q.field_of, pb.field_of[perm]) and np.array_equal(q.rhs, pb.rhs[perm])
+    if nranks == 1:
+        assert np.array_equal(perm, np.arange(pb.n))
+        assert np.array_equal(q.col_indices, pb.col_indices) and np.array_equal(q.values, pb.values)
