@@ -295,6 +295,7 @@ struct NcclTransport : Transport {
         if (n <= 0) return;
         nccl_check(nccl().AllReduce(buf, buf, (size_t)n, NCCL_FLOAT64, NCCL_SUM, comm, s), "ncclAllReduce");
     }
+    bool capturable() const override { return true; }
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank, int nranks) {
@@ -327,9 +328,11 @@ struct Space {
     bool triples = false;          // close ghost sets under node triples (BSR operators)
     DBuf<int64_t> gdev;            // my ghosts on the device
     int64_t lo = 0, hi = 0, nlow = 0;
+    int64_t pad = 0;               // gap before the owned range: off() is a multiple of 96
+    int64_t off() const { return nlow + pad; }
     std::shared_ptr<Halo> halo;
     int64_t n_own() const { return hi - lo; }
-    int64_t n_ext() const { return (int64_t)ghosts_me->size() + n_own(); }
+    int64_t n_ext() const { return (int64_t)ghosts_me->size() + pad + n_own(); }
     const std::vector<int64_t> *ghosts_me = nullptr;
 };
 
@@ -350,7 +353,8 @@ __global__ void k_mark_outside(int64_t n, const int64_t *ro, int64_t r0, const i
 }
 
 __global__ void k_localize(int64_t n, const int64_t *ro, int64_t r0, const int32_t *ci, const double *v, int64_t c0,
-                           int64_t c1, int64_t nlow, const int64_t *ghosts, int64_t ng, int64_t *lro, int32_t *lci,
+                           int64_t c1, int64_t nlow, int64_t pad, const int64_t *ghosts, int64_t ng, int64_t *lro,
+                           int32_t *lci,
                            double *lv) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
@@ -361,7 +365,7 @@ __global__ void k_localize(int64_t n, const int64_t *ro, int64_t r0, const int32
         const int64_t c = ci[q];
         int64_t pos;
         if (c >= c0 && c < c1) {
-            pos = nlow + (c - c0);
+            pos = nlow + pad + (c - c0);
         } else {
             int64_t a = 0, b = ng;  // lower_bound in the sorted ghost list
             while (a < b) {
@@ -369,7 +373,7 @@ __global__ void k_localize(int64_t n, const int64_t *ro, int64_t r0, const int32
                 if (ghosts[m] < c) a = m + 1;
                 else b = m;
             }
-            pos = a < nlow ? a : a + (c1 - c0);
+            pos = a < nlow ? a : a + pad + (c1 - c0);
         }
         lci[q - base] = (int32_t)pos;
         lv[q - base] = v[q];
@@ -486,6 +490,8 @@ struct Builder {
         sp->ghosts_me = &sp->ghosts[rank];
         const auto &gm = sp->ghosts[rank];
         sp->nlow = std::lower_bound(gm.begin(), gm.end(), sp->lo) - gm.begin();
+        // owned range 768-byte aligned (16-byte vector loads; node triples stay aligned)
+        sp->pad = (96 - sp->nlow % 96) % 96;
         sp->gdev.alloc((int64_t)gm.size());
         if (!gm.empty())
             PMGR_CUDA(cudaMemcpyAsync(sp->gdev.p, gm.data(), sizeof(int64_t) * gm.size(), cudaMemcpyHostToDevice, s));
@@ -494,7 +500,7 @@ struct Builder {
         h->tr = tr;
         h->id = sp->id;
         h->n_own = sp->n_own();
-        h->off = sp->nlow;
+        h->off = sp->off();
         h->n_ext = sp->n_ext();
         for (int p = 0; p < nranks; ++p) {
             if (p == rank) continue;
@@ -502,7 +508,7 @@ struct Builder {
             const int64_t b = std::lower_bound(gm.begin(), gm.end(), sp->start[p + 1]) - gm.begin();
             if (b > a) {
                 h->rpeer.push_back(p);
-                h->roff.push_back(a < sp->nlow ? a : a + sp->n_own());
+                h->roff.push_back(a < sp->nlow ? a : a + sp->pad + sp->n_own());
                 h->rcnt.push_back(b - a);
             }
         }
@@ -541,12 +547,12 @@ struct Builder {
         out.ro.alloc(n + 1);
         out.ci.alloc(out.nnz);
         out.v.alloc(out.nnz);
-        k_localize<<<grid_for(n + 1, 128), 128, 0, s>>>(n, Y.ro.p, r0, Y.ci.p, Y.v.p, C->lo, C->hi, C->nlow,
+        k_localize<<<grid_for(n + 1, 128), 128, 0, s>>>(n, Y.ro.p, r0, Y.ci.p, Y.v.p, C->lo, C->hi, C->nlow, C->pad,
                                                         C->gdev.p, (int64_t)C->ghosts_me->size(), out.ro.p,
                                                         out.ci.p, out.v.p);
         PMGR_LAUNCHED();
         csr_finalize(out, s);
-        out.row_off = R->nlow;
+        out.row_off = R->off();
         out.lanes = spmv_lanes(Y.view());
         // a pure block operator keeps its blocks (same blocks, same order as the
         // global copy); a block-prefix operator (A0 on the original layout)
@@ -562,7 +568,7 @@ struct Builder {
         ext.alloc(sp->n_ext());
         PMGR_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(double) * (size_t)(ext.n > 0 ? ext.n : 1), s));
         if (sp->n_own() > 0)
-            PMGR_CUDA(cudaMemcpyAsync(ext.p + sp->nlow, glob + sp->lo, sizeof(double) * sp->n_own(),
+            PMGR_CUDA(cudaMemcpyAsync(ext.p + sp->off(), glob + sp->lo, sizeof(double) * sp->n_own(),
                                       cudaMemcpyDeviceToDevice, s));
     }
     void ext_buffer(const Space *sp, DBuf<double> &ext) {
@@ -575,8 +581,8 @@ struct Builder {
         ext.alloc(over->n_ext());
         PMGR_CUDA(cudaMemsetAsync(ext.p, 0xff, sizeof(int64_t) * (size_t)(ext.n > 0 ? ext.n : 1), s));
         if (over->n_own() > 0) {
-            k_map_owned<<<grid_for(over->n_own(), 256), 256, 0, s>>>(over->n_own(), glob, over->lo, to->lo, to->nlow,
-                                                                      ext.p, over->nlow, keep_negative ? 1 : 0);
+            k_map_owned<<<grid_for(over->n_own(), 256), 256, 0, s>>>(over->n_own(), glob, over->lo, to->lo, to->off(),
+                                                                      ext.p, over->off(), keep_negative ? 1 : 0);
             PMGR_LAUNCHED();
         }
     }
@@ -619,7 +625,7 @@ std::unique_ptr<pmgr_amg> build_amg(Builder &B, const AmgPlan &P) {
         AmgLevel &L = h->levels[l];
         Space *S = P.sp[l];
         L.jacobi = true;
-        L.off = S->nlow;
+        L.off = S->off();
         L.halo = S->halo;
         auto A = std::make_shared<Csr>();
         if (l < G.collapse_from) {
@@ -697,7 +703,7 @@ std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int
     D->n_global = A0.nrows;
     D->lo = M0->lo;
     D->n_own = M0->n_own();
-    D->off = M0->nlow;
+    D->off = M0->off();
     D->n_ext = M0->n_ext();
     D->halo0 = M0->halo;
     B.localize(A0, M0, M0, D->A);
@@ -715,9 +721,9 @@ std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int
         L.n = Mi->n_own();
         L.nf = F->n_own();
         L.nc = C->n_own();
-        L.off = Mi->nlow;
-        L.off_f = F->nlow;
-        L.off_c = C->nlow;
+        L.off = Mi->off();
+        L.off_f = F->off();
+        L.off_c = C->off();
         L.halo_f = F->halo;
         L.halo_c = C->halo;
         L.f_relax = G.f_relax;
@@ -762,48 +768,6 @@ void DistSolver::ensure_work() {
     PMGR_CUDA(cudaMemset(we.p, 0, sizeof(double) * we.n));
 }
 
-namespace {
-__global__ void k_dot_partial(const double *a, const double *b, int64_t n, double *part) {
-    __shared__ double sh[8];
-    double t = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        t = fma(a[i], b[i], t);
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double u = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) u += sh[w];
-        part[blockIdx.x] = u;
-    }
-}
-__global__ void k_sum_part(const double *part, int n, double *out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < n; ++i) s += part[i];
-        *out = s;
-    }
-}
-__global__ void k_scale_to(const double *x, double a, int64_t n, double *y) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) y[i] = x[i] * a;
-}
-__global__ void k_resid_own(const double *b, const double *ax, int64_t n, double *r) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) r[i] = b[i] - ax[i];
-}
-}  // namespace
-
-// global dot of two owned vectors into *out (device), all ranks equal
-static void gdot(DistSolver &D, const double *a, const double *b, double *out, cudaStream_t s) {
-    const int nb = 148;
-    TBuf<double> part(nb, s);
-    k_dot_partial<<<nb, 256, 0, s>>>(a, b, D.n_own, part.p);
-    PMGR_LAUNCHED();
-    k_sum_part<<<1, 32, 0, s>>>(part.p, nb, out);
-    PMGR_LAUNCHED();
-    if (D.tr) D.tr->allreduce(out, 1, s);
-}
 
 // y = A x for an owned x (halo exchange into the ext buffer first)
 static void dist_spmv(DistSolver &D, const double *x_own, double *y_own, cudaStream_t s) {
@@ -817,134 +781,30 @@ static void dist_spmv(DistSolver &D, const double *x_own, double *y_own, cudaStr
 }
 
 // Right-preconditioned restarted GMRES (krylov.py:39-117) on row-distributed
-// vectors: CGS with one re-orthogonalisation (one all-reduce per pass), the
-// small Hessenberg / Givens algebra replicated on every rank (identical
-// all-reduced inputs => identical control flow everywhere).
+// vectors: the single-GPU Arnoldi kernels in split mode (krylov.cu), with the
+// projections (2(m+1) doubles) and the squared norm all-reduced across ranks;
+// the Hessenberg / Givens state is replicated (identical all-reduced inputs,
+// identical control flow on every rank).  With NCCL one step is a captured
+// CUDA graph (apply with its halo exchanges, SpMV, Arnoldi, all-reduces).
 void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const pmgr_gmres_cfg &cfg,
                 pmgr_gmres_stats &st, double *history, int32_t history_cap, cudaStream_t s) {
-    const int64_t n = D.n_own;
-    const int m = cfg.restart > 0 ? cfg.restart : 50;
-    if (m > 1000) fail(PMGR_ERR_INVALID, "restart too large for the distributed solver");
-    const int maxit = cfg.max_iters;
-    DBuf<double> V((int64_t)(m + 1) * (n > 0 ? n : 1)), w(n > 0 ? n : 1), z(n > 0 ? n : 1), r(n > 0 ? n : 1),
-        u(n > 0 ? n : 1), h((int64_t)m + 2), sc(2);
-    if (!nonzero_x0 && n > 0) PMGR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
-    auto to_host = [&](const double *dv, double *hv, int cnt) {
-        PMGR_CUDA(cudaMemcpyAsync(hv, dv, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
-        PMGR_CUDA(cudaStreamSynchronize(s));
+    D.ensure_work();
+    SplitOps ops;
+    ops.n = D.n_own;
+    ops.vin = D.ve.p + D.off;
+    ops.w = D.we.p + D.off;
+    ops.capturable = D.tr && D.tr->capturable();
+    ops.step = [&](cudaStream_t q) {
+        mgr_apply_direct(*D.M, D.ve.p, D.ze.p, q);
+        halo_exchange(D.halo0.get(), D.ze.p, q);
+        spmv(D.A.view(), D.ze.p, D.we.p, q);
     };
-    auto norm = [&](const double *a) {
-        gdot(D, a, a, sc.p, s);
-        double v;
-        to_host(sc.p, &v, 1);
-        return std::sqrt(v);
+    ops.spmv = [&](const double *xo, double *yo, cudaStream_t q) { dist_spmv(D, xo, yo, q); };
+    ops.apply = [&](const double *uo, double *zo, cudaStream_t q) { dist_apply(D, uo, zo, q); };
+    ops.allreduce = [&](double *buf, int64_t cnt, cudaStream_t q) {
+        if (D.tr) D.tr->allreduce(buf, cnt, q);
     };
-    // r = b - A x
-    auto residual = [&]() {
-        dist_spmv(D, x, w.p, s);
-        if (n > 0) {
-            k_resid_own<<<grid_for(n, 256), 256, 0, s>>>(b, w.p, n, r.p);
-            PMGR_LAUNCHED();
-        }
-    };
-    residual();
-    double beta = norm(r.p);
-    const double bnorm = nonzero_x0 ? norm(b) : beta;
-    const double tol = std::max(cfg.rtol * bnorm, cfg.atol);
-    std::vector<double> hist{beta};
-    int total = 0, restarts = 0;
-    bool brk = false;
-    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hc(m + 2);
-    while (beta > tol && total < maxit) {
-        std::fill(H.begin(), H.end(), 0.0);
-        std::fill(g.begin(), g.end(), 0.0);
-        g[0] = beta;
-        if (n > 0) {
-            k_scale_to<<<grid_for(n, 256), 256, 0, s>>>(r.p, 1.0 / beta, n, V.p);
-            PMGR_LAUNCHED();
-        }
-        int j = 0;
-        while (j < m && total < maxit) {
-            double *vj = V.p + (int64_t)j * n;
-            dist_apply(D, vj, z.p, s);
-            dist_spmv(D, z.p, w.p, s);
-            std::fill(hc.begin(), hc.end(), 0.0);
-            for (int pass = 0; pass < 2; ++pass) {
-                if (n > 0) multidot(V.p, n, j + 1, w.p, h.p, s);
-                else PMGR_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * (j + 1), s));
-                if (D.tr) D.tr->allreduce(h.p, j + 1, s);
-                if (n > 0) multiaxpy(V.p, n, j + 1, h.p, w.p, s);
-                std::vector<double> hp(j + 1);
-                to_host(h.p, hp.data(), j + 1);
-                for (int i = 0; i <= j; ++i) hc[i] += hp[i];
-            }
-            const double hn = norm(w.p);
-            double cn = 0.0;
-            for (int i = 0; i <= j; ++i) cn += hc[i] * hc[i];
-            cn = std::sqrt(cn + hn * hn);
-            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hc[i];
-            H[(size_t)(j + 1) * m + j] = hn;
-            if (hn > 1e-12 * std::max(cn, 1e-300)) {
-                if (n > 0) {
-                    k_scale_to<<<grid_for(n, 256), 256, 0, s>>>(w.p, 1.0 / hn, n, V.p + (int64_t)(j + 1) * n);
-                    PMGR_LAUNCHED();
-                }
-            } else {
-                brk = true;
-            }
-            for (int i = 0; i < j; ++i) {
-                const double t = H[(size_t)i * m + j];
-                H[(size_t)i * m + j] = cs[i] * t + sn[i] * H[(size_t)(i + 1) * m + j];
-                H[(size_t)(i + 1) * m + j] = -sn[i] * t + cs[i] * H[(size_t)(i + 1) * m + j];
-            }
-            const double rho = std::hypot(H[(size_t)j * m + j], H[(size_t)(j + 1) * m + j]);
-            if (rho == 0.0) {
-                brk = true;
-                break;
-            }
-            cs[j] = H[(size_t)j * m + j] / rho;
-            sn[j] = H[(size_t)(j + 1) * m + j] / rho;
-            H[(size_t)j * m + j] = rho;
-            H[(size_t)(j + 1) * m + j] = 0.0;
-            g[j + 1] = -sn[j] * g[j];
-            g[j] = cs[j] * g[j];
-            ++total;
-            ++j;
-            hist.push_back(std::fabs(g[j]));
-            if (std::fabs(g[j]) <= tol || brk) break;
-        }
-        if (j > 0) {
-            std::vector<double> y(j);
-            for (int i = j - 1; i >= 0; --i) {
-                double t = g[i];
-                for (int k = i + 1; k < j; ++k) t -= H[(size_t)i * m + k] * y[k];
-                y[i] = t / H[(size_t)i * m + i];
-            }
-            // u = V y ; x += M u
-            if (n > 0) {
-                PMGR_CUDA(cudaMemsetAsync(u.p, 0, sizeof(double) * n, s));
-                std::vector<double> ny(j);
-                for (int i = 0; i < j; ++i) ny[i] = -y[i];
-                PMGR_CUDA(cudaMemcpyAsync(h.p, ny.data(), sizeof(double) * j, cudaMemcpyHostToDevice, s));
-                multiaxpy(V.p, n, j, h.p, u.p, s);  // u -= V (-y)
-                PMGR_CUDA(cudaStreamSynchronize(s));  // ny is a host temporary
-            }
-            dist_apply(D, u.p, z.p, s);
-            if (n > 0) vec_axpy(1.0, z.p, x, n, s);
-            residual();
-            beta = norm(r.p);
-            hist.back() = beta;
-        }
-        if (brk) break;
-        if (beta > tol && total < maxit) ++restarts;
-    }
-    PMGR_CUDA(cudaStreamSynchronize(s));
-    st.iterations = total;
-    st.converged = beta <= tol ? 1 : 0;
-    st.restarts = restarts;
-    st.history_len = (int32_t)std::min<size_t>(hist.size(), history ? (size_t)history_cap : 0);
-    if (history)
-        for (int i = 0; i < (int)hist.size() && i < history_cap; ++i) history[i] = hist[i];
+    gmres_split(ops, b, x, nonzero_x0, cfg, st, history, history_cap, s);
 }
 
 // ====================================================== one-GPU emulation

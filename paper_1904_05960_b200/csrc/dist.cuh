@@ -15,6 +15,7 @@ struct Transport {
     virtual void exchange(Halo &h, double *ext, cudaStream_t s) = 0;
     virtual void gather(Gather &g, const double *own, double *full, cudaStream_t s) = 0;
     virtual void allreduce(double *buf, int64_t n, cudaStream_t s) = 0;
+    virtual bool capturable() const { return false; }  // may be recorded into a CUDA graph
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank, int nranks);

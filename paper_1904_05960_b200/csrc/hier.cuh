@@ -1,6 +1,7 @@
 // hier.cuh -- device-resident AMG and MGR hierarchies.
 #pragma once
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -163,6 +164,20 @@ void gmres_forget(const void *obj);  // drop cached solve workspaces of a matrix
 void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, int nonzero_x0,
                   const pmgr_gmres_cfg &cfg, pmgr_gmres_stats &stats, double *history,
                   int32_t history_cap, cudaStream_t s);
+// GMRES over row-distributed vectors: the caller provides w = A M vin for
+// the owned slices (halo exchanges inside), the owned-slice operators for the
+// restart update and the cross-rank all-reduce (dist.cu)
+struct SplitOps {
+    int64_t n = 0;          // owned rows
+    double *vin = nullptr;  // owned slice the preconditioner reads
+    double *w = nullptr;    // owned slice the operator writes
+    bool capturable = false;
+    std::function<void(cudaStream_t)> step;
+    std::function<void(const double *, double *, cudaStream_t)> spmv, apply;
+    std::function<void(double *, int64_t, cudaStream_t)> allreduce;
+};
+void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, const pmgr_gmres_cfg &cfg,
+                 pmgr_gmres_stats &stats, double *history, int32_t history_cap, cudaStream_t s);
 void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double *h, cudaStream_t s);
 void multiaxpy(const double *V, int64_t n, int32_t nvec, const double *h, double *w, cudaStream_t s);
 }  // namespace pmgr

@@ -103,6 +103,9 @@ struct AoParams {
     cudaGraphConditionalHandle cond;
     int use_cond;
     unsigned long long *stamps;  // PMGR_ARNOLDI_STAMPS: phase timestamps of block 0 (diagnostics)
+    // split modes (row-distributed GMRES): projections and the squared norm
+    // leave the kernel for a cross-rank all-reduce
+    double *red, *nrm2;
 };
 
 __device__ __forceinline__ void stamp(const AoParams &P, int slot) {
@@ -127,7 +130,12 @@ __device__ __forceinline__ double block_sum1(double v, double *sh) {
 // SM = true: the block's slices of w and V_j live in shared memory, so the
 // basis stream is the only per-vector L2/HBM traffic and w never returns to
 // global memory (small and medium n); SM = false streams them from L2.
-template <bool SM>
+// MODE 0: the whole step in one cooperative launch.  Split modes for the
+// row-distributed solve (each a plain launch; all-reduces in between):
+// 1 = projections' slice partials, 2 = their block sums into red (a, g),
+// 3 = coefficients h and the update w -= V h with slice norms, 4 = the
+// normalisation with ||w||^2 from nrm2 and the Givens bookkeeping.
+template <bool SM, int MODE = 0>
 __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double slice[];  // SM: w slice, then V_j slice
@@ -161,7 +169,7 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     // vectors at a time and issues every 16-byte load of both slices before
     // consuming them (one memory latency per pair for slices up to 640 rows);
     // slices are 256-byte aligned (ldv, chunk multiples of 32).
-    {
+    if constexpr (MODE == 0 || MODE == 1) {
         const int len = (int)(hi - lo), len2 = len >> 1;
         const double2 *w2 = reinterpret_cast<const double2 *>(SM ? wsl : P.w + lo);
         const double2 *v2 = reinterpret_cast<const double2 *>(SM ? vsl : vjg + lo);
@@ -209,10 +217,12 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
             }
         }
     }
+    if constexpr (MODE == 1) return;
     stamp(P, 1);
-    grid.sync();
+    if constexpr (MODE == 0) grid.sync();
     stamp(P, 2);
     // phase 2a: a_k and the Gram column, one block per coefficient
+    if constexpr (MODE == 0 || MODE == 2)
     for (int k = b; k <= j; k += nblk) {
         double sa = 0.0, sg = 0.0;
         for (int t = threadIdx.x; t < nblk; t += AO_THREADS) {
@@ -222,14 +232,21 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
         sa = block_sum1(sa, sh);
         sg = block_sum1(sg, sh);
         if (threadIdx.x == 0) {
-            P.a[k] = sa;
-            P.G[(int64_t)k * P.ldg + j] = sg;
-            P.G[(int64_t)j * P.ldg + k] = sg;
+            if constexpr (MODE == 2) {
+                P.red[k] = sa;
+                P.red[P.ldg + k] = sg;
+            } else {
+                P.a[k] = sa;
+                P.G[(int64_t)k * P.ldg + j] = sg;
+                P.G[(int64_t)j * P.ldg + k] = sg;
+            }
         }
     }
+    if constexpr (MODE == 2) return;
     stamp(P, 3);
-    grid.sync();
+    if constexpr (MODE == 0) grid.sync();
     stamp(P, 4);
+    if constexpr (MODE == 0 || MODE == 3) {
     // phase 2b: h = a + (a - G a), every block for itself.  G is symmetric,
     // so (G a)_k = sum_l G[l][k] a_l: warps split l, lanes take k (coalesced
     // rows of G, every load of a lane independent), then a fixed-order sum
@@ -307,13 +324,21 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     }
     nrm = block_sum1(nrm, sh);
     if (threadIdx.x == 0) P.pn[b] = nrm;
+    }  // phases 2b and 3
+    if constexpr (MODE == 3) return;
     stamp(P, 5);
-    grid.sync();
+    if constexpr (MODE == 0) grid.sync();
     stamp(P, 6);
     // phase 4: ||w||, breakdown test, normalisation (every block, same order)
     double s2 = 0.0;
-    for (int t = threadIdx.x; t < nblk; t += AO_THREADS) s2 += P.pn[t];
-    s2 = block_sum1(s2, sh);
+    if constexpr (MODE == 4) {
+        for (int k = threadIdx.x; k <= j; k += AO_THREADS) hs[k] = P.h[k];
+        __syncthreads();
+        s2 = *P.nrm2;
+    } else {
+        for (int t = threadIdx.x; t < nblk; t += AO_THREADS) s2 += P.pn[t];
+        s2 = block_sum1(s2, sh);
+    }
     const double hn = sqrt(s2);
     double c2 = 0.0;
     for (int k = 0; k <= j; ++k) c2 += hs[k] * hs[k];
@@ -453,6 +478,30 @@ __global__ void k_norm_final(const double *pn, int npn, double *out) {
     for (int b = threadIdx.x; b < npn; b += 32) s += pn[b];
     s = warp_sum(s);
     if (threadIdx.x == 0) *out = sqrt(s);
+}
+
+// split-mode helpers (row-distributed GMRES)
+__global__ void k_split_fix(Dev *dev, const double *red, int ldg, double *a, double *G) {
+    const int j = dev->j;
+    for (int k = threadIdx.x; k <= j; k += blockDim.x) {
+        a[k] = red[k];
+        G[(int64_t)k * ldg + j] = red[ldg + k];
+        G[(int64_t)j * ldg + k] = red[ldg + k];
+    }
+}
+__global__ void k_sum_fixed(const double *p, int np, double *out) {  // one thread: fixed order
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < np; ++i) s += p[i];
+        *out = s;
+    }
+}
+__global__ void k_sqrt_inplace(double *x) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *x = sqrt(*x);
+}
+__global__ void k_sub(const double *b, const double *y, int64_t n, double *r) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) r[i] = b[i] - y[i];
 }
 
 // generic helpers for the Python-callable path
@@ -802,6 +851,202 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
     stats.history_len = nh < history_cap ? nh : history_cap;
     if (history)
         for (int32_t i = 0; i < stats.history_len; ++i) history[i] = hist[i];
+}
+
+// ---------------------------------------------------------------------------
+// GMRES over row-distributed vectors (dist.cu supplies the operators and the
+// all-reduce): the same Arnoldi kernels as the single-GPU path in split mode,
+// one host synchronisation per step to read the device state.
+// ---------------------------------------------------------------------------
+
+void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, const pmgr_gmres_cfg &cfg,
+                 pmgr_gmres_stats &stats, double *history, int32_t history_cap, cudaStream_t s) {
+    if (cfg.restart < 1) fail(PMGR_ERR_INVALID, "restart must be >= 1");
+    if (cfg.restart > 1000) fail(PMGR_ERR_INVALID, "restart above 1000 is not supported");
+    if (!(cfg.rtol > 0) || !(cfg.atol > 0)) fail(PMGR_ERR_INVALID, "tolerances must be positive");
+    const int64_t n = ops.n;
+    const int m = cfg.restart;
+    const int max_iters = cfg.max_iters > 0 ? cfg.max_iters : 0;
+    const int64_t ldv = (n + 31) / 32 * 32 + 32;
+    const int nblk = 2 * num_sms();
+    const int64_t chunk = ((n + nblk - 1) / nblk + 31) / 32 * 32;
+    const int nparts = 4 * num_sms();
+    DBuf<double> V((int64_t)(m + 1) * ldv), r(ldv), u(ldv), z(ldv), t(ldv), H((int64_t)(m + 1) * m),
+        G((int64_t)(m + 1) * (m + 1)), cs(m + 1), sn(m + 1), g(m + 2), a(m + 1), h(m + 1), y(m + 1),
+        hist((int64_t)max_iters + 2), pa((int64_t)(m + 1) * nblk), pg((int64_t)(m + 1) * nblk),
+        pn(nparts > nblk ? nparts : nblk), red(2 * (int64_t)(m + 1)), nrm2(1), beta(1);
+    DBuf<Dev> dev(1);
+    Dev *hdev = nullptr;
+    PMGR_CUDA(cudaMallocHost((void **)&hdev, sizeof(Dev)));
+    std::unique_ptr<Dev, void (*)(Dev *)> hold(hdev, [](Dev *p) { cudaFreeHost(p); });
+    PMGR_CUDA(cudaMemsetAsync(red.p, 0, sizeof(double) * red.n, s));
+
+    auto gnorm = [&](const double *v, double *out) {  // out = ||v|| over all ranks
+        k_norm_partial<<<nparts, DOT_BLOCK, 0, s>>>(v, n, pn.p);
+        PMGR_LAUNCHED();
+        k_sum_fixed<<<1, 32, 0, s>>>(pn.p, nparts, out);
+        PMGR_LAUNCHED();
+        ops.allreduce(out, 1, s);
+        k_sqrt_inplace<<<1, 32, 0, s>>>(out);
+        PMGR_LAUNCHED();
+    };
+    auto residual = [&]() {  // r = b - A x
+        ops.spmv(x, t.p, s);
+        if (n > 0) {
+            k_sub<<<grid_for(n, 256), 256, 0, s>>>(b, t.p, n, r.p);
+            PMGR_LAUNCHED();
+        }
+    };
+    AoParams P = {};
+    P.V = V.p;
+    P.n = n;
+    P.ldv = ldv;
+    P.chunk = chunk;
+    P.w = ops.w;
+    P.vin = ops.vin;
+    P.dev = dev.p;
+    P.pa = pa.p;
+    P.pg = pg.p;
+    P.pn = pn.p;
+    P.G = G.p;
+    P.ldg = m + 1;
+    P.a = a.p;
+    P.h = h.p;
+    P.H = H.p;
+    P.cs = cs.p;
+    P.sn = sn.p;
+    P.g = g.p;
+    P.hist = hist.p;
+    P.red = red.p;
+    P.nrm2 = nrm2.p;
+    auto step = [&](cudaStream_t st) {
+        ops.step(st);  // w = A M vin
+        k_arnoldi<false, 1><<<nblk, AO_THREADS, 0, st>>>(P);
+        PMGR_LAUNCHED();
+        k_arnoldi<false, 2><<<nblk, AO_THREADS, 0, st>>>(P);
+        PMGR_LAUNCHED();
+        ops.allreduce(red.p, 2 * (int64_t)(m + 1), st);
+        k_split_fix<<<1, 256, 0, st>>>(dev.p, red.p, m + 1, a.p, G.p);
+        PMGR_LAUNCHED();
+        k_arnoldi<false, 3><<<nblk, AO_THREADS, 0, st>>>(P);
+        PMGR_LAUNCHED();
+        k_sum_fixed<<<1, 32, 0, st>>>(pn.p, nblk, nrm2.p);
+        PMGR_LAUNCHED();
+        ops.allreduce(nrm2.p, 1, st);
+        k_arnoldi<false, 4><<<nblk, AO_THREADS, 0, st>>>(P);
+        PMGR_LAUNCHED();
+    };
+    // one captured graph per step when the transport can be captured (NCCL;
+    // a device-side WHILE loop around NCCL calls measured 20x slower)
+    cudaGraphExec_t exec = nullptr, cycle = nullptr;
+    int64_t graph_kernels = 0;
+    if (!cycle && ops.capturable && use_cycle_graphs()) {
+        cudaStream_t cap;
+        PMGR_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t graph = nullptr;
+        PMGR_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        g_capture_count = &graph_kernels;
+        try {
+            step(cap);
+        } catch (...) {
+            g_capture_count = nullptr;
+            cudaStreamEndCapture(cap, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            cudaStreamDestroy(cap);
+            throw;
+        }
+        g_capture_count = nullptr;
+        PMGR_CUDA(cudaStreamEndCapture(cap, &graph));
+        PMGR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        PMGR_CUDA(cudaGraphDestroy(graph));
+        PMGR_CUDA(cudaStreamDestroy(cap));
+    }
+    struct ExecGuard {
+        cudaGraphExec_t e;
+        ~ExecGuard() {
+            if (e) cudaGraphExecDestroy(e);
+        }
+    } eg{exec}, eg2{cycle};
+
+    std::vector<double> hl;
+    if (!nonzero_x0 && n > 0) PMGR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    residual();
+    gnorm(r.p, beta.p);
+    double bt = read_scalar(beta.p, s);
+    hl.push_back(bt);
+    double bnorm = bt;
+    if (nonzero_x0) {
+        gnorm(b, nrm2.p);
+        bnorm = read_scalar(nrm2.p, s);
+    }
+    const double tol = std::fmax(cfg.rtol * bnorm, cfg.atol);
+    Dev d0 = {};
+    d0.m = m;
+    d0.max_iters = max_iters;
+    d0.tol = tol;
+    PMGR_CUDA(cudaMemcpyAsync(dev.p, &d0, sizeof(Dev), cudaMemcpyHostToDevice, s));
+    int total = 0, restarts = 0;
+    bool brk = false;
+    while (bt > tol && total < max_iters) {
+        k_cycle_init<<<1, 256, 0, s>>>(dev.p, H.p, G.p, m + 1, cs.p, sn.p, g.p, m, beta.p);
+        PMGR_LAUNCHED();
+        if (n > 0) {
+            k_scale2<<<vec_grid(n), 256, 0, s>>>(r.p, n, beta.p, V.p, ops.vin);
+            PMGR_LAUNCHED();
+        }
+        if (cycle) {
+            PMGR_CUDA(cudaGraphLaunch(cycle, s));
+            PMGR_CUDA(cudaMemcpyAsync(hdev, dev.p, sizeof(Dev), cudaMemcpyDeviceToHost, s));
+            PMGR_CUDA(cudaStreamSynchronize(s));
+            g_launches.fetch_add(graph_kernels * (hdev->total - total + (hdev->dead ? 1 : 0)),
+                                 std::memory_order_relaxed);
+        }
+        while (!cycle) {
+            PMGR_CUDA(cudaMemcpyAsync(hdev, dev.p, sizeof(Dev), cudaMemcpyDeviceToHost, s));
+            PMGR_CUDA(cudaStreamSynchronize(s));
+            if (!hdev->active) break;
+            if (exec) {
+                PMGR_CUDA(cudaGraphLaunch(exec, s));
+                g_launches.fetch_add(graph_kernels, std::memory_order_relaxed);
+            } else {
+                step(s);
+            }
+        }
+        const Dev dv = *hdev;
+        const int j = dv.j;
+        if (dv.total > total) {
+            std::vector<double> hh(dv.total - total);
+            PMGR_CUDA(cudaMemcpyAsync(hh.data(), hist.p + total, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost,
+                                      s));
+            PMGR_CUDA(cudaStreamSynchronize(s));
+            hl.insert(hl.end(), hh.begin(), hh.end());
+        }
+        total = dv.total;
+        brk = dv.brk != 0;
+        if (j > 0) {
+            k_trsv<<<1, 256, sizeof(double) * j, s>>>(H.p, m, j, g.p, y.p);
+            PMGR_LAUNCHED();
+            if (n > 0) {
+                k_combine<<<vec_grid(n), 256, 0, s>>>(V.p, n, ldv, j, y.p, u.p);
+                PMGR_LAUNCHED();
+            }
+            ops.apply(u.p, z.p, s);
+            if (n > 0) vec_axpy(1.0, z.p, x, n, s);
+            residual();
+            gnorm(r.p, beta.p);
+            bt = read_scalar(beta.p, s);
+            hl.back() = bt;
+        }
+        ++restarts;
+        if (bt <= tol || brk) break;
+    }
+    stats.iterations = total;
+    stats.converged = bt <= tol;
+    stats.restarts = restarts;
+    const int32_t nh = (int32_t)hl.size();
+    stats.history_len = history ? (nh < history_cap ? nh : history_cap) : nh;
+    if (history)
+        for (int32_t i = 0; i < stats.history_len; ++i) history[i] = hl[i];
 }
 
 void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double *h, cudaStream_t s) {
