@@ -433,3 +433,37 @@ class MatvecOperator:
 
 def operator(A) -> MatvecOperator:
     return MatvecOperator(A)
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market IO (reference sparse.py:484-502: general real coordinate
+# format, 1-based on disk, 17 significant digits so values round-trip)
+# ---------------------------------------------------------------------------
+
+
+def write_matrix_market(path, A: CsrMatrix) -> None:
+    from scipy.io import mmwrite
+
+    mmwrite(str(path), A.to_scipy().tocoo(), precision=17, symmetry="general")
+
+
+def read_matrix_market(path) -> CsrMatrix:
+    import scipy.sparse as sp
+    from scipy.io import mmread
+
+    m = mmread(str(path), spmatrix=False) if "spmatrix" in mmread.__code__.co_varnames else mmread(str(path))
+    if not sp.issparse(m):
+        raise ValueError(f"{path}: not a coordinate-format matrix")
+    return CsrMatrix.from_scipy(sp.csr_matrix(m))
+
+
+def write_vector(path, v) -> None:
+    from scipy.io import mmwrite
+
+    mmwrite(str(path), np.asarray(v, dtype=np.float64).reshape(-1, 1), precision=17)
+
+
+def read_vector(path) -> np.ndarray:
+    from scipy.io import mmread
+
+    return np.asarray(mmread(str(path)), dtype=np.float64).ravel()
