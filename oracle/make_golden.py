@@ -147,6 +147,26 @@ VARIANTS = {
     "v2": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg"),
                        dict(f={Field.S}, c={Field.P}, f_relax="jacobi", f_relax_sweeps=2)),
                cfg=dict(terminal_cycles=2, f_relax_position="post")),
+    # hybrid l1-GS (the reference's default smoother semantics) with 16 partitions
+    "v4": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi")),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre"), f_parts=16, t_parts=16),
+    # level-2 global smoothers of default_three_level (mgr.py:104-120)
+    "v5": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi", global_smoother="ilu", ilu_fill=1)),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre", npartitions=1)),
+    "v6": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi", global_smoother="ilu", ilu_fill=1)),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre", npartitions=8)),
+    "v7": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi", global_smoother="hbgs", hbgs_sweeps=3)),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre", npartitions=1), interleaved=True),
+    "v8": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi", global_smoother="hbgs", hbgs_sweeps=3)),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre", npartitions=4), interleaved=True),
+    "v9": dict(levels=(dict(f={Field.U}, c={Field.S, Field.P}, f_relax="amg", n_max=4),
+                       dict(f={Field.S}, c={Field.P}, f_relax="jacobi", global_smoother="ilu", ilu_fill=0)),
+               cfg=dict(terminal_cycles=1, f_relax_position="pre", npartitions=3)),
 }
 
 
@@ -155,9 +175,11 @@ def dump_problem(tag, pb, n_max, full, restart=100, four_field=False, variant=No
     lay = FieldLayout(pb.field_of, pb.entity_of)
     if variant is not None:
         V = VARIANTS[variant]
+        if V.get("interleaved"):
+            lay = FieldLayout(pb.field_of, pb.entity_of, psp.Ordering.FLOW_INTERLEAVED)
         levels = tuple(pmgr.MgrLevelSpec(lv["f"], lv["c"], **{k: x for k, x in lv.items() if k not in ("f", "c")})
                        for lv in V["levels"])
-        base = parity_config(levels)
+        base = parity_config(levels, V.get("f_parts", JACOBI), V.get("t_parts", JACOBI))
         cfg = pmgr.MgrConfig(levels=levels, amg_f_relax=base.amg_f_relax, amg_terminal=base.amg_terminal,
                              **V["cfg"])
         h = pmgr.mgr_setup(A, lay, cfg)
@@ -184,6 +206,14 @@ def dump_problem(tag, pb, n_max, full, restart=100, four_field=False, variant=No
             d[k + "coarse_sha"] = dcsr(nxt)
         if isinstance(lv.f_relax, pmgr._AmgFRelax):
             dump_amg(d, k + "amg_", lv.f_relax.hierarchy, full)
+        if isinstance(lv.global_smoother, pmgr._IluGlobal):
+            put_csr(d, k + "ilu", lv.global_smoother.factors.lu)
+            d[k + "ilu_dpos"] = lv.global_smoother.factors.diag_pos
+        if lv.global_smoother is not None:
+            rng_s = np.random.default_rng(99)
+            vs = rng_s.standard_normal(lv.A.nrows)
+            d[k + "gs_v"] = vs
+            d[k + "gs_z"] = lv.global_smoother.apply(vs)
     dump_amg(d, "term_", h.terminal_solver, full)
     rng = np.random.default_rng(1234)
     v = rng.standard_normal(pb.n)
@@ -283,6 +313,9 @@ def main():
         dump_problem("c2_6_v2", problems.make_c2(seed=5, n=6), None, True, variant="v2")
     if "c2_6_v3" in which:
         dump_problem("c2_6_v3", problems.make_c2(seed=5, n=6), None, True, variant="v3")
+    for v in ("v4", "v5", "v6", "v7", "v8", "v9"):
+        if f"c2_6_{v}" in which:
+            dump_problem(f"c2_6_{v}", problems.make_c2(seed=5, n=6), None, True, variant=v)
     if "c3_16" in which:
         dump_problem("c3_16", problems.make_c3(seed=0, n=16), 4, False, restart=100)
 

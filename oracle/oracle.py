@@ -54,8 +54,7 @@ class _OCsr(ctypes.Structure):
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            build()
+        build()  # no-op unless oracle.c is newer than the library
         _lib = ctypes.CDLL(_LIB_PATH)
         _lib.o_free.argtypes = [ctypes.c_void_p]
         for name in ("o_direct_interp", "o_l1diag", "o_lu_factor"):
@@ -187,6 +186,119 @@ def l1_sweep(A: Csr, b, x, starts, dtilde, forward: bool) -> np.ndarray:
                  ctypes.c_int64(len(starts) - 1), _p(starts), _p(dtilde), _p(b), _p(out), _p(pre),
                  ctypes.c_int(1 if forward else 0))
     return out
+
+
+# ---------------------------------------------------------------------------
+# level-2 global smoothers (reference smoothers.py:127-224, mgr.py:275-292)
+# ---------------------------------------------------------------------------
+
+
+class ZeroPivotError(ArithmeticError):
+    def __init__(self, row: int):
+        self.row = int(row)
+        super().__init__(f"zero pivot at row {int(row)}")
+
+
+def restrict_to_partitions(A: Csr, starts: np.ndarray) -> Csr:
+    """Drop couplings crossing partition boundaries (smoothers.py:215-224)."""
+    rows = A.rows_of_entries()
+    part = np.searchsorted(starts, rows, side="right") - 1
+    keep = (A.ci >= starts[part]) & (A.ci < starts[part + 1])
+    kept = np.flatnonzero(keep)
+    ro = np.concatenate([[0], np.cumsum(np.bincount(rows[kept], minlength=A.nrows))]).astype(np.int64)
+    return Csr(A.nrows, A.ncols, ro, A.ci[kept], A.v[kept])
+
+
+def _iluk(A: Csr, k: int):
+    L = lib()
+    n = A.nrows
+    lptr = np.zeros(n + 1, dtype=np.int64)
+    dpos = np.full(n, -1, dtype=np.int64)
+    tot = ctypes.c_int64()
+    L.o_iluk_symbolic.restype = ctypes.c_int64
+    cnt = L.o_iluk_symbolic(ctypes.c_int64(n), _p(A.ro), _p(A.ci), ctypes.c_int(k), ctypes.c_int64(0), _p(lptr),
+                            None, None, _p(dpos), ctypes.byref(tot))
+    ind = np.zeros(max(cnt, 1), dtype=np.int32)
+    lev = np.zeros(max(cnt, 1), dtype=np.int32)
+    L.o_iluk_symbolic(ctypes.c_int64(n), _p(A.ro), _p(A.ci), ctypes.c_int(k), ctypes.c_int64(max(cnt, 1)), _p(lptr),
+                      _p(ind), _p(lev), _p(dpos), None)
+    data = np.zeros(max(cnt, 1))
+    L.o_iluk_numeric.restype = ctypes.c_int64
+    fail = L.o_iluk_numeric(ctypes.c_int64(n), _p(A.ro), _p(A.ci), _p(A.v), _p(lptr), _p(ind), _p(dpos), _p(data))
+    return Csr(n, n, lptr, ind[:cnt], data[:cnt]), dpos, int(fail)
+
+
+def ilu_factor(A: Csr, k: int, zero_pivot_shift=None):
+    """ILU(k) without pivoting; on a zero pivot, retry once on
+    A + shift*max(|diag|, 1)*I (scipy sum: exact zeros dropped) (smoothers.py:159-188)."""
+    lu, dpos, fail = _iluk(A, k)
+    if fail >= 0:
+        if zero_pivot_shift is None:
+            raise ZeroPivotError(fail)
+        shift = zero_pivot_shift * max(float(np.max(np.abs(A.diagonal()))), 1.0)
+        import scipy.sparse as sp
+        S = sp.csr_matrix((A.v, A.ci, A.ro), shape=(A.nrows, A.ncols)) + shift * sp.identity(A.nrows, format="csr")
+        S = S.tocsr()
+        S.sort_indices()
+        lu, dpos, fail = _iluk(Csr(S.shape[0], S.shape[1], S.indptr.astype(np.int64), S.indices.astype(np.int32),
+                                   S.data.astype(np.float64)), k)
+        if fail >= 0:
+            raise ZeroPivotError(fail)
+    return lu, dpos
+
+
+def ilu_solve(lu: Csr, dpos: np.ndarray, r) -> np.ndarray:
+    z = np.empty(lu.nrows)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    lib().o_ilu_solve(ctypes.c_int64(lu.nrows), _p(lu.ro), _p(lu.ci), _p(lu.v), _p(dpos), _p(r), _p(z))
+    return z
+
+
+def offpart_abs_rowsum(A: Csr, starts: np.ndarray) -> np.ndarray:
+    out = np.empty(A.nrows)
+    lib().o_offpart_abs(ctypes.c_int64(A.nrows), _p(A.ro), _p(A.ci), _p(A.v), ctypes.c_int64(len(starts) - 1),
+                        _p(starts), _p(out))
+    return out
+
+
+def hbgs_sweeps(A: Csr, field_of, entity_of, b, nsweeps: int, starts: np.ndarray) -> np.ndarray:
+    """Hybrid block Gauss-Seidel over per-cell 2x2 (s, p) blocks from x = 0
+    (smoothers.py:127-152): S / P dofs paired by entity."""
+    s = np.flatnonzero(field_of == 1)
+    s = s[np.argsort(entity_of[s], kind="stable")].astype(np.int64)
+    p = np.flatnonzero(field_of == 2)
+    p = p[np.argsort(entity_of[p], kind="stable")].astype(np.int64)
+    add = offpart_abs_rowsum(A, starts)
+    x = np.zeros(A.nrows)
+    pre = np.empty(A.nrows)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    L = lib()
+    L.o_hbgs_sweep.restype = ctypes.c_int64
+    for _ in range(nsweeps):
+        bad = L.o_hbgs_sweep(ctypes.c_int64(A.nrows), _p(A.ro), _p(A.ci), _p(A.v), ctypes.c_int64(len(starts) - 1),
+                             _p(starts), _p(add), _p(b), _p(x), _p(pre), ctypes.c_int64(len(s)), _p(s), _p(p),
+                             ctypes.c_int(1))
+        if bad >= 0:
+            raise ValueError(f"singular 2x2 diagonal block at cell {int(entity_of[s[bad]])}")
+    return x
+
+
+class GlobalSmoother:
+    """_IluGlobal / _HbgsGlobal (mgr.py:275-292)."""
+
+    def __init__(self, A: Csr, field_of, entity_of, spec, npartitions: int):
+        self.kind = spec.global_smoother
+        self.starts = partition_starts(A.nrows, npartitions, align=2)
+        if self.kind == "ilu":
+            local = restrict_to_partitions(A, self.starts) if len(self.starts) > 2 else A
+            self.lu, self.dpos = ilu_factor(local, spec.ilu_fill, zero_pivot_shift=1e-8)
+        else:
+            self.A, self.fo, self.eo, self.nsweeps = A, field_of, entity_of, spec.hbgs_sweeps
+
+    def apply(self, v):
+        if self.kind == "ilu":
+            return ilu_solve(self.lu, self.dpos, v)
+        return hbgs_sweeps(self.A, self.fo, self.eo, v, self.nsweeps, self.starts)
 
 
 # ---------------------------------------------------------------------------
@@ -352,6 +464,9 @@ class MgrLevelSpec:
     f_relax_sweeps: int = 1
     n_max: int | None = None
     interp: str = "injection_jacobi"  # | "injection_only" (mgr.py:151-152)
+    global_smoother: str = "none"     # | "ilu" | "hbgs" (mgr.py:388-396)
+    ilu_fill: int = 1
+    hbgs_sweeps: int = 3
 
 
 @dataclass(frozen=True)
@@ -361,6 +476,7 @@ class MgrConfig:
     amg_f_relax: AmgConfig = field(default_factory=lambda: AmgConfig(strength_threshold=0.5, num_functions=3))
     amg_terminal: AmgConfig = field(default_factory=lambda: AmgConfig(strength_threshold=0.25))
     f_relax_position: str = "pre"
+    npartitions: int = 1              # global smoothers' partitions (mgr.py:391)
 
 
 @dataclass
@@ -374,6 +490,7 @@ class MgrLevel:
     f_relax: object
     spec: MgrLevelSpec
     dinv: np.ndarray
+    smoother: object = None
 
 
 @dataclass
@@ -497,8 +614,10 @@ def mgr_setup(A: Csr, field_of: np.ndarray, entity_of: np.ndarray, cfg: MgrConfi
             frelax = ("jacobi", blocks[0], max(1, spec.f_relax_sweeps))
         else:
             frelax = None
+        smoother = (GlobalSmoother(cur, fo, eo, spec, cfg.npartitions) if spec.global_smoother != "none"
+                    else None)
         coarse = build_coarse(cur, eo[is_c], is_c, blocks, P, spec.n_max)
-        levels.append(MgrLevel(cur, fo, eo, is_c, blocks, P, frelax, spec, dinv))
+        levels.append(MgrLevel(cur, fo, eo, is_c, blocks, P, frelax, spec, dinv, smoother))
         fo, eo = fo[is_c], eo[is_c]
         cur = coarse
     term = amg_setup(cur, cfg.amg_terminal)
@@ -531,9 +650,15 @@ def _apply_level(h, l, v):
     lv = h.levels[l]
     f_rows = np.flatnonzero(~lv.is_c)
     z = None
+    if lv.smoother is not None:
+        z = lv.smoother.apply(v)
     if h.f_relax_position == "pre" and lv.f_relax is not None:
-        z = np.zeros(len(v))
-        z[f_rows] += _f_relax_apply(lv, v[f_rows])
+        if z is None:
+            z = np.zeros(len(v))
+            r = v
+        else:
+            r = v - spmv(lv.A, z)
+        z[f_rows] += _f_relax_apply(lv, r[f_rows])
     r = v - spmv(lv.A, z) if z is not None else v
     ec = _apply_level(h, l + 1, r[lv.is_c])
     corr = spmv(lv.P, ec)

@@ -74,18 +74,46 @@ VARIANT_SPECS = {
                  dict(f={S_}, c={P_}, f_relax="jacobi", f_relax_sweeps=2)], 2, "post"),
     "c2_6_v3": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
                  dict(f={S_}, c={P_}, f_relax="none")], 1, "pre"),
+    # hybrid l1-GS AMG smoothing with 16 partitions (both AMGs)
+    "c2_6_v4": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi")], 1, "pre", dict(f_parts=16, t_parts=16)),
+    # level-2 global smoothers (default_three_level, mgr.py:104-120)
+    "c2_6_v5": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi", global_smoother="ilu", ilu_fill=1)], 1, "pre",
+                dict(npartitions=1)),
+    "c2_6_v6": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi", global_smoother="ilu", ilu_fill=1)], 1, "pre",
+                dict(npartitions=8)),
+    "c2_6_v7": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi", global_smoother="hbgs", hbgs_sweeps=3)], 1, "pre",
+                dict(npartitions=1, interleaved=True)),
+    "c2_6_v8": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi", global_smoother="hbgs", hbgs_sweeps=3)], 1, "pre",
+                dict(npartitions=4, interleaved=True)),
+    "c2_6_v9": ([dict(f={U_}, c={S_, P_}, f_relax="amg", n_max=4),
+                 dict(f={S_}, c={P_}, f_relax="jacobi", global_smoother="ilu", ilu_fill=0)], 1, "pre",
+                dict(npartitions=3)),
 }
 
 
+def variant_options(tag):
+    spec = VARIANT_SPECS[tag]
+    return spec[3] if len(spec) > 3 else {}
+
+
 def oracle_variant_hierarchy(tag):
-    levels, tc, pos = VARIANT_SPECS[tag]
+    levels, tc, pos = VARIANT_SPECS[tag][:3]
+    opt = variant_options(tag)
     pb = problems.make_c2(seed=5, n=6)
     specs = tuple(O.MgrLevelSpec(frozenset(lv["f"]), frozenset(lv["c"]), lv.get("f_relax", "jacobi"),
-                                 lv.get("f_relax_sweeps", 1), lv.get("n_max"), lv.get("interp", "injection_jacobi"))
+                                 lv.get("f_relax_sweeps", 1), lv.get("n_max"), lv.get("interp", "injection_jacobi"),
+                                 lv.get("global_smoother", "none"), lv.get("ilu_fill", 1), lv.get("hbgs_sweeps", 3))
                   for lv in levels)
-    base = oracle_config(specs)
-    cfg = O.MgrConfig(levels=specs, terminal_cycles=tc, amg_f_relax=base.amg_f_relax, amg_terminal=base.amg_terminal,
-                      f_relax_position=pos)
+    fp, tp = opt.get("f_parts", JACOBI), opt.get("t_parts", JACOBI)
+    cfg = O.MgrConfig(levels=specs, terminal_cycles=tc,
+                      amg_f_relax=O.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=fp),
+                      amg_terminal=O.AmgConfig(strength_threshold=0.25, npartitions=tp),
+                      f_relax_position=pos, npartitions=opt.get("npartitions", 1))
     return pb, O.mgr_setup(problem_csr(pb), pb.field_of, pb.entity_of, cfg)
 
 

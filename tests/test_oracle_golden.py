@@ -124,6 +124,12 @@ def check_problem(tag, pb, h):
             assert dcsr(nxt) == str(d[k + "coarse_sha"])
         if lv.f_relax is not None and lv.f_relax[0] == "amg":
             check_amg(d, k + "amg_", lv.f_relax[1], full)
+        if k + "ilu_ro" in d.files:  # ILU(k) factors of the global smoother, bitwise
+            same_csr(lv.smoother.lu, get_csr(d, k + "ilu"))
+            assert np.array_equal(lv.smoother.dpos, d[k + "ilu_dpos"])
+        if k + "gs_v" in d.files:
+            zs = lv.smoother.apply(d[k + "gs_v"])
+            assert np.array_equal(zs, d[k + "gs_z"]), np.abs(zs - d[k + "gs_z"]).max()
     check_amg(d, "term_", h.terminal, full)
     z = h.apply(d["apply_v"])
     zr = d["apply_z"]
