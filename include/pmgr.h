@@ -46,7 +46,8 @@ typedef enum {
     PMGR_ERR_NOT_SUPPORTED = 6,     /* NotImplementedError (option outside the hot path) */
     PMGR_ERR_OOM = 7,               /* MemoryError                                       */
     PMGR_ERR_INTERP_DIAG = 8,       /* ValueError "direct interpolation requires nonzero diagonals" (amg.py:137-138) */
-    PMGR_ERR_FIELDS = 9             /* ValueError level spec fields vs present fields (mgr.py:338-344) */
+    PMGR_ERR_FIELDS = 9,            /* ValueError level spec fields vs present fields (mgr.py:338-344) */
+    PMGR_ERR_ZERO_PIVOT = 10        /* ZeroPivotError "zero pivot at row N" (smoothers.py:38)           */
 } pmgr_status;
 
 typedef struct pmgr_csr pmgr_csr;     /* device CSR matrix              (CsrMatrix, sparse.py:65)      */
@@ -116,10 +117,12 @@ typedef struct {                 /* MgrLevelSpec (mgr.py:53-83)                 
     int32_t restrict_;           /* PMGR_RESTRICT_*                               */
     int32_t f_relax;             /* PMGR_FRELAX_*                                 */
     int32_t f_relax_sweeps;
-    int32_t global_smoother;     /* PMGR_SMOOTHER_* (only NONE on this path)      */
+    int32_t global_smoother;     /* PMGR_SMOOTHER_* (mgr.py:388-396)               */
     int32_t n_max;               /* < 0: no dropping (n_max=None)                 */
     int32_t quasi_impes;
     int32_t amg_num_functions;   /* F-relax AMG functions (3 when F = {U})        */
+    int32_t ilu_fill;            /* MgrLevelSpec.ilu_fill (ILU(k) level of fill)   */
+    int32_t hbgs_sweeps;         /* MgrLevelSpec.hbgs_sweeps                       */
 } pmgr_level_spec;
 
 typedef struct {                 /* MgrConfig (mgr.py:86-123)                     */
@@ -127,6 +130,8 @@ typedef struct {                 /* MgrConfig (mgr.py:86-123)                   
     int32_t f_relax_post;        /* 0: "pre", 1: "post"                           */
     pmgr_amg_cfg amg_f_relax;
     pmgr_amg_cfg amg_terminal;
+    int64_t npartitions;         /* MgrConfig.npartitions (global smoothers)       */
+    int32_t flow_interleaved;    /* FieldLayout.ordering == FLOW_INTERLEAVED       */
 } pmgr_mgr_cfg;
 
 /* Replaces mgr_setup (mgr.py:329-371).  field_of (int8) / entity_of (int32)
@@ -140,7 +145,8 @@ PMGR_API int pmgr_mgr_num_levels(const pmgr_mgr *h, int32_t *nlevels);
 PMGR_API int pmgr_mgr_level_sizes(const pmgr_mgr *h, int64_t *sizes);
 /* z = mgr_apply(h, v) (mgr.py:399-429), device vectors. */
 PMGR_API int pmgr_mgr_apply(pmgr_mgr *h, const double *v_dev, double *z_dev, void *stream);
-/* Parity export: what = 0 P_l, 1 next coarse operator; returns a new handle. */
+/* Parity export: what = 0 P_l, 1 next coarse operator, 2 the level's ILU(k)
+ * factors (combined L\U, IluFactors.lu); returns a new handle. */
 PMGR_API int pmgr_mgr_export_csr(const pmgr_mgr *h, int32_t level, int32_t what, void *stream,
                         pmgr_csr **out);
 /* what = 0: is_c (int8) of level `level` into host memory. */

@@ -28,6 +28,7 @@ PMGR_ERR_NOT_SUPPORTED = 6
 PMGR_ERR_OOM = 7
 PMGR_ERR_INTERP_DIAG = 8
 PMGR_ERR_FIELDS = 9
+PMGR_ERR_ZERO_PIVOT = 10
 
 INTERP = {"injection_only": 0, "injection_jacobi": 1, "ideal": 2}
 RESTRICT = {"injection": 0, "jacobi": 1, "ideal": 2}
@@ -45,12 +46,13 @@ class LevelSpec(ctypes.Structure):
     _fields_ = [("f_mask", ctypes.c_uint64), ("c_mask", ctypes.c_uint64), ("interp", ctypes.c_int32),
                 ("restrict_", ctypes.c_int32), ("f_relax", ctypes.c_int32), ("f_relax_sweeps", ctypes.c_int32),
                 ("global_smoother", ctypes.c_int32), ("n_max", ctypes.c_int32), ("quasi_impes", ctypes.c_int32),
-                ("amg_num_functions", ctypes.c_int32)]
+                ("amg_num_functions", ctypes.c_int32), ("ilu_fill", ctypes.c_int32), ("hbgs_sweeps", ctypes.c_int32)]
 
 
 class MgrCfg(ctypes.Structure):
     _fields_ = [("terminal_cycles", ctypes.c_int32), ("f_relax_post", ctypes.c_int32),
-                ("amg_f_relax", AmgCfg), ("amg_terminal", AmgCfg)]
+                ("amg_f_relax", AmgCfg), ("amg_terminal", AmgCfg), ("npartitions", ctypes.c_int64),
+                ("flow_interleaved", ctypes.c_int32)]
 
 
 class GmresCfg(ctypes.Structure):
@@ -159,6 +161,8 @@ def check(status: int):
         raise ValueError(msg)
     if status == PMGR_ERR_NOT_SUPPORTED:
         raise NotImplementedError(msg)
+    if status == PMGR_ERR_ZERO_PIVOT:
+        raise ZeroPivotError(int(L.pmgr_last_error_index()))
     if status == PMGR_ERR_OOM:
         raise MemoryError(msg)
     raise RuntimeError(msg)

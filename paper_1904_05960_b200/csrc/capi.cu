@@ -247,6 +247,10 @@ int pmgr_mgr_export_csr(const pmgr_mgr *h, int32_t level, int32_t what, void *st
         auto m = std::make_shared<pmgr::Csr>();
         if (what == 0) {
             pmgr::csr_copy(h->levels[level].P.view(), *m, S(stream));
+        } else if (what == 2) {
+            const auto &g = h->levels[level].smoother;
+            require(g && g->kind == PMGR_SMOOTHER_ILU, "level has no ILU smoother");
+            pmgr::csr_copy(g->lu.view(), *m, S(stream));
         } else {
             const pmgr::Csr &nx = (level + 1 < (int32_t)h->levels.size()) ? *h->levels[level + 1].A : *h->terminal_A;
             pmgr::csr_copy(nx.view(), *m, S(stream));

@@ -671,6 +671,7 @@ std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int
     if (M->f_relax_post || M->terminal_cycles != 1)
         fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports pre F-relaxation and one terminal cycle");
     for (const MgrLevel &L : M->levels) {
+        if (L.smoother) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution of a level with a global smoother");
         if (L.f_relax == PMGR_FRELAX_NONE || L.f_relax_sweeps != 1)
             fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports single-sweep AMG / Jacobi F-relaxation");
     }

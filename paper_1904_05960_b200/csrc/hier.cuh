@@ -94,6 +94,23 @@ bool amg_entry(pmgr_amg &h, double **b, double **x, const double **dtilde);
 // V-cycle from zero once amg_entry's buffers are filled
 void amg_cycle_prefilled(pmgr_amg &h, double *out, cudaStream_t s);
 
+// Level-2 global smoother (smooth.cu; reference mgr.py:275-292)
+struct GlobalSmoother {
+    int kind = 0;  // PMGR_SMOOTHER_ILU / _HBGS
+    int64_t n = 0, nparts = 1;
+    DBuf<int64_t> starts;               // partition boundaries (align 2)
+    Csr lu;                             // ILU(k): combined L\U, unit lower implicit
+    DBuf<int64_t> dpos;                 // diagonal position per row
+    std::shared_ptr<const Csr> A;       // HBGS: the level operator
+    DBuf<double> add, xpre;             // off-partition |a| row sums, sweep copy
+    DBuf<int64_t> cstart, cs, cp;       // cells per partition: s / p rows
+    int nsweeps = 0;
+};
+std::unique_ptr<GlobalSmoother> smoother_build(std::shared_ptr<const Csr> A, int kind, int ilu_fill, int hbgs_sweeps,
+                                               int64_t npartitions, bool interleaved, const int8_t *field_of,
+                                               const int32_t *entity_of, cudaStream_t s);
+void smoother_apply(GlobalSmoother &g, const double *v, double *z, cudaStream_t s);
+
 // One MGR reduction level (reference mgr.py:300-311).
 struct MgrLevel {
     std::shared_ptr<const Csr> A;  // level operator
@@ -108,6 +125,9 @@ struct MgrLevel {
     int32_t f_relax_sweeps = 1;
     std::shared_ptr<const Csr> A_ff;  // for Jacobi sweeps > 1
     std::unique_ptr<pmgr_amg> amg;    // F-relaxation AMG
+    std::unique_ptr<GlobalSmoother> smoother;  // optional global smoother
+    Csr A_c;                          // C rows of A (residual after a global smoother)
+    DBuf<double> zs, rr;              // smoother workspace
     // workspace
     DBuf<double> vf, zf, rc, zc, tmpf;
     // row distribution: owned offsets of the level (M), F and C spaces; halos

@@ -227,6 +227,43 @@ void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
     }
 }
 
+// A level with a global smoother (mgr.py:411-429): z = S v; F-relaxation on
+// the residual v - A z; C residual of the smoothed z; coarse correction.
+void apply_level_smoothed(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s) {
+    MgrLevel &L = h.levels[l];
+    const int64_t n = L.n;
+    smoother_apply(*L.smoother, v, L.zs.p, s);
+    auto f_relax_on = [&](const double *r, double *zacc) {  // zacc[F] += M_FF^{-1} r[F]
+        bool done = false;
+        if (L.f_relax_sweeps == 1) {
+            if (L.f_relax == PMGR_FRELAX_AMG) {
+                done = amg_cycle_rows(*L.amg, r, L.f_rows.p, L.zf.p, s);
+            } else {
+                vec_scale_gather(r, L.f_rows.p, L.dinv_ff.p, L.nf, L.zf.p, s);
+                done = true;
+            }
+        }
+        if (!done) {
+            vec_gather(r, L.f_rows.p, L.nf, L.vf.p, s);
+            f_relax_apply(L, L.vf.p, L.zf.p, s);
+        }
+        k_scatter_add<<<grid_for(L.nf, 256), 256, 0, s>>>(L.zf.p, L.f_rows.p, L.nf, zacc);
+        PMGR_LAUNCHED();
+    };
+    if (!h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
+        spmv_residual(L.A->view(), L.zs.p, v, L.rr.p, s);
+        f_relax_on(L.rr.p, L.zs.p);
+    }
+    spmv_resid_rows(L.A_c.view(), L.zs.p, v, L.c_rows.p, L.rc.p, ResidNext{}, s);
+    apply_level(h, l + 1, L.rc.p, L.zc.p, s, false);
+    vec_copy(L.zs.p, z, n, s);
+    spmv_add(L.P.view(), L.zc.p, z, s);
+    if (h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
+        spmv_residual(L.A->view(), z, v, L.rr.p, s);
+        f_relax_on(L.rr.p, z);
+    }
+}
+
 // prefilled: the producer of v already ran this level's first step (the
 // terminal AMG's l1-Jacobi entry, or a single Jacobi F-relaxation)
 void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s, bool prefilled) {
@@ -243,6 +280,10 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
         return;
     }
     MgrLevel &L = h.levels[l];
+    if (L.smoother) {
+        apply_level_smoothed(h, l, v, z, s);
+        return;
+    }
     const bool pre = !h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE;
     double *rc = L.rc.p;
     bool next_prefilled = false;
@@ -275,7 +316,7 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
             }
         } else {
             MgrLevel &N = h.levels[l + 1];
-            if (N.f_relax == PMGR_FRELAX_JACOBI && N.f_relax_sweeps == 1) {
+            if (N.f_relax == PMGR_FRELAX_JACOBI && N.f_relax_sweeps == 1 && !N.smoother) {
                 nx.sidx = N.f_index.p;
                 nx.sd = N.dinv_ff.p;
                 nx.sz = N.zf.p;
@@ -315,8 +356,26 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
     std::vector<int8_t> fo(field_of_host, field_of_host + A0->nrows);
     std::vector<int32_t> eo(entity_of_host, entity_of_host + A0->nrows);
     std::shared_ptr<const Csr> cur = A0;
+    // FieldLayout ordering: interleaved while every restriction keeps the S/P
+    // pairing, else downgraded (the mgr.py:359 x sparse.py:180-189 shim)
+    bool interleaved = cfg.flow_interleaved != 0;
     for (int li = 0; li < nlevels; ++li) {
         const pmgr_level_spec &sp = specs[li];
+        if (interleaved) {
+            std::vector<int64_t> sv, pv;
+            for (int64_t i = 0; i < (int64_t)fo.size(); ++i) {
+                if (fo[i] == 1) sv.push_back(i);
+                else if (fo[i] == 2) pv.push_back(i);
+            }
+            auto by_ent = [&](std::vector<int64_t> &v) {
+                std::stable_sort(v.begin(), v.end(), [&](int64_t a, int64_t b) { return eo[a] < eo[b]; });
+            };
+            by_ent(sv);
+            by_ent(pv);
+            bool ok = sv.size() == pv.size();
+            for (size_t t = 0; ok && t < sv.size(); ++t) ok = (sv[t] - pv[t] == 1 || pv[t] - sv[t] == 1);
+            if (!ok) interleaved = false;
+        }
         std::set<int> present;
         {
             bool seen[256] = {};
@@ -332,8 +391,9 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             fail(PMGR_ERR_FIELDS, "level spec fields " + field_names(spec_f) + " do not cover the fields present " +
                                       field_names(present));
         if (!sp.c_mask) fail(PMGR_ERR_INVALID, "empty C set: nothing to reduce onto");
-        if (sp.global_smoother != PMGR_SMOOTHER_NONE)
-            fail(PMGR_ERR_NOT_SUPPORTED, "global smoothers (hbgs/ilu) are not on the device path yet");
+        if (sp.global_smoother != PMGR_SMOOTHER_NONE && sp.global_smoother != PMGR_SMOOTHER_ILU &&
+            sp.global_smoother != PMGR_SMOOTHER_HBGS)
+            fail(PMGR_ERR_INVALID, "unknown global smoother");
         if (sp.interp == PMGR_INTERP_IDEAL || sp.restrict_ != PMGR_RESTRICT_INJECTION)
             fail(PMGR_ERR_NOT_SUPPORTED, "only injection restriction with injection/injection_jacobi "
                                          "interpolation is on the device path");
@@ -425,6 +485,16 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         }
         if (sp.f_relax == PMGR_FRELAX_JACOBI && L.f_relax_sweeps > 1) L.A_ff = A_ff;
         setup_trace("mgr F-relax AMG", li, s);
+        // ---- global smoother (_build_global_smoother, mgr.py:388-396)
+        if (sp.global_smoother != PMGR_SMOOTHER_NONE) {
+            L.smoother = smoother_build(cur, sp.global_smoother, sp.ilu_fill, sp.hbgs_sweeps,
+                                        cfg.npartitions > 0 ? cfg.npartitions : 1, interleaved, fo.data(), eo.data(), s);
+            rows_of(Av, L.c_rows.p, L.nc, L.A_c, s);
+            csr_finalize(L.A_c, s);
+            L.zs.alloc(n);
+            L.rr.alloc(n);
+            setup_trace("mgr global smoother", li, s);
+        }
         // ---- coarse operator (build_coarse, mgr.py:212-231)
         auto coarse = std::make_shared<Csr>();
         {

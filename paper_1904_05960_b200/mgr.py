@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from .amg import AmgConfig, AmgHierarchy
-from .sparse import (CfSplitting, CsrMatrix, DeviceCsr, Field, FieldLayout, as_device_csr, back_like,
+from .sparse import (CfSplitting, CsrMatrix, DeviceCsr, Field, FieldLayout, Ordering, as_device_csr, back_like,
                      current_stream, empty_device, ptr, to_device)
 
 __all__ = ["MgrLevelSpec", "MgrConfig", "MgrHierarchy", "mgr_setup", "mgr_apply"]
@@ -77,7 +77,7 @@ class MgrLevelSpec:
         return _lib.LevelSpec(fm, cm, _lib.INTERP[self.interp], _lib.RESTRICT[self.restrict],
                               _lib.FRELAX[self.f_relax], int(self.f_relax_sweeps),
                               _lib.SMOOTHER[self.global_smoother], -1 if self.n_max is None else int(self.n_max),
-                              1 if self.quasi_impes else 0, nfun)
+                              1 if self.quasi_impes else 0, nfun, int(self.ilu_fill), int(self.hbgs_sweeps))
 
 
 @dataclass(frozen=True)
@@ -114,7 +114,7 @@ class MgrConfig:
 
     def to_c(self) -> _lib.MgrCfg:
         return _lib.MgrCfg(max(1, int(self.terminal_cycles)), 1 if self.f_relax_position == "post" else 0,
-                           self.amg_f_relax.to_c(), self.amg_terminal.to_c())
+                           self.amg_f_relax.to_c(), self.amg_terminal.to_c(), int(min(self.npartitions, 2 ** 62)), 0)
 
 
 @dataclass
@@ -155,6 +155,10 @@ class MgrHierarchy:
         s = np.zeros(self._nlev + 1, dtype=np.int64)
         _lib.check(_lib.lib().pmgr_mgr_level_sizes(self._h, s.ctypes.data_as(_lib.c_i64p)))
         return [int(v) for v in s]
+
+    def ilu_factors(self, level: int) -> CsrMatrix:
+        """Combined L\\U factors of the level's ILU(k) global smoother."""
+        return self._export(level, 2)
 
     def _export(self, level, what) -> CsrMatrix:
         out = ctypes.c_void_p()
@@ -223,6 +227,7 @@ def mgr_setup(A, layout: FieldLayout, config: MgrConfig) -> MgrHierarchy:
                        len(set(np.unique(fo).tolist())))
     specs = (_lib.LevelSpec * max(1, len(config.levels)))(*[s.to_c() for s in config.levels])
     cfg = config.to_c()
+    cfg.flow_interleaved = 1 if layout.ordering == Ordering.FLOW_INTERLEAVED else 0
     out = ctypes.c_void_p()
     fo0 = np.ascontiguousarray(layout.field_of, dtype=np.int8)
     eo0 = np.ascontiguousarray(layout.entity_of, dtype=np.int32)

@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests._golden import CASES, VARIANT_SPECS, dcsr, get_csr, load, oracle_config, oracle_levels, vec_sha
+from tests._golden import (CASES, VARIANT_SPECS, dcsr, get_csr, load, oracle_config, oracle_levels, variant_options,
+                           vec_sha)
 
 pytestmark = pytest.mark.gpu
 
@@ -233,7 +234,11 @@ def test_mgr_errors_match_reference(pk):
     with pytest.raises(ValueError, match="fields"):
         mgr.mgr_setup(A, lay, cfg2)
     with pytest.raises(NotImplementedError):
-        mgr.mgr_setup(A, lay, mgr.MgrConfig(levels=(mgr.MgrLevelSpec({F.U}, {F.P}, global_smoother="ilu"),)))
+        mgr.mgr_setup(A, lay, mgr.MgrConfig(levels=(mgr.MgrLevelSpec({F.U}, {F.P}, interp="ideal"),)))
+    # HBGS needs the interleaved flow layout (smoothers.py:135-136)
+    with pytest.raises(ValueError, match="interleaved flow layout"):
+        mgr.mgr_setup(sparse.CsrMatrix.from_dense(np.eye(4)), lay,
+                      mgr.MgrConfig(levels=(mgr.MgrLevelSpec({F.U}, {F.P}, global_smoother="hbgs"),)))
 
 def test_launch_counter_moves(pk):
     from paper_1904_05960_b200 import _lib
@@ -321,15 +326,19 @@ def test_mgr_option_variants(pk, tag):
     sparse, amg, mgr, krylov = pk
     from paper_1904_05960_b200 import problems
 
-    levels, tc, pos = VARIANT_SPECS[tag]
+    levels, tc, pos = VARIANT_SPECS[tag][:3]
+    opt = variant_options(tag)
     pb = problems.make_c2(seed=5, n=6)
     A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
     specs = tuple(mgr.MgrLevelSpec({sparse.Field(t) for t in lv["f"]}, {sparse.Field(t) for t in lv["c"]},
                                    **{k: v for k, v in lv.items() if k not in ("f", "c")}) for lv in levels)
     cfg = mgr.MgrConfig(levels=specs, terminal_cycles=tc, f_relax_position=pos,
-                        amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=JACOBI),
-                        amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=JACOBI))
-    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of), cfg)
+                        npartitions=opt.get("npartitions", 1),
+                        amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3,
+                                                  npartitions=opt.get("f_parts", JACOBI)),
+                        amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=opt.get("t_parts", JACOBI)))
+    order = sparse.Ordering.FLOW_INTERLEAVED if opt.get("interleaved") else sparse.Ordering.FIELD_BLOCKED
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of, order), cfg)
     d = load(tag)
     assert h.level_sizes() == list(d["mgr_sizes"])
     for i, lv in enumerate(h.levels):
@@ -337,6 +346,12 @@ def test_mgr_option_variants(pk, tag):
         assert np.array_equal(lv.split.is_c, d[k + "isc"])
         same_csr(host_csr(lv.P), get_csr(d, k + "P"), k + "P")
         same_csr(host_csr(lv.coarse), get_csr(d, k + "coarse"), k + "coarse")
+        a = h.amg(i)
+        if a is not None:  # hybrid l1-GS partitions change d~ (bitwise)
+            check_amg(d, k + "amg_", a, True)
+        if k + "ilu_ro" in d.files:  # ILU(k) factors bitwise (iluk_symbolic / iluk_numeric)
+            same_csr(host_csr(h.ilu_factors(i)), get_csr(d, k + "ilu"), k + "ilu")
+    check_amg(d, "term_", h.terminal_solver, True)
     z = h.apply(d["apply_v"])
     zr = d["apply_z"]
     assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(zr)
@@ -347,3 +362,4 @@ def test_mgr_option_variants(pk, tag):
     else:
         assert st.iterations == int(d["gmres_iters"])
         assert np.allclose(st.residual_history[:20], d["gmres_hist"][:20], rtol=1e-6)
+
