@@ -101,6 +101,9 @@ struct GlobalSmoother {
     DBuf<int64_t> starts;               // partition boundaries (align 2)
     Csr lu;                             // ILU(k): combined L\U, unit lower implicit
     DBuf<int64_t> dpos;                 // diagonal position per row
+    bool leveled = false;               // substitutions by level schedule
+    DBuf<int32_t> frows, brows;         // rows grouped by forward / backward level
+    std::vector<int64_t> fptr, bptr;    // level boundaries
     std::shared_ptr<const Csr> A;       // HBGS: the level operator
     DBuf<double> add, xpre;             // off-partition |a| row sums, sweep copy
     DBuf<int64_t> cstart, cs, cp;       // cells per partition: s / p rows
