@@ -640,7 +640,12 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
     int64_t total = 0;
     TBuf<int32_t> tci;
     TBuf<double> tv;
-    if (Y.ncols <= DENSE_COLS) {
+    static const int64_t dense_cols = [] {
+        const char *e = getenv("PMGR_DENSE_COLS");
+        const int64_t v = e ? atoll(e) : (int64_t)DENSE_COLS;
+        return v < DENSE_COLS ? v : (int64_t)DENSE_COLS;
+    }();
+    if (Y.ncols <= dense_cols) {
         const int W = (int)((Y.ncols + 31) / 32);
         const size_t fbytes = sizeof(unsigned) * (size_t)((W + 1) & ~1);
         const size_t smem_num = fbytes + sizeof(double) * (size_t)Y.ncols;
