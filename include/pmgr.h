@@ -198,6 +198,25 @@ PMGR_API int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const d
 PMGR_API int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h_dev,
                    double *w_dev, void *stream);
 
+/* ---- on-device assembly ---------------------------
+ * The synthetic poromechanics Jacobian of paper_1904_05960_b200/problems.py
+ * (Q1 elasticity, TPFA flow with upwinded Corey / Stone-I mobilities, Biot
+ * coupling, bottom Dirichlet rows) assembled directly into device CSR from
+ * host per-cell fields (arrays of nz*ny*nx, x fastest; sats nsat x cells)
+ * and the 24x24 unit-E element stiffness / Biot vector; bitwise the host
+ * generator's matrix. */
+typedef struct {
+    int32_t nx, ny, nz;
+    int32_t phases;              /* 1 single, 2 two (s, p), 3 three (s, s2, p)   */
+    double h, V;                 /* cell size and volume h**3 (host-rounded)     */
+    double phi, ct, dt, biot;
+    double mu[3];                /* phase viscosities                            */
+    const double *E, *kx, *ky, *kz, *sats, *pstate;
+    const double *K0;            /* 24 x 24 row-major */
+    const double *bvec;          /* 24 */
+} pmgr_assembly;
+PMGR_API int pmgr_assemble_poromech(const pmgr_assembly *a, void *stream, pmgr_csr **out);
+
 /* ---- row distribution (the reference is single-process) ---
  * Every rank builds the global A / MGR hierarchy on its own GPU (replicated
  * setup), then pmgr_dist_create keeps its rows of every operator.  `bounds`

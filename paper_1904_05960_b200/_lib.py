@@ -64,6 +64,13 @@ class NcclId(ctypes.Structure):
     _fields_ = [("internal", ctypes.c_char * 128)]
 
 
+class Assembly(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32), ("phases", ctypes.c_int32),
+                ("h", ctypes.c_double), ("V", ctypes.c_double), ("phi", ctypes.c_double), ("ct", ctypes.c_double),
+                ("dt", ctypes.c_double), ("biot", ctypes.c_double), ("mu", ctypes.c_double * 3)] + \
+               [(nm, ctypes.c_void_p) for nm in ("E", "kx", "ky", "kz", "sats", "pstate", "K0", "bvec")]
+
+
 class GmresStats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32), ("history_len", ctypes.c_int32),
                 ("restarts", ctypes.c_int32)]
@@ -117,6 +124,7 @@ SIGNATURES = {
     "pmgr_dist_gmres": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.POINTER(GmresCfg),
                                        ctypes.POINTER(GmresStats), vp, ctypes.c_int32, vp]),
     "pmgr_dist_destroy": (ctypes.c_int, [vp]),
+    "pmgr_assemble_poromech": (ctypes.c_int, [ctypes.POINTER(Assembly), vp, ctypes.POINTER(vp)]),
     "pmgr_dist_emulate": (ctypes.c_int, [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, vp, vp,
                                          ctypes.POINTER(GmresCfg), ctypes.POINTER(GmresStats), vp]),
 }

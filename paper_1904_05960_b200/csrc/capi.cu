@@ -437,3 +437,14 @@ int pmgr_dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int
         pmgr::dist_emulate(A, M, bounds, nranks, what, in_dev, out_dev, cfg, stats, S(stream));
     });
 }
+
+// ---------------------------------------------------------------- assembly
+
+int pmgr_assemble_poromech(const pmgr_assembly *a, void *stream, pmgr_csr **out) {
+    return guard([&] {
+        require(a && out && a->E && a->kx && a->ky && a->kz && a->pstate && a->K0 && a->bvec, "NULL argument");
+        require(a->phases == 1 || a->sats, "NULL saturations");
+        init_pool();
+        *out = wrap(pmgr::assemble_poromech(*a, S(stream)));
+    });
+}

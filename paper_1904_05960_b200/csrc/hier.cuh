@@ -94,6 +94,9 @@ bool amg_entry(pmgr_amg &h, double **b, double **x, const double **dtilde);
 // V-cycle from zero once amg_entry's buffers are filled
 void amg_cycle_prefilled(pmgr_amg &h, double *out, cudaStream_t s);
 
+// on-device assembly of the synthetic Jacobian (assemble.cu)
+std::shared_ptr<Csr> assemble_poromech(const pmgr_assembly &a, cudaStream_t s);
+
 // Level-2 global smoother (smooth.cu; reference mgr.py:275-292)
 struct GlobalSmoother {
     int kind = 0;  // PMGR_SMOOTHER_ILU / _HBGS

@@ -386,6 +386,85 @@ def assemble(nx, ny, nz, *, E, kx, ky, kz, phases="single", sats=None,
                    dict(h=h, dt=dt, phases=phases))
 
 
+@dataclass
+class DeviceProblem:
+    """A generated system whose matrix was assembled on the GPU (libpmgr,
+    SURVEY.md §8f row 3): `A` is a sparse.DeviceCsr; layout and rhs on the host."""
+
+    name: str
+    nx: int
+    ny: int
+    nz: int
+    A: object
+    field_of: np.ndarray
+    entity_of: np.ndarray
+    rhs: np.ndarray
+    cell_fields: tuple
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return self.A.nrows
+
+    @property
+    def nnz(self) -> int:
+        return self.A.nnz
+
+    @property
+    def n_u(self) -> int:
+        return 3 * (self.nx + 1) * (self.ny + 1) * (self.nz + 1)
+
+
+def assemble_device(nx, ny, nz, *, E, kx, ky, kz, phases="single", sats=None,
+                    pstate=None, mu=(1.0,), phi=0.2, ct=1e-3, dt=1.0, biot=1.0,
+                    nu=0.25, h=None, rhs_rng=None, name="custom") -> DeviceProblem:
+    """`assemble` with the matrix built on the device (pmgr_assemble_poromech):
+    same arguments, bitwise the same CSR, no host matrix and no host-to-device
+    copy of it (only the per-cell fields travel)."""
+    import ctypes
+
+    from . import _lib
+    from .sparse import DeviceCsr, current_stream
+
+    if h is None:
+        h = 1.0 / max(nx, ny)
+    K0, bvec = element_matrices(h, nu)
+    nph = {"single": 1, "two": 2, "three": 3}[phases]
+    cell_fields = {1: (FIELD_P,), 2: (FIELD_S, FIELD_P), 3: (FIELD_S, FIELD_S2, FIELD_P)}[nph]
+    shape = (nz, ny, nx)
+    arr = lambda a: np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), shape))  # noqa: E731
+    Ea, kxa, kya, kza = arr(E), arr(kx), arr(ky), arr(kz)
+    pa = arr(pstate if pstate is not None else np.zeros(shape))
+    sa = np.ascontiguousarray(sats, dtype=np.float64).reshape(nph - 1, *shape) if nph > 1 else None
+    K0 = np.ascontiguousarray(K0)
+    bvec = np.ascontiguousarray(bvec)
+    a = _lib.Assembly()
+    a.nx, a.ny, a.nz, a.phases = nx, ny, nz, nph
+    a.h, a.V = float(h), float(h ** 3)
+    a.phi, a.ct, a.dt, a.biot = float(phi), float(ct), float(dt), float(biot)
+    for t in range(3):
+        a.mu[t] = float(mu[t]) if t < len(mu) else 1.0
+    a.E, a.kx, a.ky, a.kz = Ea.ctypes.data, kxa.ctypes.data, kya.ctypes.data, kza.ctypes.data
+    a.sats = sa.ctypes.data if sa is not None else None
+    a.pstate, a.K0, a.bvec = pa.ctypes.data, K0.ctypes.data, bvec.ctypes.data
+    out = ctypes.c_void_p()
+    _lib.check(_lib.lib().pmgr_assemble_poromech(ctypes.byref(a), current_stream(), ctypes.byref(out)))
+    nr, nc_, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().pmgr_csr_info(out, ctypes.byref(nr), ctypes.byref(nc_), ctypes.byref(nnz)))
+    A = DeviceCsr(out, nr.value, nc_.value, nnz.value)
+    n_u = 3 * (nx + 1) * (ny + 1) * (nz + 1)
+    ncell = nx * ny * nz
+    nf = len(cell_fields)
+    n = n_u + nf * ncell
+    field_of = np.concatenate([np.full(n_u, FIELD_U, dtype=np.int8),
+                               np.tile(np.array(cell_fields, dtype=np.int8), ncell)])
+    entity_of = np.concatenate([(np.arange(n_u) // 3).astype(np.int32),
+                                np.repeat(np.arange(ncell, dtype=np.int32), nf)])
+    rhs = rhs_rng.standard_normal(n) if rhs_rng is not None else np.zeros(n)
+    return DeviceProblem(name, nx, ny, nz, A, field_of, entity_of, rhs, cell_fields,
+                         dict(h=h, dt=dt, phases=phases, device=True))
+
+
 # ---------------------------------------------------------------------------
 # the BASELINE.json configurations
 # ---------------------------------------------------------------------------
@@ -408,17 +487,17 @@ def _pressure_state(rng, nx, ny, nz, h, noise=0.3):
 _DT_MULTIPHASE = 0.002
 
 
-def make_c1(seed=0, n=16):
+def make_c1(seed=0, n=16, device=False):
     """C1: single-phase Biot on n^3 (BASELINE.json configs[0])."""
     rE, rk, _rs, _rp, rb = _streams(seed)
     E = np.exp(0.5 * rE.standard_normal((n, n, n)))
     k = np.exp(1.0 * rk.standard_normal((n, n, n)))
     p = np.zeros((n, n, n))
-    return assemble(n, n, n, E=E, kx=k, ky=k, kz=k, phases="single", pstate=p,
+    return (assemble_device if device else assemble)(n, n, n, E=E, kx=k, ky=k, kz=k, phases="single", pstate=p,
                     phi=0.2, ct=1e-3, dt=1.0, rhs_rng=rb, name=f"C1-{n}^3")
 
 
-def make_c2(seed=0, n=32):
+def make_c2(seed=0, n=32, device=False):
     """C2: two-phase Corey, mu ratio 10, s ~ U(0.2, 0.8) (configs[1])."""
     rE, rk, rs, rp, rb = _streams(seed)
     E = np.exp(0.5 * rE.standard_normal((n, n, n)))
@@ -426,12 +505,12 @@ def make_c2(seed=0, n=32):
     s = rs.uniform(0.2, 0.8, (1, n, n, n))
     h = 1.0 / n
     p = _pressure_state(rp, n, n, n, h)
-    return assemble(n, n, n, E=E, kx=k, ky=k, kz=k, phases="two", sats=s, pstate=p,
+    return (assemble_device if device else assemble)(n, n, n, E=E, kx=k, ky=k, kz=k, phases="two", sats=s, pstate=p,
                     mu=(1.0, 10.0), phi=0.2, ct=1e-3, dt=_DT_MULTIPHASE, rhs_rng=rb,
                     name=f"C2-{n}^3")
 
 
-def make_c3(seed=0, n=64):
+def make_c3(seed=0, n=64, device=False):
     """C3: layered lognormal sigma=2 (4-cell z-layers, corr 8), kz=0.1 kx,
     E contrast 1e3 between alternating layer pairs (configs[2])."""
     rE, rk, rs, rp, rb = _streams(seed)
@@ -444,12 +523,12 @@ def make_c3(seed=0, n=64):
     s = rs.uniform(0.2, 0.8, (1, n, n, n))
     h = 1.0 / n
     p = _pressure_state(rp, n, n, n, h)
-    return assemble(n, n, n, E=E, kx=kx, ky=kx, kz=kz, phases="two", sats=s, pstate=p,
+    return (assemble_device if device else assemble)(n, n, n, E=E, kx=kx, ky=kx, kz=kz, phases="two", sats=s, pstate=p,
                     mu=(1.0, 10.0), phi=0.2, ct=1e-3, dt=_DT_MULTIPHASE, rhs_rng=rb,
                     name=f"C3-{n}^3")
 
 
-def make_c4(seed=0, n=128):
+def make_c4(seed=0, n=128, device=False):
     """C4: three-phase, Stone-I-like, saturations ~ Dirichlet(2,2,2),
     perm sigma=1.5 (configs[3])."""
     rE, rk, rs, rp, rb = _streams(seed)
@@ -459,12 +538,12 @@ def make_c4(seed=0, n=128):
     sats = np.stack([d[..., 0], d[..., 1]])
     h = 1.0 / n
     p = _pressure_state(rp, n, n, n, h)
-    return assemble(n, n, n, E=E, kx=k, ky=k, kz=k, phases="three", sats=sats, pstate=p,
+    return (assemble_device if device else assemble)(n, n, n, E=E, kx=k, ky=k, kz=k, phases="three", sats=sats, pstate=p,
                     mu=(1.0, 0.2, 5.0), phi=0.2, ct=1e-3, dt=_DT_MULTIPHASE, rhs_rng=rb,
                     name=f"C4-{n}^3")
 
 
-def make_c5(seed=0, nxy=128, nz_per_gpu=128, gpus=1):
+def make_c5(seed=0, nxy=128, nz_per_gpu=128, gpus=1, device=False):
     """C5: weak-scaling slab stack nxy x nxy x (nz_per_gpu * gpus) (configs[4]).
 
     The random fields are drawn for the global grid, so a slab does not depend
@@ -477,7 +556,7 @@ def make_c5(seed=0, nxy=128, nz_per_gpu=128, gpus=1):
     s = rs.uniform(0.2, 0.8, (1, nz, nxy, nxy))
     h = 1.0 / nxy
     p = _pressure_state(rp, nxy, nxy, nz, h)
-    return assemble(nxy, nxy, nz, E=E, kx=k, ky=k, kz=k, phases="two", sats=s, pstate=p,
+    return (assemble_device if device else assemble)(nxy, nxy, nz, E=E, kx=k, ky=k, kz=k, phases="two", sats=s, pstate=p,
                     mu=(1.0, 10.0), phi=0.2, ct=1e-3, dt=_DT_MULTIPHASE, rhs_rng=rb,
                     name=f"C5-{nxy}x{nxy}x{nz}")
 
