@@ -54,10 +54,10 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def workload(cfg_name, seed):
+def workload(cfg_name, seed, device=False):
     from paper_1904_05960_b200 import problems
 
-    pb = problems.make(cfg_name, seed=seed)
+    pb = problems.make(cfg_name, seed=seed, device=device)
     if pb.cell_fields == (problems.FIELD_P,):
         levels = [("amg", {0}, {2}, None)]
     elif len(pb.cell_fields) == 3:
@@ -319,7 +319,8 @@ def run_gpu(args, rank, world, local_rank):
 
     from paper_1904_05960_b200 import _lib, amg, krylov, mgr, sparse
 
-    pb, levels = workload(args.config, args.seed)
+    device_asm = args.config not in ("C1", "C2")  # large systems: assemble on the GPU (problems.py, bitwise)
+    pb, levels = workload(args.config, args.seed, device=device_asm)
     F = sparse.Field
     specs = tuple(mgr.MgrLevelSpec({F(t) for t in f}, {F(t) for t in c}, f_relax=relax, n_max=nm)
                   for relax, f, c, nm in levels)
@@ -327,8 +328,11 @@ def run_gpu(args, rank, world, local_rank):
                         amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=10 ** 9),
                         amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=10 ** 9))
     stream = torch.cuda.current_stream()
-    A = sparse.DeviceCsr.from_arrays(pb.n, pb.n, torch.from_numpy(pb.row_offsets).cuda(),
-                                     torch.from_numpy(pb.col_indices).cuda(), torch.from_numpy(pb.values).cuda())
+    if device_asm:
+        A = pb.A
+    else:
+        A = sparse.DeviceCsr.from_arrays(pb.n, pb.n, torch.from_numpy(pb.row_offsets).cuda(),
+                                         torch.from_numpy(pb.col_indices).cuda(), torch.from_numpy(pb.values).cuda())
     lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
     b = torch.from_numpy(pb.rhs).cuda()
     gcfg = krylov.GmresConfig(restart=args.restart, max_iters=1000, rtol=args.rtol)
@@ -466,7 +470,7 @@ def run_gpu(args, rank, world, local_rank):
         return
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not device_asm:
         os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
         setup_c, solve_c = oracle_solve(pb, levels, args.restart, args.rtol)
         tc, its_c, _ = solve_c()
