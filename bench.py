@@ -202,7 +202,8 @@ def run_gpu_dist(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    base = problems.make_c5(seed=args.seed, nxy=32, nz_per_gpu=32, gpus=world)
+    # the global slab stack assembled on the GPU and renumbered rank-major there
+    base = problems.make_c5(seed=args.seed, nxy=32, nz_per_gpu=32, gpus=world, device=True)
     pb, bounds = problems.rank_major(base, world)
     del base
     _, levels = workload("C2", args.seed)
@@ -213,8 +214,7 @@ def run_gpu_dist(args, rank, world, local_rank):
                         amg_f_relax=amg.AmgConfig(strength_threshold=0.5, num_functions=3, npartitions=10 ** 9),
                         amg_terminal=amg.AmgConfig(strength_threshold=0.25, npartitions=10 ** 9))
     stream = torch.cuda.current_stream()
-    A = sparse.DeviceCsr.from_arrays(pb.n, pb.n, torch.from_numpy(pb.row_offsets).cuda(),
-                                     torch.from_numpy(pb.col_indices).cuda(), torch.from_numpy(pb.values).cuda())
+    A = pb.A
     lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

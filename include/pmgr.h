@@ -74,6 +74,9 @@ PMGR_API int pmgr_csr_info(const pmgr_csr *A, int64_t *nrows, int64_t *ncols, in
 PMGR_API int pmgr_csr_download(const pmgr_csr *A, int64_t *row_offsets, int32_t *col_indices,
                       double *values, int to_device, void *stream);
 /* y = A x, replaces sparse.matvec (sparse.py:261-266). */
+/* B = P A P^T for a host permutation (row i of B = row perm[i] of A, columns
+ * renumbered and sorted): problems.rank_major on the device. */
+PMGR_API int pmgr_csr_permute(const pmgr_csr *A, const int64_t *perm_host, void *stream, pmgr_csr **out);
 PMGR_API int pmgr_spmv(const pmgr_csr *A, const double *x_dev, double *y_dev, void *stream);
 
 /* ---- classical AMG (amg.py) -------------------------------------------- */

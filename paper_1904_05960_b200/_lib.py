@@ -88,6 +88,7 @@ SIGNATURES = {
     "pmgr_csr_info": (ctypes.c_int, [vp, c_i64p, c_i64p, c_i64p]),
     "pmgr_csr_download": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, vp]),
     "pmgr_spmv": (ctypes.c_int, [vp, vp, vp, vp]),
+    "pmgr_csr_permute": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(vp)]),
     "pmgr_amg_setup": (ctypes.c_int, [vp, ctypes.POINTER(AmgCfg), vp, ctypes.POINTER(vp)]),
     "pmgr_amg_destroy": (ctypes.c_int, [vp]),
     "pmgr_amg_num_levels": (ctypes.c_int, [vp, c_i32p]),

@@ -448,3 +448,10 @@ int pmgr_assemble_poromech(const pmgr_assembly *a, void *stream, pmgr_csr **out)
         *out = wrap(pmgr::assemble_poromech(*a, S(stream)));
     });
 }
+
+int pmgr_csr_permute(const pmgr_csr *A, const int64_t *perm_host, void *stream, pmgr_csr **out) {
+    return guard([&] {
+        require(A && perm_host && out, "NULL argument");
+        *out = wrap(pmgr::csr_permute(*A->m, perm_host, S(stream)));
+    });
+}

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -244,6 +245,8 @@ struct Csr {
 // and pcol columns are node-blocked by 3 (prow = nrows, pcol = ncols: pure
 // BSR3); keeps the plain CSR when the blocks would be too sparse (unless force)
 void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force = false);
+// B = P A P^T (row i of B = row perm[i] of A), columns re-sorted
+std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_host, cudaStream_t s);
 
 // record the longest row of a finished operator (setup time, synchronises)
 void csr_finalize(Csr &A, cudaStream_t s);

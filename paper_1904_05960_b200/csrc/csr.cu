@@ -798,3 +798,58 @@ int64_t csr_diag_inverse(const CsrView &A, double *dinv, cudaStream_t s) {
 }
 
 }  // namespace pmgr
+
+namespace pmgr {
+namespace {
+__global__ void k_perm_count(int64_t n, const int64_t *ro, const int64_t *perm, int64_t *cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) cnt[i] = ro[perm[i] + 1] - ro[perm[i]];
+}
+__global__ void k_perm_fill(int64_t n, const int64_t *ro, const int32_t *ci, const double *v, const int64_t *perm,
+                            const int64_t *inv, const int64_t *nro, int32_t *nci, double *nv) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t r = perm[i];
+    int64_t w = nro[i];
+    for (int64_t q = ro[r]; q < ro[r + 1]; ++q, ++w) {
+        nci[w] = (int32_t)inv[ci[q]];
+        nv[w] = v[q];
+    }
+}
+}  // namespace
+
+// B = P A P^T: row i of B is row perm[i] of A, columns renumbered by the
+// inverse permutation and re-sorted (problems.rank_major on the device)
+std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_h, cudaStream_t s) {
+    if (A.nrows != A.ncols) fail(PMGR_ERR_INVALID, "permutation needs a square matrix");
+    const int64_t n = A.nrows;
+    std::vector<int64_t> inv_h(n, -1);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = perm_h[i];
+        if (p < 0 || p >= n || inv_h[p] >= 0) fail(PMGR_ERR_INVALID, "not a permutation", i);
+        inv_h[p] = i;
+    }
+    TBuf<int64_t> perm(n, s), inv(n, s), cnt(n, s);
+    PMGR_CUDA(cudaMemcpyAsync(perm.p, perm_h, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    PMGR_CUDA(cudaMemcpyAsync(inv.p, inv_h.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    auto B = std::make_shared<Csr>();
+    B->nrows = B->ncols = n;
+    B->ro.alloc(n + 1);
+    if (n > 0) {
+        k_perm_count<<<grid_for(n, 256), 256, 0, s>>>(n, A.ro.p, perm.p, cnt.p);
+        PMGR_LAUNCHED();
+    }
+    B->nnz = exclusive_scan_total(cnt.p, B->ro.p, n, s);
+    B->ci.alloc(B->nnz);
+    B->v.alloc(B->nnz);
+    if (n > 0) {
+        k_perm_fill<<<grid_for(n, 256), 256, 0, s>>>(n, A.ro.p, A.ci.p, A.v.p, perm.p, inv.p, B->ro.p, B->ci.p,
+                                                     B->v.p);
+        PMGR_LAUNCHED();
+    }
+    segmented_sort_pairs(B->ci.p, B->v.p, B->nnz, B->ro.p, n, s);
+    csr_finalize(*B, s);
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    return B;
+}
+}  // namespace pmgr

@@ -791,6 +791,7 @@ void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const
                 pmgr_gmres_stats &st, double *history, int32_t history_cap, cudaStream_t s) {
     D.ensure_work();
     SplitOps ops;
+    ops.cache = &D.gws;
     ops.n = D.n_own;
     ops.vin = D.ve.p + D.off;
     ops.w = D.we.p + D.off;

@@ -33,6 +33,7 @@ struct DistSolver {
     std::vector<std::shared_ptr<Halo>> halos;
     std::vector<int> spaces;
     DBuf<double> ve, ze, we;            // ext workspaces of the level-0 space
+    std::shared_ptr<SplitWs> gws;       // GMRES workspace / captured step
     void ensure_work();
 };
 

@@ -193,7 +193,9 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
 // GMRES over row-distributed vectors: the caller provides w = A M vin for
 // the owned slices (halo exchanges inside), the owned-slice operators for the
 // restart update and the cross-rank all-reduce (dist.cu)
+struct SplitWs;  // persistent GMRES workspace + captured step (krylov.cu)
 struct SplitOps {
+    std::shared_ptr<SplitWs> *cache = nullptr;  // caller-owned slot, reused across solves
     int64_t n = 0;          // owned rows
     double *vin = nullptr;  // owned slice the preconditioner reads
     double *w = nullptr;    // owned slice the operator writes

@@ -859,6 +859,22 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
 // one host synchronisation per step to read the device state.
 // ---------------------------------------------------------------------------
 
+struct SplitWs {
+    int m = 0, max_iters = 0;
+    int64_t n = 0, ldv = 0, chunk = 0;
+    int nblk = 0, nparts = 0;
+    DBuf<double> V, r, u, z, t, H, G, cs, sn, g, a, h, y, hist, pa, pg, pn, red, nrm2, beta;
+    DBuf<Dev> dev;
+    Dev *hdev = nullptr;
+    cudaGraphExec_t exec = nullptr;  // one captured Arnoldi step
+    bool captured = false;
+    int64_t graph_kernels = 0;
+    ~SplitWs() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (hdev) cudaFreeHost(hdev);
+    }
+};
+
 void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, const pmgr_gmres_cfg &cfg,
                  pmgr_gmres_stats &stats, double *history, int32_t history_cap, cudaStream_t s) {
     if (cfg.restart < 1) fail(PMGR_ERR_INVALID, "restart must be >= 1");
@@ -867,19 +883,51 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
     const int64_t n = ops.n;
     const int m = cfg.restart;
     const int max_iters = cfg.max_iters > 0 ? cfg.max_iters : 0;
-    const int64_t ldv = (n + 31) / 32 * 32 + 32;
-    const int nblk = 2 * num_sms();
-    const int64_t chunk = ((n + nblk - 1) / nblk + 31) / 32 * 32;
-    const int nparts = 4 * num_sms();
-    DBuf<double> V((int64_t)(m + 1) * ldv), r(ldv), u(ldv), z(ldv), t(ldv), H((int64_t)(m + 1) * m),
-        G((int64_t)(m + 1) * (m + 1)), cs(m + 1), sn(m + 1), g(m + 2), a(m + 1), h(m + 1), y(m + 1),
-        hist((int64_t)max_iters + 2), pa((int64_t)(m + 1) * nblk), pg((int64_t)(m + 1) * nblk),
-        pn(nparts > nblk ? nparts : nblk), red(2 * (int64_t)(m + 1)), nrm2(1), beta(1);
-    DBuf<Dev> dev(1);
-    Dev *hdev = nullptr;
-    PMGR_CUDA(cudaMallocHost((void **)&hdev, sizeof(Dev)));
-    std::unique_ptr<Dev, void (*)(Dev *)> hold(hdev, [](Dev *p) { cudaFreeHost(p); });
-    PMGR_CUDA(cudaMemsetAsync(red.p, 0, sizeof(double) * red.n, s));
+    // workspace (and the captured step graph) persist across solves in the caller's slot
+    std::shared_ptr<SplitWs> &slot = *ops.cache;
+    if (!slot || slot->m != m || slot->max_iters != max_iters || slot->n != n) {
+        auto w = std::make_shared<SplitWs>();
+        w->m = m;
+        w->max_iters = max_iters;
+        w->n = n;
+        w->ldv = (n + 31) / 32 * 32 + 32;
+        w->nblk = 2 * num_sms();
+        w->chunk = ((n + w->nblk - 1) / w->nblk + 31) / 32 * 32;
+        w->nparts = 4 * num_sms();
+        const int64_t ldv = w->ldv;
+        w->V.alloc((int64_t)(m + 1) * ldv);
+        w->r.alloc(ldv);
+        w->u.alloc(ldv);
+        w->z.alloc(ldv);
+        w->t.alloc(ldv);
+        w->H.alloc((int64_t)(m + 1) * m);
+        w->G.alloc((int64_t)(m + 1) * (m + 1));
+        w->cs.alloc(m + 1);
+        w->sn.alloc(m + 1);
+        w->g.alloc(m + 2);
+        w->a.alloc(m + 1);
+        w->h.alloc(m + 1);
+        w->y.alloc(m + 1);
+        w->hist.alloc((int64_t)max_iters + 2);
+        w->pa.alloc((int64_t)(m + 1) * w->nblk);
+        w->pg.alloc((int64_t)(m + 1) * w->nblk);
+        w->pn.alloc(w->nparts > w->nblk ? w->nparts : w->nblk);
+        w->red.alloc(2 * (int64_t)(m + 1));
+        w->nrm2.alloc(1);
+        w->beta.alloc(1);
+        w->dev.alloc(1);
+        PMGR_CUDA(cudaMallocHost((void **)&w->hdev, sizeof(Dev)));
+        PMGR_CUDA(cudaMemsetAsync(w->red.p, 0, sizeof(double) * w->red.n, s));
+        slot = w;
+    }
+    SplitWs &W = *slot;
+    const int64_t ldv = W.ldv, chunk = W.chunk;
+    const int nblk = W.nblk, nparts = W.nparts;
+    DBuf<double> &V = W.V, &r = W.r, &u = W.u, &z = W.z, &t = W.t, &H = W.H, &G = W.G, &cs = W.cs, &sn = W.sn,
+                 &g = W.g, &a = W.a, &h = W.h, &y = W.y, &hist = W.hist, &pa = W.pa, &pg = W.pg, &pn = W.pn,
+                 &red = W.red, &nrm2 = W.nrm2, &beta = W.beta;
+    DBuf<Dev> &dev = W.dev;
+    Dev *hdev = W.hdev;
 
     auto gnorm = [&](const double *v, double *out) {  // out = ||v|| over all ranks
         k_norm_partial<<<nparts, DOT_BLOCK, 0, s>>>(v, n, pn.p);
@@ -937,10 +985,12 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
         PMGR_LAUNCHED();
     };
     // one captured graph per step when the transport can be captured (NCCL;
-    // a device-side WHILE loop around NCCL calls measured 20x slower)
-    cudaGraphExec_t exec = nullptr, cycle = nullptr;
-    int64_t graph_kernels = 0;
-    if (!cycle && ops.capturable && use_cycle_graphs()) {
+    // a device-side WHILE loop around NCCL calls measured 20x slower);
+    // captured once per workspace
+    if (!W.captured && ops.capturable && use_cycle_graphs()) {
+        W.captured = true;
+        int64_t &graph_kernels = W.graph_kernels;
+        cudaGraphExec_t &exec = W.exec;
         cudaStream_t cap;
         PMGR_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
         cudaGraph_t graph = nullptr;
@@ -961,12 +1011,8 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
         PMGR_CUDA(cudaGraphDestroy(graph));
         PMGR_CUDA(cudaStreamDestroy(cap));
     }
-    struct ExecGuard {
-        cudaGraphExec_t e;
-        ~ExecGuard() {
-            if (e) cudaGraphExecDestroy(e);
-        }
-    } eg{exec}, eg2{cycle};
+    cudaGraphExec_t exec = W.exec, cycle = nullptr;
+    const int64_t graph_kernels = W.graph_kernels;
 
     std::vector<double> hl;
     if (!nonzero_x0 && n > 0) PMGR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));

@@ -592,6 +592,20 @@ def rank_major(pb: Problem, nranks: int):
     n = pb.n
     if len(perm) != n:
         raise AssertionError("rank-major permutation does not cover the dofs")
+    if isinstance(pb, DeviceProblem):  # permute the device matrix in place on the GPU
+        import ctypes
+
+        from . import _lib
+        from .sparse import DeviceCsr, current_stream
+
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        out = ctypes.c_void_p()
+        _lib.check(_lib.lib().pmgr_csr_permute(pb.A.handle, perm.ctypes.data, current_stream(), ctypes.byref(out)))
+        A = DeviceCsr(out, pb.A.nrows, pb.A.ncols, pb.A.nnz)
+        new = DeviceProblem(pb.name + f"-rm{nranks}", pb.nx, pb.ny, pb.nz, A, pb.field_of[perm],
+                            pb.entity_of[perm], pb.rhs[perm], pb.cell_fields,
+                            dict(pb.meta, rank_bounds=list(bounds), perm=perm))
+        return new, np.array(bounds, dtype=np.int64)
     inv = np.empty(n, dtype=np.int64)
     inv[perm] = np.arange(n)
     ro = pb.row_offsets

@@ -55,3 +55,16 @@ def test_device_assembled_system_solves(pk):
     x2, st2 = krylov.gmres(A, h2.apply, host.rhs, cfg=krylov.GmresConfig(restart=100, max_iters=400))
     assert st.converged and st.iterations == st2.iterations
     assert np.array_equal(x, x2)
+
+
+@pytest.mark.parametrize("nranks", [1, 3])
+def test_device_rank_major_matches_host(pk, nranks):
+    problems, sparse = pk
+    host, b1 = problems.rank_major(problems.make("C2", seed=4, n=6), nranks)
+    dev, b2 = problems.rank_major(problems.make("C2", seed=4, n=6, device=True), nranks)
+    assert np.array_equal(b1, b2)
+    H = dev.A.to_host()
+    assert np.array_equal(H.row_offsets, host.row_offsets)
+    assert np.array_equal(H.col_indices, host.col_indices)
+    assert np.array_equal(H.values, host.values)
+    assert np.array_equal(dev.field_of, host.field_of) and np.array_equal(dev.rhs, host.rhs)
