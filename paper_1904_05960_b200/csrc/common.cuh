@@ -212,6 +212,10 @@ struct CsrView {
     const int64_t *rro = nullptr;
     const int32_t *rci = nullptr;
     const double *rv = nullptr;
+    // rows longer than long_len (> 0) are summed by a whole block each (the
+    // nlong rows listed in lrows); the lane group then fits the other rows
+    int64_t long_len = 0, nlong = 0;
+    const int32_t *lrows = nullptr;
 };
 
 struct Csr {
@@ -235,9 +239,12 @@ struct Csr {
     DBuf<int64_t> bro, rro;
     DBuf<int32_t> bci, rci;
     DBuf<double> bval, rv;
+    int64_t long_len = 0, nlong = 0;
+    DBuf<int32_t> lrows;
     CsrView view() const {
-        return CsrView{nrows,  ncols,   nnz,  ro.p,  ci.p,  v.p,    maxrow, row_off, lanes,
-                       ci16.p, nbrows, nblocks, nrem, bro.p, bci.p, bval.p, rro.p, rci.p, rv.p};
+        return CsrView{nrows,  ncols,  nnz,     ro.p,  ci.p,  v.p,    maxrow, row_off,  lanes, ci16.p,
+                       nbrows, nblocks, nrem,   bro.p, bci.p, bval.p, rro.p,  rci.p,    rv.p,  long_len,
+                       nlong,  lrows.p};
     }
 };
 
@@ -250,6 +257,8 @@ std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_host, cudaStr
 
 // record the longest row of a finished operator (setup time, synchronises)
 void csr_finalize(Csr &A, cudaStream_t s);
+// list the rows longer than A.long_len (0: none) for the block-per-row path
+void csr_long_rows(Csr &A, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // warp helpers
@@ -382,6 +391,8 @@ void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf,
 void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,
                const double *b, double *x, double *xpre, bool forward, cudaStream_t s);
 int spmv_lanes(const CsrView &A);
+// lane group per row for a mean row length (no skew correction)
+int spmv_lanes_mean(double mean);
 // y[0:nrows) = M[0:nrows, 0:ncols) x (row-distributed collapsed operators)
 void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld, const double *x, double *y,
                        cudaStream_t s);

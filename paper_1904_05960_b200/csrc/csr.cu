@@ -448,6 +448,33 @@ __global__ void k_maxrow(int64_t n, const int64_t *ro, unsigned long long *out) 
 }  // namespace
 
 namespace {
+__global__ void k_long_flag(int64_t n, const int64_t *ro, int64_t len, int32_t *flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = (ro[i + 1] - ro[i]) > len ? 1 : 0;
+}
+__global__ void k_long_fill(int64_t n, const int32_t *flag, const int64_t *pos, int32_t *lrows) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) lrows[pos[i]] = (int32_t)i;
+}
+}  // namespace
+
+void csr_long_rows(Csr &A, cudaStream_t s) {
+    A.nlong = 0;
+    A.lrows.release();
+    if (A.long_len <= 0 || A.nrows == 0) return;
+    TBuf<int32_t> flag(A.nrows, s);
+    TBuf<int64_t> pos(A.nrows + 1, s);
+    k_long_flag<<<grid_for(A.nrows, 256), 256, 0, s>>>(A.nrows, A.ro.p, A.long_len, flag.p);
+    PMGR_LAUNCHED();
+    const int64_t nl = exclusive_scan_total_i32(flag.p, pos.p, A.nrows, s);
+    if (nl == 0) return;
+    A.lrows.alloc(nl);
+    k_long_fill<<<grid_for(A.nrows, 256), 256, 0, s>>>(A.nrows, flag.p, pos.p, A.lrows.p);
+    PMGR_LAUNCHED();
+    A.nlong = nl;
+}
+
+namespace {
 __global__ void k_to16(int64_t nnz, const int32_t *ci, uint16_t *c16) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q < nnz) c16[q] = (uint16_t)ci[q];
@@ -465,6 +492,16 @@ void csr_finalize(Csr &A, cudaStream_t s) {
     k_maxrow<<<g < 1024 ? g : 1024, 256, 0, s>>>(A.nrows, A.ro.p, m.p);
     PMGR_LAUNCHED();
     A.maxrow = (int64_t)read_scalar(m.p, s);
+    // skewed operators (a few dense coarse-grid rows next to short ones): the
+    // long rows get a block each, the lane group fits the mean
+    static const bool no_long = getenv("PMGR_NO_LONG_ROWS") && getenv("PMGR_NO_LONG_ROWS")[0] != '0';
+    if (!no_long) {
+        const int gm = spmv_lanes_mean((double)A.nnz / (double)A.nrows);
+        if (A.maxrow > 16 * gm) {
+            A.long_len = 16 * gm;
+            csr_long_rows(A, s);
+        }
+    }
     // narrow column indices for the solve-phase SpMV (10 instead of 12 bytes per entry)
     static const bool no16 = getenv("PMGR_NO_CI16") && getenv("PMGR_NO_CI16")[0] != '0';
     if (!no16 && A.ncols <= 65536 && A.nnz > 0) {
@@ -472,6 +509,11 @@ void csr_finalize(Csr &A, cudaStream_t s) {
         k_to16<<<grid_for(A.nnz, 256), 256, 0, s>>>(A.nnz, A.ci.p, A.ci16.p);
         PMGR_LAUNCHED();
     }
+    static const bool stats = getenv("PMGR_HIER_STATS") && getenv("PMGR_HIER_STATS")[0] != '0';
+    if (stats)
+        fprintf(stderr, "[pmgr] operator %lld x %lld nnz %lld (%.1f/row, max %lld, long rows %lld > %lld)\n",
+                (long long)A.nrows, (long long)A.ncols, (long long)A.nnz, (double)A.nnz / (double)A.nrows,
+                (long long)A.maxrow, (long long)A.nlong, (long long)A.long_len);
 }
 
 namespace {

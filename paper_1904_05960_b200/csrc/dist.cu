@@ -554,6 +554,9 @@ struct Builder {
         csr_finalize(out, s);
         out.row_off = R->off();
         out.lanes = spmv_lanes(Y.view());
+        // the same rows take the block-per-row path as in the global operator
+        out.long_len = Y.long_len;
+        csr_long_rows(out, s);
         // a pure block operator keeps its blocks (same blocks, same order as the
         // global copy); a block-prefix operator (A0 on the original layout)
         // is sliced as CSR

@@ -39,16 +39,54 @@ __device__ __forceinline__ int ldc(const uint16_t *p) {
 template <int G, bool STREAM, class Op, class IT>
 __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
                                               const IT *__restrict__ ci,
-                                              const double *__restrict__ v, Op op, int64_t row_off, int trigger) {
+                                              const double *__restrict__ v, Op op, int64_t row_off, int trigger,
+                                              int64_t long_len, const int32_t *__restrict__ lrows,
+                                              unsigned nshort) {
     pdl_wait();
     if (trigger) pdl_trigger();
+    if (blockIdx.x >= nshort) {
+        // a long row: the whole block, four independent load chains per
+        // thread, then a fixed-order reduction (warps, then the 8 warp sums)
+        __shared__ double ws[8];
+        const int64_t row = __ldg(lrows + (blockIdx.x - nshort));
+        const int64_t b = __ldg(ro + row), e = __ldg(ro + row + 1);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t q = b + threadIdx.x;
+        for (; q + 768 < e; q += 1024) {
+            const double v0 = ldv<STREAM>(v + q), v1 = ldv<STREAM>(v + q + 256), v2 = ldv<STREAM>(v + q + 512),
+                         v3 = ldv<STREAM>(v + q + 768);
+            const int c0 = ldc<STREAM>(ci + q), c1 = ldc<STREAM>(ci + q + 256), c2 = ldc<STREAM>(ci + q + 512),
+                      c3 = ldc<STREAM>(ci + q + 768);
+            s0 = fma(v0, op.x(c0), s0);
+            s1 = fma(v1, op.x(c1), s1);
+            s2 = fma(v2, op.x(c2), s2);
+            s3 = fma(v3, op.x(c3), s3);
+        }
+        for (; q < e; q += 256) s0 = fma(ldv<STREAM>(v + q), op.x(ldc<STREAM>(ci + q)), s0);
+        double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) t += ws[w];
+            op.out(row + row_off, t);
+        }
+        return;
+    }
     const int lane = threadIdx.x & (G - 1);
     const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-    const bool active = row < nrows;
+    bool active = row < nrows;
     int64_t b = 0, e = 0;
     if (active) {
         b = __ldg(ro + row);
         e = __ldg(ro + row + 1);
+        if (long_len > 0 && e - b > long_len) {  // summed by its own block
+            active = false;
+            e = b;
+        }
     }
     // two independent accumulators keep two (value, column, x) load chains
     // in flight per lane; matrix streams use evict-first loads so the
@@ -220,16 +258,18 @@ struct OpProlong {
 template <int G, class Op, class IT>
 void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_t s) {
     const int block = 256;
-    const unsigned grid = grid_for(A.nrows * G, block);
+    const unsigned nshort = grid_for(A.nrows * G, block);
+    const int64_t nlong = A.long_len > 0 ? A.nlong : 0;
+    const unsigned grid = nshort + (unsigned)nlong;
     // let the next kernel's launch overlap this one only when this grid is a
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
     if (stream)
         launch_pdl(k_spmv<G, true, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
-                   trigger);
+                   trigger, A.long_len, A.lrows, nshort);
     else
         launch_pdl(k_spmv<G, false, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
-                   trigger);
+                   trigger, A.long_len, A.lrows, nshort);
 }
 
 template <int G, class Op>
@@ -242,19 +282,21 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
 
 // lane group per row the CSR kernel picks for A (row-distributed copies of an
 // operator reuse the global choice so their per-row sums are bitwise equal)
-int spmv_lanes(const CsrView &A) {
-    double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
-    // skewed rows (a few dense coarse-grid rows next to short ones) get a
-    // whole warp, otherwise the longest row serialises its lane group
-    if (A.maxrow >= 0) {
-        int g = mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= 160.0 ? 16 : 32;
-        if (A.maxrow > 16 * g) mean = 1e9;
-    }
+int spmv_lanes_mean(double mean) {
     static const double g32_mean = [] {
         const char *e = getenv("PMGR_SPMV_G32_MEAN");
         return e ? atof(e) : 100.0;
     }();
     return mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= g32_mean ? 16 : 32;
+}
+
+int spmv_lanes(const CsrView &A) {
+    double mean = A.nrows ? (double)A.nnz / (double)A.nrows : 0.0;
+    // skewed rows (a few dense coarse-grid rows next to short ones) get a
+    // whole warp unless they have the block-per-row path, otherwise the
+    // longest row serialises its lane group
+    if (A.maxrow >= 0 && A.long_len <= 0 && A.maxrow > 16 * spmv_lanes_mean(mean)) mean = 1e9;
+    return spmv_lanes_mean(mean);
 }
 
 namespace {
