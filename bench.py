@@ -413,6 +413,18 @@ def run_gpu(args, rank, world, local_rank):
                       "avg_us": (ms.value * 1e3 / c.value) if c.value else None,
                       "gbs": (by.value / (ms.value / 1e3) / 1e9) if ms.value > 0 and by.value > 0 else None}
     L.pmgr_prof_enable(0)
+    # SURVEY 8(d)'s algorithmic bytes of an Arnoldi step, 8 n (2 (j+1) + 5): the
+    # basis read for the projections and again for the update.  The library
+    # records the compulsory bytes 8 n ((j+1) + 4) (the basis once: the update
+    # pass re-reads it from L2 when it fits); both are reported.
+    o = prof["cgs2_step"]
+    if o["launches"]:
+        comp = o["bytes_total"]
+        o["bytes_total_compulsory"] = comp
+        o["gbs_compulsory"] = o["gbs"]
+        o["bytes_total"] = 2.0 * comp - 24.0 * pb.n * o["launches"]
+        o["gbs"] = o["bytes_total"] / (o["ms_total"] / 1e3) / 1e9 if o["ms_total"] > 0 else None
+        o["bytes_rule"] = "8 n (2 (j+1) + 5) per step (SURVEY 8(d)); *_compulsory: 8 n ((j+1) + 4)"
 
     mean = statistics.mean(times)
     t_max = mean
@@ -461,8 +473,13 @@ def run_gpu(args, rank, world, local_rank):
         roof = {"kernel": dom, "bound": "hbm", "achieved": d["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": d["gbs"] / peak, "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
                 "bytes_per_launch": d["bytes_total"] / d["launches"], "avg_launch_us": d["avg_us"],
+                "bytes_rule": d.get("bytes_rule", "SURVEY 8(d)"),
                 "traffic": traffic, "traffic_source": "profiles/roofline_traffic.json (ncu --set full, "
                                                        "dram__bytes_read.sum + dram__bytes_write.sum)"}
+
+    if roof and prof[dom].get("gbs_compulsory"):
+        roof["achieved_compulsory"] = prof[dom]["gbs_compulsory"]
+        roof["frac_compulsory"] = prof[dom]["gbs_compulsory"] / peak
 
     if rank != 0:
         if dist is not None:

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
 // contiguous values feeding the three row sums, 76 B per 9 entries instead
 // of CSR's 108 B.  Remainder entries (coupling columns, rows past the
 // prefix) are read as CSR by three 10-lane groups, one per row.
-template <class Op>
+template <class Op, bool STREAM = false>
 __global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
                                               const int32_t *__restrict__ bci, const double *__restrict__ bval,
                                               const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
@@ -134,10 +134,10 @@ __global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t
             for (int t = 0; t < 3; ++t) {
                 const int64_t k = kb + kk + 10 * t;
                 const bool ok = lane < 30 && k < k1;
-                cc[t] = ok ? __ldg(bci + k) : -1;
+                cc[t] = ok ? ldc<STREAM>(bci + k) : -1;
                 const double *p = bval + 9 * k + 3 * c;
 #pragma unroll
-                for (int r = 0; r < 3; ++r) vv[t][r] = ok ? __ldg(p + r) : 0.0;
+                for (int r = 0; r < 3; ++r) vv[t][r] = ok ? ldv<STREAM>(p + r) : 0.0;
             }
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
@@ -158,12 +158,12 @@ __global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t
             double t0 = 0.0, t1 = 0.0;
             int64_t q = __ldg(rro + row) + gl;
             for (; q + 10 < q1; q += 20) {
-                const double v0 = __ldg(rv + q), v1 = __ldg(rv + q + 10);
-                const int c0 = __ldg(rci + q), c1 = __ldg(rci + q + 10);
+                const double v0 = ldv<STREAM>(rv + q), v1 = ldv<STREAM>(rv + q + 10);
+                const int c0 = ldc<STREAM>(rci + q), c1 = ldc<STREAM>(rci + q + 10);
                 t0 = fma(v0, op.x(c0), t0);
                 t1 = fma(v1, op.x(c1), t1);
             }
-            if (q < q1) t0 = fma(__ldg(rv + q), op.x(__ldg(rci + q)), t0);
+            if (q < q1) t0 = fma(ldv<STREAM>(rv + q), op.x(ldc<STREAM>(rci + q)), t0);
             const double t = t0 + t1;
             if (g == 0) a0 += t;
             else if (g == 1) a1 += t;
@@ -308,8 +308,18 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
         const int64_t ntrip = A.rro ? (A.nrows + 2) / 3 : A.nbrows;
         const unsigned grid = grid_for(ntrip * 32, 256);
         const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
-        launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval, A.rro,
-                   A.rci, A.rv, op, A.row_off, trigger);
+        // PMGR_BSR_STREAM: evict-first loads for block-prefix operators with a
+        // remainder (the Krylov operator A0: read once per iteration) = 1, for all = 2
+        static const int bstream = [] {
+            const char *e = getenv("PMGR_BSR_STREAM");
+            return e ? atoi(e) : 0;
+        }();
+        if (bstream == 2 || (bstream == 1 && A.rro != nullptr))
+            launch_pdl(k_bsr3<Op, true>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
+                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+        else
+            launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
+                       A.rro, A.rci, A.rv, op, A.row_off, trigger);
         PMGR_LAUNCHED();
         return;
     }
@@ -357,7 +367,7 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
 // columns, so a lane's x element is loaded once and reused for the 8 rows
 // whose 8 independent matrix loads are in flight together.  PAIR: ld even,
 // 16-byte loads of column pairs.
-template <bool PAIR>
+template <bool PAIR, bool STREAM = false>
 __global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t nrows, int64_t n, int64_t ld,
                                                       const double *__restrict__ x, double *__restrict__ y) {
     pdl_wait();
@@ -376,7 +386,8 @@ __global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__
             double2 m[RB];
 #pragma unroll
             for (int r = 0; r < RB; ++r)
-                m[r] = r < nr ? __ldg(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + p)
+                m[r] = r < nr ? (STREAM ? __ldcs(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + p)
+                                        : __ldg(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + p))
                               : make_double2(0.0, 0.0);
 #pragma unroll
             for (int r = 0; r < RB; ++r) acc[r] = fma(m[r].y, xv.y, fma(m[r].x, xv.x, acc[r]));
@@ -535,7 +546,12 @@ void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld
                        cudaStream_t s) {
     if (nrows == 0) return;
     const unsigned blocks = (unsigned)((nrows + 7) / 8);
-    if (ld % 2 == 0)
+    // the collapsed operators are read once per cycle: evict-first loads keep
+    // the sparse levels' operators (read again on the way up) in L2
+    static const bool stream = !(getenv("PMGR_DENSE_STREAM") && getenv("PMGR_DENSE_STREAM")[0] == '0');
+    if (ld % 2 == 0 && stream)
+        launch_pdl(k_dense_matvec<true, true>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+    else if (ld % 2 == 0)
         launch_pdl(k_dense_matvec<true>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
     else
         launch_pdl(k_dense_matvec<false>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
