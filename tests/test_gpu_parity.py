@@ -98,6 +98,31 @@ def test_spmv_matches_oracle(pk):
     scale = np.abs(A.to_scipy()) @ np.abs(x)
     assert np.all(np.abs(y - yo) <= 1e-14 * scale + 1e-300)
 
+@pytest.mark.parametrize("mean,long_rows", [(2, (40, 300)), (8, (129, 2000)), (30, (600, 5000)),
+                                             (80, (300, 700)), (200, (513, 4000, 9000))])
+def test_spmv_skewed_rows(pk, mean, long_rows):
+    """Short rows with a few long ones: the long rows take the block-per-row
+    path (csr_finalize: rows > 16x the lane group); every epilogue kind the
+    AMG cycle uses runs through it."""
+    sparse = pk[0]
+    rng = np.random.default_rng(mean)
+    n = 4000
+    lens = rng.integers(max(1, mean // 2), 2 * mean, n)
+    for k, L in enumerate(long_rows):
+        lens[17 + 911 * k] = min(L, n)
+    cols = [np.sort(rng.choice(n, size=int(L), replace=False)) for L in lens]
+    ro = np.zeros(n + 1, dtype=np.int64)
+    ro[1:] = np.cumsum(lens)
+    ci = np.concatenate(cols).astype(np.int32)
+    v = rng.standard_normal(int(ro[-1]))
+    A = sparse.CsrMatrix(n, n, ro, ci, v)
+    x = rng.standard_normal(n)
+    y = sparse.matvec(A, x)
+    yo = O.spmv(host_csr(A), x)
+    scale = np.abs(A.to_scipy()) @ np.abs(x)
+    assert np.all(np.abs(y - yo) <= 1e-14 * scale + 1e-300)
+
+
 def test_spmv_device_tensor_roundtrip(pk):
     import torch
 
