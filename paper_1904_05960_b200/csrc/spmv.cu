@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
 // contiguous values feeding the three row sums, 76 B per 9 entries instead
 // of CSR's 108 B.  Remainder entries (coupling columns, rows past the
 // prefix) are read as CSR by three 10-lane groups, one per row.
-template <class Op, bool STREAM = false>
-__global__ void __launch_bounds__(256) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
+template <class Op, bool STREAM = false, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
                                               const int32_t *__restrict__ bci, const double *__restrict__ bval,
                                               const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
                                               const double *__restrict__ rv, Op op, int64_t row_off, int trigger) {
@@ -314,7 +314,15 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
             const char *e = getenv("PMGR_BSR_STREAM");
             return e ? atoi(e) : 0;
         }();
-        if (bstream == 2 || (bstream == 1 && A.rro != nullptr))
+        // full occupancy (32 registers, a few spilled to L1) beats 40 registers at 75 %
+        static const int minb = [] {
+            const char *e = getenv("PMGR_BSR_MINB");
+            return e ? atoi(e) : 8;
+        }();
+        if (minb == 8)
+            launch_pdl(k_bsr3<Op, false, 8>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
+                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+        else if (bstream == 2 || (bstream == 1 && A.rro != nullptr))
             launch_pdl(k_bsr3<Op, true>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
                        A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
         else
