@@ -375,11 +375,11 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
 // columns, so a lane's x element is loaded once and reused for the 8 rows
 // whose 8 independent matrix loads are in flight together.  PAIR: ld even,
 // 16-byte loads of column pairs.
-template <bool PAIR, bool STREAM = false>
+template <bool PAIR, bool STREAM = false, int RB = 8>
 __global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t nrows, int64_t n, int64_t ld,
                                                       const double *__restrict__ x, double *__restrict__ y) {
     pdl_wait();
-    constexpr int RB = 8, W = 8;
+    constexpr int W = 8;
     __shared__ double red[W][RB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = (int64_t)blockIdx.x * RB;
@@ -553,16 +553,30 @@ void dense_matvec(const double *M, int64_t n, int64_t ld, const double *x, doubl
 void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld, const double *x, double *y,
                        cudaStream_t s) {
     if (nrows == 0) return;
-    const unsigned blocks = (unsigned)((nrows + 7) / 8);
     // the collapsed operators are read once per cycle: evict-first loads keep
     // the sparse levels' operators (read again on the way up) in L2
     static const bool stream = !(getenv("PMGR_DENSE_STREAM") && getenv("PMGR_DENSE_STREAM")[0] == '0');
-    if (ld % 2 == 0 && stream)
-        launch_pdl(k_dense_matvec<true, true>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
-    else if (ld % 2 == 0)
-        launch_pdl(k_dense_matvec<true>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
-    else
-        launch_pdl(k_dense_matvec<false>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+    static const int rb = [] {
+        const char *e = getenv("PMGR_DENSE_RB");
+        return e ? atoi(e) : 8;
+    }();
+    const unsigned blocks = (unsigned)((nrows + rb - 1) / rb);
+    if (ld % 2 == 0 && stream) {
+        if (rb == 4)
+            launch_pdl(k_dense_matvec<true, true, 4>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+        else if (rb == 2)
+            launch_pdl(k_dense_matvec<true, true, 2>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+        else if (rb == 16)
+            launch_pdl(k_dense_matvec<true, true, 16>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+        else
+            launch_pdl(k_dense_matvec<true, true, 8>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+    } else if (ld % 2 == 0) {
+        const unsigned b8 = (unsigned)((nrows + 7) / 8);
+        launch_pdl(k_dense_matvec<true>, dim3(b8), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+    } else {
+        const unsigned b8 = (unsigned)((nrows + 7) / 8);
+        launch_pdl(k_dense_matvec<false>, dim3(b8), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+    }
     PMGR_LAUNCHED();
 }
 
