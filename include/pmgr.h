@@ -239,6 +239,18 @@ PMGR_API int pmgr_transport_nccl_create(const pmgr_nccl_id *id, int32_t rank, in
 PMGR_API int pmgr_transport_destroy(pmgr_transport *t);
 PMGR_API int pmgr_dist_create(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t rank,
                               int32_t nranks, pmgr_transport *t, void *stream, pmgr_dist **out);
+/* Distributed setup (replaces mgr_setup, mgr.py:329-371, when the rows are
+ * spread over ranks): A_rows is this rank's rows [bounds[rank],
+ * bounds[rank+1]) of the rank-major global matrix, in the GLOBAL row space
+ * (every other row empty); field_of / entity_of are the global layout.
+ * Every rank calls it.  Each rank sets up the owned rows of every operator
+ * (bitwise equal to the single-GPU rows: strength, MIS rounds with status
+ * exchanges, interpolation, Galerkin products over fetched ghost rows) and
+ * the coarse levels below PMGR_DIST_REPLICATE_ROWS (20000) redundantly. */
+PMGR_API int pmgr_dist_setup(const pmgr_csr *A_rows, const int8_t *field_of, const int32_t *entity_of,
+                             const pmgr_level_spec *levels, int32_t nlevels, const pmgr_mgr_cfg *cfg,
+                             const int64_t *bounds, int32_t rank, int32_t nranks, pmgr_transport *t, void *stream,
+                             pmgr_dist **out);
 /* global index of the first owned row and the number of owned rows */
 PMGR_API int pmgr_dist_info(const pmgr_dist *d, int64_t *lo, int64_t *n_own);
 /* owned slices (n_own doubles) in and out */
@@ -254,6 +266,13 @@ PMGR_API int pmgr_dist_destroy(pmgr_dist *d);
 PMGR_API int pmgr_dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t nranks,
                                int32_t what, const double *in_dev, double *out_dev,
                                const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, void *stream);
+/* Same, with the distributed setup (pmgr_dist_setup) run by the emulated
+ * ranks from their row slices of the global A. */
+PMGR_API int pmgr_dist_setup_emulate(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                                     const pmgr_level_spec *levels, int32_t nlevels, const pmgr_mgr_cfg *mcfg,
+                                     const int64_t *bounds, int32_t nranks, int32_t what, const double *in_dev,
+                                     double *out_dev, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats,
+                                     void *stream);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 
+#include "dsetup.cuh"
 #include "hier.cuh"
 
 namespace pmgr {
@@ -97,10 +98,10 @@ __device__ __forceinline__ bool earlier(int32_t mu, int64_t u, int32_t mv, int64
 }
 
 // one round of lexicographically-first MIS; status 0 undecided, 1 C, 2 F
-__global__ void k_mis_round(int64_t n, const int64_t *__restrict__ sro, const int32_t *__restrict__ sci,
+__global__ void k_mis_round(int64_t lo, int64_t n, const int64_t *__restrict__ sro, const int32_t *__restrict__ sci,
                             const int64_t *__restrict__ tro, const int32_t *__restrict__ tci,
                             const int32_t *__restrict__ meas, int8_t *status, int *undecided) {
-    int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
     volatile int8_t *st = status;
     if (st[v] != 0) return;
@@ -142,11 +143,11 @@ __global__ void k_cindex(int64_t n, const int8_t *is_c, const int64_t *scan, int
 }
 
 // direct interpolation pass 1: per-row alpha and entry count (warp per row)
-__global__ void k_interp_count(int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
+__global__ void k_interp_count(int64_t lo, int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
                                const double *__restrict__ v, const uint8_t *__restrict__ strong,
                                const int8_t *__restrict__ is_c, const int32_t *__restrict__ funcs,
                                double *alpha, double *diag, int64_t *cnt, int *zero_diag, int *flagged) {
-    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t i = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
     if (i >= n) return;
     const int64_t b = ro[i], e = ro[i + 1];
@@ -201,12 +202,12 @@ __global__ void k_interp_count(int64_t n, const int64_t *__restrict__ ro, const 
 }
 
 // direct interpolation pass 2: fill P (warp per row)
-__global__ void k_interp_fill(int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
+__global__ void k_interp_fill(int64_t lo, int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
                               const double *__restrict__ v, const uint8_t *__restrict__ strong,
                               const int8_t *__restrict__ is_c, const int64_t *__restrict__ cidx,
                               const double *__restrict__ alpha, const double *__restrict__ diag,
                               const int64_t *__restrict__ pro, int32_t *pci, double *pv) {
-    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t i = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
     if (i >= n) return;
     int64_t w = pro[i];
@@ -239,10 +240,10 @@ __global__ void k_interp_fill(int64_t n, const int64_t *__restrict__ ro, const i
 }
 
 // l1 diagonal: a_ii + seq sum over off-partition |a_ij| (warp per row)
-__global__ void k_l1diag(int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
+__global__ void k_l1diag(int64_t lo0, int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci,
                          const double *__restrict__ v, int64_t nparts, const int64_t *__restrict__ starts,
                          int jacobi, double *dt, unsigned long long *bad) {
-    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t i = lo0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
     if (i >= n) return;
     int64_t lo = i, hi = i + 1;
@@ -286,6 +287,11 @@ __global__ void k_l1diag(int64_t n, const int64_t *__restrict__ ro, const int32_
         dt[i] = r;
         if (r == 0.0) atomicMin(bad, (unsigned long long)i);
     }
+}
+
+__global__ void k_meas_from_ro(int64_t lo, int64_t hi, const int64_t *ro, int32_t *meas) {
+    const int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < hi) meas[i] = (int32_t)(ro[i + 1] - ro[i]);
 }
 
 __global__ void k_gather_i32(const int32_t *src, const int64_t *cidx, int64_t n, int32_t *dst) {
@@ -472,7 +478,8 @@ std::vector<int64_t> partition_starts(int64_t n, int64_t nparts) {
 
 }  // namespace
 
-std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_amg_cfg &cfg, cudaStream_t s) {
+std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_amg_cfg &cfg, cudaStream_t s,
+                                    const DistSetup *dist) {
     if (A0->nrows != A0->ncols) fail(PMGR_ERR_INVALID, "amg_setup requires a square matrix");
     if (!(cfg.strength_threshold >= 0.0 && cfg.strength_threshold < 1.0))
         fail(PMGR_ERR_INVALID, "strength_threshold must be in [0, 1)");
@@ -481,6 +488,20 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
     h->cfg = cfg;
     const int nfun = cfg.num_functions > 0 ? cfg.num_functions : 1;
     std::shared_ptr<const Csr> cur = A0;
+    // distributed setup (dsetup.cuh): operators hold the owned rows of their
+    // global row space; small levels are gathered and built on every rank
+    std::unique_ptr<DistSetup> dd;
+    if (dist && dist->nranks > 1) dd.reset(new DistSetup(*dist));
+    auto replicate = [&](bool force) {
+        if (dd && (force || cur->nrows <= dd->replicate_below)) {
+            auto full = std::make_shared<Csr>();
+            ds_gather_rows(*dd, *cur, *full, s);
+            csr_finalize(*full, s);
+            cur = full;
+            dd.reset();
+        }
+    };
+    replicate(false);
     TBuf<int32_t> funcs(cur->nrows, s);
     if (cur->nrows) {
         k_funcs_init<<<grid_for(cur->nrows, 256), 256, 0, s>>>(funcs.p, cur->nrows, nfun);
@@ -489,6 +510,7 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
     while (cur->nrows > cfg.coarse_size_cutoff && (int64_t)h->levels.size() < (int64_t)cfg.max_levels - 1) {
         const CsrView Av = cur->view();
         const int64_t n = Av.nrows;
+        const int64_t rlo = dd ? dd->lo() : 0, rhi = dd ? dd->hi() : n, nown = rhi - rlo;
         // ---- strength
         TBuf<uint8_t> mask(Av.nnz, s);
         TBuf<int64_t> scnt(n, s), sro(n + 1, s);
@@ -513,6 +535,29 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         TBuf<int32_t> tci(snnz, s);
         k_transpose_pattern<<<grid_for(n, 256), 256, 0, s>>>(n, sro.p, sci.p, cursor.p, tci.p);
         PMGR_LAUNCHED();
+        const int64_t *trop = tro.p;
+        const int32_t *tcip = tci.p;
+        Csr ST;
+        if (dd) {
+            // my rows' strong entries, by column, assembled at the columns'
+            // owners: every owned point gets its full in-neighbourhood
+            Csr STl;
+            STl.nrows = STl.ncols = n;
+            STl.nnz = snnz;
+            STl.ro.alloc(n + 1);
+            STl.ci.alloc(snnz);
+            PMGR_CUDA(cudaMemcpyAsync(STl.ro.p, tro.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+            if (snnz) PMGR_CUDA(cudaMemcpyAsync(STl.ci.p, tci.p, sizeof(int32_t) * snnz, cudaMemcpyDeviceToDevice, s));
+            ds_rows_to_owners(*dd, STl, ST, s);
+            PMGR_CUDA(cudaMemsetAsync(meas.p, 0, sizeof(int32_t) * n, s));
+            if (nown > 0) {
+                k_meas_from_ro<<<grid_for(nown, 256), 256, 0, s>>>(rlo, rhi, ST.ro.p, meas.p);
+                PMGR_LAUNCHED();
+            }
+            ds_gather_segment(*dd, meas.p, sizeof(int32_t), s);
+            trop = ST.ro.p;
+            tcip = ST.ci.p;
+        }
         setup_trace("amg measure+transpose", (int64_t)h->levels.size(), s);
         // ---- lexicographically-first MIS rounds
         TBuf<int8_t> status(n, s);
@@ -520,10 +565,17 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         PMGR_CUDA(cudaMemsetAsync(status.p, 0, n, s));
         for (int round = 0;; ++round) {
             PMGR_CUDA(cudaMemsetAsync(undec.p, 0, sizeof(int), s));
-            k_mis_round<<<grid_for(n, 256), 256, 0, s>>>(n, sro.p, sci.p, tro.p, tci.p, meas.p, status.p,
-                                                         undec.p);
-            PMGR_LAUNCHED();
-            if (read_scalar(undec.p, s) == 0) break;
+            if (nown > 0) {
+                k_mis_round<<<grid_for(nown, 256), 256, 0, s>>>(rlo, rhi, sro.p, sci.p, trop, tcip, meas.p,
+                                                                 status.p, undec.p);
+                PMGR_LAUNCHED();
+            }
+            int64_t left = read_scalar(undec.p, s);
+            if (dd) {
+                ds_gather_segment(*dd, status.p, 1, s);
+                left = ds_allsum(*dd, left, s);
+            }
+            if (left == 0) break;
             if (round > 100000) fail(PMGR_ERR_CUDA, "MIS rounds did not terminate");
         }
         AmgLevel lev;
@@ -541,12 +593,20 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         TBuf<int64_t> pcnt(n, s);
         TBuf<int> flags(2, s);
         PMGR_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 2, s));
-        k_interp_count<<<grid_for(n * 32, 256), 256, 0, s>>>(n, Av.ro, Av.ci, Av.v, mask.p, lev.is_c.p, funcs.p,
-                                                             alpha.p, diag.p, pcnt.p, flags.p, flags.p + 1);
-        PMGR_LAUNCHED();
+        PMGR_CUDA(cudaMemsetAsync(pcnt.p, 0, sizeof(int64_t) * n, s));
+        if (nown > 0) {
+            k_interp_count<<<grid_for(nown * 32, 256), 256, 0, s>>>(rlo, rhi, Av.ro, Av.ci, Av.v, mask.p,
+                                                                    lev.is_c.p, funcs.p, alpha.p, diag.p, pcnt.p,
+                                                                    flags.p, flags.p + 1);
+            PMGR_LAUNCHED();
+        }
         int hflags[2];
         PMGR_CUDA(cudaMemcpyAsync(hflags, flags.p, sizeof(hflags), cudaMemcpyDeviceToHost, s));
         PMGR_CUDA(cudaStreamSynchronize(s));
+        if (dd) {
+            hflags[0] = (int)ds_allsum(*dd, hflags[0], s);
+            hflags[1] = (int)ds_allsum(*dd, hflags[1], s);
+        }
         if (hflags[0]) fail(PMGR_ERR_INTERP_DIAG, "direct interpolation requires nonzero diagonals");
         h->flagged += hflags[1];
         lev.P.nrows = n;
@@ -555,25 +615,53 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         lev.P.nnz = exclusive_scan_total(pcnt.p, lev.P.ro.p, n, s);
         lev.P.ci.alloc(lev.P.nnz);
         lev.P.v.alloc(lev.P.nnz);
-        k_interp_fill<<<grid_for(n * 32, 256), 256, 0, s>>>(n, Av.ro, Av.ci, Av.v, mask.p, lev.is_c.p, cidx.p,
-                                                            alpha.p, diag.p, lev.P.ro.p, lev.P.ci.p, lev.P.v.p);
-        PMGR_LAUNCHED();
+        if (nown > 0) {
+            k_interp_fill<<<grid_for(nown * 32, 256), 256, 0, s>>>(rlo, rhi, Av.ro, Av.ci, Av.v, mask.p, lev.is_c.p,
+                                                                   cidx.p, alpha.p, diag.p, lev.P.ro.p, lev.P.ci.p,
+                                                                   lev.P.v.p);
+            PMGR_LAUNCHED();
+        }
         setup_trace("amg interpolation", (int64_t)h->levels.size(), s);
         // ---- Galerkin (P^T A) P, zero dropping after each product
-        csr_finalize(lev.P, s);
-        csr_transpose(lev.P.view(), lev.R, s);
-        csr_finalize(lev.R, s);
-        Csr T1;
-        spgemm(lev.R.view(), Av, 0, T1, s);
+        ds_finalize(dd.get(), lev.P, s);
         auto next = std::make_shared<Csr>();
-        spgemm(T1.view(), lev.P.view(), 0, *next, s);
-        csr_finalize(*next, s);
+        std::vector<int64_t> cstart;
+        if (!dd) {
+            csr_transpose(lev.P.view(), lev.R, s);
+            csr_finalize(lev.R, s);
+            Csr T1;
+            spgemm(lev.R.view(), Av, 0, T1, s);
+            spgemm(T1.view(), lev.P.view(), 0, *next, s);
+            csr_finalize(*next, s);
+        } else {
+            // R = P^T: my fine rows' entries assembled at the coarse owners
+            // (pieces in rank order = ascending fine index, as csr_transpose
+            // orders them); rows of A and P behind the products' middle
+            // indices fetched from their owners
+            cstart = ds_sub_bounds(dd->start, lev.is_c.p, n, true, s);
+            const DistSetup dc = dd->with(cstart);
+            Csr Rp;
+            csr_transpose(lev.P.view(), Rp, s);
+            ds_rows_to_owners(dc, Rp, lev.R, s);
+            ds_finalize(&dc, lev.R, s);
+            Csr Aext, T1, Pext;
+            ds_fetch_rows(*dd, *cur, ds_cols_outside(lev.R, dc.lo(), dc.hi(), rlo, rhi, s), Aext, s);
+            spgemm(lev.R.view(), Aext.view(), 0, T1, s);
+            ds_fetch_rows(*dd, lev.P, ds_cols_outside(T1, dc.lo(), dc.hi(), rlo, rhi, s), Pext, s);
+            spgemm(T1.view(), Pext.view(), 0, *next, s);
+            ds_finalize(&dc, *next, s);
+        }
         setup_trace("amg Galerkin", (int64_t)h->levels.size(), s);
+        static const bool dstats = getenv("PMGR_HIER_STATS") && getenv("PMGR_HIER_STATS")[0] != '0';
+        if (dd && dstats)
+            fprintf(stderr, "[pmgr] rank %d distributed AMG level %d: %lld rows (own %lld) -> %lld\n", dd->rank,
+                    (int)h->levels.size(), (long long)n, (long long)nown, (long long)nc);
         // ---- l1 diagonal with the contiguous partitions
         lev.jacobi = cfg.npartitions >= n;
         lev.dtilde.alloc(n);
         std::vector<int64_t> st;
         if (!lev.jacobi) {
+            if (dd) fail(PMGR_ERR_NOT_SUPPORTED, "distributed setup needs l1-Jacobi AMG levels (npartitions >= n)");
             st = partition_starts(n, cfg.npartitions);
             lev.nparts = (int64_t)st.size() - 1;
             lev.jacobi = lev.nparts == n;  // one row per partition anyway
@@ -584,12 +672,19 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         }
         TBuf<unsigned long long> bad(1, s);
         PMGR_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), s));
-        k_l1diag<<<grid_for(n * 32, 256), 256, 0, s>>>(n, Av.ro, Av.ci, Av.v, lev.nparts,
-                                                       lev.jacobi ? nullptr : lev.starts.p, lev.jacobi ? 1 : 0,
-                                                       lev.dtilde.p, bad.p);
-        PMGR_LAUNCHED();
-        unsigned long long b = read_scalar(bad.p, s);
-        if (b != ~0ull) fail(PMGR_ERR_L1_VANISHES, "l1 diagonal vanishes at row " + std::to_string(b), (int64_t)b);
+        if (nown > 0) {
+            k_l1diag<<<grid_for(nown * 32, 256), 256, 0, s>>>(rlo, rhi, Av.ro, Av.ci, Av.v, lev.nparts,
+                                                              lev.jacobi ? nullptr : lev.starts.p, lev.jacobi ? 1 : 0,
+                                                              lev.dtilde.p, bad.p);
+            PMGR_LAUNCHED();
+        }
+        const unsigned long long b = read_scalar(bad.p, s);
+        int64_t bi = b == ~0ull ? -1 : (int64_t)b;
+        if (dd) {  // the first vanishing row over all ranks
+            const int64_t g = ds_allmax(*dd, bi < 0 ? INT64_MIN : -bi, s);
+            bi = g == INT64_MIN ? -1 : -g;
+        }
+        if (bi >= 0) fail(PMGR_ERR_L1_VANISHES, "l1 diagonal vanishes at row " + std::to_string(bi), bi);
         setup_trace("amg l1 diagonal", (int64_t)h->levels.size(), s);
         // ---- next level functions
         TBuf<int32_t> nfuncs(nc, s);
@@ -605,7 +700,12 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         if (!lev.jacobi) lev.xpre.alloc(n);
         h->levels.push_back(std::move(lev));
         cur = next;
+        if (dd) {
+            dd->start = cstart;
+            replicate(false);
+        }
     }
+    replicate(true);
     const int64_t nc = cur->nrows;
     if (nc > DENSE_SOLVE_CAP)
         fail(PMGR_ERR_DENSE_CAP, "coarsest AMG level of size " + std::to_string(nc) + " is too large for a dense solve");

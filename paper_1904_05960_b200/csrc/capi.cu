@@ -438,6 +438,41 @@ int pmgr_dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int
     });
 }
 
+int pmgr_dist_setup(const pmgr_csr *A_rows, const int8_t *field_of, const int32_t *entity_of,
+                    const pmgr_level_spec *levels, int32_t nlevels, const pmgr_mgr_cfg *cfg, const int64_t *bounds,
+                    int32_t rank, int32_t nranks, pmgr_transport *t, void *stream, pmgr_dist **out) {
+    return guard([&] {
+        require(A_rows && field_of && entity_of && cfg && bounds && out, "NULL argument");
+        require(nlevels >= 0 && (nlevels == 0 || levels), "bad level list");
+        require(nranks == 1 || t, "a transport is required for more than one rank");
+        init_pool();
+        auto *d = new pmgr_dist;
+        try {
+            d->d = pmgr::dist_setup(A_rows, field_of, entity_of, levels, nlevels, *cfg, bounds, rank, nranks,
+                                    t ? t->t.get() : nullptr, S(stream));
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
+int pmgr_dist_setup_emulate(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                            const pmgr_level_spec *levels, int32_t nlevels, const pmgr_mgr_cfg *mcfg,
+                            const int64_t *bounds, int32_t nranks, int32_t what, const double *in_dev, double *out_dev,
+                            const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, void *stream) {
+    return guard([&] {
+        require(A && field_of && entity_of && mcfg && bounds && in_dev && out_dev, "NULL argument");
+        require(nlevels >= 0 && (nlevels == 0 || levels), "bad level list");
+        require(what == 0 || (cfg && stats), "NULL argument");
+        require(nranks >= 1, "nranks must be positive");
+        init_pool();
+        pmgr::dist_setup_emulate(A, field_of, entity_of, levels, nlevels, *mcfg, bounds, nranks, what, in_dev, out_dev,
+                                 cfg, stats, S(stream));
+    });
+}
+
 // ---------------------------------------------------------------- assembly
 
 int pmgr_assemble_poromech(const pmgr_assembly *a, void *stream, pmgr_csr **out) {

@@ -97,12 +97,17 @@ void cycle_block(pmgr_amg &h, size_t l, int64_t k, const double *B, double *XO, 
 
 }  // namespace
 
-void collapse_tail(pmgr_amg &h, cudaStream_t s) {
+int64_t collapse_limit() {
     static const int64_t limit = [] {
         const char *e = getenv("PMGR_COLLAPSE_ROWS");
         const int64_t v = e ? atoll(e) : (int64_t)3584;  // <= ~100 MB dense, read once per cycle
         return v < 65535 ? v : (int64_t)65535;
     }();
+    return limit;
+}
+
+void collapse_tail(pmgr_amg &h, cudaStream_t s) {
+    const int64_t limit = collapse_limit();
     if (limit <= 0 || h.levels.empty()) return;
     // deepest contiguous run of l1-Jacobi levels, starting at the first level
     // small enough for a dense operator

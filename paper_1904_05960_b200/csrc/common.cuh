@@ -251,7 +251,9 @@ struct Csr {
 // build the block-prefix solve copy of an operator whose leading prow rows
 // and pcol columns are node-blocked by 3 (prow = nrows, pcol = ncols: pure
 // BSR3); keeps the plain CSR when the blocks would be too sparse (unless force)
-void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force = false);
+struct DistSetup;
+void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force = false,
+                   const DistSetup *dist = nullptr);
 // B = P A P^T (row i of B = row perm[i] of A), columns re-sorted
 std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_host, cudaStream_t s);
 

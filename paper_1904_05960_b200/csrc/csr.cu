@@ -18,6 +18,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
+#include "dsetup.cuh"
 
 namespace pmgr {
 
@@ -591,7 +592,7 @@ __global__ void k_rem_fill(int64_t n, int64_t prow, int32_t prefix, const int64_
 }
 }  // namespace
 
-void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force) {
+void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force, const DistSetup *dist) {
     static const bool off = getenv("PMGR_NO_BSR") && getenv("PMGR_NO_BSR")[0] != '0';
     if (off || prow % 3 != 0 || pcol % 3 != 0 || prow <= 0 || prow > A.nrows || pcol > A.ncols) return;
     const int64_t nb = prow / 3, n = A.nrows;
@@ -608,8 +609,14 @@ void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool forc
     A.rro.alloc(n + 1);
     nrem = exclusive_scan_total(rc.p, A.rro.p, n, s);
     if (nrem == 0) A.rro.release();
-    // only worth it when the blocks are (nearly) full
-    if (!force && 9.0 * (double)nblk > 1.25 * (double)(A.nnz - nrem)) {
+    // only worth it when the blocks are (nearly) full (a distributed operator
+    // decides on its global counts, like the single-GPU copy)
+    double gblk = (double)nblk, gin = (double)(A.nnz - nrem);
+    if (dist && dist->nranks > 1) {
+        gblk = (double)ds_allsum(*dist, nblk, s);
+        gin = (double)ds_allsum(*dist, A.nnz - nrem, s);
+    }
+    if (!force && 9.0 * gblk > 1.25 * gin) {
         A.bro.release();
         A.rro.release();
         return;

@@ -36,6 +36,7 @@
 #include <thrust/unique.h>
 
 #include "dist.cuh"
+#include "dsetup.cuh"
 
 namespace pmgr {
 
@@ -73,7 +74,7 @@ struct LoopbackHub {
     uint64_t gen = 0;
     bool failed = false;
     std::string why;
-    enum Kind { EXCHANGE, GATHER, ALLREDUCE };
+    enum Kind { EXCHANGE, GATHER, ALLREDUCE, COUNTS, ALLTOALLV };
     struct Post {
         Kind kind;
         Halo *h = nullptr;
@@ -81,6 +82,10 @@ struct LoopbackHub {
         double *p = nullptr;
         const double *cp = nullptr;
         int64_t cnt = 0;
+        const std::vector<int64_t> *csend = nullptr, *sbytes = nullptr, *rbytes = nullptr;
+        std::vector<int64_t> *crecv = nullptr;
+        const std::vector<const void *> *sptr = nullptr;
+        const std::vector<void *> *rptr = nullptr;
     };
     std::vector<Post> posts;
     explicit LoopbackHub(int nr) : n(nr), posts(nr) {}
@@ -115,6 +120,20 @@ struct LoopbackHub {
                                                   cudaMemcpyDeviceToDevice, s));
                 }
             }
+        } else if (k == COUNTS) {
+            for (int r = 0; r < n; ++r) {
+                posts[r].crecv->assign(n, 0);
+                for (int p = 0; p < n; ++p) (*posts[r].crecv)[p] = (*posts[p].csend)[r];
+            }
+        } else if (k == ALLTOALLV) {
+            for (int r = 0; r < n; ++r)
+                for (int p = 0; p < n; ++p) {
+                    const int64_t b = (*posts[p].sbytes)[r];
+                    if (b != (*posts[r].rbytes)[p]) fail(PMGR_ERR_INVALID, "loopback all-to-all sizes disagree");
+                    if (b > 0)
+                        PMGR_CUDA(cudaMemcpyAsync((*posts[r].rptr)[p], (*posts[p].sptr)[r], (size_t)b,
+                                                  cudaMemcpyDeviceToDevice, s));
+                }
         } else {
             if (n > MAX_RANKS) fail(PMGR_ERR_NOT_SUPPORTED, "loopback all-reduce: too many ranks");
             PtrPack pk;
@@ -186,6 +205,24 @@ struct LoopbackTransport : Transport {
         p.cnt = n;
         hub->arrive(rank, p, s);
     }
+    void alltoall_counts(const std::vector<int64_t> &send, std::vector<int64_t> &recv, cudaStream_t s) override {
+        LoopbackHub::Post p;
+        p.kind = LoopbackHub::COUNTS;
+        p.csend = &send;
+        p.crecv = &recv;
+        hub->arrive(rank, p, s);
+    }
+    void alltoallv(const std::vector<const void *> &sptr, const std::vector<int64_t> &sbytes,
+                   const std::vector<void *> &rptr, const std::vector<int64_t> &rbytes, cudaStream_t s) override {
+        LoopbackHub::Post p;
+        p.kind = LoopbackHub::ALLTOALLV;
+        p.sptr = &sptr;
+        p.sbytes = &sbytes;
+        p.rptr = &rptr;
+        p.rbytes = &rbytes;
+        hub->arrive(rank, p, s);
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
 };
 
 // ---- NCCL, resolved at run time (the process's libnccl, e.g. torch's) ----
@@ -204,6 +241,7 @@ struct NcclApi {
     const char *(*GetErrorString)(nres_t) = nullptr;
 };
 constexpr int NCCL_FLOAT64 = 8;  // ncclFloat64 / ncclDouble
+constexpr int NCCL_INT8 = 0;     // ncclInt8 / ncclChar
 constexpr int NCCL_SUM = 0;      // ncclSum
 
 NcclApi &nccl() {
@@ -296,6 +334,36 @@ struct NcclTransport : Transport {
         nccl_check(nccl().AllReduce(buf, buf, (size_t)n, NCCL_FLOAT64, NCCL_SUM, comm, s), "ncclAllReduce");
     }
     bool capturable() const override { return true; }
+    void alltoall_counts(const std::vector<int64_t> &send, std::vector<int64_t> &recv, cudaStream_t s) override {
+        TBuf<int64_t> sb(nranks, s), rb(nranks, s);
+        PMGR_CUDA(cudaMemcpyAsync(sb.p, send.data(), sizeof(int64_t) * nranks, cudaMemcpyHostToDevice, s));
+        std::vector<const void *> sp(nranks);
+        std::vector<void *> rp(nranks);
+        std::vector<int64_t> by(nranks, 8);
+        for (int p = 0; p < nranks; ++p) {
+            sp[p] = sb.p + p;
+            rp[p] = rb.p + p;
+        }
+        alltoallv(sp, by, rp, by, s);
+        recv.assign(nranks, 0);
+        PMGR_CUDA(cudaMemcpyAsync(recv.data(), rb.p, sizeof(int64_t) * nranks, cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+    void alltoallv(const std::vector<const void *> &sptr, const std::vector<int64_t> &sbytes,
+                   const std::vector<void *> &rptr, const std::vector<int64_t> &rbytes, cudaStream_t s) override {
+        if (sbytes[rank] != rbytes[rank]) fail(PMGR_ERR_INVALID, "all-to-all self sizes disagree");
+        if (sbytes[rank] > 0)
+            PMGR_CUDA(cudaMemcpyAsync(rptr[rank], sptr[rank], (size_t)sbytes[rank], cudaMemcpyDeviceToDevice, s));
+        NcclApi &a = nccl();
+        nccl_check(a.GroupStart(), "ncclGroupStart");
+        for (int p = 0; p < nranks; ++p) {
+            if (p == rank) continue;
+            if (sbytes[p] > 0) nccl_check(a.Send(sptr[p], (size_t)sbytes[p], NCCL_INT8, p, comm, s), "ncclSend");
+            if (rbytes[p] > 0) nccl_check(a.Recv(rptr[p], (size_t)rbytes[p], NCCL_INT8, p, comm, s), "ncclRecv");
+        }
+        nccl_check(a.GroupEnd(), "ncclGroupEnd");
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank, int nranks) {
@@ -403,6 +471,11 @@ struct Builder {
     std::vector<std::unique_ptr<Space>> spaces;
     std::vector<std::vector<Reader>> readers;  // per space id
 
+    // partial: the operators hold this rank's rows only (distributed setup);
+    // ghost lists then travel to their owners instead of being derived from
+    // every rank's rows
+    bool partial = false;
+
     Builder(int r, int nr, Transport *t, cudaStream_t st) : rank(r), nranks(nr), tr(t), s(st) {}
 
     Space *root(int64_t n, const int64_t *bounds) {
@@ -444,10 +517,47 @@ struct Builder {
 
     void read(Space *cols, const Csr *Y, Space *rows) { readers[cols->id].push_back({Y, rows}); }
 
+    // partial mode: every rank learns which of its entries each peer reads
+    // (ghosts[q] keeps the part of q's ghost list this rank owns)
+    void exchange_ghosts(Space *sp) {
+        const std::vector<int64_t> mine = sp->ghosts[rank];
+        std::vector<int64_t> scnt(nranks), soff(nranks + 1, 0), rcnt;
+        for (int q = 0; q < nranks; ++q) {
+            const auto a = std::lower_bound(mine.begin(), mine.end(), sp->start[q]);
+            const auto b = std::lower_bound(mine.begin(), mine.end(), sp->start[q + 1]);
+            soff[q] = a - mine.begin();
+            scnt[q] = b - a;
+        }
+        tr->alltoall_counts(scnt, rcnt, s);
+        std::vector<int64_t> roff(nranks + 1, 0);
+        for (int q = 0; q < nranks; ++q) roff[q + 1] = roff[q] + rcnt[q];
+        TBuf<int64_t> sd((int64_t)mine.size() > 0 ? (int64_t)mine.size() : 1, s), rd(roff[nranks] > 0 ? roff[nranks] : 1, s);
+        if (!mine.empty())
+            PMGR_CUDA(cudaMemcpyAsync(sd.p, mine.data(), sizeof(int64_t) * mine.size(), cudaMemcpyHostToDevice, s));
+        std::vector<const void *> sp_(nranks);
+        std::vector<void *> rp(nranks);
+        std::vector<int64_t> sb(nranks), rb(nranks);
+        for (int q = 0; q < nranks; ++q) {
+            const bool self = q == rank;
+            sp_[q] = sd.p + soff[q];
+            sb[q] = self ? 0 : 8 * scnt[q];
+            rp[q] = rd.p + roff[q];
+            rb[q] = self ? 0 : 8 * rcnt[q];
+        }
+        tr->alltoallv(sp_, sb, rp, rb, s);
+        std::vector<int64_t> all(roff[nranks]);
+        if (!all.empty())
+            PMGR_CUDA(cudaMemcpyAsync(all.data(), rd.p, sizeof(int64_t) * all.size(), cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        for (int q = 0; q < nranks; ++q)
+            if (q != rank) sp->ghosts[q].assign(all.begin() + roff[q], all.begin() + roff[q + 1]);
+    }
+
     // ghost sets of every rank, my halo plan
     void finalize(Space *sp) {
         sp->ghosts.assign(nranks, {});
         for (int q = 0; q < nranks; ++q) {
+            if (partial && q != rank) continue;
             std::vector<int64_t> all;
             for (const Reader &rd : readers[sp->id]) {
                 const int64_t r0 = rd.rows->start[q], r1 = rd.rows->start[q + 1];
@@ -485,6 +595,7 @@ struct Builder {
                       all.end());
             sp->ghosts[q] = std::move(all);
         }
+        if (partial) exchange_ghosts(sp);
         sp->lo = sp->start[rank];
         sp->hi = sp->start[rank + 1];
         sp->ghosts_me = &sp->ghosts[rank];
@@ -553,7 +664,7 @@ struct Builder {
         PMGR_LAUNCHED();
         csr_finalize(out, s);
         out.row_off = R->off();
-        out.lanes = spmv_lanes(Y.view());
+        out.lanes = Y.lanes > 0 ? Y.lanes : spmv_lanes(Y.view());
         // the same rows take the block-per-row path as in the global operator
         out.long_len = Y.long_len;
         csr_long_rows(out, s);
@@ -664,8 +775,39 @@ std::unique_ptr<pmgr_amg> build_amg(Builder &B, const AmgPlan &P) {
 
 }  // namespace
 
+namespace {
+std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int rank,
+                                            int nranks, Transport *tr, cudaStream_t s, bool partial);
+}
+
 std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int rank, int nranks,
                                        Transport *tr, cudaStream_t s) {
+    return dist_build_impl(A, M, bounds, rank, nranks, tr, s, false);
+}
+
+std::unique_ptr<DistSolver> dist_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                                       const pmgr_level_spec *levels, int nlevels, const pmgr_mgr_cfg &cfg,
+                                       const int64_t *bounds, int rank, int nranks, Transport *tr, cudaStream_t s) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(PMGR_ERR_INVALID, "bad rank / nranks");
+    if (nranks > 1 && (!tr || tr->rank != rank || tr->nranks != nranks))
+        fail(PMGR_ERR_INVALID, "transport rank mismatch");
+    DistSetup d;
+    d.tr = tr;
+    d.rank = rank;
+    d.nranks = nranks;
+    d.start.assign(bounds, bounds + nranks + 1);
+    // small levels are set up redundantly on every rank; the collapsed coarse
+    // cycle needs its levels whole
+    const char *e = getenv("PMGR_DIST_REPLICATE_ROWS");
+    d.replicate_below = std::max(e ? (int64_t)atoll(e) : (int64_t)20000, collapse_limit());
+    if (nranks > 1) ds_finalize(&d, *A->m, s);  // the global operator's lane group
+    std::unique_ptr<pmgr_mgr> M = mgr_build(A->m, field_of, entity_of, levels, nlevels, cfg, s, &d);
+    return dist_build_impl(A, M.get(), bounds, rank, nranks, tr, s, nranks > 1);
+}
+
+namespace {
+std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int rank,
+                                            int nranks, Transport *tr, cudaStream_t s, bool partial) {
     if (!M || M->dist) fail(PMGR_ERR_INVALID, "row distribution needs a global hierarchy");
     if (nranks < 1 || rank < 0 || rank >= nranks) fail(PMGR_ERR_INVALID, "bad rank / nranks");
     if (tr && (tr->rank != rank || tr->nranks != nranks)) fail(PMGR_ERR_INVALID, "transport rank mismatch");
@@ -680,6 +822,7 @@ std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int
     }
     if (!M->terminal) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution needs a terminal AMG");
     Builder B(rank, nranks, tr, s);
+    B.partial = partial;
     // ---- phase 1: spaces and who reads them
     Space *M0 = B.root(A0.nrows, bounds);
     B.read(M0, &A0, M0);
@@ -750,6 +893,7 @@ std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int
     for (auto &sp : B.spaces) D->halos.push_back(sp->halo);
     return D;
 }
+}  // namespace
 
 // ========================================================= apply, GMRES
 
@@ -813,6 +957,63 @@ void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const
 }
 
 // ====================================================== one-GPU emulation
+
+void dist_setup_emulate(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                        const pmgr_level_spec *levels, int nlevels, const pmgr_mgr_cfg &mcfg, const int64_t *bounds,
+                        int nranks, int what, const double *in, double *out, const pmgr_gmres_cfg *cfg,
+                        pmgr_gmres_stats *stats, cudaStream_t s) {
+    LoopbackHub hub(nranks);
+    std::vector<std::unique_ptr<LoopbackTransport>> trs;
+    std::vector<pmgr_csr> parts(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        trs.emplace_back(new LoopbackTransport(&hub, r));
+        parts[r].m = std::make_shared<Csr>();
+        ds_partial_rows(*A->m, bounds[r], bounds[r + 1], *parts[r].m, s);
+    }
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    int dev = 0;
+    PMGR_CUDA(cudaGetDevice(&dev));
+    std::vector<std::string> errs(nranks);
+    std::vector<pmgr_gmres_stats> st(nranks);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r) {
+        th.emplace_back([&, r] {
+            try {
+                PMGR_CUDA(cudaSetDevice(dev));
+                auto D = dist_setup(&parts[r], field_of, entity_of, levels, nlevels, mcfg, bounds, r, nranks,
+                                    trs[r].get(), s);
+                if (what == 0) {
+                    dist_apply(*D, in + D->lo, out + D->lo, s);
+                } else {
+                    pmgr_gmres_stats z = {};
+                    dist_gmres(*D, in + D->lo, out + D->lo, 0, *cfg, z, nullptr, 0, s);
+                    st[r] = z;
+                }
+                PMGR_CUDA(cudaStreamSynchronize(s));
+            } catch (const Error &e) {
+                errs[r] = e.msg.empty() ? "error" : e.msg;
+                hub.abort(errs[r]);
+            } catch (const std::exception &e) {
+                errs[r] = e.what();
+                hub.abort(e.what());
+            }
+        });
+    }
+    for (auto &t : th) t.join();
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < nranks; ++r)
+        if (!errs[r].empty() && errs[r].find("loopback peer failed") == std::string::npos &&
+            errs[r].find("loopback exchange failed") == std::string::npos)
+            fail(PMGR_ERR_CUDA, "rank " + std::to_string(r) + ": " + errs[r]);
+    for (int r = 0; r < nranks; ++r)
+        if (!errs[r].empty()) fail(PMGR_ERR_CUDA, "rank " + std::to_string(r) + ": " + errs[r]);
+    if (stats && what == 1) {
+        *stats = st[0];
+        for (int r = 1; r < nranks; ++r)
+            if (st[r].iterations != st[0].iterations)
+                fail(PMGR_ERR_INVALID, "emulated ranks disagree on the iteration count");
+    }
+}
 
 void dist_emulate(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int nranks, int what, const double *in,
                   double *out, const pmgr_gmres_cfg *cfg, pmgr_gmres_stats *stats, cudaStream_t s) {

@@ -16,6 +16,12 @@ struct Transport {
     virtual void gather(Gather &g, const double *own, double *full, cudaStream_t s) = 0;
     virtual void allreduce(double *buf, int64_t n, cudaStream_t s) = 0;
     virtual bool capturable() const { return false; }  // may be recorded into a CUDA graph
+    // setup-phase collectives (synchronising): one int64 to / from every rank,
+    // and a personalised exchange of device byte ranges (peer p's send to me
+    // lands in rptr[p]; sizes must match the peers' counts)
+    virtual void alltoall_counts(const std::vector<int64_t> &send, std::vector<int64_t> &recv, cudaStream_t s) = 0;
+    virtual void alltoallv(const std::vector<const void *> &sptr, const std::vector<int64_t> &sbytes,
+                           const std::vector<void *> &rptr, const std::vector<int64_t> &rbytes, cudaStream_t s) = 0;
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank, int nranks);
@@ -39,6 +45,17 @@ struct DistSolver {
 
 std::unique_ptr<DistSolver> dist_build(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int rank, int nranks,
                                        Transport *tr, cudaStream_t s);
+// distributed setup: A holds this rank's rows (global row space, the rest
+// empty); field_of / entity_of are global (replicated); every rank calls
+std::unique_ptr<DistSolver> dist_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                                       const pmgr_level_spec *levels, int nlevels, const pmgr_mgr_cfg &cfg,
+                                       const int64_t *bounds, int rank, int nranks, Transport *tr, cudaStream_t s);
+// N ranks emulated on this GPU, distributed setup included (threads meet at
+// every collective); what 0 = one MGR application, 1 = a GMRES solve
+void dist_setup_emulate(const pmgr_csr *A, const int8_t *field_of, const int32_t *entity_of,
+                        const pmgr_level_spec *levels, int nlevels, const pmgr_mgr_cfg &mcfg, const int64_t *bounds,
+                        int nranks, int what, const double *in, double *out, const pmgr_gmres_cfg *cfg,
+                        pmgr_gmres_stats *stats, cudaStream_t s);
 void dist_apply(DistSolver &D, const double *v_own, double *z_own, cudaStream_t s);
 void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const pmgr_gmres_cfg &cfg,
                 pmgr_gmres_stats &st, double *history, int32_t history_cap, cudaStream_t s);

@@ -58,6 +58,8 @@ struct AmgLevel {
 
 // coarse end of the V-cycle as one dense operator (collapse.cu)
 void collapse_tail(pmgr_amg &h, cudaStream_t s);
+// largest level the collapse densifies (PMGR_COLLAPSE_ROWS, default 3584)
+int64_t collapse_limit();
 
 }  // namespace pmgr
 
@@ -80,8 +82,10 @@ struct pmgr_amg {
 
 namespace pmgr {
 
+struct DistSetup;
+// dist: distributed setup of a partial operator (dsetup.cuh), null on one GPU
 std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A, const pmgr_amg_cfg &cfg,
-                                    cudaStream_t s);
+                                    cudaStream_t s, const DistSetup *dist = nullptr);
 // out = V-cycle(h, b, x); x may be null (zero initial guess).  b/out are
 // length n_0 device vectors; out may alias neither b nor x.
 void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaStream_t s);
@@ -179,7 +183,8 @@ struct pmgr_mgr {
 namespace pmgr {
 std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A, const int8_t *field_of_host,
                                     const int32_t *entity_of_host, const pmgr_level_spec *specs,
-                                    int nlevels, const pmgr_mgr_cfg &cfg, cudaStream_t s);
+                                    int nlevels, const pmgr_mgr_cfg &cfg, cudaStream_t s,
+                                    const DistSetup *dist = nullptr);
 void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);
 void mgr_collect(pmgr_mgr &h);  // fold finished graph timing events into the totals
 void mgr_apply_direct(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);  // no graph (for capture)

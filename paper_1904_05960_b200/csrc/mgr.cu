@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <set>
 
+#include "dsetup.cuh"
 #include "hier.cuh"
 
 namespace pmgr {
@@ -103,10 +104,10 @@ __global__ void k_rows_of(int64_t nout, const int64_t *rows, const int64_t *ro, 
 
 // P = [W_p; I] in level order
 template <bool FILL>
-__global__ void k_build_p(int64_t n, const int8_t *is_c, const int64_t *c_index, const int64_t *f_index,
+__global__ void k_build_p(int64_t lo, int64_t n, const int8_t *is_c, const int64_t *c_index, const int64_t *f_index,
                           const int64_t *fc_ro, const int32_t *fc_ci, const double *fc_v, const double *dinv,
                           int with_wp, int64_t *cnt, const int64_t *pro, int32_t *pci, double *pv) {
-    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t i = lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
     if (i >= n) return;
     if (is_c[i]) {
@@ -346,8 +347,12 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
 
 std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t *field_of_host,
                                     const int32_t *entity_of_host, const pmgr_level_spec *specs, int nlevels,
-                                    const pmgr_mgr_cfg &cfg, cudaStream_t s) {
+                                    const pmgr_mgr_cfg &cfg, cudaStream_t s, const DistSetup *dist) {
     if (A0->nrows != A0->ncols) fail(PMGR_ERR_INVALID, "mgr_setup requires a square matrix");
+    // distributed setup (dsetup.cuh): every operator keeps the owned rows of
+    // its global row space; dd tracks the owned ranges of the level space
+    std::unique_ptr<DistSetup> dd;
+    if (dist && dist->nranks > 1) dd.reset(new DistSetup(*dist));
     auto h = std::make_unique<pmgr_mgr>();
     h->n = A0->nrows;
     h->terminal_cycles = cfg.terminal_cycles > 1 ? cfg.terminal_cycles : 1;
@@ -427,6 +432,14 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                                                      L.c_rows.p, L.f_rows.p);
         PMGR_LAUNCHED();
         setup_trace("mgr split", li, s);
+        // owned ranges of the level, F and C spaces (distributed setup)
+        std::unique_ptr<DistSetup> dF, dC;
+        if (dd) {
+            dF.reset(new DistSetup(dd->with(ds_sub_bounds(dd->start, L.is_c.p, n, false, s))));
+            dC.reset(new DistSetup(dd->with(ds_sub_bounds(dd->start, L.is_c.p, n, true, s))));
+            if (sp.global_smoother != PMGR_SMOOTHER_NONE)
+                fail(PMGR_ERR_NOT_SUPPORTED, "distributed setup of a level with a global smoother");
+        }
         // ---- blocks (extract_blocks, sparse.py:269-288)
         const CsrView Av = cur->view();
         auto A_ff = std::make_shared<Csr>();
@@ -438,18 +451,26 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         setup_trace("mgr blocks", li, s);
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
-        csr_finalize(*A_ff, s);
-        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3) csr_make_bsr3(*A_ff, A_ff->nrows, A_ff->ncols, s);
+        ds_finalize(dF.get(), *A_ff, s);
+        if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3)
+            csr_make_bsr3(*A_ff, A_ff->nrows, A_ff->ncols, s, false, dF.get());
         if (li == 0 && A_ff->nbrows > 0) {
             // F rows first, then C rows: the same blocks lead A0 itself
             bool prefix = true;
             for (int64_t i = 0; i < n && prefix; ++i) prefix = (((sp.c_mask >> (fo[i] & 63)) & 1ull) != 0) == (i >= L.nf);
             if (prefix) h->block_prefix = L.nf;
         }
-        csr_finalize(L.A_cf, s);
+        ds_finalize(dC.get(), L.A_cf, s);
         if (need_dinv) {
             L.dinv_ff.alloc(L.nf);
-            int64_t bad = csr_diag_inverse(A_ff->view(), L.dinv_ff.p, s);
+            int64_t bad;
+            if (dd) {  // owned F rows; the first singular row over all ranks
+                bad = ds_diag_inverse(*A_ff, dF->lo(), dF->hi(), L.dinv_ff.p, s);
+                const int64_t g = ds_allmax(*dd, bad < 0 ? INT64_MIN : -bad, s);
+                bad = g == INT64_MIN ? -1 : -g;
+            } else {
+                bad = csr_diag_inverse(A_ff->view(), L.dinv_ff.p, s);
+            }
             if (bad >= 0)
                 fail(PMGR_ERR_SINGULAR_DIAG, "singular diagonal: zero or missing entry at row " + std::to_string(bad),
                      bad);
@@ -460,19 +481,25 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             L.P.nrows = n;
             L.P.ncols = L.nc;
             L.P.ro.alloc(n + 1);
-            k_build_p<false><<<grid_for(n * 32, 256), 256, 0, s>>>(n, L.is_c.p, c_index.p, L.f_index.p, A_fc.ro.p,
-                                                                  A_fc.ci.p, A_fc.v.p, L.dinv_ff.p, with_wp, cnt.p,
-                                                                  nullptr, nullptr, nullptr);
-            PMGR_LAUNCHED();
+            const int64_t plo = dd ? dd->lo() : 0, phi = dd ? dd->hi() : n;
+            PMGR_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (size_t)(n > 0 ? n : 1), s));
+            if (phi > plo) {
+                k_build_p<false><<<grid_for((phi - plo) * 32, 256), 256, 0, s>>>(
+                    plo, phi, L.is_c.p, c_index.p, L.f_index.p, A_fc.ro.p, A_fc.ci.p, A_fc.v.p, L.dinv_ff.p, with_wp,
+                    cnt.p, nullptr, nullptr, nullptr);
+                PMGR_LAUNCHED();
+            }
             L.P.nnz = exclusive_scan_total(cnt.p, L.P.ro.p, n, s);
             L.P.ci.alloc(L.P.nnz);
             L.P.v.alloc(L.P.nnz);
-            k_build_p<true><<<grid_for(n * 32, 256), 256, 0, s>>>(n, L.is_c.p, c_index.p, L.f_index.p, A_fc.ro.p,
-                                                                 A_fc.ci.p, A_fc.v.p, L.dinv_ff.p, with_wp, nullptr,
-                                                                 L.P.ro.p, L.P.ci.p, L.P.v.p);
-            PMGR_LAUNCHED();
+            if (phi > plo) {
+                k_build_p<true><<<grid_for((phi - plo) * 32, 256), 256, 0, s>>>(
+                    plo, phi, L.is_c.p, c_index.p, L.f_index.p, A_fc.ro.p, A_fc.ci.p, A_fc.v.p, L.dinv_ff.p, with_wp,
+                    nullptr, L.P.ro.p, L.P.ci.p, L.P.v.p);
+                PMGR_LAUNCHED();
+            }
         }
-        csr_finalize(L.P, s);
+        ds_finalize(dd.get(), L.P, s);
         setup_trace("mgr transfers", li, s);
         // ---- F-relaxation (_build_f_relax, mgr.py:374-386)
         L.f_relax = sp.f_relax;
@@ -480,7 +507,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         if (sp.f_relax == PMGR_FRELAX_AMG) {
             pmgr_amg_cfg acfg = cfg.amg_f_relax;
             acfg.num_functions = sp.amg_num_functions > 0 ? sp.amg_num_functions : 1;
-            L.amg = amg_build(A_ff, acfg, s);
+            L.amg = amg_build(A_ff, acfg, s, dF.get());
             L.amg->prof_tag = (li == 0);
         }
         if (sp.f_relax == PMGR_FRELAX_JACOBI && L.f_relax_sweeps > 1) L.A_ff = A_ff;
@@ -500,10 +527,14 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         {
             Csr RA, T;
             rows_of(Av, L.c_rows.p, L.nc, RA, s);
+            // distributed: the rows of P behind RA's columns, fetched from their owners
+            Csr Pext;
+            if (dd) ds_fetch_rows(*dd, L.P, ds_cols_outside(RA, dC->lo(), dC->hi(), dd->lo(), dd->hi(), s), Pext, s);
+            const CsrView Pv = dd ? Pext.view() : L.P.view();
             if (sp.n_max < 0) {
-                spgemm(RA.view(), L.P.view(), 1, *coarse, s);
+                spgemm(RA.view(), Pv, 1, *coarse, s);
             } else {
-                spgemm(RA.view(), L.P.view(), 1, T, s);
+                spgemm(RA.view(), Pv, 1, T, s);
                 Csr corr, kept;
                 csr_subtract(A_cc.view(), T.view(), corr, s);
                 TBuf<int32_t> ent(L.nc, s);
@@ -517,7 +548,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                 PMGR_CUDA(cudaStreamSynchronize(s));
             }
         }
-        csr_finalize(*coarse, s);
+        ds_finalize(dC.get(), *coarse, s);
         setup_trace("mgr coarse RAP", li, s);
         // ---- workspace
         L.vf.alloc(L.nf);
@@ -537,10 +568,11 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         eo.swap(eo2);
         h->levels.push_back(std::move(L));
         cur = coarse;
+        if (dd) dd->start = dC->start;
         PMGR_CUDA(cudaStreamSynchronize(s));
     }
     h->terminal_A = cur;
-    h->terminal = amg_build(cur, cfg.amg_terminal, s);
+    h->terminal = amg_build(cur, cfg.amg_terminal, s, dd.get());
     h->tz.alloc(cur->nrows);
     PMGR_CUDA(cudaStreamSynchronize(s));
     return h;

@@ -340,6 +340,72 @@ class DeviceDistSolver:
         return x, SolveStats(int(st.iterations), hist[:st.history_len].copy(), bool(st.converged))
 
 
+class DeviceDistSetupSolver(DeviceDistSolver):
+    """Rank `rank`'s solver from the DISTRIBUTED setup (pmgr_dist_setup):
+    `A_rows` holds only this rank's rows (global row space), the layout is
+    global; every rank calls this collectively.  Each rank builds the owned
+    rows of every operator of the hierarchy (bitwise equal to the single-GPU
+    setup) and the small coarse levels redundantly."""
+
+    def __init__(self, A_rows, layout, config, bounds, rank: int, nranks: int, transport=None):
+        from . import _lib
+        from .mgr import setup_args
+        from .sparse import as_device_csr, current_stream
+
+        self.h, self.rank, self.nranks = None, rank, nranks
+        self.transport = transport
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        if len(self.bounds) != nranks + 1:
+            raise ValueError("bounds must have nranks + 1 entries")
+        dA = as_device_csr(A_rows)
+        self._A = dA
+        specs, cfg, fo0, eo0 = setup_args(dA, layout, config)
+        out = ctypes.c_void_p()
+        th = transport.h if transport is not None else None
+        _lib.check(_lib.lib().pmgr_dist_setup(dA.handle, fo0.ctypes.data, eo0.ctypes.data, specs,
+                                              len(config.levels), ctypes.byref(cfg), self.bounds.ctypes.data,
+                                              rank, nranks, th, current_stream(), ctypes.byref(out)))
+        self._d = _Handle(out, "pmgr_dist_destroy")
+        lo, no = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().pmgr_dist_info(self._d.h, ctypes.byref(lo), ctypes.byref(no)))
+        self.lo, self.n_own = lo.value, no.value
+
+
+def _emulate_setup(A, layout, config, bounds, what, vin, cfg=None):
+    from . import _lib
+    from .krylov import GmresConfig
+    from .mgr import setup_args
+    from .sparse import as_device_csr, current_stream, empty_device, ptr, to_device
+
+    dA = as_device_csr(A)
+    specs, mcfg, fo0, eo0 = setup_args(dA, layout, config)
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    vd = to_device(vin, dA.nrows).contiguous()
+    z = empty_device(dA.nrows).zero_()
+    c = st = None
+    if what == 1:
+        cfg = cfg or GmresConfig()
+        c = _lib.GmresCfg(int(cfg.restart), int(cfg.max_iters), float(cfg.rtol), float(cfg.atol))
+        st = _lib.GmresStats()
+    _lib.check(_lib.lib().pmgr_dist_setup_emulate(dA.handle, fo0.ctypes.data, eo0.ctypes.data, specs,
+                                                  len(config.levels), ctypes.byref(mcfg), b.ctypes.data, len(b) - 1,
+                                                  what, ptr(vd), ptr(z), ctypes.byref(c) if c else None,
+                                                  ctypes.byref(st) if st else None, current_stream()))
+    return z, st
+
+
+def emulate_setup_apply(A, layout, config, bounds, v):
+    """z = M v where M comes from the distributed setup over len(bounds)-1
+    ranks emulated on this GPU (each rank sets up from its row slice)."""
+    return _emulate_setup(A, layout, config, bounds, 0, v)[0]
+
+
+def emulate_setup_gmres(A, layout, config, bounds, rhs, cfg=None):
+    """Distributed setup + distributed GMRES(MGR) from x0 = 0 over emulated ranks."""
+    x, st = _emulate_setup(A, layout, config, bounds, 1, rhs, cfg)
+    return x, int(st.iterations), bool(st.converged)
+
+
 def emulate_apply(h, bounds, v):
     """z = M v with the hierarchy row-distributed over len(bounds)-1 ranks
     emulated on this GPU (loopback transport): the parity harness of §8e."""

@@ -199,6 +199,16 @@ class MgrHierarchy:
 def mgr_setup(A, layout: FieldLayout, config: MgrConfig) -> MgrHierarchy:
     """Build the reduction hierarchy for operator A laid out by `layout`."""
     dA = as_device_csr(A)
+    specs, cfg, fo0, eo0 = setup_args(dA, layout, config)
+    out = ctypes.c_void_p()
+    _lib.check(_lib.lib().pmgr_mgr_setup(dA.handle, fo0.ctypes.data, eo0.ctypes.data, specs, len(config.levels),
+                                         ctypes.byref(cfg), current_stream(), ctypes.byref(out)))
+    return MgrHierarchy(out, dA, config, config.levels)
+
+
+def setup_args(dA, layout: FieldLayout, config: MgrConfig):
+    """Validate (mgr.py:337-352) and marshal the setup arguments of the C ABI:
+    level specs, configuration, field / entity tags."""
     if dA.nrows != dA.ncols:
         raise ValueError("mgr_setup requires a square matrix")
     if layout.ndofs != dA.nrows:
@@ -228,12 +238,9 @@ def mgr_setup(A, layout: FieldLayout, config: MgrConfig) -> MgrHierarchy:
     specs = (_lib.LevelSpec * max(1, len(config.levels)))(*[s.to_c() for s in config.levels])
     cfg = config.to_c()
     cfg.flow_interleaved = 1 if layout.ordering == Ordering.FLOW_INTERLEAVED else 0
-    out = ctypes.c_void_p()
     fo0 = np.ascontiguousarray(layout.field_of, dtype=np.int8)
     eo0 = np.ascontiguousarray(layout.entity_of, dtype=np.int32)
-    _lib.check(_lib.lib().pmgr_mgr_setup(dA.handle, fo0.ctypes.data, eo0.ctypes.data, specs, len(config.levels),
-                                         ctypes.byref(cfg), current_stream(), ctypes.byref(out)))
-    return MgrHierarchy(out, dA, config, config.levels)
+    return specs, cfg, fo0, eo0
 
 
 def mgr_apply(h: MgrHierarchy, v):
