@@ -216,18 +216,37 @@ def run_gpu_dist(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     A = pb.A
     lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    h = mgr.mgr_setup(A, lay, cfg)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    setup_s = e0.elapsed_time(e1) / 1e3
     tr = D.nccl_transport(rank, world, tdist)
-    t0 = time.perf_counter()
-    solver = D.DeviceDistSolver(h, bounds, rank, world, tr)
     torch.cuda.synchronize()
-    dist_setup_s = time.perf_counter() - t0
+    levels_info = None
+    if args.replicated_setup:
+        # every rank builds the global hierarchy, then keeps its rows
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h = mgr.mgr_setup(A, lay, cfg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        setup_s = e0.elapsed_time(e1) / 1e3
+        levels_info = h.level_sizes()
+        t0 = time.perf_counter()
+        solver = D.DeviceDistSolver(h, bounds, rank, world, tr)
+        torch.cuda.synchronize()
+        dist_setup_s = time.perf_counter() - t0
+    else:
+        # distributed setup: each rank sets up from its own rows (warm-up build
+        # first, then the timed one; wall time max over ranks)
+        lo_r, hi_r = int(bounds[rank]), int(bounds[rank + 1])
+        A_rows = D.row_slice(A, lo_r, hi_r)
+        solver = D.DeviceDistSetupSolver(A_rows, lay, cfg, bounds, rank, world, tr)
+        del solver
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver = D.DeviceDistSetupSolver(A_rows, lay, cfg, bounds, rank, world, tr)
+        torch.cuda.synchronize()
+        setup_s = time.perf_counter() - t0
+        dist_setup_s = None
     lo, no = solver.lo, solver.n_own
     b_own = torch.from_numpy(pb.rhs[lo:lo + no].copy()).cuda()
     gcfg = krylov.GmresConfig(restart=args.restart, max_iters=1000, rtol=args.rtol)
@@ -263,6 +282,7 @@ def run_gpu_dist(args, rank, world, local_rank):
         return float(t)
 
     t_max = tmax(statistics.mean(times))
+    setup_s = tmax(setup_s)
     # e2e: host b slice in, host x slice out, inside the timed region
     e2e_times = []
     bh = pb.rhs[lo:lo + no].copy()
@@ -291,11 +311,15 @@ def run_gpu_dist(args, rank, world, local_rank):
                                    "rank-major z-slabs), 3-level MGR (U AMG, N_max=4 -> S Jacobi -> P AMG)",
                        "n_dofs": pb.n, "n_dofs_per_gpu": int(np.diff(bounds).max()), "nnz": pb.nnz,
                        "restart": args.restart, "rtol": args.rtol, "gmres_iterations": st.iterations,
-                       "true_relative_residual": rel, "mgr_levels": h.level_sizes(),
+                       "true_relative_residual": rel, "mgr_levels": levels_info,
                        "l2": "flushed between steps (512 MiB write, untimed)",
-                       "parallelism": f"row-distributed z-slabs over {world} GPU(s): replicated setup, "
-                                      "NCCL halo exchange / all-gather / all-reduce inside libpmgr"},
-            "setup_s": setup_s, "dist_setup_s": dist_setup_s,
+                       "parallelism": f"row-distributed z-slabs over {world} GPU(s): "
+                                      + ("replicated setup" if args.replicated_setup else
+                                         "distributed setup (pmgr_dist_setup)")
+                                      + ", NCCL halo exchange / all-gather / all-reduce inside libpmgr"},
+            "setup_s": setup_s, "setup_timing": "max over ranks" + ("" if args.replicated_setup else
+                                                                     ", host wall clock around pmgr_dist_setup"),
+            "dist_setup_s": dist_setup_s,
             "e2e": {"value": pb.n / e2e_mean / 1e6, "unit": UNIT, "h2d_bytes_per_step": 8 * no,
                     "d2h_bytes_per_step": 8 * no, "ms_per_step": e2e_mean * 1e3, "note": "per-rank slices"},
             "gpu_launches": launches, "clocks": clk, "roofline": None, "cpu_baseline": None,
@@ -529,6 +553,9 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent C2 solves instead of the "
                                                                 "row-distributed slab stack")
     ap.add_argument("--dist", action="store_true", help="use the row-distributed path even at N = 1")
+    ap.add_argument("--replicated-setup", action="store_true",
+                    help="distributed path: build the global hierarchy on every rank instead of the "
+                         "distributed setup")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the roofline kernel (profiles/), echoed into the JSON")
     args = ap.parse_args()

@@ -76,6 +76,9 @@ PMGR_API int pmgr_csr_download(const pmgr_csr *A, int64_t *row_offsets, int32_t 
 /* y = A x, replaces sparse.matvec (sparse.py:261-266). */
 /* B = P A P^T for a host permutation (row i of B = row perm[i] of A, columns
  * renumbered and sorted): problems.rank_major on the device. */
+/* Rows [lo, hi) of A in A's row space (every other row empty): one rank's
+ * slice for pmgr_dist_setup. */
+PMGR_API int pmgr_csr_rows(const pmgr_csr *A, int64_t lo, int64_t hi, void *stream, pmgr_csr **out);
 PMGR_API int pmgr_csr_permute(const pmgr_csr *A, const int64_t *perm_host, void *stream, pmgr_csr **out);
 PMGR_API int pmgr_spmv(const pmgr_csr *A, const double *x_dev, double *y_dev, void *stream);
 

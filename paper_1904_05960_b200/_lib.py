@@ -128,6 +128,7 @@ SIGNATURES = {
     "pmgr_assemble_poromech": (ctypes.c_int, [ctypes.POINTER(Assembly), vp, ctypes.POINTER(vp)]),
     "pmgr_dist_emulate": (ctypes.c_int, [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, vp, vp,
                                          ctypes.POINTER(GmresCfg), ctypes.POINTER(GmresStats), vp]),
+    "pmgr_csr_rows": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.POINTER(vp)]),
     "pmgr_dist_setup": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int32, ctypes.POINTER(MgrCfg), vp, ctypes.c_int32,
                                        ctypes.c_int32, vp, vp, ctypes.POINTER(vp)]),
     "pmgr_dist_setup_emulate": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int32, ctypes.POINTER(MgrCfg), vp,

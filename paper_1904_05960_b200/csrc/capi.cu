@@ -7,6 +7,7 @@
 #include <string>
 
 #include "dist.cuh"
+#include "dsetup.cuh"
 
 namespace {
 thread_local std::string g_msg;
@@ -481,6 +482,17 @@ int pmgr_assemble_poromech(const pmgr_assembly *a, void *stream, pmgr_csr **out)
         require(a->phases == 1 || a->sats, "NULL saturations");
         init_pool();
         *out = wrap(pmgr::assemble_poromech(*a, S(stream)));
+    });
+}
+
+int pmgr_csr_rows(const pmgr_csr *A, int64_t lo, int64_t hi, void *stream, pmgr_csr **out) {
+    return guard([&] {
+        require(A && out, "NULL argument");
+        require(lo >= 0 && lo <= hi && hi <= A->m->nrows, "row range out of bounds");
+        auto m = std::make_shared<pmgr::Csr>();
+        pmgr::ds_partial_rows(*A->m, lo, hi, *m, S(stream));
+        pmgr::csr_finalize(*m, S(stream));
+        *out = wrap(m);
     });
 }
 

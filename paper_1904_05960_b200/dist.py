@@ -340,6 +340,20 @@ class DeviceDistSolver:
         return x, SolveStats(int(st.iterations), hist[:st.history_len].copy(), bool(st.converged))
 
 
+def row_slice(A, lo: int, hi: int):
+    """Rows [lo, hi) of A in A's global row space, every other row empty (a
+    rank's input to the distributed setup), as a device matrix."""
+    from . import _lib
+    from .sparse import DeviceCsr, as_device_csr, current_stream
+
+    dA = as_device_csr(A)
+    out = ctypes.c_void_p()
+    _lib.check(_lib.lib().pmgr_csr_rows(dA.handle, int(lo), int(hi), current_stream(), ctypes.byref(out)))
+    nr, nc, nz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().pmgr_csr_info(out, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nz)))
+    return DeviceCsr(out, nr.value, nc.value, nz.value)
+
+
 class DeviceDistSetupSolver(DeviceDistSolver):
     """Rank `rank`'s solver from the DISTRIBUTED setup (pmgr_dist_setup):
     `A_rows` holds only this rank's rows (global row space), the layout is
