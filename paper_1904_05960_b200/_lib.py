@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmgr.so")
+LIB_PATH = os.environ.get("PMGR_LIB") or os.path.join(_HERE, "libpmgr.so")  # PMGR_LIB: A/B tooling only
 
 c_i8p = ctypes.POINTER(ctypes.c_int8)
 c_i32p = ctypes.POINTER(ctypes.c_int32)

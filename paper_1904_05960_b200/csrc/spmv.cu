@@ -42,14 +42,18 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
                                               const double *__restrict__ v, Op op, int64_t row_off, int trigger,
                                               int64_t long_len, const int32_t *__restrict__ lrows,
                                               unsigned nshort) {
-    pdl_wait();
-    if (trigger) pdl_trigger();
+    // The operator is constant during the solve: its row bounds (and, in the
+    // short-row path, the first two entries per lane) are loaded before
+    // griddepcontrol.wait, overlapping the predecessor's tail; only the
+    // gathers of x and the epilogue wait for it.
     if (blockIdx.x >= nshort) {
         // a long row: the whole block, four independent load chains per
         // thread, then a fixed-order reduction (warps, then the 8 warp sums)
         __shared__ double ws[8];
         const int64_t row = __ldg(lrows + (blockIdx.x - nshort));
         const int64_t b = __ldg(ro + row), e = __ldg(ro + row + 1);
+        pdl_wait();
+        if (trigger) pdl_trigger();
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int64_t q = b + threadIdx.x;
         for (; q + 768 < e; q += 1024) {
@@ -91,8 +95,24 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
     // two independent accumulators keep two (value, column, x) load chains
     // in flight per lane; matrix streams use evict-first loads so the
     // gathered vector stays in L2
-    double s0 = 0.0, s1 = 0.0;
     int64_t q = b + lane;
+    const bool h0 = q < e, h1 = q + G < e;
+    double v0 = 0.0, v1 = 0.0;
+    int c0 = 0, c1 = 0;
+    if (h0) {
+        v0 = ldv<STREAM>(v + q);
+        c0 = ldc<STREAM>(ci + q);
+    }
+    if (h1) {
+        v1 = ldv<STREAM>(v + q + G);
+        c1 = ldc<STREAM>(ci + q + G);
+    }
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    double s0 = 0.0, s1 = 0.0;
+    if (h0) s0 = fma(v0, op.x(c0), s0);
+    if (h1) s1 = fma(v1, op.x(c1), s1);
+    q += 2 * G;
     for (; q + G < e; q += 2 * G) {
         const double v0 = ldv<STREAM>(v + q), v1 = ldv<STREAM>(v + q + G);
         const int c0 = ldc<STREAM>(ci + q), c1 = ldc<STREAM>(ci + q + G);
@@ -117,14 +137,19 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, i
                                               const int32_t *__restrict__ bci, const double *__restrict__ bval,
                                               const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
                                               const double *__restrict__ rv, Op op, int64_t row_off, int trigger) {
-    pdl_wait();
-    if (trigger) pdl_trigger();
     const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int kk = lane / 3, c = lane - 3 * kk;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    // the row bounds do not depend on the predecessor: loaded before the wait
+    int64_t k0 = 0, k1 = 0;
     if (I < nb) {
-        const int64_t k0 = __ldg(bro + I), k1 = __ldg(bro + I + 1);
+        k0 = __ldg(bro + I);
+        k1 = __ldg(bro + I + 1);
+    }
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    if (I < nb) {
         // batches of 30 blocks: every column index and value load of a lane's
         // three blocks is issued before the dependent x gathers
         for (int64_t kb = k0; kb < k1; kb += 30) {
@@ -255,6 +280,16 @@ struct OpProlong {
     }
 };
 
+// a kernel lets its successor launch early (PDL) only when its own grid is
+// at most this many blocks per SM, so the early blocks never crowd out its own
+int trigger_blocks_per_sm() {
+    static const int v = [] {
+        const char *e = getenv("PMGR_TRIG_BPS");
+        return e ? atoi(e) : 2;
+    }();
+    return v;
+}
+
 template <int G, class Op, class IT>
 void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_t s) {
     const int block = 256;
@@ -263,7 +298,7 @@ void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_
     const unsigned grid = nshort + (unsigned)nlong;
     // let the next kernel's launch overlap this one only when this grid is a
     // single wave (its early blocks must not crowd out ours)
-    const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
+    const int trigger = grid <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
     if (stream)
         launch_pdl(k_spmv<G, true, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
                    trigger, A.long_len, A.lrows, nshort);
@@ -307,7 +342,7 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nbrows > 0) {
         const int64_t ntrip = A.rro ? (A.nrows + 2) / 3 : A.nbrows;
         const unsigned grid = grid_for(ntrip * 32, 256);
-        const int trigger = grid <= (unsigned)(2 * num_sms()) ? 1 : 0;
+        const int trigger = grid <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
         // PMGR_BSR_STREAM: evict-first loads for block-prefix operators with a
         // remainder (the Krylov operator A0: read once per iteration) = 1, for all = 2
         static const int bstream = [] {
@@ -377,8 +412,7 @@ __global__ void k_hybrid_gs(int64_t nparts, const int64_t *__restrict__ starts,
 // 16-byte loads of column pairs.
 template <bool PAIR, bool STREAM = false, int RB = 8>
 __global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__ M, int64_t nrows, int64_t n, int64_t ld,
-                                                      const double *__restrict__ x, double *__restrict__ y) {
-    pdl_wait();
+                                                      const double *__restrict__ x, double *__restrict__ y, int trigger) {
     constexpr int W = 8;
     __shared__ double red[W][RB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -389,17 +423,29 @@ __global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__
     for (int r = 0; r < RB; ++r) acc[r] = 0.0;
     if (PAIR) {
         const int64_t np = n >> 1;
-        for (int64_t p = warp * 32 + lane; p < np; p += W * 32) {
+        // M is constant: the first column pairs of the block's rows are
+        // loaded before griddepcontrol.wait (overlapping the predecessor),
+        // then each batch's loads are issued before the previous batch's FMAs
+        double2 m[RB];
+        int64_t p = warp * 32 + lane;
+#define PMGR_DENSE_LOAD(P)                                                                                   \
+    _Pragma("unroll") for (int r = 0; r < RB; ++r) m[r] =                                                     \
+        (r < nr && (P) < np) ? (STREAM ? __ldcs(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + (P))   \
+                                       : __ldg(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + (P)))   \
+                             : make_double2(0.0, 0.0);
+        PMGR_DENSE_LOAD(p)
+        pdl_wait();
+        if (trigger) pdl_trigger();
+        for (; p < np; p += W * 32) {
             const double2 xv = make_double2(__ldg(x + 2 * p), __ldg(x + 2 * p + 1));
-            double2 m[RB];
+            double2 mc[RB];
 #pragma unroll
-            for (int r = 0; r < RB; ++r)
-                m[r] = r < nr ? (STREAM ? __ldcs(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + p)
-                                        : __ldg(reinterpret_cast<const double2 *>(M + (r0 + r) * ld) + p))
-                              : make_double2(0.0, 0.0);
+            for (int r = 0; r < RB; ++r) mc[r] = m[r];
+            PMGR_DENSE_LOAD(p + W * 32)
 #pragma unroll
-            for (int r = 0; r < RB; ++r) acc[r] = fma(m[r].y, xv.y, fma(m[r].x, xv.x, acc[r]));
+            for (int r = 0; r < RB; ++r) acc[r] = fma(mc[r].y, xv.y, fma(mc[r].x, xv.x, acc[r]));
         }
+#undef PMGR_DENSE_LOAD
         if ((n & 1) && warp == 0 && lane == 0) {
             const double xl = __ldg(x + n - 1);
 #pragma unroll
@@ -407,6 +453,8 @@ __global__ void __launch_bounds__(256) k_dense_matvec(const double *__restrict__
                 if (r < nr) acc[r] = fma(__ldg(M + (r0 + r) * ld + n - 1), xl, acc[r]);
         }
     } else {
+        pdl_wait();
+        if (trigger) pdl_trigger();
         for (int64_t c = warp * 32 + lane; c < n; c += W * 32) {
             const double xv = __ldg(x + c);
             double m[RB];
@@ -440,9 +488,10 @@ __global__ void k_gather(const double *__restrict__ src, const int64_t *__restri
 }
 __global__ void k_scale_gather(const double *__restrict__ src, const int64_t *__restrict__ idx,
                                const double *__restrict__ d, int64_t n, double *__restrict__ dst) {
-    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) dst[i] = d[i] * src[idx[i]];
+    const int64_t k = i < n ? idx[i] : 0;  // constant index map: before the wait
+    pdl_wait();
+    if (i < n) dst[i] = d[i] * src[k];
 }
 __global__ void k_zero(double *x, int64_t n) {
     pdl_wait();
@@ -501,10 +550,11 @@ namespace {
 __global__ void k_gather_div(const double *__restrict__ v, const int64_t *__restrict__ rows,
                              const double *__restrict__ d, int64_t n, double *__restrict__ bo,
                              double *__restrict__ xo) {
-    pdl_wait();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t row = i < n ? rows[i] : 0;  // constant index map: before the wait
+    pdl_wait();
     if (i < n) {
-        const double t = v[rows[i]];
+        const double t = v[row];
         bo[i] = t;
         xo[i] = t / d[i];
     }
@@ -561,21 +611,22 @@ void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld
         return e ? atoi(e) : 8;
     }();
     const unsigned blocks = (unsigned)((nrows + rb - 1) / rb);
+    const int trig = (int64_t)((nrows + 7) / 8) <= (int64_t)trigger_blocks_per_sm() * num_sms() ? 1 : 0;
     if (ld % 2 == 0 && stream) {
         if (rb == 4)
-            launch_pdl(k_dense_matvec<true, true, 4>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+            launch_pdl(k_dense_matvec<true, true, 4>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y, trig);
         else if (rb == 2)
-            launch_pdl(k_dense_matvec<true, true, 2>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+            launch_pdl(k_dense_matvec<true, true, 2>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y, trig);
         else if (rb == 16)
-            launch_pdl(k_dense_matvec<true, true, 16>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+            launch_pdl(k_dense_matvec<true, true, 16>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y, trig);
         else
-            launch_pdl(k_dense_matvec<true, true, 8>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+            launch_pdl(k_dense_matvec<true, true, 8>, dim3(blocks), dim3(256), 0, s, M, nrows, ncols, ld, x, y, trig);
     } else if (ld % 2 == 0) {
         const unsigned b8 = (unsigned)((nrows + 7) / 8);
-        launch_pdl(k_dense_matvec<true>, dim3(b8), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+        launch_pdl(k_dense_matvec<true>, dim3(b8), dim3(256), 0, s, M, nrows, ncols, ld, x, y, trig);
     } else {
         const unsigned b8 = (unsigned)((nrows + 7) / 8);
-        launch_pdl(k_dense_matvec<false>, dim3(b8), dim3(256), 0, s, M, nrows, ncols, ld, x, y);
+        launch_pdl(k_dense_matvec<false>, dim3(b8), dim3(256), 0, s, M, nrows, ncols, ld, x, y, trig);
     }
     PMGR_LAUNCHED();
 }
