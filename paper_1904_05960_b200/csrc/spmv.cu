@@ -205,6 +205,121 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, i
         op.out(3 * I + lane + row_off, lane == 0 ? a0 : lane == 1 ? a1 : a2);
 }
 
+// Software-pipelined variant: a grid of resident warps strides over the
+// row triples; the next triple's row bounds are fetched two triples ahead
+// and its first batch of blocks is issued before the current triple's x
+// gathers are consumed, so every warp keeps one triple's stream in flight
+// instead of paying row-bound, stream and gather latencies in sequence.
+template <class Op, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_bsr3p(int64_t ntrip, int64_t nb, int64_t n,
+                                                     const int64_t *__restrict__ bro,
+                                                     const int32_t *__restrict__ bci, const double *__restrict__ bval,
+                                                     const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
+                                                     const double *__restrict__ rv, Op op, int64_t row_off,
+                                                     int trigger) {
+    const int lane = threadIdx.x & 31;
+    const int kk = lane / 3, c = lane - 3 * kk;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int cc[3];
+    double vv[3][3];
+    int64_t k0 = 0, k1 = 0;
+#define PMGR_BSR3P_BATCH(KB, K1, CC, VV)                                                  \
+    _Pragma("unroll") for (int t = 0; t < 3; ++t) {                                      \
+        const int64_t k = (KB) + kk + 10 * t;                                            \
+        const bool ok = lane < 30 && k < (K1);                                           \
+        CC[t] = ok ? __ldg(bci + k) : -1;                                                \
+        const double *p = bval + 9 * k + 3 * c;                                          \
+        _Pragma("unroll") for (int r = 0; r < 3; ++r) VV[t][r] = ok ? __ldg(p + r) : 0.0; \
+    }
+    if (I < nb) {
+        k0 = __ldg(bro + I);
+        k1 = __ldg(bro + I + 1);
+    }
+    PMGR_BSR3P_BATCH(k0, k1, cc, vv)
+    // bounds of the next triple
+    int64_t n0 = 0, n1 = 0;
+    if (I + nw < nb) {
+        n0 = __ldg(bro + I + nw);
+        n1 = __ldg(bro + I + nw + 1);
+    }
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    for (; I < ntrip; I += nw) {
+        double xv[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) xv[t] = cc[t] >= 0 ? op.x(3 * cc[t] + c) : 0.0;
+        // issue the next triple's first batch (and the bounds after it)
+        int ncc[3];
+        double nvv[3][3];
+        PMGR_BSR3P_BATCH(n0, n1, ncc, nvv)
+        const int64_t c0 = k0, c1 = k1;
+        k0 = n0;
+        k1 = n1;
+        n0 = n1 = 0;
+        if (I + 2 * nw < nb) {
+            n0 = __ldg(bro + I + 2 * nw);
+            n1 = __ldg(bro + I + 2 * nw + 1);
+        }
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            if (cc[t] >= 0) {
+                a0 = fma(vv[t][0], xv[t], a0);
+                a1 = fma(vv[t][1], xv[t], a1);
+                a2 = fma(vv[t][2], xv[t], a2);
+            }
+        }
+        // rows with more than 30 blocks: the rest unpipelined
+        for (int64_t kb = c0 + 30; kb < c1; kb += 30) {
+            PMGR_BSR3P_BATCH(kb, c1, cc, vv)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                if (cc[t] >= 0) {
+                    const double x = op.x(3 * cc[t] + c);
+                    a0 = fma(vv[t][0], x, a0);
+                    a1 = fma(vv[t][1], x, a1);
+                    a2 = fma(vv[t][2], x, a2);
+                }
+            }
+        }
+        if (rro != nullptr) {
+            const int g = lane / 10, gl = lane - 10 * g;
+            const int64_t row = 3 * I + g;
+            if (g < 3 && row < n) {
+                const int64_t q1 = __ldg(rro + row + 1);
+                double t0 = 0.0, t1 = 0.0;
+                int64_t q = __ldg(rro + row) + gl;
+                for (; q + 10 < q1; q += 20) {
+                    const double v0 = __ldg(rv + q), v1 = __ldg(rv + q + 10);
+                    const int e0 = __ldg(rci + q), e1 = __ldg(rci + q + 10);
+                    t0 = fma(v0, op.x(e0), t0);
+                    t1 = fma(v1, op.x(e1), t1);
+                }
+                if (q < q1) t0 = fma(__ldg(rv + q), op.x(__ldg(rci + q)), t0);
+                const double t = t0 + t1;
+                if (g == 0) a0 += t;
+                else if (g == 1) a1 += t;
+                else a2 += t;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a0 += __shfl_xor_sync(FULL, a0, o);
+            a1 += __shfl_xor_sync(FULL, a1, o);
+            a2 += __shfl_xor_sync(FULL, a2, o);
+        }
+        if (lane < 3 && 3 * I + lane < n) op.out(3 * I + lane + row_off, lane == 0 ? a0 : lane == 1 ? a1 : a2);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            cc[t] = ncc[t];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) vv[t][r] = nvv[t][r];
+        }
+    }
+#undef PMGR_BSR3P_BATCH
+}
+
 struct OpY {
     const double *xv;
     double *y;
@@ -354,7 +469,29 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
             const char *e = getenv("PMGR_BSR_MINB");
             return e ? atoi(e) : 8;
         }();
-        if (minb == 8)
+        // PMGR_BSR_PIPE: the software-pipelined variant with that many
+        // blocks per SM (2..4; default 4), a resident grid striding over the
+        // triples, for pure block operators (the level-0 F-relaxation sweeps:
+        // 24.8 -> 22.3 us at C2); operators with a CSR remainder (A0) measured
+        // faster on the one-triple-per-warp kernel
+        static const int pipe = [] {
+            const char *e = getenv("PMGR_BSR_PIPE");
+            return e ? atoi(e) : 4;
+        }();
+        if (pipe >= 2 && pipe <= 4 && A.rro == nullptr) {
+            const int64_t want = (int64_t)pipe * num_sms();
+            const unsigned pg = (unsigned)((int64_t)grid < want ? (int64_t)grid : want);
+            const int ptrig = pg <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
+            if (pipe == 2)
+                launch_pdl(k_bsr3p<Op, 2>, dim3(pg), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
+                           A.rro, A.rci, A.rv, op, A.row_off, ptrig);
+            else if (pipe == 3)
+                launch_pdl(k_bsr3p<Op, 3>, dim3(pg), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
+                           A.rro, A.rci, A.rv, op, A.row_off, ptrig);
+            else
+                launch_pdl(k_bsr3p<Op, 4>, dim3(pg), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
+                           A.rro, A.rci, A.rv, op, A.row_off, ptrig);
+        } else if (minb == 8)
             launch_pdl(k_bsr3<Op, false, 8>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
                        A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
         else if (bstream == 2 || (bstream == 1 && A.rro != nullptr))
