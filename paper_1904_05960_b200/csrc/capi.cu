@@ -209,7 +209,11 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
         auto h = pmgr::mgr_build(A->m, field_of, entity_of, levels, nlevels, *cfg, S(stream));
         // solve-phase block copy of A0 for the Krylov SpMV (node-blocked F prefix)
         if (h->block_prefix > 0 && A->m->nbrows == 0) {
-            pmgr::csr_make_bsr3(*A->m, h->block_prefix, h->block_prefix, S(stream));
+            static const bool share = !(getenv("PMGR_NO_BSR_SHARE") && getenv("PMGR_NO_BSR_SHARE")[0] != '0');
+            if (share && h->block_src)
+                pmgr::csr_make_bsr3_shared(*A->m, h->block_prefix, h->block_src, S(stream));
+            else
+                pmgr::csr_make_bsr3(*A->m, h->block_prefix, h->block_prefix, S(stream));
             PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         }
         *out = h.release();

@@ -241,9 +241,15 @@ struct Csr {
     DBuf<double> bval, rv;
     int64_t long_len = 0, nlong = 0;
     DBuf<int32_t> lrows;
+    // blocks shared with another operator whose blocks are this one's block
+    // prefix (A0 and its level-0 A_FF = A_uu: one copy of the displacement
+    // blocks, so the Krylov SpMV re-reads what the last F-relaxation sweep
+    // left in L2)
+    std::shared_ptr<const Csr> blk_src;
     CsrView view() const {
-        return CsrView{nrows,  ncols,  nnz,     ro.p,  ci.p,  v.p,    maxrow, row_off,  lanes, ci16.p,
-                       nbrows, nblocks, nrem,   bro.p, bci.p, bval.p, rro.p,  rci.p,    rv.p,  long_len,
+        const Csr &b = blk_src ? *blk_src : *this;
+        return CsrView{nrows,  ncols,  nnz,     ro.p,    ci.p,    v.p,      maxrow, row_off,  lanes, ci16.p,
+                       nbrows, nblocks, nrem,   b.bro.p, b.bci.p, b.bval.p, rro.p,  rci.p,    rv.p,  long_len,
                        nlong,  lrows.p};
     }
 };
@@ -254,6 +260,9 @@ struct Csr {
 struct DistSetup;
 void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool force = false,
                    const DistSetup *dist = nullptr);
+// the block-prefix copy of A reusing src's blocks (src: a pure BSR3 operator
+// equal to A's leading prefix x prefix block); builds only A's remainder
+void csr_make_bsr3_shared(Csr &A, int64_t prefix, std::shared_ptr<const Csr> src, cudaStream_t s);
 // B = P A P^T (row i of B = row perm[i] of A), columns re-sorted
 std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_host, cudaStream_t s);
 

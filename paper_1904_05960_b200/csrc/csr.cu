@@ -637,6 +637,33 @@ void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool forc
     A.nrem = nrem;
 }
 
+void csr_make_bsr3_shared(Csr &A, int64_t prefix, std::shared_ptr<const Csr> src, cudaStream_t s) {
+    if (!src || src->nbrows <= 0 || src->rro.p || 3 * src->nbrows != prefix || prefix > A.nrows ||
+        prefix > A.ncols || src->blk_src) {
+        csr_make_bsr3(A, prefix, prefix, s);
+        return;
+    }
+    const int64_t n = A.nrows;
+    TBuf<int64_t> rc(n, s);
+    k_rem_count<<<grid_for(n, 128), 128, 0, s>>>(n, prefix, (int32_t)prefix, A.ro.p, A.ci.p, rc.p);
+    PMGR_LAUNCHED();
+    A.rro.alloc(n + 1);
+    const int64_t nrem = exclusive_scan_total(rc.p, A.rro.p, n, s);
+    if (nrem == 0) {
+        A.rro.release();
+    } else {
+        A.rci.alloc(nrem);
+        A.rv.alloc(nrem);
+        k_rem_fill<<<grid_for(n, 128), 128, 0, s>>>(n, prefix, (int32_t)prefix, A.ro.p, A.ci.p, A.v.p, A.rro.p,
+                                                    A.rci.p, A.rv.p);
+        PMGR_LAUNCHED();
+    }
+    A.blk_src = std::move(src);
+    A.nbrows = A.blk_src->nbrows;
+    A.nblocks = A.blk_src->nblocks;
+    A.nrem = nrem;
+}
+
 void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {
     B.alloc(A.nrows, A.ncols, A.nnz);
     PMGR_CUDA(cudaMemcpyAsync(B.ro.p, A.ro, sizeof(int64_t) * (A.nrows + 1), cudaMemcpyDeviceToDevice, s));

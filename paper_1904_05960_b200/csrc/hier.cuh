@@ -176,6 +176,7 @@ struct pmgr_mgr {
     int32_t f_relax_post = 0;
     int64_t n = 0;
     int64_t block_prefix = 0;  // level-0 F rows: a node-blocked prefix of A0 (0: none)
+    std::shared_ptr<const pmgr::Csr> block_src;  // level-0 A_FF with its BSR3 blocks
     bool dist = false;         // a rank's row slice of a hierarchy (dist.cu)
     pmgr::DBuf<double> tz;  // terminal scratch
 };

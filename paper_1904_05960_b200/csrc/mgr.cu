@@ -458,7 +458,10 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             // F rows first, then C rows: the same blocks lead A0 itself
             bool prefix = true;
             for (int64_t i = 0; i < n && prefix; ++i) prefix = (((sp.c_mask >> (fo[i] & 63)) & 1ull) != 0) == (i >= L.nf);
-            if (prefix) h->block_prefix = L.nf;
+            if (prefix) {
+                h->block_prefix = L.nf;
+                if (!dd) h->block_src = A_ff;
+            }
         }
         ds_finalize(dC.get(), L.A_cf, s);
         if (need_dinv) {

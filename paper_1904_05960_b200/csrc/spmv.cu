@@ -127,10 +127,10 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
 }
 
 // Block-prefix SpMV: a warp per row triple.  Triples inside the node-blocked
-// prefix stream their 3x3 blocks (column-major): lane 3k+c (k < 10) owns
-// column c of every 10th block -- one column index, one x gather and three
-// contiguous values feeding the three row sums, 76 B per 9 entries instead
-// of CSR's 108 B.  Remainder entries (coupling columns, rows past the
+// prefix stream their 3x3 blocks: lane 3k+c (k < 10) owns column c of every
+// 10th block -- one column index, one x gather and three values feeding the
+// three row sums, 76 B per 9 entries instead of CSR's 108 B (blocks stored
+// column-major).  Remainder entries (coupling columns, rows past the
 // prefix) are read as CSR by three 10-lane groups, one per row.
 template <class Op, bool STREAM = false, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
@@ -189,6 +189,124 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, i
                 t1 = fma(v1, op.x(c1), t1);
             }
             if (q < q1) t0 = fma(ldv<STREAM>(rv + q), op.x(ldc<STREAM>(rci + q)), t0);
+            const double t = t0 + t1;
+            if (g == 0) a0 += t;
+            else if (g == 1) a1 += t;
+            else a2 += t;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(FULL, a0, o);
+        a1 += __shfl_xor_sync(FULL, a1, o);
+        a2 += __shfl_xor_sync(FULL, a2, o);
+    }
+    if (I < ntrip && lane < 3 && 3 * I + lane < n)
+        op.out(3 * I + lane + row_off, lane == 0 ? a0 : lane == 1 ? a1 : a2);
+}
+
+// Operators with a CSR remainder (A0: displacement blocks plus the coupling
+// columns and the flow rows): the same per-row arithmetic as k_bsr3, but the
+// remainder's row bounds are read before the PDL wait and its first four
+// entries per lane are issued together with the first block batch, so a
+// warp pays one load round trip and one gather round trip instead of two of
+// each.  Summation order (and hence every bit) matches k_bsr3.
+template <class Op, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_bsr3r(int64_t ntrip, int64_t nb, int64_t n,
+                                                     const int64_t *__restrict__ bro,
+                                                     const int32_t *__restrict__ bci, const double *__restrict__ bval,
+                                                     const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
+                                                     const double *__restrict__ rv, Op op, int64_t row_off,
+                                                     int trigger) {
+    const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int kk = lane / 3, c = lane - 3 * kk;
+    const int g = lane / 10, gl = lane - 10 * g;
+    const int64_t row = 3 * I + g;
+    const bool rok = g < 3 && I < ntrip && row < n;
+    int64_t k0 = 0, k1 = 0, q0 = 0, q1 = 0;
+    if (I < nb) {
+        k0 = __ldg(bro + I);
+        k1 = __ldg(bro + I + 1);
+    }
+    if (rok) {
+        q0 = __ldg(rro + row) + gl;
+        q1 = __ldg(rro + row + 1);
+    }
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    int cc[3];
+    double vv[3][3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const int64_t k = k0 + kk + 10 * t;
+        const bool ok = lane < 30 && k < k1;
+        cc[t] = ok ? __ldg(bci + k) : -1;
+        const double *p = bval + 9 * k + 3 * c;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) vv[t][r] = ok ? __ldg(p + r) : 0.0;
+    }
+    int rc[4];
+    double rvv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + 10 * u;
+        const bool ok = q < q1;
+        rc[u] = ok ? __ldg(rci + q) : -1;
+        rvv[u] = ok ? __ldg(rv + q) : 0.0;
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    {
+        double xv[3], rx[4];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) xv[t] = cc[t] >= 0 ? op.x(3 * cc[t] + c) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rx[u] = rc[u] >= 0 ? op.x(rc[u]) : 0.0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            if (cc[t] >= 0) {
+                a0 = fma(vv[t][0], xv[t], a0);
+                a1 = fma(vv[t][1], xv[t], a1);
+                a2 = fma(vv[t][2], xv[t], a2);
+            }
+        }
+        // rows with more than 30 blocks
+        for (int64_t kb = k0 + 30; kb < k1; kb += 30) {
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int64_t k = kb + kk + 10 * t;
+                const bool ok = lane < 30 && k < k1;
+                cc[t] = ok ? __ldg(bci + k) : -1;
+                const double *p = bval + 9 * k + 3 * c;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) vv[t][r] = ok ? __ldg(p + r) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                if (cc[t] >= 0) {
+                    const double x = op.x(3 * cc[t] + c);
+                    a0 = fma(vv[t][0], x, a0);
+                    a1 = fma(vv[t][1], x, a1);
+                    a2 = fma(vv[t][2], x, a2);
+                }
+            }
+        }
+        if (rok) {
+            // k_bsr3's order: entries gl, gl+20, ... into t0 and gl+10,
+            // gl+30, ... into t1
+            double t0 = 0.0, t1 = 0.0;
+            if (rc[0] >= 0) t0 = fma(rvv[0], rx[0], t0);
+            if (rc[1] >= 0) t1 = fma(rvv[1], rx[1], t1);
+            if (rc[2] >= 0) t0 = fma(rvv[2], rx[2], t0);
+            if (rc[3] >= 0) t1 = fma(rvv[3], rx[3], t1);
+            int64_t q = q0 + 40;
+            for (; q + 10 < q1; q += 20) {
+                const double v0 = __ldg(rv + q), v1 = __ldg(rv + q + 10);
+                const int e0 = __ldg(rci + q), e1 = __ldg(rci + q + 10);
+                t0 = fma(v0, op.x(e0), t0);
+                t1 = fma(v1, op.x(e1), t1);
+            }
+            if (q < q1) t0 = fma(__ldg(rv + q), op.x(__ldg(rci + q)), t0);
             const double t = t0 + t1;
             if (g == 0) a0 += t;
             else if (g == 1) a1 += t;
@@ -478,7 +596,23 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
             const char *e = getenv("PMGR_BSR_PIPE");
             return e ? atoi(e) : 4;
         }();
-        if (pipe >= 2 && pipe <= 4 && A.rro == nullptr) {
+        // PMGR_BSR_RMINB: blocks per SM of k_bsr3r for operators with a
+        // remainder (0: the plain k_bsr3)
+        static const int rminb = [] {
+            const char *e = getenv("PMGR_BSR_RMINB");
+            return e ? atoi(e) : 4;
+        }();
+        if (A.rro != nullptr && (rminb == 4 || rminb == 6 || rminb == 8)) {
+            if (rminb == 4)
+                launch_pdl(k_bsr3r<Op, 4>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
+                           A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+            else if (rminb == 6)
+                launch_pdl(k_bsr3r<Op, 6>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
+                           A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+            else
+                launch_pdl(k_bsr3r<Op, 8>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
+                           A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+        } else if (pipe >= 2 && pipe <= 4 && A.rro == nullptr) {
             const int64_t want = (int64_t)pipe * num_sms();
             const unsigned pg = (unsigned)((int64_t)grid < want ? (int64_t)grid : want);
             const int ptrig = pg <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
