@@ -67,6 +67,36 @@ const pmgr::AmgLevel &amg_level(const pmgr_amg *h, int32_t level) {
 }
 }  // namespace
 
+namespace {
+// per-thread grow-only pinned staging buffer for the host-array GMRES entry
+struct PinnedStage {
+    void *p = nullptr;
+    size_t cap = 0;
+    ~PinnedStage() {
+        if (p) cudaFreeHost(p);
+    }
+};
+double *pinned_stage(size_t bytes) {
+    thread_local PinnedStage st;
+    if (st.cap < bytes) {
+        if (st.p) cudaFreeHost(st.p);
+        st.p = nullptr;
+        st.cap = 0;
+        PMGR_CUDA(cudaMallocHost(&st.p, bytes));
+        st.cap = bytes;
+    }
+    return static_cast<double *>(st.p);
+}
+bool is_pinned(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
 extern "C" {
 
 int pmgr_version(void) { return 1; }
@@ -304,15 +334,33 @@ int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_host, double
         require(A && cfg && stats && b_host && x_host, "NULL argument");
         require(cfg->restart <= 1000, "restart above 1000 is not supported");
         const int64_t n = A->m->nrows;
+        const size_t bytes = sizeof(double) * (size_t)n;
         pmgr::TBuf<double> b(n, S(stream)), x(n, S(stream));
-        PMGR_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, S(stream)));
-        if (nonzero_x0)
-            PMGR_CUDA(cudaMemcpyAsync(x.p, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, S(stream)));
-        else
-            PMGR_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, S(stream)));
+        // pageable caller arrays go through a pinned staging buffer (one host
+        // memcpy + a DMA at full link speed instead of the driver's chunked
+        // pageable path); pinned ones are copied directly
+        double *stage = pinned_stage(bytes);
+        auto h2d = [&](double *dst, const double *src) {
+            if (is_pinned(src)) {
+                PMGR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream)));
+            } else {
+                PMGR_CUDA(cudaStreamSynchronize(S(stream)));  // the stage is free
+                std::memcpy(stage, src, bytes);
+                PMGR_CUDA(cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyHostToDevice, S(stream)));
+            }
+        };
+        h2d(b.p, b_host);
+        if (nonzero_x0) h2d(x.p, x_host);
+        else PMGR_CUDA(cudaMemsetAsync(x.p, 0, bytes, S(stream)));
         pmgr::gmres_device(A, M, b.p, x.p, nonzero_x0, *cfg, *stats, history_host, history_cap, S(stream));
-        PMGR_CUDA(cudaMemcpyAsync(x_host, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(stream)));
-        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        if (is_pinned(x_host)) {
+            PMGR_CUDA(cudaMemcpyAsync(x_host, x.p, bytes, cudaMemcpyDeviceToHost, S(stream)));
+            PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        } else {
+            PMGR_CUDA(cudaMemcpyAsync(stage, x.p, bytes, cudaMemcpyDeviceToHost, S(stream)));
+            PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+            std::memcpy(x_host, stage, bytes);
+        }
     });
 }
 

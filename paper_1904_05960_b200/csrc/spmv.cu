@@ -36,7 +36,7 @@ __device__ __forceinline__ int ldc(const uint16_t *p) {
                         : __ldg(reinterpret_cast<const unsigned short *>(p)));
 }
 
-template <int G, bool STREAM, class Op, class IT>
+template <int G, bool STREAM, class Op, class IT, int U = 2>
 __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__restrict__ ro,
                                               const IT *__restrict__ ci,
                                               const double *__restrict__ v, Op op, int64_t row_off, int trigger,
@@ -92,34 +92,41 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
             e = b;
         }
     }
-    // two independent accumulators keep two (value, column, x) load chains
-    // in flight per lane; matrix streams use evict-first loads so the
-    // gathered vector stays in L2
+    // U independent accumulators keep U (value, column, x) load chains in
+    // flight per lane (U = 4 for the long-row lane groups); the first U
+    // entries per lane are loaded before the wait, and every later round
+    // issues its U predicated loads at once, so a row of up to U G entries
+    // costs one gather round trip after the wait
     int64_t q = b + lane;
-    const bool h0 = q < e, h1 = q + G < e;
-    double v0 = 0.0, v1 = 0.0;
-    int c0 = 0, c1 = 0;
-    if (h0) {
-        v0 = ldv<STREAM>(v + q);
-        c0 = ldc<STREAM>(ci + q);
-    }
-    if (h1) {
-        v1 = ldv<STREAM>(v + q + G);
-        c1 = ldc<STREAM>(ci + q + G);
+    double vv[U];
+    int cc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const bool h = q + u * G < e;
+        vv[u] = h ? ldv<STREAM>(v + q + u * G) : 0.0;
+        cc[u] = h ? ldc<STREAM>(ci + q + u * G) : -1;
     }
     pdl_wait();
     if (trigger) pdl_trigger();
-    double s0 = 0.0, s1 = 0.0;
-    if (h0) s0 = fma(v0, op.x(c0), s0);
-    if (h1) s1 = fma(v1, op.x(c1), s1);
-    q += 2 * G;
-    for (; q + G < e; q += 2 * G) {
-        const double v0 = ldv<STREAM>(v + q), v1 = ldv<STREAM>(v + q + G);
-        const int c0 = ldc<STREAM>(ci + q), c1 = ldc<STREAM>(ci + q + G);
-        s0 = fma(v0, op.x(c0), s0);
-        s1 = fma(v1, op.x(c1), s1);
+    double sa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sa[u] = cc[u] >= 0 ? fma(vv[u], op.x(cc[u]), 0.0) : 0.0;
+    for (q += U * G; q < e; q += U * G) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool h = q + u * G < e;
+            vv[u] = h ? ldv<STREAM>(v + q + u * G) : 0.0;
+            cc[u] = h ? ldc<STREAM>(ci + q + u * G) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (cc[u] >= 0) sa[u] = fma(vv[u], op.x(cc[u]), sa[u]);
     }
-    if (q < e) s0 = fma(ldv<STREAM>(v + q), op.x(ldc<STREAM>(ci + q)), s0);
+    double s0 = sa[0], s1 = sa[1];
+    if constexpr (U == 4) {
+        s0 += sa[2];
+        s1 += sa[3];
+    }
     double s = s0 + s1;
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
@@ -132,11 +139,55 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
 // three row sums, 76 B per 9 entries instead of CSR's 108 B (blocks stored
 // column-major).  Remainder entries (coupling columns, rows past the
 // prefix) are read as CSR by three 10-lane groups, one per row.
+//
+// tail_blk0 < gridDim.x: the rows past the prefix (A0's flow rows, no blocks)
+// are summed by the blocks from tail_blk0 on, 8 lanes per row with four
+// entries per lane in flight, instead of by 10-lane groups of row triples.
 template <class Op, bool STREAM = false, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, int64_t n, const int64_t *__restrict__ bro,
                                               const int32_t *__restrict__ bci, const double *__restrict__ bval,
                                               const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
-                                              const double *__restrict__ rv, Op op, int64_t row_off, int trigger) {
+                                              const double *__restrict__ rv, Op op, int64_t row_off, int trigger,
+                                              unsigned tail_blk0 = 0xffffffffu) {
+    if (blockIdx.x >= tail_blk0) {
+        const int gl = threadIdx.x & 7;
+        const int64_t row = 3 * nb + ((int64_t)(blockIdx.x - tail_blk0) * blockDim.x + threadIdx.x) / 8;
+        const bool act = row < n;
+        int64_t q = 0, e = 0;
+        if (act) {
+            q = __ldg(rro + row) + gl;
+            e = __ldg(rro + row + 1);
+        }
+        double vv[4];
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool h = q + 8 * u < e;
+            vv[u] = h ? ldv<STREAM>(rv + q + 8 * u) : 0.0;
+            cc[u] = h ? ldc<STREAM>(rci + q + 8 * u) : -1;
+        }
+        pdl_wait();
+        if (trigger) pdl_trigger();
+        double sa[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sa[u] = cc[u] >= 0 ? fma(vv[u], op.x(cc[u]), 0.0) : 0.0;
+        for (q += 32; q < e; q += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool h = q + 8 * u < e;
+                vv[u] = h ? ldv<STREAM>(rv + q + 8 * u) : 0.0;
+                cc[u] = h ? ldc<STREAM>(rci + q + 8 * u) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (cc[u] >= 0) sa[u] = fma(vv[u], op.x(cc[u]), sa[u]);
+        }
+        double t = (sa[0] + sa[2]) + (sa[1] + sa[3]);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o, 8);
+        if (act && gl == 0) op.out(row + row_off, t);
+        return;
+    }
     const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int kk = lane / 3, c = lane - 3 * kk;
@@ -532,9 +583,22 @@ void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_
     // let the next kernel's launch overlap this one only when this grid is a
     // single wave (its early blocks must not crowd out ours)
     const int trigger = grid <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
-    if (stream)
+    // PMGR_SPMV_U4: lane groups of at least this many lanes keep four
+    // entries per lane in flight (0: always two)
+    static const int u4 = [] {
+        const char *e = getenv("PMGR_SPMV_U4");
+        return e ? atoi(e) : 16;
+    }();
+    const bool four = u4 > 0 && G >= u4;
+    if (stream && four)
+        launch_pdl(k_spmv<G, true, Op, IT, 4>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op,
+                   A.row_off, trigger, A.long_len, A.lrows, nshort);
+    else if (stream)
         launch_pdl(k_spmv<G, true, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
                    trigger, A.long_len, A.lrows, nshort);
+    else if (four)
+        launch_pdl(k_spmv<G, false, Op, IT, 4>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op,
+                   A.row_off, trigger, A.long_len, A.lrows, nshort);
     else
         launch_pdl(k_spmv<G, false, Op, IT>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op, A.row_off,
                    trigger, A.long_len, A.lrows, nshort);
@@ -600,9 +664,20 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
         // remainder (0: the plain k_bsr3)
         static const int rminb = [] {
             const char *e = getenv("PMGR_BSR_RMINB");
-            return e ? atoi(e) : 4;
+            return e ? atoi(e) : 0;  // C2 +-0 %, C4 outer SpMV 2.37 -> 2.69 ms: off
         }();
-        if (A.rro != nullptr && (rminb == 4 || rminb == 6 || rminb == 8)) {
+        // PMGR_BSR_TAIL=0: rows past the prefix as 10-lane groups of triples
+        static const int tailsplit = [] {
+            const char *e = getenv("PMGR_BSR_TAIL");
+            return e ? atoi(e) : 1;
+        }();
+        if (A.rro != nullptr && minb == 8 && tailsplit && A.nrows > 3 * A.nbrows && rminb == 0) {
+            const unsigned gb = grid_for(A.nbrows * 32, 256);
+            const unsigned gt = grid_for((A.nrows - 3 * A.nbrows) * 8, 256);
+            const int ttrig = gb + gt <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
+            launch_pdl(k_bsr3<Op, false, 8>, dim3(gb + gt), dim3(256), 0, s, A.nbrows, A.nbrows, A.nrows, A.bro,
+                       A.bci, A.bval, A.rro, A.rci, A.rv, op, A.row_off, ttrig, gb);
+        } else if (A.rro != nullptr && (rminb == 4 || rminb == 6 || rminb == 8)) {
             if (rminb == 4)
                 launch_pdl(k_bsr3r<Op, 4>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
                            A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
@@ -627,13 +702,13 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
                            A.rro, A.rci, A.rv, op, A.row_off, ptrig);
         } else if (minb == 8)
             launch_pdl(k_bsr3<Op, false, 8>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
-                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger, 0xffffffffu);
         else if (bstream == 2 || (bstream == 1 && A.rro != nullptr))
             launch_pdl(k_bsr3<Op, true>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
-                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger);
+                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger, 0xffffffffu);
         else
             launch_pdl(k_bsr3<Op>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
-                       A.rro, A.rci, A.rv, op, A.row_off, trigger);
+                       A.rro, A.rci, A.rv, op, A.row_off, trigger, 0xffffffffu);
         PMGR_LAUNCHED();
         return;
     }
