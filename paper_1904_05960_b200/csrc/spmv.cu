@@ -135,6 +135,97 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t nrows, const int64_t *__re
     if (active && lane == 0) op.out(row + row_off, s);
 }
 
+// Software-pipelined CSR SpMV (G lanes per row, U entries per lane in
+// flight): a resident grid of lane groups strides over the rows; the next
+// row's bounds are fetched two rows ahead and its first U G entries are
+// issued before the current row's gathers are consumed.  Per-row arithmetic
+// is exactly k_spmv<G, ..., U>'s (same lanes, accumulators and reduction).
+template <int G, int U, class Op, class IT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_spmv_pipe(int64_t nrows, const int64_t *__restrict__ ro,
+                                                         const IT *__restrict__ ci, const double *__restrict__ v,
+                                                         Op op, int64_t row_off, int trigger) {
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / G);
+    int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    int64_t b0 = 0, e0 = 0, nb = 0, ne = 0;
+    if (I < nrows) {
+        b0 = __ldg(ro + I);
+        e0 = __ldg(ro + I + 1);
+    }
+    double vv[U];
+    int cc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t q = b0 + lane + G * u;
+        const bool h = q < e0;
+        vv[u] = h ? __ldg(v + q) : 0.0;
+        cc[u] = h ? ldc<false>(ci + q) : -1;
+    }
+    if (I + nw < nrows) {
+        nb = __ldg(ro + I + nw);
+        ne = __ldg(ro + I + nw + 1);
+    }
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    // every lane of a warp runs the same number of iterations (the shuffles
+    // need the whole warp): the loop bound is the warp's first row group's
+    const int64_t warp_first = ((blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) / G);
+    for (int64_t Iw = warp_first; Iw < nrows; Iw += nw, I += nw) {
+        double xs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xs[u] = cc[u] >= 0 ? op.x(cc[u]) : 0.0;
+        double nvv[U];
+        int ncc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = nb + lane + G * u;
+            const bool h = q < ne;
+            nvv[u] = h ? __ldg(v + q) : 0.0;
+            ncc[u] = h ? ldc<false>(ci + q) : -1;
+        }
+        const int64_t cb = b0, ce = e0;
+        b0 = nb;
+        e0 = ne;
+        nb = ne = 0;
+        if (I + 2 * nw < nrows) {
+            nb = __ldg(ro + I + 2 * nw);
+            ne = __ldg(ro + I + 2 * nw + 1);
+        }
+        double sa[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) sa[u] = cc[u] >= 0 ? fma(vv[u], xs[u], 0.0) : 0.0;
+        for (int64_t q = cb + lane + U * G; q < ce; q += U * G) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool h = q + G * u < ce;
+                vv[u] = h ? __ldg(v + q + G * u) : 0.0;
+                cc[u] = h ? ldc<false>(ci + q + G * u) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (cc[u] >= 0) sa[u] = fma(vv[u], op.x(cc[u]), sa[u]);
+        }
+        double s0 = sa[0], s1 = sa[1];
+        if constexpr (U == 4) {
+            s0 += sa[2];
+            s1 += sa[3];
+        }
+        double t = s0 + s1;
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o, G);
+        if (lane == 0 && I < nrows) {
+            Op o = op;
+            o.pre(I + row_off);
+            o.out(I + row_off, t);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            vv[u] = nvv[u];
+            cc[u] = ncc[u];
+        }
+    }
+}
+
 // Block-prefix SpMV: a warp per row triple.  Triples inside the node-blocked
 // prefix stream their 3x3 blocks: lane 3k+c (k < 10) owns column c of every
 // 10th block -- one column index, one x gather and three values feeding the
@@ -630,6 +721,36 @@ void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_
 
 template <int G, class Op>
 void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
+    // PMGR_SPMV_PIPE: blocks per SM of the pipelined warp-per-row kernel for
+    // lane group 32 without block-per-row long rows (0: off)
+    static const int pipe = [] {
+        const char *e = getenv("PMGR_SPMV_PIPE");
+        return e ? atoi(e) : 4;
+    }();
+    static const int u4 = [] {
+        const char *e = getenv("PMGR_SPMV_U4");
+        return e ? atoi(e) : 16;
+    }();
+    // PMGR_SPMV_PIPE_MIN: smallest lane group that takes the pipelined kernel
+    static const int pmin = [] {
+        const char *e = getenv("PMGR_SPMV_PIPE_MIN");
+        return e ? atoi(e) : 32;
+    }();
+    if (G >= 8 && G >= pmin && pipe == 4 && !stream && A.long_len <= 0) {
+        const int64_t want = (int64_t)pipe * num_sms();
+        const unsigned need = grid_for(A.nrows * G, 256);
+        const unsigned pg = (unsigned)((int64_t)need < want ? (int64_t)need : want);
+        const int trig = pg <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
+        const bool four = u4 > 0 && G >= u4;
+        if (four) {
+            if (A.ci16) launch_pdl(k_spmv_pipe<G, 4, Op, uint16_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci16, A.v, op, A.row_off, trig);
+            else launch_pdl(k_spmv_pipe<G, 4, Op, int32_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci, A.v, op, A.row_off, trig);
+        } else {
+            if (A.ci16) launch_pdl(k_spmv_pipe<G, 2, Op, uint16_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci16, A.v, op, A.row_off, trig);
+            else launch_pdl(k_spmv_pipe<G, 2, Op, int32_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci, A.v, op, A.row_off, trig);
+        }
+        return;
+    }
     if (A.ci16) go_t<G>(A, A.ci16, op, stream, s);
     else go_t<G>(A, A.ci, op, stream, s);
 }
