@@ -689,6 +689,18 @@ int trigger_blocks_per_sm() {
     return v;
 }
 
+// operators at least this large (PMGR_SPMV_BIG_NNZ; streamed from HBM, far
+// beyond L2) keep four entries per lane in flight and take the pipelined
+// kernel whatever their lane group: the small, latency-bound levels stay on
+// two entries (more resident warps)
+int64_t big_nnz() {
+    static const int64_t v = [] {
+        const char *e = getenv("PMGR_SPMV_BIG_NNZ");
+        return e ? atoll(e) : (int64_t)1 << 62;  // off: C4 MGR apply 7.87 -> 8.00 ms with 2^25
+    }();
+    return v;
+}
+
 template <int G, class Op, class IT>
 void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_t s) {
     const int block = 256;
@@ -704,7 +716,7 @@ void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_
         const char *e = getenv("PMGR_SPMV_U4");
         return e ? atoi(e) : 16;
     }();
-    const bool four = u4 > 0 && G >= u4;
+    const bool four = (u4 > 0 && G >= u4) || (G >= 4 && A.nnz >= big_nnz());
     if (stream && four)
         launch_pdl(k_spmv<G, true, Op, IT, 4>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op,
                    A.row_off, trigger, A.long_len, A.lrows, nshort);
@@ -736,12 +748,19 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
         const char *e = getenv("PMGR_SPMV_PIPE_MIN");
         return e ? atoi(e) : 32;
     }();
-    if (G >= 8 && G >= pmin && pipe == 4 && !stream && A.long_len <= 0) {
+    // PMGR_SPMV_PIPE_MAXNNZ: the pipelined kernel helps latency-bound levels
+    // (C2: 24.6 -> 24.1 ms) but not HBM-streaming ones (C4 MGR apply 7.76 ->
+    // 7.88 ms), so operators above this size keep the one-row-per-group kernel
+    static const int64_t pmax = [] {
+        const char *e = getenv("PMGR_SPMV_PIPE_MAXNNZ");
+        return e ? atoll(e) : (int64_t)1 << 23;
+    }();
+    if (G >= 8 && (G >= pmin || A.nnz >= big_nnz()) && pipe == 4 && !stream && A.long_len <= 0 && A.nnz <= pmax) {
         const int64_t want = (int64_t)pipe * num_sms();
         const unsigned need = grid_for(A.nrows * G, 256);
         const unsigned pg = (unsigned)((int64_t)need < want ? (int64_t)need : want);
         const int trig = pg <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
-        const bool four = u4 > 0 && G >= u4;
+        const bool four = (u4 > 0 && G >= u4) || A.nnz >= big_nnz();
         if (four) {
             if (A.ci16) launch_pdl(k_spmv_pipe<G, 4, Op, uint16_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci16, A.v, op, A.row_off, trig);
             else launch_pdl(k_spmv_pipe<G, 4, Op, int32_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci, A.v, op, A.row_off, trig);
