@@ -800,7 +800,7 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
         spmv(L.R.view(), L.r.p, h.cb.p, s);
         e = coarse_solve(h, s);
     }
-    spmv_add(L.P.view(), e, L.x.p, s);
+    spmv_add_pre(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_JACOBI : PROF_KINDS, pass, s);
         halo_exchange(L.halo.get(), L.x.p, s);

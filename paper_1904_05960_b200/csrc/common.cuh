@@ -381,6 +381,8 @@ void spmv_jacobi(const CsrView &A, const double *x, const double *b, const doubl
 void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x,
                           double *r, cudaStream_t s);
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s);
+// the same, for call sites whose predecessor kernel does not write x
+void spmv_add_pre(const CsrView &A, const double *e, double *x, cudaStream_t s);
 void spmv_restrict_div(const CsrView &R, const double *r, const double *d, double *b, double *x,
                        cudaStream_t s);
 void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s);

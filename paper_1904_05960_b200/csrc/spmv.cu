@@ -640,6 +640,17 @@ struct OpAdd {
     __device__ void pre(int64_t) {}
     __device__ void out(int64_t i, double s) const { xio[i] += s; }
 };
+// x += P e where the predecessor kernel does not write x (the AMG cycle's
+// prolongation: x was written by the level's pre-sweep, long before), so
+// x_i is read before the PDL wait
+struct OpAddPre {
+    const double *e;
+    double *xio;
+    double xi = 0.0;
+    __device__ double x(int j) const { return __ldg(e + j); }
+    __device__ void pre(int64_t i) { xi = xio[i]; }
+    __device__ void out(int64_t i, double s) const { xio[i] = xi + s; }
+};
 struct OpResidRows {
     const double *zf, *v;
     const int64_t *rows;
@@ -674,9 +685,15 @@ struct OpProlong {
     const int64_t *findex;
     double *z;
     __device__ double x(int j) const { return __ldg(ec + j); }
+    // pre: the F map and z_F (written by this level's F-relaxation, never by
+    // the coarse levels that run between it and this kernel)
     int64_t fi = -1;
-    __device__ void pre(int64_t i) { fi = findex ? __ldg(findex + i) : -1; }
-    __device__ void out(int64_t i, double s) const { z[i] = (fi >= 0 ? zf[fi] : 0.0) + s; }
+    double zfv = 0.0;
+    __device__ void pre(int64_t i) {
+        fi = findex ? __ldg(findex + i) : -1;
+        zfv = fi >= 0 ? zf[fi] : 0.0;
+    }
+    __device__ void out(int64_t i, double s) const { z[i] = zfv + s; }
 };
 
 // a kernel lets its successor launch early (PDL) only when its own grid is
@@ -1082,6 +1099,10 @@ void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, doubl
     if (n == 0) return;
     launch_pdl(k_copy_div, dim3(grid_for(n, 256)), dim3(256), 0, s, b, d, n, bo, xo);
     PMGR_LAUNCHED();
+}
+
+void spmv_add_pre(const CsrView &A, const double *e, double *x, cudaStream_t s) {
+    launch(A, OpAddPre{e, x}, s);
 }
 
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s) {
