@@ -804,7 +804,7 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_JACOBI : PROF_KINDS, pass, s);
         halo_exchange(L.halo.get(), L.x.p, s);
-        spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, y, s);
+        spmv_jacobi_bpre(A, L.x.p, L.b.p, L.dtilde.p, y, s);
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);
         vec_copy(L.x.p, y, A.nrows, s);

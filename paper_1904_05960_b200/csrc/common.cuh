@@ -378,6 +378,9 @@ void spmv(const CsrView &A, const double *x, double *y, cudaStream_t s);
 void spmv_residual(const CsrView &A, const double *x, const double *b, double *r, cudaStream_t s);
 void spmv_jacobi(const CsrView &A, const double *x, const double *b, const double *d,
                  double *xo, cudaStream_t s);
+// the same when the predecessor kernel does not write b
+void spmv_jacobi_bpre(const CsrView &A, const double *x, const double *b, const double *d,
+                 double *xo, cudaStream_t s);
 void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x,
                           double *r, cudaStream_t s);
 void spmv_add(const CsrView &A, const double *e, double *x, cudaStream_t s);

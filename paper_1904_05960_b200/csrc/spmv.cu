@@ -611,6 +611,19 @@ struct OpJacobi {
     __device__ void pre(int64_t i) { di = __ldg(d + i); }
     __device__ void out(int64_t i, double s) const { xo[i] = xv[i] + (b[i] - s) / di; }
 };
+// post-sweep whose right-hand side is not written by the predecessor kernel
+// (the AMG cycle: b_l was written by the restriction, long before)
+struct OpJacobiPre {
+    const double *xv, *b, *d;
+    double *xo;
+    double di = 1.0, bi = 0.0;
+    __device__ double x(int j) const { return __ldg(xv + j); }
+    __device__ void pre(int64_t i) {
+        di = __ldg(d + i);
+        bi = b[i];
+    }
+    __device__ void out(int64_t i, double s) const { xo[i] = xv[i] + (bi - s) / di; }
+};
 struct OpSweep0 {
     const double *b, *d;
     double *xo, *r;
@@ -1048,6 +1061,11 @@ void spmv_residual(const CsrView &A, const double *x, const double *b, double *r
 void spmv_jacobi(const CsrView &A, const double *x, const double *b, const double *d, double *xo,
                  cudaStream_t s) {
     launch(A, OpJacobi{x, b, d, xo}, s);
+}
+
+void spmv_jacobi_bpre(const CsrView &A, const double *x, const double *b, const double *d, double *xo,
+                      cudaStream_t s) {
+    launch(A, OpJacobiPre{x, b, d, xo}, s);
 }
 
 void spmv_sweep0_residual(const CsrView &A, const double *b, const double *d, double *x, double *r,
