@@ -216,6 +216,7 @@ struct CsrView {
     // nlong rows listed in lrows); the lane group then fits the other rows
     int64_t long_len = 0, nlong = 0;
     const int32_t *lrows = nullptr;
+    int lanes_u = 0;  // entries per lane in flight (2 / 4; 0: from this operator's mean)
 };
 
 struct Csr {
@@ -241,6 +242,7 @@ struct Csr {
     DBuf<double> bval, rv;
     int64_t long_len = 0, nlong = 0;
     DBuf<int32_t> lrows;
+    int lanes_u = 0;
     // blocks shared with another operator whose blocks are this one's block
     // prefix (A0 and its level-0 A_FF = A_uu: one copy of the displacement
     // blocks, so the Krylov SpMV re-reads what the last F-relaxation sweep
@@ -250,7 +252,7 @@ struct Csr {
         const Csr &b = blk_src ? *blk_src : *this;
         return CsrView{nrows,  ncols,  nnz,     ro.p,    ci.p,    v.p,      maxrow, row_off,  lanes, ci16.p,
                        nbrows, nblocks, nrem,   b.bro.p, b.bci.p, b.bval.p, rro.p,  rci.p,    rv.p,  long_len,
-                       nlong,  lrows.p};
+                       nlong,  lrows.p, lanes_u};
     }
 };
 
@@ -409,6 +411,10 @@ void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const do
 int spmv_lanes(const CsrView &A);
 // lane group per row for a mean row length (no skew correction)
 int spmv_lanes_mean(double mean);
+// entries per lane the CSR kernel keeps in flight for lane group G (4 when
+// rows average more than two entries per lane); row-distributed copies
+// inherit the global operator's choice (lanes_u) so their sums stay bitwise
+int spmv_u_for(int64_t nnz, int64_t nrows, int G);
 // y[0:nrows) = M[0:nrows, 0:ncols) x (row-distributed collapsed operators)
 void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld, const double *x, double *y,
                        cudaStream_t s);

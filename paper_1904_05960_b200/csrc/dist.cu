@@ -665,6 +665,7 @@ struct Builder {
         csr_finalize(out, s);
         out.row_off = R->off();
         out.lanes = Y.lanes > 0 ? Y.lanes : spmv_lanes(Y.view());
+        out.lanes_u = Y.lanes_u > 0 ? Y.lanes_u : spmv_u_for(Y.nnz, Y.nrows, out.lanes);
         // the same rows take the block-per-row path as in the global operator
         out.long_len = Y.long_len;
         csr_long_rows(out, s);

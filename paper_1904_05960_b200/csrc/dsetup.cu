@@ -466,6 +466,7 @@ void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s) {
     A.long_len = (!no_long && gmax > 16 * gm) ? 16 * gm : 0;
     csr_long_rows(A, s);
     A.lanes = (A.long_len > 0 || gmax <= 16 * gm) ? gm : 32;
+    A.lanes_u = spmv_u_for(gnnz, A.nrows, A.lanes);
 }
 
 int64_t ds_diag_inverse(const Csr &A, int64_t lo, int64_t hi, double *dinv, cudaStream_t s) {

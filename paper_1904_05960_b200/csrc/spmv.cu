@@ -746,7 +746,7 @@ void go_t(const CsrView &A, const IT *ci, const Op &op, bool stream, cudaStream_
         const char *e = getenv("PMGR_SPMV_U4");
         return e ? atoi(e) : 16;
     }();
-    const bool four = (u4 > 0 && G >= u4) || (G >= 4 && A.nnz >= big_nnz());
+    const bool four = A.lanes_u > 0 ? A.lanes_u == 4 : spmv_u_for(A.nnz, A.nrows, G) == 4;
     if (stream && four)
         launch_pdl(k_spmv<G, true, Op, IT, 4>, dim3(grid), dim3(block), 0, s, A.nrows, A.ro, ci, A.v, op,
                    A.row_off, trigger, A.long_len, A.lrows, nshort);
@@ -790,7 +790,7 @@ void go(const CsrView &A, const Op &op, bool stream, cudaStream_t s) {
         const unsigned need = grid_for(A.nrows * G, 256);
         const unsigned pg = (unsigned)((int64_t)need < want ? (int64_t)need : want);
         const int trig = pg <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
-        const bool four = (u4 > 0 && G >= u4) || A.nnz >= big_nnz();
+        const bool four = A.lanes_u > 0 ? A.lanes_u == 4 : spmv_u_for(A.nnz, A.nrows, G) == 4;
         if (four) {
             if (A.ci16) launch_pdl(k_spmv_pipe<G, 4, Op, uint16_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci16, A.v, op, A.row_off, trig);
             else launch_pdl(k_spmv_pipe<G, 4, Op, int32_t, 4>, dim3(pg), dim3(256), 0, s, A.nrows, A.ro, A.ci, A.v, op, A.row_off, trig);
@@ -814,6 +814,23 @@ int spmv_lanes_mean(double mean) {
         return e ? atof(e) : 100.0;
     }();
     return mean <= 3.0 ? 2 : mean <= 12.0 ? 4 : mean <= 48.0 ? 8 : mean <= g32_mean ? 16 : 32;
+}
+
+int spmv_u_for(int64_t nnz, int64_t nrows, int G) {
+    static const int u4 = [] {
+        const char *e = getenv("PMGR_SPMV_U4");
+        return e ? atoi(e) : 16;
+    }();
+    // PMGR_SPMV_U4_MEAN: four entries once rows average more than this many
+    // per lane (C2: 24.11 -> 23.94 ms at 2; 0: lane-group rule only)
+    static const int umean = [] {
+        const char *e = getenv("PMGR_SPMV_U4_MEAN");
+        return e ? atoi(e) : 2;
+    }();
+    if (u4 > 0 && G >= u4) return 4;
+    if (nnz >= big_nnz() && G >= 4) return 4;
+    if (umean > 0 && nrows > 0 && nnz > (int64_t)umean * G * nrows) return 4;
+    return 2;
 }
 
 int spmv_lanes(const CsrView &A) {
