@@ -226,6 +226,51 @@ __global__ void __launch_bounds__(256, MINB) k_spmv_pipe(int64_t nrows, const in
     }
 }
 
+// rows past the block prefix (A0's flow rows): 8 lanes per row, four entries
+// per lane in flight, for the blocks from tail_blk0 on (k_bsr3, k_bsr3p)
+template <bool STREAM, class Op>
+__device__ __forceinline__ void bsr3_tail_rows(int64_t nb, int64_t n, const int64_t *__restrict__ rro,
+                                               const int32_t *__restrict__ rci, const double *__restrict__ rv,
+                                               Op op, int64_t row_off, int trigger, unsigned tail_blk0) {
+    const int gl = threadIdx.x & 7;
+    const int64_t row = 3 * nb + ((int64_t)(blockIdx.x - tail_blk0) * blockDim.x + threadIdx.x) / 8;
+    const bool act = row < n;
+    int64_t q = 0, e = 0;
+    if (act) {
+        q = __ldg(rro + row) + gl;
+        e = __ldg(rro + row + 1);
+    }
+    double vv[4];
+    int cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const bool h = q + 8 * u < e;
+        vv[u] = h ? ldv<STREAM>(rv + q + 8 * u) : 0.0;
+        cc[u] = h ? ldc<STREAM>(rci + q + 8 * u) : -1;
+    }
+    if (act && gl == 0) op.pre(row + row_off);
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    double sa[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sa[u] = cc[u] >= 0 ? fma(vv[u], op.x(cc[u]), 0.0) : 0.0;
+    for (q += 32; q < e; q += 32) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool h = q + 8 * u < e;
+            vv[u] = h ? ldv<STREAM>(rv + q + 8 * u) : 0.0;
+            cc[u] = h ? ldc<STREAM>(rci + q + 8 * u) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (cc[u] >= 0) sa[u] = fma(vv[u], op.x(cc[u]), sa[u]);
+    }
+    double t = (sa[0] + sa[2]) + (sa[1] + sa[3]);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o, 8);
+    if (act && gl == 0) op.out(row + row_off, t);
+}
+
 // Block-prefix SpMV: a warp per row triple.  Triples inside the node-blocked
 // prefix stream their 3x3 blocks: lane 3k+c (k < 10) owns column c of every
 // 10th block -- one column index, one x gather and three values feeding the
@@ -243,43 +288,7 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3(int64_t ntrip, int64_t nb, i
                                               const double *__restrict__ rv, Op op, int64_t row_off, int trigger,
                                               unsigned tail_blk0 = 0xffffffffu) {
     if (blockIdx.x >= tail_blk0) {
-        const int gl = threadIdx.x & 7;
-        const int64_t row = 3 * nb + ((int64_t)(blockIdx.x - tail_blk0) * blockDim.x + threadIdx.x) / 8;
-        const bool act = row < n;
-        int64_t q = 0, e = 0;
-        if (act) {
-            q = __ldg(rro + row) + gl;
-            e = __ldg(rro + row + 1);
-        }
-        double vv[4];
-        int cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const bool h = q + 8 * u < e;
-            vv[u] = h ? ldv<STREAM>(rv + q + 8 * u) : 0.0;
-            cc[u] = h ? ldc<STREAM>(rci + q + 8 * u) : -1;
-        }
-        if (act && gl == 0) op.pre(row + row_off);
-        pdl_wait();
-        if (trigger) pdl_trigger();
-        double sa[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) sa[u] = cc[u] >= 0 ? fma(vv[u], op.x(cc[u]), 0.0) : 0.0;
-        for (q += 32; q < e; q += 32) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const bool h = q + 8 * u < e;
-                vv[u] = h ? ldv<STREAM>(rv + q + 8 * u) : 0.0;
-                cc[u] = h ? ldc<STREAM>(rci + q + 8 * u) : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (cc[u] >= 0) sa[u] = fma(vv[u], op.x(cc[u]), sa[u]);
-        }
-        double t = (sa[0] + sa[2]) + (sa[1] + sa[3]);
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o, 8);
-        if (act && gl == 0) op.out(row + row_off, t);
+        bsr3_tail_rows<STREAM>(nb, n, rro, rci, rv, op, row_off, trigger, tail_blk0);
         return;
     }
     const int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -481,10 +490,15 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3p(int64_t ntrip, int64_t nb, 
                                                      const int32_t *__restrict__ bci, const double *__restrict__ bval,
                                                      const int64_t *__restrict__ rro, const int32_t *__restrict__ rci,
                                                      const double *__restrict__ rv, Op op, int64_t row_off,
-                                                     int trigger) {
+                                                     int trigger, unsigned tail_blk0 = 0xffffffffu) {
+    if (blockIdx.x >= tail_blk0) {
+        bsr3_tail_rows<false>(nb, n, rro, rci, rv, op, row_off, trigger, tail_blk0);
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const int kk = lane / 3, c = lane - 3 * kk;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const unsigned nbr = tail_blk0 < gridDim.x ? tail_blk0 : gridDim.x;  // block-role blocks
+    const int64_t nw = (int64_t)nbr * (blockDim.x >> 5);
     int64_t I = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int cc[3];
     double vv[3][3];
@@ -882,7 +896,24 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
             const char *e = getenv("PMGR_BSR_TAIL");
             return e ? atoi(e) : 1;
         }();
-        if (A.rro != nullptr && minb == 8 && tailsplit && A.nrows > 3 * A.nbrows && rminb == 0) {
+        // PMGR_BSR_PIPE_A0=1: A0's block role as the pipelined kernel (resident
+        // grid), its flow rows as extra blocks of the same launch
+        static const int pipe_a0 = [] {
+            const char *e = getenv("PMGR_BSR_PIPE_A0");
+            return e ? atoi(e) : 1;
+        }();
+        // (latency-bound sizes only: C2 outer SpMV 37.2 -> 36.1 us, but C4's
+        // 8.6 GB pass 2.01 -> 2.19 ms)
+        if (A.rro != nullptr && tailsplit && A.nrows > 3 * A.nbrows && rminb == 0 && pipe_a0 &&
+            csr_pass_bytes(A) <= 512.0 * 1024 * 1024) {
+            const unsigned need = grid_for(A.nbrows * 32, 256);
+            const int64_t want = 4 * (int64_t)num_sms();
+            const unsigned gb = (unsigned)((int64_t)need < want ? (int64_t)need : want);
+            const unsigned gt = grid_for((A.nrows - 3 * A.nbrows) * 8, 256);
+            const int ttrig = gb + gt <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
+            launch_pdl(k_bsr3p<Op, 4>, dim3(gb + gt), dim3(256), 0, s, A.nbrows, A.nbrows, A.nrows, A.bro, A.bci,
+                       A.bval, A.rro, A.rci, A.rv, op, A.row_off, ttrig, gb);
+        } else if (A.rro != nullptr && minb == 8 && tailsplit && A.nrows > 3 * A.nbrows && rminb == 0) {
             const unsigned gb = grid_for(A.nbrows * 32, 256);
             const unsigned gt = grid_for((A.nrows - 3 * A.nbrows) * 8, 256);
             const int ttrig = gb + gt <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
@@ -904,13 +935,13 @@ void launch(const CsrView &A, const Op &op, cudaStream_t s) {
             const int ptrig = pg <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
             if (pipe == 2)
                 launch_pdl(k_bsr3p<Op, 2>, dim3(pg), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
-                           A.rro, A.rci, A.rv, op, A.row_off, ptrig);
+                           A.rro, A.rci, A.rv, op, A.row_off, ptrig, 0xffffffffu);
             else if (pipe == 3)
                 launch_pdl(k_bsr3p<Op, 3>, dim3(pg), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
-                           A.rro, A.rci, A.rv, op, A.row_off, ptrig);
+                           A.rro, A.rci, A.rv, op, A.row_off, ptrig, 0xffffffffu);
             else
                 launch_pdl(k_bsr3p<Op, 4>, dim3(pg), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci, A.bval,
-                           A.rro, A.rci, A.rv, op, A.row_off, ptrig);
+                           A.rro, A.rci, A.rv, op, A.row_off, ptrig, 0xffffffffu);
         } else if (minb == 8)
             launch_pdl(k_bsr3<Op, false, 8>, dim3(grid), dim3(256), 0, s, ntrip, A.nbrows, A.nrows, A.bro, A.bci,
                        A.bval, A.rro, A.rci, A.rv, op, A.row_off, trigger, 0xffffffffu);
