@@ -378,7 +378,13 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     nrm = block_sum1(nrm, sh);
     if (threadIdx.x == 0) P.pn[b] = nrm;
     }  // phases 2b and 3
-    if constexpr (MODE == 3) return;
+    if constexpr (MODE == 3) {
+        if constexpr (SM) {  // the next split launch reads w from global memory
+            __syncthreads();
+            for (int64_t i = lo + threadIdx.x; i < hi; i += AO_THREADS) P.w[i] = wsl[i - lo];
+        }
+        return;
+    }
     stamp(P, 5);
     if constexpr (MODE == 0) grid.sync();
     stamp(P, 6);
@@ -1025,21 +1031,35 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
     P.hist = hist.p;
     P.red = red.p;
     P.nrm2 = nrm2.p;
+    // slices in shared memory (projections read w and V_j once; the update is
+    // the balanced warps-over-vectors pass) when they fit, as in the
+    // single-GPU kernel; PMGR_SPLIT_SM=0 keeps the global-memory variant
+    static const bool split_sm = !(getenv("PMGR_SPLIT_SM") && getenv("PMGR_SPLIT_SM")[0] == '0');
+    const size_t smem = (size_t)(16 * chunk) + (size_t)AO_WARPS * 32 * AO_UM * 16;
+    const bool sm = split_sm && n > 0 && chunk <= 3072;
+    if (sm) {
+        PMGR_CUDA(cudaFuncSetAttribute(k_arnoldi<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PMGR_CUDA(cudaFuncSetAttribute(k_arnoldi<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PMGR_CUDA(cudaFuncSetAttribute(k_arnoldi<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
     auto step = [&](cudaStream_t st) {
         ops.step(st);  // w = A M vin
-        k_arnoldi<false, 1><<<nblk, AO_THREADS, 0, st>>>(P);
+        if (sm) k_arnoldi<true, 1><<<nblk, AO_THREADS, smem, st>>>(P);
+        else k_arnoldi<false, 1><<<nblk, AO_THREADS, 0, st>>>(P);
         PMGR_LAUNCHED();
         k_arnoldi<false, 2><<<nblk, AO_THREADS, 0, st>>>(P);
         PMGR_LAUNCHED();
         ops.allreduce(red.p, 2 * (int64_t)(m + 1), st);
         k_split_fix<<<1, 256, 0, st>>>(dev.p, red.p, m + 1, a.p, G.p);
         PMGR_LAUNCHED();
-        k_arnoldi<false, 3><<<nblk, AO_THREADS, 0, st>>>(P);
+        if (sm) k_arnoldi<true, 3><<<nblk, AO_THREADS, smem, st>>>(P);
+        else k_arnoldi<false, 3><<<nblk, AO_THREADS, 0, st>>>(P);
         PMGR_LAUNCHED();
         k_sum_fixed<<<1, 32, 0, st>>>(pn.p, nblk, nrm2.p);
         PMGR_LAUNCHED();
         ops.allreduce(nrm2.p, 1, st);
-        k_arnoldi<false, 4><<<nblk, AO_THREADS, 0, st>>>(P);
+        if (sm) k_arnoldi<true, 4><<<nblk, AO_THREADS, smem, st>>>(P);
+        else k_arnoldi<false, 4><<<nblk, AO_THREADS, 0, st>>>(P);
         PMGR_LAUNCHED();
     };
     // one captured graph per step when the transport can be captured (NCCL;
