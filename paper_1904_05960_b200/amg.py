@@ -114,7 +114,7 @@ class AmgHierarchy:
         return amg_vcycle(self, b, x)
 
     def __del__(self):
-        if getattr(self, "_owner", None) is None and getattr(self, "_h", None) and _lib._lib is not None:
+        if getattr(self, "_owner", None) is None and getattr(self, "_h", None) and _lib is not None and _lib._lib is not None:
             _lib._lib.pmgr_amg_destroy(self._h)
             self._h = None
 

@@ -273,7 +273,7 @@ class _Handle:
     def __del__(self):
         from . import _lib
 
-        if getattr(self, "h", None) and _lib._lib is not None:
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
             getattr(_lib._lib, self._destroy)(self.h)
             self.h = None
 

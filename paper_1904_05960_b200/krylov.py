@@ -100,8 +100,12 @@ def _gmres_native(A: DeviceCsr, M, b, x0, cfg):
         bh = np.ascontiguousarray(b, dtype=np.float64)
         if len(bh) != n:
             raise ValueError("b does not match the operator")
-        x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
-        nz = 1 if np.any(x) else 0
+        if x0 is None:  # the library zeroes x on the device and writes every entry back
+            x = np.empty(n)
+            nz = 0
+        else:
+            x = np.array(x0, dtype=np.float64, copy=True)
+            nz = 1 if np.any(x) else 0
         _lib.check(L.pmgr_gmres_host(A.handle, mh, bh.ctypes.data, x.ctypes.data, nz, ctypes.byref(c),
                                      ctypes.byref(st), hist.ctypes.data, cap, current_stream()))
     return x, SolveStats(int(st.iterations), hist[:st.history_len].copy(), bool(st.converged))

@@ -191,7 +191,7 @@ class MgrHierarchy:
         return self.amg(-1)
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib._lib is not None:
+        if getattr(self, "_h", None) and _lib is not None and _lib._lib is not None:
             _lib._lib.pmgr_mgr_destroy(self._h)
             self._h = None
 

@@ -170,7 +170,7 @@ class DeviceCsr:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._lib is not None:
+        if h is not None and h.value and _lib is not None and _lib._lib is not None:
             _lib._lib.pmgr_csr_destroy(h)
             self._h = None
 
