@@ -724,11 +724,16 @@ struct OpProlong {
 };
 
 // a kernel lets its successor launch early (PDL) only when its own grid is
-// at most this many blocks per SM, so the early blocks never crowd out its own
+// at most this many blocks per SM (PMGR_TRIG_BPS).  Default: every grid
+// triggers (the successor's blocks take free slots during the last wave and
+// issue their setup-constant loads): C2 solve 23.84 -> 23.05 ms against a
+// 2-blocks-per-SM limit, C4 unchanged.  Safe for any value: every kernel
+// triggers after its own griddepcontrol.wait, so a kernel's pre-wait reads
+// never overtake the kernel two launches back.
 int trigger_blocks_per_sm() {
     static const int v = [] {
         const char *e = getenv("PMGR_TRIG_BPS");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 1 << 20;
     }();
     return v;
 }
