@@ -232,6 +232,16 @@ def test_gmres_device_vectors_and_generic_path(pk):
                           cfg=krylov.GmresConfig(restart=100))
     assert s2.converged and abs(s2.iterations - s1.iterations) <= 1
     assert np.linalg.norm(x2 - x1.cpu().numpy()) <= 1e-6 * np.linalg.norm(x2)
+    # host arrays (pmgr_gmres_host): the same solve bit for bit, with and
+    # without a nonzero starting vector
+    x3, s3 = krylov.gmres(A, h.apply, pb.rhs, cfg=krylov.GmresConfig(restart=100))
+    assert isinstance(x3, np.ndarray) and s3.iterations == s1.iterations
+    assert np.array_equal(x3, x1.cpu().numpy())
+    x0 = np.full(pb.n, 0.5)
+    x4, s4 = krylov.gmres(A, h.apply, pb.rhs, x0=x0, cfg=krylov.GmresConfig(restart=100))
+    x5, s5 = krylov.gmres(A, h.apply, b, x0=torch.from_numpy(x0).cuda(), cfg=krylov.GmresConfig(restart=100))
+    assert s4.iterations == s5.iterations and np.array_equal(x4, x5.cpu().numpy())
+    assert np.all(x0 == 0.5)  # the caller's start vector is not modified
 
 def test_gmres_zero_rhs_and_identity(pk):
     sparse, _, _, krylov = pk
