@@ -149,6 +149,10 @@ PMGR_API int pmgr_mgr_destroy(pmgr_mgr *h);
 /* MgrHierarchy.level_sizes (mgr.py:325): nlevels_built + 1 sizes. */
 PMGR_API int pmgr_mgr_num_levels(const pmgr_mgr *h, int32_t *nlevels);
 PMGR_API int pmgr_mgr_level_sizes(const pmgr_mgr *h, int64_t *sizes);
+/* Algorithmic HBM bytes (SURVEY.md §8(d) per-pass rules, summed over every
+ * operator pass, vector pass and dense collapsed product) and kernel count of
+ * one mgr_apply; computed from a dry capture, nothing executes. */
+PMGR_API int pmgr_mgr_apply_bytes(pmgr_mgr *h, double *bytes, int64_t *kernels);
 /* z = mgr_apply(h, v) (mgr.py:399-429), device vectors. */
 PMGR_API int pmgr_mgr_apply(pmgr_mgr *h, const double *v_dev, double *z_dev, void *stream);
 /* Parity export: what = 0 P_l, 1 next coarse operator, 2 the level's ILU(k)
@@ -203,6 +207,15 @@ PMGR_API int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const d
                   double *h_dev, void *stream);
 PMGR_API int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h_dev,
                    double *w_dev, void *stream);
+/* ||x||_2 of a device vector, returned on the host (synchronises the stream);
+ * y = a x + b y (b = 0: y = a x, y's old contents ignored); u = sum_k y_k V_k
+ * over nvec rows of V (leading dimension ldv, y on the device).  These replace
+ * the reference's numpy vector algebra in krylov.py:52-117 on the generic
+ * (Python-callable) GMRES path. */
+PMGR_API int pmgr_vec_norm2(const double *x_dev, int64_t n, double *out_host, void *stream);
+PMGR_API int pmgr_vec_axpby(double a, const double *x_dev, double b, double *y_dev, int64_t n, void *stream);
+PMGR_API int pmgr_combine(const double *V_dev, int64_t n, int64_t ldv, int32_t nvec, const double *y_dev,
+                          double *u_dev, void *stream);
 
 /* ---- on-device assembly ---------------------------
  * The synthetic poromechanics Jacobian of paper_1904_05960_b200/problems.py

@@ -93,26 +93,43 @@ def levels_for(pb, n_max):
             pmgr.MgrLevelSpec({Field.S}, {Field.P}, f_relax="jacobi", n_max=None))
 
 
-def setup_4field(A, layout, n_max, cfg):
+def setup_4field(A, layout, n_max, cfg, opts=None):
     """Shim 2: U -> S2 -> S1 -> P built from reference primitives
-    (mgr.py:300-326 containers)."""
+    (mgr.py:300-326 containers).  `opts` (problems.
+    solver_options) supplies the per-level F-relaxation sweeps and global
+    smoothers; the spec objects only carry mode strings, so the S2 level is
+    described to the reference as an S level."""
     cur, lay = A, layout
     levs = []
-    order = [(problems.FIELD_U, "amg", n_max), (problems.FIELD_S2, "jacobi", None),
-             (problems.FIELD_S, "jacobi", None)]
-    for tag, relax, nm in order:
+    tags = [problems.FIELD_U, problems.FIELD_S2, problems.FIELD_S]
+    lvopts = opts["levels"] if opts else [dict(f_relax="amg", n_max=n_max), dict(f_relax="jacobi"),
+                                          dict(f_relax="jacobi")]
+    for tag, lo in zip(tags, lvopts):
         fspec = {Field.U} if tag == problems.FIELD_U else {Field.S}
-        spec = pmgr.MgrLevelSpec(fspec, {Field.P}, f_relax=relax, n_max=nm)
+        spec = pmgr.MgrLevelSpec(fspec, {Field.P}, f_relax=lo.get("f_relax", "jacobi"),
+                                 f_relax_sweeps=lo.get("f_relax_sweeps", 1), n_max=lo.get("n_max"),
+                                 global_smoother=lo.get("global_smoother", "none"))
         split = CfSplitting(lay.field_of != tag)
         blocks = extract_blocks(cur, split)
         P, R = pmgr.build_transfers(blocks, split, spec, cfg.ideal_size_cap)
         f_relax = pmgr._build_f_relax(blocks[0], spec, cfg)
+        smoother = pmgr._build_global_smoother(cur, lay, spec, cfg)
         coarse = pmgr.build_coarse(cur, lay, split, blocks, P, R, spec)
-        levs.append(pmgr._MgrLevel(cur, lay, split, blocks, P, R, f_relax, None, spec))
+        levs.append(pmgr._MgrLevel(cur, lay, split, blocks, P, R, f_relax, smoother, spec))
         lay = FieldLayout(lay.field_of[split.c_rows()], lay.entity_of[split.c_rows()])
         cur = coarse
     term = amg_setup(cur, cfg.amg_terminal)
-    return pmgr.MgrHierarchy(levs, cur, "amg", term, 1, "pre")
+    return pmgr.MgrHierarchy(levs, cur, "amg", term, max(1, cfg.terminal_cycles), cfg.f_relax_position)
+
+
+def config_from_options(opts):
+    """Reference MgrConfig for problems.solver_options (two/one flow fields)."""
+    levels = tuple(pmgr.MgrLevelSpec({Field(t) for t in lv["f"]}, {Field(t) for t in lv["c"]},
+                                     **{k: v for k, v in lv.items() if k not in ("f", "c")})
+                   for lv in opts["levels"]) if len(opts["levels"]) < 3 else ()
+    return pmgr.MgrConfig(levels=levels, terminal_cycles=opts["terminal_cycles"],
+                          f_relax_position=opts["f_relax_position"], npartitions=opts["npartitions"],
+                          amg_f_relax=AmgConfig(**opts["amg_f_relax"]), amg_terminal=AmgConfig(**opts["amg_terminal"]))
 
 
 def dump_amg(d, prefix, h, full):
@@ -170,10 +187,14 @@ VARIANTS = {
 }
 
 
-def dump_problem(tag, pb, n_max, full, restart=100, four_field=False, variant=None):
+def dump_problem(tag, pb, n_max, full, restart=100, four_field=False, variant=None, opts=None, max_iters=1000):
     A = CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
     lay = FieldLayout(pb.field_of, pb.entity_of)
-    if variant is not None:
+    if opts is not None:  # problems.solver_options (the production configurations)
+        cfg = config_from_options(opts)
+        restart, max_iters = opts["restart"], opts["max_iters"]
+        h = setup_4field(A, lay, None, cfg, opts) if four_field else pmgr.mgr_setup(A, lay, cfg)
+    elif variant is not None:
         V = VARIANTS[variant]
         if V.get("interleaved"):
             lay = FieldLayout(pb.field_of, pb.entity_of, psp.Ordering.FLOW_INTERLEAVED)
@@ -220,7 +241,7 @@ def dump_problem(tag, pb, n_max, full, restart=100, four_field=False, variant=No
     d["apply_v"] = v
     d["apply_z"] = pmgr.mgr_apply(h, v)
     x, st = gmres(lambda y: matvec(A, y), h.apply, pb.rhs,
-                  cfg=GmresConfig(restart=restart, max_iters=1000, rtol=1e-6))
+                  cfg=GmresConfig(restart=restart, max_iters=max_iters, rtol=1e-6))
     d["gmres_iters"] = np.array(st.iterations)
     d["gmres_hist"] = st.residual_history
     d["gmres_x"] = x
@@ -318,6 +339,19 @@ def main():
             dump_problem(f"c2_6_{v}", problems.make_c2(seed=5, n=6), None, True, variant=v)
     if "c3_16" in which:
         dump_problem("c3_16", problems.make_c3(seed=0, n=16), 4, False, restart=100)
+    # the production configurations (problems.solver_options) at 32^3
+    if "c3_32p" in which:
+        pb = problems.make_c3(seed=0, n=32)
+        dump_problem("c3_32p", pb, None, False, opts=problems.solver_options("C3", pb))
+    if "c4_32p" in which:
+        pb = problems.make_c4(seed=0, n=32)
+        dump_problem("c4_32p", pb, None, False, four_field=True, opts=problems.solver_options("C4", pb))
+    # parity configuration at 32^3: the iteration counts the GPU must reproduce
+    # (C3 stalls into 2801 iterations -- the algorithm, not the device)
+    if "c4_32" in which:
+        dump_problem("c4_32", problems.make_c4(seed=0, n=32), 4, False, four_field=True)
+    if "c3_32" in which:
+        dump_problem("c3_32", problems.make_c3(seed=0, n=32), 4, False, max_iters=3000)
 
 
 if __name__ == "__main__":

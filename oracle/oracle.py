@@ -508,6 +508,18 @@ class MgrHierarchy:
         return [lv.A.nrows for lv in self.levels] + [self.terminal_A.nrows]
 
 
+def config_from_options(opts: dict) -> MgrConfig:
+    """Oracle MgrConfig from problems.solver_options' plain-data description
+    (the same description the library's mgr.config_from_options reads)."""
+    specs = tuple(MgrLevelSpec(frozenset(lv["f"]), frozenset(lv["c"]), lv.get("f_relax", "jacobi"),
+                               lv.get("f_relax_sweeps", 1), lv.get("n_max"), lv.get("interp", "injection_jacobi"),
+                               lv.get("global_smoother", "none"), lv.get("ilu_fill", 1), lv.get("hbgs_sweeps", 3))
+                  for lv in opts["levels"])
+    return MgrConfig(levels=specs, terminal_cycles=opts.get("terminal_cycles", 1),
+                     amg_f_relax=AmgConfig(**opts["amg_f_relax"]), amg_terminal=AmgConfig(**opts["amg_terminal"]),
+                     f_relax_position=opts.get("f_relax_position", "pre"), npartitions=opts.get("npartitions", 1))
+
+
 def extract_blocks(A: Csr, is_c: np.ndarray):
     """A_FF, A_FC, A_CF, A_CC with order-preserving renumbering and explicit
     zeros kept (reference sparse.py:269-288)."""

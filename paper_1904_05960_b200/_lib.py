@@ -102,6 +102,7 @@ SIGNATURES = {
     "pmgr_mgr_destroy": (ctypes.c_int, [vp]),
     "pmgr_mgr_num_levels": (ctypes.c_int, [vp, c_i32p]),
     "pmgr_mgr_level_sizes": (ctypes.c_int, [vp, c_i64p]),
+    "pmgr_mgr_apply_bytes": (ctypes.c_int, [vp, vp, vp]),
     "pmgr_mgr_apply": (ctypes.c_int, [vp, vp, vp, vp]),
     "pmgr_mgr_export_csr": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_int32, vp, ctypes.POINTER(vp)]),
     "pmgr_mgr_export_vec": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_int32, vp, vp]),
@@ -114,6 +115,9 @@ SIGNATURES = {
     "pmgr_prof_query": (ctypes.c_int, [ctypes.c_int32, c_i64p, c_dp, c_dp]),
     "pmgr_multidot": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
     "pmgr_multiaxpy": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
+    "pmgr_vec_norm2": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp]),
+    "pmgr_vec_axpby": (ctypes.c_int, [ctypes.c_double, vp, ctypes.c_double, vp, ctypes.c_int64, vp]),
+    "pmgr_combine": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
     "pmgr_nccl_get_id": (ctypes.c_int, [ctypes.POINTER(NcclId)]),
     "pmgr_transport_nccl_create": (ctypes.c_int, [ctypes.POINTER(NcclId), ctypes.c_int32, ctypes.c_int32,
                                                   ctypes.POINTER(vp)]),

@@ -61,12 +61,16 @@ class AmgLevelView:
     dtilde: np.ndarray
 
 
-def _export_csr(h, level, what) -> CsrMatrix:
+def _export_dev(h, level, what) -> DeviceCsr:
     out = ctypes.c_void_p()
     _lib.check(_lib.lib().pmgr_amg_export_csr(h, level, what, current_stream(), ctypes.byref(out)))
     nr, nc, nz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     _lib.check(_lib.lib().pmgr_csr_info(out, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nz)))
-    return DeviceCsr(out, nr.value, nc.value, nz.value).to_host()
+    return DeviceCsr(out, nr.value, nc.value, nz.value)
+
+
+def _export_csr(h, level, what) -> CsrMatrix:
+    return _export_dev(h, level, what).to_host()
 
 
 class AmgHierarchy:
@@ -109,6 +113,21 @@ class AmgHierarchy:
     @property
     def coarse_A(self) -> CsrMatrix:
         return _export_csr(self._h, 0, 2)
+
+    def export_raw(self):
+        """[(A, P, is_c, dtilde) per level], coarse A as unvalidated host arrays
+        ((nrows, ncols, ro, ci, v) tuples) -- bulk export for host-side tools."""
+        sizes = self.level_sizes()
+        out = []
+        for l in range(self._nlev):
+            isc = np.zeros(sizes[l], dtype=np.int8)
+            dt = np.zeros(sizes[l])
+            _lib.check(_lib.lib().pmgr_amg_export_vec(self._h, l, 0, isc.ctypes.data, current_stream()))
+            _lib.check(_lib.lib().pmgr_amg_export_vec(self._h, l, 1, dt.ctypes.data, current_stream()))
+            a, p = _export_dev(self._h, l, 0), _export_dev(self._h, l, 1)
+            out.append(((a.nrows, a.ncols) + a.download(), (p.nrows, p.ncols) + p.download(), isc.astype(bool), dt))
+        c = _export_dev(self._h, 0, 2)
+        return out, (c.nrows, c.ncols) + c.download()
 
     def vcycle(self, b, x=None):
         return amg_vcycle(self, b, x)

@@ -261,6 +261,10 @@ int pmgr_mgr_num_levels(const pmgr_mgr *h, int32_t *nlevels) {
     return guard([&] { *nlevels = (int32_t)h->levels.size(); });
 }
 
+int pmgr_mgr_apply_bytes(pmgr_mgr *h, double *bytes, int64_t *kernels) {
+    return guard([&] { pmgr::mgr_apply_bytes(*h, bytes, kernels); });
+}
+
 int pmgr_mgr_level_sizes(const pmgr_mgr *h, int64_t *sizes) {
     return guard([&] {
         size_t i = 0;
@@ -382,6 +386,19 @@ int pmgr_multidot(const double *V_dev, int64_t n, int32_t nvec, const double *w_
 int pmgr_multiaxpy(const double *V_dev, int64_t n, int32_t nvec, const double *h_dev, double *w_dev,
                    void *stream) {
     return guard([&] { pmgr::multiaxpy(V_dev, n, nvec, h_dev, w_dev, S(stream)); });
+}
+
+int pmgr_vec_norm2(const double *x_dev, int64_t n, double *out_host, void *stream) {
+    return guard([&] { *out_host = pmgr::vec_norm2(x_dev, n, S(stream)); });
+}
+
+int pmgr_vec_axpby(double a, const double *x_dev, double b, double *y_dev, int64_t n, void *stream) {
+    return guard([&] { pmgr::vec_axpby(a, x_dev, b, y_dev, n, S(stream)); });
+}
+
+int pmgr_combine(const double *V_dev, int64_t n, int64_t ldv, int32_t nvec, const double *y_dev, double *u_dev,
+                 void *stream) {
+    return guard([&] { pmgr::vec_combine(V_dev, n, ldv, nvec, y_dev, u_dev, S(stream)); });
 }
 
 }  // extern "C"

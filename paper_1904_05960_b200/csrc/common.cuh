@@ -56,6 +56,13 @@ extern std::atomic<int64_t> g_launches;
 extern thread_local int64_t *g_capture_count;
 
 // Count + check a kernel launch issued just before.
+// algorithmic-byte ledger: while set (a dry capture of one MGR application,
+// pmgr_mgr_apply_bytes), every streaming launch adds the bytes it must move
+extern thread_local double *g_byte_ledger;
+inline void ledger(double bytes) {
+    if (g_byte_ledger) *g_byte_ledger += bytes;
+}
+
 #define PMGR_LAUNCHED()                                                                \
     do {                                                                               \
         if (::pmgr::g_capture_count) ++*::pmgr::g_capture_count;                       \

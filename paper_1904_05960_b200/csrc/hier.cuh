@@ -189,6 +189,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A, const int8_t *
 void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);
 void mgr_collect(pmgr_mgr &h);  // fold finished graph timing events into the totals
 void mgr_apply_direct(pmgr_mgr &h, const double *v, double *z, cudaStream_t s);  // no graph (for capture)
+void mgr_apply_bytes(pmgr_mgr &h, double *bytes, int64_t *kernels);
 }  // namespace pmgr
 
 namespace pmgr {
@@ -214,4 +215,7 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
                  pmgr_gmres_stats &stats, double *history, int32_t history_cap, cudaStream_t s);
 void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double *h, cudaStream_t s);
 void multiaxpy(const double *V, int64_t n, int32_t nvec, const double *h, double *w, cudaStream_t s);
+double vec_norm2(const double *x, int64_t n, cudaStream_t s);
+void vec_axpby(double a, const double *x, double b, double *y, int64_t n, cudaStream_t s);
+void vec_combine(const double *V, int64_t n, int64_t ldv, int32_t nvec, const double *y, double *u, cudaStream_t s);
 }  // namespace pmgr

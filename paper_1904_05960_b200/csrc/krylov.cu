@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <tuple>
 
 #include <cooperative_groups.h>
@@ -626,12 +627,27 @@ struct Ws {
     }
 };
 
-std::map<std::tuple<const pmgr_csr *, pmgr_mgr *, int, int>, std::unique_ptr<Ws>> g_ws;
+// keyed on (A, M, restart): max_iters only sizes the history buffer, which
+// grows on demand (the captured cycle graph is rebuilt when it moves).  One
+// mutex serialises the solves that share the cache (ctypes releases the GIL).
+std::map<std::tuple<const pmgr_csr *, pmgr_mgr *, int>, std::unique_ptr<Ws>> g_ws;
+std::recursive_mutex g_ws_mu;
 
 Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
-    auto key = std::make_tuple(A, M, m, max_iters);
+    auto key = std::make_tuple(A, M, m);
     auto it = g_ws.find(key);
-    if (it != g_ws.end()) return *it->second;
+    if (it != g_ws.end()) {
+        Ws &w = *it->second;
+        if (max_iters > w.max_iters) {
+            w.hist.alloc((int64_t)max_iters + 2);
+            w.max_iters = max_iters;
+            if (w.cycle) {
+                cudaGraphExecDestroy(w.cycle);
+                w.cycle = nullptr;
+            }
+        }
+        return w;
+    }
     auto w = std::make_unique<Ws>();
     w->A = A;
     w->M = M;
@@ -805,6 +821,7 @@ bool use_cycle_graphs() {
 }  // namespace
 
 void gmres_forget(const void *obj) {
+    std::lock_guard<std::recursive_mutex> lk(g_ws_mu);
     for (auto it = g_ws.begin(); it != g_ws.end();) {
         if ((const void *)std::get<0>(it->first) == obj || (const void *)std::get<1>(it->first) == obj)
             it = g_ws.erase(it);
@@ -824,6 +841,7 @@ void gmres_device(const pmgr_csr *A, pmgr_mgr *M, const double *b, double *x, in
     const int64_t n = Av.nrows;
     const int m = cfg.restart;
     const int max_iters = cfg.max_iters > 0 ? cfg.max_iters : 0;
+    std::lock_guard<std::recursive_mutex> lk(g_ws_mu);
     Ws &W = workspace(A, M, m, max_iters, n);
     const bool prof = prof_on();
     const bool graph_mode = use_cycle_graphs() && !prof;
@@ -1098,12 +1116,8 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
     gnorm(r.p, beta.p);
     double bt = read_scalar(beta.p, s);
     hl.push_back(bt);
-    double bnorm = bt;
-    if (nonzero_x0) {
-        gnorm(b, nrm2.p);
-        bnorm = read_scalar(nrm2.p, s);
-    }
-    const double tol = std::fmax(cfg.rtol * bnorm, cfg.atol);
+    // reference krylov.py: tol = max(rtol * ||b - A x0||, atol)
+    const double tol = std::fmax(cfg.rtol * bt, cfg.atol);
     Dev d0 = {};
     d0.m = m;
     d0.max_iters = max_iters;
@@ -1189,6 +1203,41 @@ void multidot(const double *V, int64_t n, int32_t nvec, const double *w, double 
 void multiaxpy(const double *V, int64_t n, int32_t nvec, const double *h, double *w, cudaStream_t s) {
     if (nvec <= 0 || nvec > 1024) fail(PMGR_ERR_INVALID, "multiaxpy supports 1..1024 vectors");
     k_maxpy<<<vec_grid(n), 256, 0, s>>>(V, n, nvec, h, w);
+    PMGR_LAUNCHED();
+}
+
+namespace {
+__global__ void k_axpby(double a, const double *__restrict__ x, double b, double *__restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = b == 0.0 ? a * x[i] : fma(b, y[i], a * x[i]);  // b = 0: y may hold garbage
+}
+}  // namespace
+
+double vec_norm2(const double *x, int64_t n, cudaStream_t s) {
+    const int np = vec_grid(n);
+    TBuf<double> part((int64_t)np + 1, s);
+    k_norm_partial<<<np, DOT_BLOCK, 0, s>>>(x, n, part.p);
+    PMGR_LAUNCHED();
+    k_norm_final<<<1, 32, 0, s>>>(part.p, np, part.p + np);
+    PMGR_LAUNCHED();
+    return read_scalar(part.p + np, s);
+}
+
+void vec_axpby(double a, const double *x, double b, double *y, int64_t n, cudaStream_t s) {
+    if (n <= 0) return;
+    k_axpby<<<vec_grid(n), 256, 0, s>>>(a, x, b, y, n);
+    PMGR_LAUNCHED();
+}
+
+void vec_combine(const double *V, int64_t n, int64_t ldv, int32_t nvec, const double *y, double *u,
+                 cudaStream_t s) {
+    if (nvec < 0 || nvec > 1024) fail(PMGR_ERR_INVALID, "combine supports 0..1024 vectors");
+    if (n <= 0) return;
+    if (nvec == 0) {
+        vec_axpby(0.0, u, 0.0, u, n, s);
+        return;
+    }
+    k_combine<<<vec_grid(n), 256, 0, s>>>(V, n, ldv, nvec, y, u);
     PMGR_LAUNCHED();
 }
 

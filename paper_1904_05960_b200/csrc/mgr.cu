@@ -220,6 +220,7 @@ void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
         vec_mul(L.dinv_ff.p, vf, zf, L.nf, s);
         for (int c = 1; c < L.f_relax_sweeps; ++c) {
             const CsrView F = L.A_ff->view();
+            ledger(csr_pass_bytes(F) + 24.0 * L.nf);
             k_jacobi_dinv<<<grid_for(L.nf * 32, 256), 256, 0, s>>>(L.nf, F.ro, F.ci, F.v, zf, vf, L.dinv_ff.p,
                                                                    L.tmpf.p);
             PMGR_LAUNCHED();
@@ -248,6 +249,7 @@ void apply_level_smoothed(pmgr_mgr &h, size_t l, const double *v, double *z, cud
             vec_gather(r, L.f_rows.p, L.nf, L.vf.p, s);
             f_relax_apply(L, L.vf.p, L.zf.p, s);
         }
+        ledger(32.0 * L.nf);
         k_scatter_add<<<grid_for(L.nf, 256), 256, 0, s>>>(L.zf.p, L.f_rows.p, L.nf, zacc);
         PMGR_LAUNCHED();
     };
@@ -338,6 +340,7 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
         spmv_residual(L.A->view(), z, v, r.p, s);
         vec_gather(r.p, L.f_rows.p, L.nf, L.vf.p, s);
         f_relax_apply(L, L.vf.p, L.zf.p, s);
+        ledger(32.0 * L.nf);
         k_scatter_add<<<grid_for(L.nf, 256), 256, 0, s>>>(L.zf.p, L.f_rows.p, L.nf, z);
         PMGR_LAUNCHED();
     }
@@ -637,6 +640,37 @@ void mgr_apply(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) {
 }
 
 void mgr_apply_direct(pmgr_mgr &h, const double *v, double *z, cudaStream_t s) { apply_level(h, 0, v, z, s); }
+
+// algorithmic bytes and kernel count of one application: a dry capture of
+// the cycle (nothing executes) with the byte ledger attached
+void mgr_apply_bytes(pmgr_mgr &h, double *bytes, int64_t *kernels) {
+    DBuf<double> v(h.n), z(h.n);
+    cudaStream_t cs;
+    PMGR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    double b = 0.0;
+    int64_t k = 0;
+    PMGR_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    g_byte_ledger = &b;
+    g_capture_count = &k;
+    try {
+        apply_level(h, 0, v.p, z.p, cs);
+    } catch (...) {
+        g_byte_ledger = nullptr;
+        g_capture_count = nullptr;
+        cudaStreamEndCapture(cs, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        cudaStreamDestroy(cs);
+        throw;
+    }
+    g_byte_ledger = nullptr;
+    g_capture_count = nullptr;
+    PMGR_CUDA(cudaStreamEndCapture(cs, &graph));
+    PMGR_CUDA(cudaGraphDestroy(graph));
+    PMGR_CUDA(cudaStreamDestroy(cs));
+    *bytes = b;
+    *kernels = k;
+}
 
 void mgr_collect(pmgr_mgr &h) {
     for (auto &e : h.graphs)

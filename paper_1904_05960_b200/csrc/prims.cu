@@ -11,6 +11,7 @@ namespace pmgr {
 
 std::atomic<int64_t> g_launches{0};
 thread_local int64_t *g_capture_count = nullptr;
+thread_local double *g_byte_ledger = nullptr;
 
 namespace {
 bool g_prof = false;

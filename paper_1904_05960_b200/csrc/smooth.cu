@@ -654,6 +654,10 @@ void smoother_apply(GlobalSmoother &g, const double *v, double *z, cudaStream_t 
     const int64_t n = g.n;
     if (n == 0) return;
     const unsigned grid = grid_for(g.nparts, 32);
+    if (g.kind == PMGR_SMOOTHER_ILU)  // one pass over L\U (+ diagonal positions), v read, z written and re-read
+        ledger(csr_pass_bytes(g.lu.nrows, g.lu.ncols, g.lu.nnz) + 8.0 * n + 16.0 * n);
+    else if (g.A)
+        ledger(g.nsweeps * (csr_pass_bytes(g.A->nrows, g.A->ncols, g.A->nnz) + 40.0 * n));
     if (g.kind == PMGR_SMOOTHER_ILU && g.leveled) {
         for (size_t l = 0; l + 1 < g.fptr.size(); ++l) {
             const int64_t c = g.fptr[l + 1] - g.fptr[l];

@@ -604,6 +604,8 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3p(int64_t ntrip, int64_t nb, 
 }
 
 struct OpY {
+    static double row_bytes(const OpY &) { return 0.0; }
+
     const double *xv;
     double *y;
     __device__ double x(int j) const { return __ldg(xv + j); }
@@ -611,6 +613,8 @@ struct OpY {
     __device__ void out(int64_t i, double s) const { y[i] = s; }
 };
 struct OpResidual {
+    static double row_bytes(const OpResidual &) { return 8.0; }  // b
+
     const double *xv, *b;
     double *r;
     __device__ double x(int j) const { return __ldg(xv + j); }
@@ -618,6 +622,8 @@ struct OpResidual {
     __device__ void out(int64_t i, double s) const { r[i] = b[i] - s; }
 };
 struct OpJacobi {
+    static double row_bytes(const OpJacobi &) { return 16.0; }  // b, d (SURVEY 8(d) sweep rule)
+
     const double *xv, *b, *d;
     double *xo;
     __device__ double x(int j) const { return __ldg(xv + j); }
@@ -628,6 +634,8 @@ struct OpJacobi {
 // post-sweep whose right-hand side is not written by the predecessor kernel
 // (the AMG cycle: b_l was written by the restriction, long before)
 struct OpJacobiPre {
+    static double row_bytes(const OpJacobiPre &) { return 16.0; }
+
     const double *xv, *b, *d;
     double *xo;
     double di = 1.0, bi = 0.0;
@@ -639,6 +647,9 @@ struct OpJacobiPre {
     __device__ void out(int64_t i, double s) const { xo[i] = xv[i] + (bi - s) / di; }
 };
 struct OpSweep0 {
+    static double row_bytes(const OpSweep0 &) { return 24.0; }  // b, d read; r written
+    static constexpr double kColBytes = 8.0;            // x(j) = b_j / d_j
+
     const double *b, *d;
     double *xo, *r;
     __device__ double x(int j) const { return __ldg(b + j) / __ldg(d + j); }
@@ -649,7 +660,9 @@ struct OpSweep0 {
         r[i] = b[i] - s;
     }
 };
-struct OpRestrictDiv {  // b_c = R r, and the first smoother iterate x_c = b_c / dtilde_c
+struct OpRestrictDiv {
+    static double row_bytes(const OpRestrictDiv &) { return 16.0; }  // d read, x_c written
+  // b_c = R r, and the first smoother iterate x_c = b_c / dtilde_c
     const double *r, *d;
     double *b, *xo;
     __device__ double x(int j) const { return __ldg(r + j); }
@@ -661,6 +674,8 @@ struct OpRestrictDiv {  // b_c = R r, and the first smoother iterate x_c = b_c /
     }
 };
 struct OpAdd {
+    static double row_bytes(const OpAdd &) { return 8.0; }  // x read
+
     const double *e;
     double *xio;
     __device__ double x(int j) const { return __ldg(e + j); }
@@ -671,6 +686,8 @@ struct OpAdd {
 // prolongation: x was written by the level's pre-sweep, long before), so
 // x_i is read before the PDL wait
 struct OpAddPre {
+    static double row_bytes(const OpAddPre &) { return 8.0; }
+
     const double *e;
     double *xio;
     double xi = 0.0;
@@ -679,6 +696,10 @@ struct OpAddPre {
     __device__ void out(int64_t i, double s) const { xio[i] = xi + s; }
 };
 struct OpResidRows {
+    static double row_bytes(const OpResidRows &o) {
+        return 16.0 + (o.x2 ? 16.0 : 0.0) + (o.sidx ? 24.0 : 0.0);  // row map, v; next level's first step
+    }
+
     const double *zf, *v;
     const int64_t *rows;
     double *r;
@@ -708,6 +729,8 @@ struct OpResidRows {
     }
 };
 struct OpProlong {
+    static double row_bytes(const OpProlong &) { return 16.0; }  // F map, z_F
+
     const double *ec, *zf;
     const int64_t *findex;
     double *z;
@@ -863,9 +886,19 @@ int spmv_lanes(const CsrView &A) {
 
 namespace {
 
+template <class Op, class = void>
+struct col_bytes_of {
+    static constexpr double v = 0.0;
+};
+template <class Op>
+struct col_bytes_of<Op, std::void_t<decltype(Op::kColBytes)>> {
+    static constexpr double v = Op::kColBytes;
+};
+
 template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
+    ledger(csr_pass_bytes(A) + Op::row_bytes(op) * A.nrows + col_bytes_of<Op>::v * A.ncols);
     if (A.nbrows > 0) {
         const int64_t ntrip = A.rro ? (A.nrows + 2) / 3 : A.nbrows;
         const unsigned grid = grid_for(ntrip * 32, 256);
@@ -1162,12 +1195,14 @@ __global__ void k_gather_div(const double *__restrict__ v, const int64_t *__rest
 void vec_gather_div(const double *v, const int64_t *rows, const double *d, int64_t n, double *bo, double *xo,
                     cudaStream_t s) {
     if (n == 0) return;
+    ledger(40.0 * n);
     launch_pdl(k_gather_div, dim3(grid_for(n, 256)), dim3(256), 0, s, v, rows, d, n, bo, xo);
     PMGR_LAUNCHED();
 }
 
 void vec_copy_div(const double *b, const double *d, int64_t n, double *bo, double *xo, cudaStream_t s) {
     if (n == 0) return;
+    ledger(32.0 * n);
     launch_pdl(k_copy_div, dim3(grid_for(n, 256)), dim3(256), 0, s, b, d, n, bo, xo);
     PMGR_LAUNCHED();
 }
@@ -1193,6 +1228,7 @@ void spmv_prolong_combine(const CsrView &P, const double *ec, const double *zf, 
 void hybrid_gs(const CsrView &A, int64_t nparts, const int64_t *starts, const double *d,
                const double *b, double *x, double *xpre, bool forward, cudaStream_t s) {
     PMGR_CUDA(cudaMemcpyAsync(xpre, x, sizeof(double) * A.nrows, cudaMemcpyDeviceToDevice, s));
+    ledger(csr_pass_bytes(A) + 16.0 * A.nrows + 8.0 * A.ncols);  // b, d; x read twice
     k_hybrid_gs<<<grid_for(nparts, 128), 128, 0, s>>>(nparts, starts, A.ro, A.ci, A.v, d, b, x, xpre,
                                                      forward ? 1 : 0);
     PMGR_LAUNCHED();
@@ -1205,6 +1241,7 @@ void dense_matvec(const double *M, int64_t n, int64_t ld, const double *x, doubl
 void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld, const double *x, double *y,
                        cudaStream_t s) {
     if (nrows == 0) return;
+    ledger(8.0 * nrows * ncols + 8.0 * ncols + 8.0 * nrows);
     // the collapsed operators are read once per cycle: evict-first loads keep
     // the sparse levels' operators (read again on the way up) in L2
     static const bool stream = !(getenv("PMGR_DENSE_STREAM") && getenv("PMGR_DENSE_STREAM")[0] == '0');
@@ -1235,6 +1272,7 @@ void dense_matvec_rows(const double *M, int64_t nrows, int64_t ncols, int64_t ld
 
 void vec_gather(const double *src, const int64_t *idx, int64_t n, double *dst, cudaStream_t s) {
     if (n == 0) return;
+    ledger(24.0 * n);
     launch_pdl(k_gather, dim3(grid_for(n, 256)), dim3(256), 0, s, src, idx, n, dst);
     PMGR_LAUNCHED();
 }
@@ -1242,29 +1280,34 @@ void vec_gather(const double *src, const int64_t *idx, int64_t n, double *dst, c
 void vec_scale_gather(const double *src, const int64_t *idx, const double *d, int64_t n, double *dst,
                       cudaStream_t s) {
     if (n == 0) return;
+    ledger(32.0 * n);
     launch_pdl(k_scale_gather, dim3(grid_for(n, 256)), dim3(256), 0, s, src, idx, d, n, dst);
     PMGR_LAUNCHED();
 }
 
 void vec_zero(double *x, int64_t n, cudaStream_t s) {
     if (n == 0) return;
+    ledger(8.0 * n);
     launch_pdl(k_zero, dim3(grid_for(n, 256)), dim3(256), 0, s, x, n);
     PMGR_LAUNCHED();
 }
 
 void vec_copy(const double *x, double *y, int64_t n, cudaStream_t s) {
     if (n == 0) return;
+    ledger(16.0 * n);
     PMGR_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
 }
 
 void vec_axpy(double a, const double *x, double *y, int64_t n, cudaStream_t s) {
     if (n == 0) return;
+    ledger(24.0 * n);
     launch_pdl(k_axpy, dim3(grid_for(n, 256)), dim3(256), 0, s, a, x, y, n);
     PMGR_LAUNCHED();
 }
 
 void vec_mul(const double *a, const double *b, double *y, int64_t n, cudaStream_t s) {
     if (n == 0) return;
+    ledger(24.0 * n);
     launch_pdl(k_mul, dim3(grid_for(n, 256)), dim3(256), 0, s, a, b, y, n);
     PMGR_LAUNCHED();
 }

@@ -172,71 +172,51 @@ class DistOperator:
         return self.local_matvec(x_ext)
 
 
+class DistVectors:
+    """krylov.gmres_loop's vector algebra on row-distributed slices: local
+    torch arithmetic plus one all-reduce per projection pass / norm."""
+
+    def __init__(self, dist, group, like):
+        self.dist, self.group, self.like = dist, group, like
+
+    def zeros(self, shape):
+        import torch
+
+        return torch.zeros(shape, dtype=self.like.dtype, device=self.like.device)
+
+    def norm(self, v) -> float:
+        return dist_norm(v, self.dist, self.group)
+
+    def axpby(self, a, x, b, y):
+        if b == 0.0:
+            y.copy_(x).mul_(a)
+        else:
+            y.mul_(b).add_(x, alpha=a)
+        return y
+
+    def project(self, V, k, w):
+        h = np.zeros(k)
+        for _ in range(2):  # CGS2, one all-reduce per pass
+            c = dist_dots(V[:k], w, self.dist, self.group)
+            w -= c @ V[:k]
+            h += c.cpu().numpy()
+        return h
+
+    def combine(self, V, j, y):
+        import torch
+
+        return torch.as_tensor(y, dtype=V.dtype, device=V.device) @ V[:j]
+
+
 def dist_gmres(apply_A, apply_M_inv, b, dist, group=None, restart=50, max_iters=500, rtol=1e-6, atol=1e-12):
     """Right-preconditioned restarted GMRES (reference krylov.py:39-117) on
-    row-distributed vectors: classical Gram-Schmidt with one
-    re-orthogonalisation, one all-reduce per projection; the small
+    row-distributed vectors: krylov.gmres_loop with classical Gram-Schmidt
+    plus one re-orthogonalisation (one all-reduce per pass); the small
     Hessenberg algebra is replicated on every rank."""
-    import torch
-    from scipy.linalg import solve_triangular
+    from .krylov import gmres_loop
 
-    n = b.numel()
-    M = (lambda v: v) if apply_M_inv is None else apply_M_inv
-    x = torch.zeros_like(b)
-    r = b.clone()
-    beta = dist_norm(r, dist, group)
-    hist = [beta]
-    tol = max(rtol * beta, atol)
-    total = 0
-    brk = False
-    while beta > tol and total < max_iters:
-        m = restart
-        V = torch.zeros((m + 1, n), dtype=b.dtype, device=b.device)
-        H = np.zeros((m + 1, m))
-        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
-        V[0] = r / beta
-        g[0] = beta
-        j = 0
-        while j < m and total < max_iters:
-            w = apply_A(M(V[j]))
-            h = np.zeros(j + 1)
-            for _ in range(2):
-                c = dist_dots(V[:j + 1], w, dist, group)
-                w = w - c @ V[:j + 1]
-                h += c.cpu().numpy()
-            H[:j + 1, j] = h
-            hn = dist_norm(w, dist, group)
-            H[j + 1, j] = hn
-            if hn > 1e-12 * max(float(np.linalg.norm(H[:j + 2, j])), 1e-300):
-                V[j + 1] = w / hn
-            else:
-                brk = True
-            for i in range(j):
-                t = H[i, j]
-                H[i, j] = cs[i] * t + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * t + cs[i] * H[i + 1, j]
-            rho = float(np.hypot(H[j, j], H[j + 1, j]))
-            if rho == 0.0:
-                brk = True
-                break
-            cs[j], sn[j] = H[j, j] / rho, H[j + 1, j] / rho
-            H[j, j], H[j + 1, j] = rho, 0.0
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            total += 1
-            j += 1
-            hist.append(abs(float(g[j])))
-            if abs(g[j]) <= tol or brk:
-                break
-        if j > 0:
-            y = solve_triangular(H[:j, :j], g[:j], lower=False)
-            x = x + M(torch.as_tensor(y, dtype=b.dtype, device=b.device) @ V[:j])
-            r = b - apply_A(x)
-            beta = dist_norm(r, dist, group)
-            hist[-1] = beta
-        if brk:
-            break
-    return x, total, np.array(hist), bool(beta <= tol)
+    return gmres_loop(DistVectors(dist, group, b), apply_A, apply_M_inv, b, b.new_zeros(b.numel()), False,
+                      restart, max_iters, rtol, atol)
 
 
 # ---------------------------------------------------------------------------

@@ -118,78 +118,123 @@ def _call(op, v):
     return out
 
 
-def _gmres_generic(apply_A, apply_M_inv, b, x0, cfg):
-    """Reference krylov.py:39-117 over device vectors and arbitrary callables."""
-    import torch
+class DeviceVectors:
+    """Vector algebra of the generic GMRES loop on libpmgr kernels (the
+    reference's numpy algebra in krylov.py:52-117): norms, CGS2 projections,
+    basis combinations and axpby all run in libpmgr.so on the current stream;
+    only the (j+1) projection coefficients and the norms reach the host, where
+    the Hessenberg/Givens algebra lives exactly as in the reference."""
+
+    def __init__(self):
+        self.L = _lib.lib()
+        self.s = current_stream()
+
+    def zeros(self, shape):
+        import torch
+
+        return torch.zeros(shape, dtype=torch.float64, device="cuda")
+
+    def norm(self, v) -> float:
+        out = ctypes.c_double()
+        _lib.check(self.L.pmgr_vec_norm2(ptr(v), v.numel(), ctypes.byref(out), self.s))
+        return out.value
+
+    def axpby(self, a, x, b, y):
+        """y = a x + b y in place (b = 0 ignores y's contents); returns y."""
+        _lib.check(self.L.pmgr_vec_axpby(float(a), ptr(x), float(b), ptr(y), y.numel(), self.s))
+        return y
+
+    def project(self, V, k, w):
+        """CGS2: w -= V[:k]^T (V[:k] w), twice; returns the summed coefficients."""
+        h = np.zeros(k)
+        hd = self.zeros(k)
+        n = w.numel()
+        for _ in range(2):
+            _lib.check(self.L.pmgr_multidot(ptr(V), n, k, ptr(w), ptr(hd), self.s))
+            _lib.check(self.L.pmgr_multiaxpy(ptr(V), n, k, ptr(hd), ptr(w), self.s))
+            h += hd.cpu().numpy()
+        return h
+
+    def combine(self, V, j, y):
+        """u = sum_{k<j} y_k V_k."""
+        yd = to_device(np.ascontiguousarray(y, dtype=np.float64))
+        n = V.shape[1]
+        u = self.zeros(n)
+        _lib.check(self.L.pmgr_combine(ptr(V), n, n, j, ptr(yd), ptr(u), self.s))
+        return u
+
+
+def gmres_loop(vec, apply_A, apply_M, b, x, nonzero_x0, restart, max_iters, rtol, atol):
+    """Restarted right-preconditioned GMRES (reference krylov.py:39-117) over
+    an abstract vector algebra `vec` (DeviceVectors here; dist.DistVectors for
+    row-distributed slices).  Returns (x, iterations, history, converged)."""
     from scipy.linalg import solve_triangular
 
+    M = (lambda v: v) if apply_M is None else apply_M
+    n = b.numel()
+    r = vec.axpby(1.0, b, -1.0, apply_A(x).clone()) if nonzero_x0 else b.clone()
+    beta = vec.norm(r)
+    hist = [beta]
+    tol = max(rtol * beta, atol)
+    total = 0
+    m = restart
+    brk = False
+    while beta > tol and total < max_iters:
+        V = vec.zeros((m + 1, n))
+        H = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        vec.axpby(1.0 / beta, r, 0.0, V[0])
+        g[0] = beta
+        j = 0
+        while j < m and total < max_iters:
+            w = apply_A(M(V[j])).contiguous()
+            if w.untyped_storage().data_ptr() == V.untyped_storage().data_ptr():
+                w = w.clone()  # an identity operator hands back the basis row itself
+            H[:j + 1, j] = vec.project(V, j + 1, w)
+            hn = vec.norm(w)
+            H[j + 1, j] = hn
+            if hn > 1e-12 * max(float(np.linalg.norm(H[:j + 2, j])), 1e-300):
+                vec.axpby(1.0 / hn, w, 0.0, V[j + 1])
+            else:
+                brk = True
+            for i in range(j):
+                t = H[i, j]
+                H[i, j] = cs[i] * t + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * t + cs[i] * H[i + 1, j]
+            rho = float(np.hypot(H[j, j], H[j + 1, j]))
+            if rho == 0.0:
+                brk = True
+                break
+            cs[j], sn[j] = H[j, j] / rho, H[j + 1, j] / rho
+            H[j, j], H[j + 1, j] = rho, 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            j += 1
+            hist.append(abs(float(g[j])))
+            if abs(g[j]) <= tol or brk:
+                break
+        if j > 0:
+            y = solve_triangular(H[:j, :j], g[:j], lower=False)
+            x = vec.axpby(1.0, M(vec.combine(V, j, y)), 1.0, x.clone())
+            r = vec.axpby(1.0, b, -1.0, apply_A(x).clone())
+            beta = vec.norm(r)
+            hist[-1] = beta
+        if brk:
+            break
+    return x, total, np.array(hist), bool(beta <= tol)
+
+
+def _gmres_generic(apply_A, apply_M_inv, b, x0, cfg):
+    """Reference krylov.py:39-117 over device vectors and arbitrary callables."""
     host_in = not is_device_tensor(b)
     bd = to_device(b)
     n = bd.numel()
-    x = torch.zeros(n, dtype=torch.float64, device="cuda") if x0 is None else to_device(x0, n).clone()
-    M = (lambda v: v) if apply_M_inv is None else apply_M_inv
-    L = _lib.lib()
-    s = current_stream()
-    r = bd - _call(apply_A, x) if bool((x != 0).any()) else bd.clone()
-    beta = float(torch.linalg.vector_norm(r))
-    hist = [beta]
-    tol = max(cfg.rtol * beta, cfg.atol)
-    total = 0
-    m = cfg.restart
-    if beta > tol:
-        while total < cfg.max_iters:
-            V = torch.zeros((m + 1, n), dtype=torch.float64, device="cuda")
-            H = np.zeros((m + 1, m))
-            cs = np.zeros(m)
-            sn = np.zeros(m)
-            g = np.zeros(m + 1)
-            V[0] = r / beta
-            g[0] = beta
-            j = 0
-            brk = False
-            hd = torch.zeros(m + 1, dtype=torch.float64, device="cuda")
-            while j < m and total < cfg.max_iters:
-                w = _call(apply_A, _call(M, V[j])).contiguous()
-                # CGS2 projections on the device
-                h = np.zeros(j + 1)
-                for _ in range(2):
-                    _lib.check(L.pmgr_multidot(ptr(V), n, j + 1, ptr(w), ptr(hd), s))
-                    _lib.check(L.pmgr_multiaxpy(ptr(V), n, j + 1, ptr(hd), ptr(w), s))
-                    h += hd[:j + 1].cpu().numpy()
-                H[:j + 1, j] = h
-                hn = float(torch.linalg.vector_norm(w))
-                H[j + 1, j] = hn
-                if hn > 1e-12 * max(float(np.linalg.norm(H[:j + 2, j])), 1e-300):
-                    V[j + 1] = w / hn
-                else:
-                    brk = True
-                for i in range(j):
-                    t = H[i, j]
-                    H[i, j] = cs[i] * t + sn[i] * H[i + 1, j]
-                    H[i + 1, j] = -sn[i] * t + cs[i] * H[i + 1, j]
-                rho = float(np.hypot(H[j, j], H[j + 1, j]))
-                if rho == 0.0:
-                    brk = True
-                    break
-                cs[j] = H[j, j] / rho
-                sn[j] = H[j + 1, j] / rho
-                H[j, j] = rho
-                H[j + 1, j] = 0.0
-                g[j + 1] = -sn[j] * g[j]
-                g[j] = cs[j] * g[j]
-                total += 1
-                j += 1
-                hist.append(abs(float(g[j])))
-                if abs(g[j]) <= tol or brk:
-                    break
-            if j > 0:
-                y = solve_triangular(H[:j, :j], g[:j], lower=False)
-                u = torch.from_numpy(y).cuda() @ V[:j]
-                x = x + _call(M, u)
-                r = bd - _call(apply_A, x)
-                beta = float(torch.linalg.vector_norm(r))
-                hist[-1] = beta
-            if beta <= tol or brk:
-                break
+    vec = DeviceVectors()
+    x = vec.zeros(n) if x0 is None else to_device(x0, n).clone()
+    nonzero = x0 is not None and bool((x != 0).any())
+    x, total, hist, conv = gmres_loop(vec, lambda v: _call(apply_A, v),
+                                      None if apply_M_inv is None else (lambda v: _call(apply_M_inv, v)),
+                                      bd, x, nonzero, cfg.restart, cfg.max_iters, cfg.rtol, cfg.atol)
     out = x.cpu().numpy() if host_in else x
-    return out, SolveStats(total, np.array(hist), bool(beta <= tol))
+    return out, SolveStats(total, hist, conv)

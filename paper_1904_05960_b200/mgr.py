@@ -117,19 +117,111 @@ class MgrConfig:
                            self.amg_f_relax.to_c(), self.amg_terminal.to_c(), int(min(self.npartitions, 2 ** 62)), 0)
 
 
-@dataclass
 class MgrLevelView:
-    """Host copy of one reduction level, for inspection and parity checks."""
+    """Host view of one reduction level with the reference `_MgrLevel`
+    attributes (mgr.py:300-310): A, layout, split, blocks, P, R, f_relax,
+    global_smoother, spec, plus `coarse` (the next level's operator).  Every
+    matrix is exported from the device on first access (exports are snapshots;
+    the device hierarchy is what apply/gmres use)."""
 
-    split: CfSplitting
-    P: CsrMatrix
-    coarse: CsrMatrix
+    def __init__(self, h: "MgrHierarchy", level: int, split: CfSplitting, layout: FieldLayout):
+        self._h, self._l = h, level
+        self.split = split
+        self.layout = layout
+        self.spec = h.specs[level] if level < len(h.specs) else None
+        self._cache = {}
+
+    def _get(self, key, fn):
+        if key not in self._cache:
+            self._cache[key] = fn()
+        return self._cache[key]
+
+    @property
+    def A(self) -> CsrMatrix:
+        if self._l == 0:
+            return self._get("A", self._h._A.to_host)
+        return self._get("A", lambda: self._h._export(self._l - 1, 1))
+
+    @property
+    def P(self) -> CsrMatrix:
+        return self._get("P", lambda: self._h._export(self._l, 0))
+
+    @property
+    def coarse(self) -> CsrMatrix:
+        return self._get("coarse", lambda: self._h._export(self._l, 1))
+
+    @property
+    def R(self) -> CsrMatrix:
+        """Injection restriction [0 I] (mgr.py:179-186 with restrict='injection')."""
+        def make():
+            c = self.split.c_rows()
+            return CsrMatrix(len(c), self.split.n, np.arange(len(c) + 1), c, np.ones(len(c)))
+        return self._get("R", make)
+
+    @property
+    def blocks(self):
+        """(A_FF, A_FC, A_CF, A_CC), reference sparse.py:269-288 semantics."""
+        def make():
+            m = self.A.to_scipy()
+            f, c = self.split.f_rows(), self.split.c_rows()
+            mf, mc = m[f], m[c]
+            return tuple(CsrMatrix.from_scipy(x) for x in (mf[:, f], mf[:, c], mc[:, f], mc[:, c]))
+        return self._get("blocks", make)
+
+    @property
+    def f_relax(self):
+        spec = self.spec
+        if spec is None or spec.f_relax == "none":
+            return None
+        if spec.f_relax == "amg":
+            return _AmgFRelaxView(self._h.amg(self._l), max(1, spec.f_relax_sweeps))
+        a_ff = self.blocks[0]
+        return _JacobiFRelaxView(a_ff, 1.0 / a_ff.diagonal(), max(1, spec.f_relax_sweeps))
+
+    @property
+    def global_smoother(self):
+        if self.spec is None or self.spec.global_smoother == "none":
+            return None
+        if self.spec.global_smoother == "ilu":
+            return _IluView(self._h.ilu_factors(self._l))
+        return _HbgsView(self.spec.hbgs_sweeps)
+
+
+@dataclass
+class _AmgFRelaxView:
+    """Reference _AmgFRelax (mgr.py:253-262): the device AMG on A_FF."""
+
+    hierarchy: AmgHierarchy
+    ncycles: int
+
+
+@dataclass
+class _JacobiFRelaxView:
+    """Reference _JacobiFRelax (mgr.py:239-250)."""
+
+    a_ff: CsrMatrix
+    dinv: np.ndarray
+    nsweeps: int
+
+
+@dataclass
+class _IluView:
+    """Reference _IluGlobal (mgr.py:275-282): the combined L\\U factors."""
+
+    lu: CsrMatrix
+
+
+@dataclass
+class _HbgsView:
+    """Reference _HbgsGlobal (mgr.py:285-292)."""
+
+    nsweeps: int
 
 
 class MgrHierarchy:
     """Device-resident reduction hierarchy (reference MgrHierarchy, mgr.py:313-326)."""
 
-    def __init__(self, handle, A_dev: DeviceCsr, config: MgrConfig, specs):
+    def __init__(self, handle, A_dev: DeviceCsr, config: MgrConfig, specs, layout: FieldLayout | None = None):
         self._h = handle
         self._A = A_dev
         self.config = config
@@ -139,6 +231,8 @@ class MgrHierarchy:
         self._nlev = n.value
         self.terminal_cycles = max(1, config.terminal_cycles)
         self.f_relax_position = config.f_relax_position
+        self._layout = layout
+        self._levels = None
 
     @property
     def handle(self):
@@ -151,6 +245,13 @@ class MgrHierarchy:
     def apply(self, v):
         return mgr_apply(self, v)
 
+    def apply_bytes(self):
+        """(algorithmic bytes, kernel launches) of one application (the
+        roofline numerator of the preconditioner; pmgr_mgr_apply_bytes)."""
+        b, k = ctypes.c_double(), ctypes.c_int64()
+        _lib.check(_lib.lib().pmgr_mgr_apply_bytes(self._h, ctypes.byref(b), ctypes.byref(k)))
+        return b.value, k.value
+
     def level_sizes(self):
         s = np.zeros(self._nlev + 1, dtype=np.int64)
         _lib.check(_lib.lib().pmgr_mgr_level_sizes(self._h, s.ctypes.data_as(_lib.c_i64p)))
@@ -160,22 +261,43 @@ class MgrHierarchy:
         """Combined L\\U factors of the level's ILU(k) global smoother."""
         return self._export(level, 2)
 
-    def _export(self, level, what) -> CsrMatrix:
+    def _export_dev(self, level, what) -> DeviceCsr:
         out = ctypes.c_void_p()
         _lib.check(_lib.lib().pmgr_mgr_export_csr(self._h, level, what, current_stream(), ctypes.byref(out)))
         nr, nc, nz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _lib.check(_lib.lib().pmgr_csr_info(out, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nz)))
-        return DeviceCsr(out, nr.value, nc.value, nz.value).to_host()
+        return DeviceCsr(out, nr.value, nc.value, nz.value)
+
+    def _export(self, level, what) -> CsrMatrix:
+        return self._export_dev(level, what).to_host()
 
     @property
     def levels(self):
-        out = []
-        sizes = self.level_sizes()
-        for l in range(self._nlev):
-            isc = np.zeros(sizes[l], dtype=np.int8)
-            _lib.check(_lib.lib().pmgr_mgr_export_vec(self._h, l, 0, isc.ctypes.data, current_stream()))
-            out.append(MgrLevelView(CfSplitting(isc.astype(bool)), self._export(l, 0), self._export(l, 1)))
-        return out
+        """Per-level views with the reference `_MgrLevel` attributes."""
+        if self._levels is None:
+            out = []
+            sizes = self.level_sizes()
+            lay = self._layout
+            for l in range(self._nlev):
+                isc = np.zeros(sizes[l], dtype=np.int8)
+                _lib.check(_lib.lib().pmgr_mgr_export_vec(self._h, l, 0, isc.ctypes.data, current_stream()))
+                split = CfSplitting(isc.astype(bool))
+                out.append(MgrLevelView(self, l, split, lay))
+                lay = lay.restrict(split.c_rows()) if lay is not None else None
+            self._levels = out
+            self._terminal_layout = lay
+        return self._levels
+
+    @property
+    def terminal_A(self) -> CsrMatrix:
+        """The operator the terminal AMG works on (reference mgr.py:316)."""
+        if self._nlev == 0:
+            return self._A.to_host()
+        return self._export(self._nlev - 1, 1)
+
+    @property
+    def terminal_kind(self) -> str:
+        return self.config.terminal
 
     def amg(self, level: int) -> AmgHierarchy | None:
         """F-relaxation AMG of `level` (-1: terminal AMG), borrowed."""
@@ -196,6 +318,15 @@ class MgrHierarchy:
             self._h = None
 
 
+def config_from_options(opts: dict) -> MgrConfig:
+    """MgrConfig from problems.solver_options' plain-data description."""
+    levels = tuple(MgrLevelSpec({Field(t) for t in lv["f"]}, {Field(t) for t in lv["c"]},
+                                **{k: v for k, v in lv.items() if k not in ("f", "c")}) for lv in opts["levels"])
+    return MgrConfig(levels=levels, terminal_cycles=opts.get("terminal_cycles", 1),
+                     f_relax_position=opts.get("f_relax_position", "pre"), npartitions=opts.get("npartitions", 1),
+                     amg_f_relax=AmgConfig(**opts["amg_f_relax"]), amg_terminal=AmgConfig(**opts["amg_terminal"]))
+
+
 def mgr_setup(A, layout: FieldLayout, config: MgrConfig) -> MgrHierarchy:
     """Build the reduction hierarchy for operator A laid out by `layout`."""
     dA = as_device_csr(A)
@@ -203,7 +334,7 @@ def mgr_setup(A, layout: FieldLayout, config: MgrConfig) -> MgrHierarchy:
     out = ctypes.c_void_p()
     _lib.check(_lib.lib().pmgr_mgr_setup(dA.handle, fo0.ctypes.data, eo0.ctypes.data, specs, len(config.levels),
                                          ctypes.byref(cfg), current_stream(), ctypes.byref(out)))
-    return MgrHierarchy(out, dA, config, config.levels)
+    return MgrHierarchy(out, dA, config, config.levels, layout)
 
 
 def setup_args(dA, layout: FieldLayout, config: MgrConfig):

@@ -157,6 +157,15 @@ class DeviceCsr:
     def shape(self):
         return (self.nrows, self.ncols)
 
+    def download(self):
+        """(row_offsets, col_indices, values) host copies, unvalidated."""
+        ro = np.empty(self.nrows + 1, dtype=np.int64)
+        ci = np.empty(self.nnz, dtype=np.int32)
+        va = np.empty(self.nnz, dtype=np.float64)
+        _lib.check(_lib.lib().pmgr_csr_download(self._h, ro.ctypes.data, ci.ctypes.data, va.ctypes.data, 0,
+                                                current_stream()))
+        return ro, ci, va
+
     def to_host(self) -> "CsrMatrix":
         ro = np.empty(self.nrows + 1, dtype=np.int64)
         ci = np.empty(self.nnz, dtype=np.int32)
@@ -191,6 +200,13 @@ class CsrMatrix:
         object.__setattr__(self, "row_offsets", np.ascontiguousarray(self.row_offsets, dtype=np.int64))
         object.__setattr__(self, "col_indices", np.ascontiguousarray(self.col_indices, dtype=np.int32))
         object.__setattr__(self, "values", np.ascontiguousarray(self.values, dtype=np.float64))
+        # the matrix is immutable (reference sparse.py:1-7) and its device copy
+        # is a snapshot taken on first use: expose read-only views so an in-place
+        # update (A.values[:] = ...) fails instead of leaving a stale device copy
+        for name in ("row_offsets", "col_indices", "values"):
+            v = getattr(self, name).view()
+            v.flags.writeable = False
+            object.__setattr__(self, name, v)
         self._validate()
 
     def _validate(self):

@@ -50,7 +50,32 @@ CASES = {
     "c2_32": (lambda: problems.make_c2(seed=0, n=32), 4, False),
     "c4_16": (lambda: problems.make_c4(seed=0, n=16), 4, True),
     "c3_16": (lambda: problems.make_c3(seed=0, n=16), 4, False),
+    # parity configuration at 32^3: C4 125 iterations, C3 2801 (the stall is the algorithm's)
+    "c4_32": (lambda: problems.make_c4(seed=0, n=32), 4, True),
+    "c3_32": (lambda: problems.make_c3(seed=0, n=32), 4, False),
 }
+
+# production configurations (problems.solver_options) at 32^3, goldens from the reference
+PROD_CASES = {
+    "c3_32p": ("C3", dict(n=32)),
+    "c4_32p": ("C4", dict(n=32)),
+}
+# full-size production goldens from the pinned oracle (oracle/make_golden_full.py)
+FULL_CASES = {
+    "c3_64p": ("C3", dict(n=64)),
+    "c4_128p": ("C4", dict(n=128)),
+}
+
+
+def gmres_options(tag, pb=None):
+    """(restart, max_iters) the golden's GMRES solve used."""
+    if tag in PROD_CASES:
+        name, kw = PROD_CASES[tag]
+        o = problems.solver_options(name, pb if pb is not None else problems.make(name, **kw))
+        return o["restart"], o["max_iters"]
+    if tag == "c3_32":
+        return 100, 3000
+    return 100, 1000
 
 
 def oracle_levels(pb, n_max, four_field):
@@ -128,6 +153,11 @@ def problem_csr(pb):
 
 
 def oracle_hierarchy(tag):
+    if tag in PROD_CASES:
+        name, kw = PROD_CASES[tag]
+        pb = problems.make(name, **kw)
+        cfg = O.config_from_options(problems.solver_options(name, pb))
+        return pb, O.mgr_setup(problem_csr(pb), pb.field_of, pb.entity_of, cfg)
     gen, n_max, four = CASES[tag]
     pb = gen()
     cfg = oracle_config(oracle_levels(pb, n_max, four))

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests._golden import (CASES, VARIANT_SPECS, dcsr, digest, get_csr, load, oracle_hierarchy,
+from tests._golden import (CASES, VARIANT_SPECS, dcsr, digest, get_csr, gmres_options, load, oracle_hierarchy,
                            oracle_variant_hierarchy, vec_sha)
 
 
@@ -93,7 +93,14 @@ SLOW = pytest.mark.skipif(not os.environ.get("PMGR_SLOW"), reason="set PMGR_SLOW
 
 @pytest.mark.parametrize("tag", ["c1_6", "c2_6", "c4_4", "c1_16", "c4_16",
                                  pytest.param("c2_32", marks=pytest.mark.slow),
-                                 pytest.param("c3_16", marks=[pytest.mark.slow, SLOW])])
+                                 pytest.param("c3_16", marks=[pytest.mark.slow, SLOW]),
+                                 # the production configurations (ILU(1) global smoother, multi-cycle AMG
+                                 # F-relaxation, long restarts): the oracle that generates the full-size
+                                 # goldens is pinned to the reference on them here
+                                 pytest.param("c4_32p", marks=pytest.mark.slow),
+                                 pytest.param("c3_32p", marks=pytest.mark.slow),
+                                 pytest.param("c4_32", marks=[pytest.mark.slow, SLOW]),
+                                 pytest.param("c3_32", marks=[pytest.mark.slow, SLOW])])
 def test_mgr_problem(tag):
     check_problem(tag, *oracle_hierarchy(tag))
 
@@ -135,8 +142,9 @@ def check_problem(tag, pb, h):
     zr = d["apply_z"]
     assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
     A = O.Csr(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
-    x, its, hist, conv = O.gmres(lambda y: O.spmv(A, y), h.apply, pb.rhs, restart=100,
-                                 max_iters=1000, rtol=1e-6)
+    restart, max_iters = gmres_options(tag, pb)
+    x, its, hist, conv = O.gmres(lambda y: O.spmv(A, y), h.apply, pb.rhs, restart=restart,
+                                 max_iters=max_iters, rtol=1e-6)
     assert conv == bool(d["gmres_conv"])
     assert its == int(d["gmres_iters"])
     if conv:
