@@ -528,19 +528,22 @@ def make_c3(seed=0, n=64, device=False):
                     name=f"C3-{n}^3")
 
 
-def make_c4(seed=0, n=128, device=False):
+def make_c4(seed=0, n=128, device=False, nz=None):
     """C4: three-phase, Stone-I-like, saturations ~ Dirichlet(2,2,2),
-    perm sigma=1.5 (configs[3])."""
+    perm sigma=1.5 (configs[3]).  nz < n: an n x n x nz slab of the same
+    generator (the bounded CPU-baseline sample, bench.py)."""
+    nz = n if nz is None else nz
     rE, rk, rs, rp, rb = _streams(seed)
-    E = np.exp(0.5 * rE.standard_normal((n, n, n)))
-    k = np.exp(1.5 * rk.standard_normal((n, n, n)))
-    d = rs.dirichlet((2.0, 2.0, 2.0), size=(n, n, n))  # (…, 3): w, g, o
+    E = np.exp(0.5 * rE.standard_normal((nz, n, n)))
+    k = np.exp(1.5 * rk.standard_normal((nz, n, n)))
+    d = rs.dirichlet((2.0, 2.0, 2.0), size=(nz, n, n))  # (…, 3): w, g, o
     sats = np.stack([d[..., 0], d[..., 1]])
     h = 1.0 / n
-    p = _pressure_state(rp, n, n, n, h)
-    return (assemble_device if device else assemble)(n, n, n, E=E, kx=k, ky=k, kz=k, phases="three", sats=sats, pstate=p,
-                    mu=(1.0, 0.2, 5.0), phi=0.2, ct=1e-3, dt=_DT_MULTIPHASE, rhs_rng=rb,
-                    name=f"C4-{n}^3")
+    p = _pressure_state(rp, n, n, nz, h)
+    return (assemble_device if device else assemble)(n, n, nz, E=E, kx=k, ky=k, kz=k, phases="three", sats=sats,
+                                                     pstate=p, mu=(1.0, 0.2, 5.0), phi=0.2, ct=1e-3,
+                                                     dt=_DT_MULTIPHASE, rhs_rng=rb,
+                                                     name=f"C4-{n}^3" if nz == n else f"C4-{n}x{n}x{nz}")
 
 
 def make_c5(seed=0, nxy=128, nz_per_gpu=128, gpus=1, device=False):
