@@ -18,10 +18,10 @@ residual history inside the timed call).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pmgr|reference] [--config C4]
 
-N > 1 (torchrun): weak scaling of the row-distributed solve (C5: the
-128 x 128 x 128 slab stacked N times in z, rank-major numbering, distributed
-setup, NCCL halo exchanges / all-reduces inside libpmgr); --strong keeps the
-global problem fixed (C4).  `--impl reference` times the CPU oracle (the
+N > 1 (torchrun): strong scaling of the row-distributed C4 solve (the N = 1
+workload split into rank-major z-slabs, distributed setup, NCCL halo
+exchanges / all-gathers / all-reduces inside libpmgr); --weak runs the C5
+weak-scaling stack instead (a 128^3 slab per GPU stacked in z).  `--impl reference` times the CPU oracle (the
 reference algorithm restated in C, oracle/) on the host cores, rank 0 only.
 """
 
@@ -316,10 +316,16 @@ def run_gpu_dist(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    # the global slab stack assembled on the GPU and renumbered rank-major there
+    # the global problem assembled on every GPU and renumbered rank-major there:
+    # weak scaling = the C5 slab stack (ns^3 cells per GPU), strong scaling =
+    # the fixed C4 128^3 problem
     ns = args.slab
-    base = problems.make_c5(seed=args.seed, nxy=ns, nz_per_gpu=ns, gpus=world, device=True)
-    opts = problems.solver_options("C5", base, variant=args.dist_variant)
+    if not args.weak:
+        base = problems.make_c4(seed=args.seed, n=128, device=True)
+        opts = problems.solver_options("C4", base, variant=args.dist_variant)
+    else:
+        base = problems.make_c5(seed=args.seed, nxy=ns, nz_per_gpu=ns, gpus=world, device=True)
+        opts = problems.solver_options("C5", base, variant=args.dist_variant)
     pb, bounds = problems.rank_major(base, world)
     del base
     cfg = mgr.config_from_options(opts)
@@ -415,10 +421,13 @@ def run_gpu_dist(args, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": METRIC, "value": pb.n / t_max / 1e6, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, paper_1904_05960_b200/problems.py)",
-            "config": {"workload": f"C5: two-phase poromechanics {ns}x{ns}x{ns * world} ({ns}^3 cells per GPU, "
-                                   "rank-major z-slabs) -- MGR-preconditioned GMRES to rtol 1e-6",
+            "config": {"workload": ("C4: three-phase poromechanics 128^3 over " + f"{world} GPU(s) (rank-major z-slabs)"
+                                    if not args.weak else
+                                    f"C5: two-phase poromechanics {ns}x{ns}x{ns * world} ({ns}^3 cells per GPU, "
+                                    "rank-major z-slabs)") + " -- MGR-preconditioned GMRES to rtol 1e-6",
                        "n_dofs": pb.n, "n_dofs_per_gpu": int(np.diff(bounds).max()), "nnz": pb.nnz,
                        "solver": solver_summary(opts), "gmres_iterations": st.iterations,
                        "true_relative_residual": rel, "mgr_levels": levels_info,
@@ -687,7 +696,10 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--restart", type=int, default=None, help="override the configuration's GMRES restart")
     ap.add_argument("--slab", type=int, default=128, help="distributed path: cells per side of each GPU's slab")
-    ap.add_argument("--dist-variant", default="parity", choices=["parity", "production"],
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: weak scaling of the C5 slab stack (--slab^3 cells per GPU) instead of the default "
+                         "strong scaling of the C4 problem (the N = 1 workload)")
+    ap.add_argument("--dist-variant", default="production", choices=["parity", "production"],
                     help="distributed path: solver configuration (problems.solver_options)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profile one solve between cudaProfilerStart/Stop and exit")
@@ -706,7 +718,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if args.dist or (world > 1 and not args.replicas and not args.ncu):
+    if args.dist or args.weak or (world > 1 and not args.replicas and not args.ncu):
         run_gpu_dist(args, rank, world, local_rank)
         return
     run_gpu(args, rank, world, local_rank)

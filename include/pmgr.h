@@ -252,6 +252,17 @@ PMGR_API int pmgr_nccl_get_id(pmgr_nccl_id *out);
 /* NCCL communicator over the process's libnccl (one GPU per rank). */
 PMGR_API int pmgr_transport_nccl_create(const pmgr_nccl_id *id, int32_t rank, int32_t nranks,
                                         pmgr_transport **out);
+/* Host-staged transport over caller-supplied collectives on HOST memory (for
+ * example torch.distributed gloo): a personalised all-to-all (sptr[p] /
+ * sbytes[p] to peer p, rptr[p] / rbytes[p] from peer p; self entries are 0)
+ * and an in-place double all-reduce (sum, the same result on every rank).
+ * Each callback returns 0 on success.  Every exchange synchronises the
+ * stream -- slow by design: several processes can share one GPU. */
+typedef int (*pmgr_alltoallv_fn)(void *ctx, const void *const *sptr, const int64_t *sbytes, void *const *rptr,
+                                 const int64_t *rbytes);
+typedef int (*pmgr_allreduce_fn)(void *ctx, double *buf, int64_t n);
+PMGR_API int pmgr_transport_host_create(int32_t rank, int32_t nranks, pmgr_alltoallv_fn alltoallv,
+                                        pmgr_allreduce_fn allreduce, void *ctx, pmgr_transport **out);
 PMGR_API int pmgr_transport_destroy(pmgr_transport *t);
 PMGR_API int pmgr_dist_create(const pmgr_csr *A, pmgr_mgr *M, const int64_t *bounds, int32_t rank,
                               int32_t nranks, pmgr_transport *t, void *stream, pmgr_dist **out);

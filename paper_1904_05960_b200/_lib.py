@@ -60,6 +60,12 @@ class GmresCfg(ctypes.Structure):
                 ("atol", ctypes.c_double)]
 
 
+ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
+                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p),
+                                ctypes.POINTER(ctypes.c_int64))
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+
+
 class NcclId(ctypes.Structure):
     _fields_ = [("internal", ctypes.c_char * 128)]
 
@@ -119,6 +125,7 @@ SIGNATURES = {
     "pmgr_vec_axpby": (ctypes.c_int, [ctypes.c_double, vp, ctypes.c_double, vp, ctypes.c_int64, vp]),
     "pmgr_combine": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]),
     "pmgr_nccl_get_id": (ctypes.c_int, [ctypes.POINTER(NcclId)]),
+    "pmgr_transport_host_create": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp]),
     "pmgr_transport_nccl_create": (ctypes.c_int, [ctypes.POINTER(NcclId), ctypes.c_int32, ctypes.c_int32,
                                                   ctypes.POINTER(vp)]),
     "pmgr_transport_destroy": (ctypes.c_int, [vp]),

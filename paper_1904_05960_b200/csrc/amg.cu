@@ -850,6 +850,23 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
     }
     AmgLevel &L = h.levels[0];
     const int64_t n = L.A->nrows;
+    if (x && h.collapse_from == 0) {
+        // the whole hierarchy is the collapsed operator M_t (the cycle from a
+        // zero guess is the linear map b -> M_t b), so the cycle from x is
+        // x + M_t (b - A x): one residual pass, the dense product, an axpy
+        const int64_t o = L.off;
+        halo_exchange(L.halo.get(), const_cast<double *>(x), s);
+        spmv_residual(L.A->view(), x, b, L.r.p, s);
+        if (h.gather) {
+            gather_full(h.gather.get(), L.r.p + o, h.full.p, s);
+            dense_matvec_rows(h.collapsed.p, n, h.gather->n_full, h.collapsed_ld, h.full.p, L.xo.p + o, s);
+        } else {
+            dense_matvec(h.collapsed.p, n, h.collapsed_ld, L.r.p, L.xo.p, s);
+        }
+        vec_copy(x + o, out + o, n, s);
+        vec_axpy(1.0, L.xo.p + o, out + o, n, s);
+        return;
+    }
     if (!x) {
         const int64_t o = L.off;
         if (L.jacobi) vec_copy_div(b + o, L.dtilde.p + o, n, L.b.p + o, L.x.p + o, s);
@@ -857,29 +874,39 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
         cycle_from_zero(h, 0, s, out);
         return;
     }
-    // nonzero initial guess at the top level: pre-sweep from x
-    vec_copy(b, L.b.p, n, s);
+    // nonzero initial guess at the top level: pre-sweep from x.  Vectors are
+    // in the level's ext layout (row-distributed hierarchies: owned range at
+    // L.off plus ghosts, exchanged before every operator that reads them; x
+    // must be an ext buffer of the level-0 space; offsets are 0 and the
+    // exchanges no-ops on one GPU)
+    const int64_t o = L.off;
+    vec_copy(b + o, L.b.p + o, n, s);
     const CsrView A = L.A->view();
     if (L.jacobi) {
+        halo_exchange(L.halo.get(), const_cast<double *>(x), s);
         spmv_jacobi(A, x, L.b.p, L.dtilde.p, L.x.p, s);
     } else {
         vec_copy(x, L.x.p, n, s);
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, true, s);
     }
+    halo_exchange(L.halo.get(), L.x.p, s);
     spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
+    halo_exchange(L.halo.get(), L.r.p, s);
     const double *e;
     if (h.levels.size() > 1) {
         AmgLevel &N = h.levels[1];
         if (N.jacobi) spmv_restrict_div(L.R.view(), L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
         else spmv(L.R.view(), L.r.p, N.b.p, s);
         cycle_from_zero(h, 1, s);
-        e = h.levels[1].xo.p;
+        halo_exchange(N.halo.get(), N.xo.p, s);
+        e = N.xo.p;
     } else {
         spmv(L.R.view(), L.r.p, h.cb.p, s);
         e = coarse_solve(h, s);
     }
     spmv_add(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
+        halo_exchange(L.halo.get(), L.x.p, s);
         spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, out, s);
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);

@@ -429,6 +429,17 @@ int pmgr_transport_nccl_create(const pmgr_nccl_id *id, int32_t rank, int32_t nra
     });
 }
 
+int pmgr_transport_host_create(int32_t rank, int32_t nranks, pmgr_alltoallv_fn alltoallv,
+                               pmgr_allreduce_fn allreduce, void *ctx, pmgr_transport **out) {
+    return guard([&] {
+        require(out && alltoallv && allreduce, "NULL argument");
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+        auto *t = new pmgr_transport;
+        t->t = pmgr::make_callback_transport(rank, nranks, alltoallv, allreduce, ctx);
+        *out = t;
+    });
+}
+
 int pmgr_transport_destroy(pmgr_transport *t) {
     return guard([&] { delete t; });
 }

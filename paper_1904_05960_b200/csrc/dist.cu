@@ -370,6 +370,138 @@ std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank,
     return std::unique_ptr<Transport>(new NcclTransport(id, rank, nranks));
 }
 
+// ---- host-staged transport over caller-supplied collectives --------------
+// (e.g. torch.distributed gloo on CPU tensors): every exchange packs on the
+// device, copies to pinned host buffers, synchronises the stream, runs the
+// caller's personalised all-to-all / all-reduce on host memory and copies the
+// received data back.  Synchronous and slow by design -- it lets several
+// processes share one GPU (no kernel ever waits on another process) and
+// exercises the multi-process setup and solve end to end without NCCL.
+struct CallbackTransport : Transport {
+    pmgr_alltoallv_fn a2a;
+    pmgr_allreduce_fn ared;
+    void *ctx;
+    std::vector<char> hs, hr;  // host staging (pageable: cudaMemcpy synchronous)
+    CallbackTransport(int r, int nr, pmgr_alltoallv_fn f, pmgr_allreduce_fn g, void *c) : a2a(f), ared(g), ctx(c) {
+        rank = r;
+        nranks = nr;
+    }
+    // host all-to-all: sbytes[p] from hsend + soff[p] to peer p, rbytes[p] into hrecv + roff[p]
+    void host_a2a(const std::vector<int64_t> &sbytes, const std::vector<int64_t> &rbytes, char *hsend, char *hrecv) {
+        std::vector<const void *> sp(nranks);
+        std::vector<void *> rp(nranks);
+        int64_t so = 0, ro = 0;
+        for (int p = 0; p < nranks; ++p) {
+            sp[p] = hsend + so;
+            rp[p] = hrecv + ro;
+            so += sbytes[p];
+            ro += rbytes[p];
+        }
+        if (a2a(ctx, sp.data(), sbytes.data(), rp.data(), rbytes.data()) != 0)
+            fail(PMGR_ERR_CUDA, "host transport: all-to-all callback failed");
+    }
+    void exchange(Halo &h, double *ext, cudaStream_t s) override {
+        const int64_t ns = h.send_idx.n;
+        if (ns > 0) {
+            k_pack<<<grid_for(ns, 256), 256, 0, s>>>(h.sbuf.p, ext + h.off, h.send_idx.p, ns);
+            PMGR_LAUNCHED();
+        }
+        std::vector<int64_t> sb(nranks, 0), rb(nranks, 0), so(nranks, 0), ro(nranks, 0);
+        for (size_t i = 0; i < h.speer.size(); ++i) {
+            sb[h.speer[i]] = 8 * h.scnt[i];
+            so[h.speer[i]] = h.soff[i];
+        }
+        for (size_t i = 0; i < h.rpeer.size(); ++i) {
+            rb[h.rpeer[i]] = 8 * h.rcnt[i];
+            ro[h.rpeer[i]] = h.roff[i];
+        }
+        int64_t st = 0, rt = 0;
+        for (int p = 0; p < nranks; ++p) {
+            st += sb[p];
+            rt += rb[p];
+        }
+        hs.resize(st > 0 ? st : 1);
+        hr.resize(rt > 0 ? rt : 1);
+        int64_t o = 0;
+        for (int p = 0; p < nranks; ++p) {  // device send buffer -> host, peer order
+            if (sb[p]) PMGR_CUDA(cudaMemcpyAsync(hs.data() + o, h.sbuf.p + so[p], sb[p], cudaMemcpyDeviceToHost, s));
+            o += sb[p];
+        }
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        host_a2a(sb, rb, hs.data(), hr.data());
+        o = 0;
+        for (int p = 0; p < nranks; ++p) {
+            if (rb[p]) PMGR_CUDA(cudaMemcpyAsync(ext + ro[p], hr.data() + o, rb[p], cudaMemcpyHostToDevice, s));
+            o += rb[p];
+        }
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+    void gather(Gather &g, const double *own, double *full, cudaStream_t s) override {
+        const int64_t mine = g.start[rank + 1] - g.start[rank];
+        std::vector<int64_t> sb(nranks), rb(nranks);
+        for (int p = 0; p < nranks; ++p) {
+            sb[p] = p == rank ? 0 : 8 * mine;
+            rb[p] = p == rank ? 0 : 8 * (g.start[p + 1] - g.start[p]);
+        }
+        hs.resize(8 * mine * (nranks - 1) + 1);
+        hr.resize(8 * (g.n_full - mine) + 1);
+        if (mine > 0) {
+            PMGR_CUDA(cudaMemcpyAsync(full + g.start[rank], own, 8 * mine, cudaMemcpyDeviceToDevice, s));
+            PMGR_CUDA(cudaMemcpyAsync(hs.data(), own, 8 * mine, cudaMemcpyDeviceToHost, s));
+        }
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        for (int c = 1; c < nranks - 1; ++c) std::memcpy(hs.data() + 8 * mine * c, hs.data(), 8 * mine);
+        host_a2a(sb, rb, hs.data(), hr.data());
+        int64_t o = 0;
+        for (int p = 0; p < nranks; ++p) {
+            if (rb[p]) PMGR_CUDA(cudaMemcpyAsync(full + g.start[p], hr.data() + o, rb[p], cudaMemcpyHostToDevice, s));
+            o += rb[p];
+        }
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+    void allreduce(double *buf, int64_t n, cudaStream_t s) override {
+        if (n <= 0) return;
+        std::vector<double> hb(n);
+        PMGR_CUDA(cudaMemcpyAsync(hb.data(), buf, 8 * n, cudaMemcpyDeviceToHost, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        if (ared(ctx, hb.data(), n) != 0) fail(PMGR_ERR_CUDA, "host transport: all-reduce callback failed");
+        PMGR_CUDA(cudaMemcpyAsync(buf, hb.data(), 8 * n, cudaMemcpyHostToDevice, s));
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+    void alltoall_counts(const std::vector<int64_t> &send, std::vector<int64_t> &recv, cudaStream_t) override {
+        std::vector<int64_t> by(nranks, 8);
+        recv.assign(nranks, 0);
+        host_a2a(by, by, (char *)send.data(), (char *)recv.data());
+    }
+    void alltoallv(const std::vector<const void *> &sptr, const std::vector<int64_t> &sbytes,
+                   const std::vector<void *> &rptr, const std::vector<int64_t> &rbytes, cudaStream_t s) override {
+        int64_t st = 0, rt = 0;
+        for (int p = 0; p < nranks; ++p) {
+            st += sbytes[p];
+            rt += rbytes[p];
+        }
+        std::vector<char> sh(st > 0 ? st : 1), rh(rt > 0 ? rt : 1);
+        int64_t o = 0;
+        for (int p = 0; p < nranks; ++p) {
+            if (sbytes[p]) PMGR_CUDA(cudaMemcpyAsync(sh.data() + o, sptr[p], sbytes[p], cudaMemcpyDeviceToHost, s));
+            o += sbytes[p];
+        }
+        PMGR_CUDA(cudaStreamSynchronize(s));
+        host_a2a(sbytes, rbytes, sh.data(), rh.data());
+        o = 0;
+        for (int p = 0; p < nranks; ++p) {
+            if (rbytes[p]) PMGR_CUDA(cudaMemcpyAsync(rptr[p], rh.data() + o, rbytes[p], cudaMemcpyHostToDevice, s));
+            o += rbytes[p];
+        }
+        PMGR_CUDA(cudaStreamSynchronize(s));
+    }
+};
+
+std::unique_ptr<Transport> make_callback_transport(int rank, int nranks, pmgr_alltoallv_fn a2a,
+                                                   pmgr_allreduce_fn ared, void *ctx) {
+    return std::unique_ptr<Transport>(new CallbackTransport(rank, nranks, a2a, ared, ctx));
+}
+
 void halo_exchange(Halo *h, double *ext, cudaStream_t s) {
     if (h && h->tr) h->tr->exchange(*h, ext, s);
 }
@@ -726,6 +858,9 @@ void plan_amg(Builder &B, const pmgr_amg &G, Space *S0, AmgPlan &P) {
         B.read(P.sp[l], &L.R, P.sp[l + 1]);
         B.read(P.sp[l + 1], &L.P, P.sp[l]);
     }
+    // a wholly collapsed hierarchy still applies its operator once per cycle
+    // from a nonzero guess (multi-cycle F-relaxation: x + M_t (b - A x))
+    if (G.collapse_from == 0) B.read(P.sp[0], G.levels[0].A.get(), P.sp[0]);
     if (G.levels[0].A->nbrows > 0) S0->triples = true;
 }
 
@@ -747,6 +882,8 @@ std::unique_ptr<pmgr_amg> build_amg(Builder &B, const AmgPlan &P) {
             B.localize(*GL.A, S, S, *A);
             B.localize(GL.P, S, P.sp[l + 1], L.P);
             B.localize(GL.R, P.sp[l + 1], S, L.R);
+        } else if (l == 0) {
+            B.localize(*GL.A, S, S, *A);
         } else {
             A->nrows = S->n_own();  // the collapsed level only needs its row count
             A->ncols = S->n_ext();
@@ -818,8 +955,9 @@ std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, cons
         fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports pre F-relaxation and one terminal cycle");
     for (const MgrLevel &L : M->levels) {
         if (L.smoother) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution of a level with a global smoother");
-        if (L.f_relax == PMGR_FRELAX_NONE || L.f_relax_sweeps != 1)
-            fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports single-sweep AMG / Jacobi F-relaxation");
+        if (L.f_relax == PMGR_FRELAX_NONE || (L.f_relax_sweeps != 1 && L.f_relax != PMGR_FRELAX_AMG))
+            fail(PMGR_ERR_NOT_SUPPORTED,
+                 "row distribution supports AMG F-relaxation (any number of cycles) or single-sweep Jacobi");
     }
     if (!M->terminal) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution needs a terminal AMG");
     Builder B(rank, nranks, tr, s);
@@ -875,7 +1013,7 @@ std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, cons
         L.halo_f = F->halo;
         L.halo_c = C->halo;
         L.f_relax = G.f_relax;
-        L.f_relax_sweeps = 1;
+        L.f_relax_sweeps = G.f_relax_sweeps;
         B.localize(G.A_cf, C, F, L.A_cf);
         B.localize(G.P, Mi, C, L.P);
         B.own_map(G.f_rows.p, F, Mi, L.f_rows, false);
@@ -883,6 +1021,10 @@ std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, cons
         B.own_map(G.f_index.p, Mi, F, L.f_index, true);
         if (G.dinv_ff.p) B.own_values(G.dinv_ff.p, F, L.dinv_ff);
         B.ext_buffer(F, L.zf);
+        if (L.f_relax_sweeps > 1) {  // multi-cycle F-relaxation: gathered rhs and the previous iterate
+            B.ext_buffer(F, L.vf);
+            B.ext_buffer(F, L.tmpf);
+        }
         B.ext_buffer(C, L.rc);
         B.ext_buffer(C, L.zc);
         if (G.f_relax == PMGR_FRELAX_AMG) L.amg = build_amg(B, fplans[l]);

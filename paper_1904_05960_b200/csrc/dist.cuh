@@ -26,6 +26,8 @@ struct Transport {
 
 std::unique_ptr<Transport> make_nccl_transport(const pmgr_nccl_id &id, int rank, int nranks);
 void nccl_unique_id(pmgr_nccl_id *out);
+std::unique_ptr<Transport> make_callback_transport(int rank, int nranks, pmgr_alltoallv_fn a2a,
+                                                   pmgr_allreduce_fn ared, void *ctx);
 
 // one rank's slice of a global (A, MGR) pair
 struct DistSolver {

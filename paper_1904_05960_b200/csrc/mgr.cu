@@ -212,8 +212,8 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
 void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
     if (L.f_relax == PMGR_FRELAX_AMG) {
         amg_cycle(*L.amg, vf, nullptr, zf, s);
-        for (int c = 1; c < L.f_relax_sweeps; ++c) {
-            vec_copy(zf, L.tmpf.p, L.nf, s);
+        for (int c = 1; c < L.f_relax_sweeps; ++c) {  // ext layout: owned range at off_f
+            vec_copy(zf + L.off_f, L.tmpf.p + L.off_f, L.nf, s);
             amg_cycle(*L.amg, vf, L.tmpf.p, zf, s);
         }
     } else {
@@ -303,7 +303,7 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
             }
         }
         if (!done) {
-            vec_gather(v, L.f_rows.p, L.nf, L.vf.p, s);
+            vec_gather(v, L.f_rows.p + L.off_f, L.nf, L.vf.p + L.off_f, s);
             f_relax_apply(L, L.vf.p, L.zf.p, s);
         }
         // the consumer's first step rides on the residual kernel

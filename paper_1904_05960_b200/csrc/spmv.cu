@@ -603,7 +603,232 @@ __global__ void __launch_bounds__(256, MINB) k_bsr3p(int64_t ntrip, int64_t nb, 
 #undef PMGR_BSR3P_BATCH
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged block SpMV (pure BSR3 operators: the level-0 F-relaxation sweeps)
+// ---------------------------------------------------------------------------
+//
+// A persistent grid of CTAs with 8 consumer warps and one producer warp.  The
+// operator is cut into tiles of TPT = 8 * TPW consecutive row triples; a
+// tile's blocks are one contiguous range of the value stream (72 B each,
+// column-major) and of the block-column stream, so the producer moves them
+// with two cp.async.bulk copies (TMA 1D) into a ring of shared-memory stages,
+// signalled through mbarriers -- the loads are decoupled from the x gathers
+// and issued by one thread instead of by every lane.  The operator is
+// constant, so the producer starts streaming before griddepcontrol.wait
+// (overlapping the predecessor's tail); only the consumers' x gathers and
+// epilogues wait.  Consumer warp w sums triples w*TPW.. of each tile with
+// exactly k_bsr3p's lane mapping and summation order (lane 3k+c owns column c
+// of blocks k, k+10, k+20 of the triple, then the xor-shuffle tree), so the
+// results are bitwise those of the register-streamed kernels.  Tiles larger
+// than a stage (rows with more than 30 blocks on average) are read straight
+// from global memory.
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_1d(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+constexpr int BT_CW = 8;               // consumer warps per CTA
+constexpr int BT_THREADS = 32 * (BT_CW + 1);
+constexpr int BT_BLK_PER_TRIPLE = 30;  // stage capacity per row triple (27-point stencil: 27)
+
+struct BsrTileGeom {
+    int64_t vb0, vbytes, cb0, cbytes;
+};
+__device__ __forceinline__ BsrTileGeom bsr_tile_geom(int64_t k0, int64_t k1) {
+    BsrTileGeom g;
+    g.vb0 = (72 * k0) & ~(int64_t)15;
+    g.vbytes = ((72 * k1 + 15) & ~(int64_t)15) - g.vb0;
+    g.cb0 = (4 * k0) & ~(int64_t)15;
+    g.cbytes = ((4 * k1 + 15) & ~(int64_t)15) - g.cb0;
+    return g;
+}
+
+template <class Op, int TPW>
+__global__ void __launch_bounds__(BT_THREADS) k_bsr3t(int64_t ntrip, int64_t nb, int64_t n,
+                                                      const int64_t *__restrict__ bro,
+                                                      const int32_t *__restrict__ bci,
+                                                      const double *__restrict__ bval, Op op, int64_t row_off,
+                                                      int trigger, int stages, unsigned capv, unsigned capc) {
+    constexpr int TPT = BT_CW * TPW;
+    extern __shared__ __align__(128) unsigned char bt_smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(bt_smem);
+    uint64_t *empty = full + stages;
+    unsigned char *buf = bt_smem + 128;  // stage s: values at s*(capv+capc), columns after them
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (nb + TPT - 1) / TPT;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < stages; ++st) {
+            mbar_init(full + st, 1);
+            mbar_init(empty + st, BT_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == BT_CW) {  // producer: one elected lane streams the tiles of this CTA
+        if (lane == 0) {
+            int st = 0;
+            unsigned ph = 0;
+            const char *vsrc = reinterpret_cast<const char *>(bval);
+            const char *csrc = reinterpret_cast<const char *>(bci);
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(empty + st, ph ^ 1);
+                const int64_t I0 = t * TPT, I1 = I0 + TPT < nb ? I0 + TPT : nb;
+                const BsrTileGeom g = bsr_tile_geom(__ldg(bro + I0), __ldg(bro + I1));
+                unsigned char *vs = buf + (size_t)st * (capv + capc);
+                if (g.vbytes <= (int64_t)capv && g.cbytes <= (int64_t)capc) {
+                    mbar_arrive_tx(full + st, (unsigned)(g.vbytes + g.cbytes));
+                    tma_1d(vs, vsrc + g.vb0, (unsigned)g.vbytes, full + st);
+                    tma_1d(vs + capv, csrc + g.cb0, (unsigned)g.cbytes, full + st);
+                } else {
+                    mbar_arrive(full + st);  // oversize tile: the consumers read global memory
+                }
+                if (++st == stages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+    const int kk = lane / 3, c = lane - 3 * kk;
+    pdl_wait();
+    if (trigger) pdl_trigger();
+    int st = 0;
+    unsigned ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t I0 = t * TPT, I1 = I0 + TPT < nb ? I0 + TPT : nb;
+        const int64_t k0 = __ldg(bro + I0);
+        const BsrTileGeom g = bsr_tile_geom(k0, __ldg(bro + I1));
+        const bool staged = g.vbytes <= (int64_t)capv && g.cbytes <= (int64_t)capc;
+        const unsigned char *vs = buf + (size_t)st * (capv + capc);
+        const double *sv = reinterpret_cast<const double *>(vs + (72 * k0 - g.vb0));
+        const int32_t *sc = reinterpret_cast<const int32_t *>(vs + capv + (4 * k0 - g.cb0));
+        int64_t kb[TPW], ke[TPW];
+        Op ops[TPW];
+#pragma unroll
+        for (int p = 0; p < TPW; ++p) {
+            const int64_t I = I0 + warp * TPW + p;
+            kb[p] = ke[p] = 0;
+            ops[p] = op;
+            if (I < nb) {
+                kb[p] = __ldg(bro + I);
+                ke[p] = __ldg(bro + I + 1);
+            }
+            // the epilogue's setup-constant row data, loaded ahead of the gathers
+            if (I < ntrip && lane < 3 && 3 * I + lane < n) ops[p].pre(3 * I + lane + row_off);
+        }
+        mbar_wait(full + st, ph);
+        double a0[TPW], a1[TPW], a2[TPW];
+        if (staged) {
+            // every smem load and gather of the warp's triples issued before the FMAs
+            int cc[TPW][3];
+            double vv[TPW][3][3], xv[TPW][3];
+#pragma unroll
+            for (int p = 0; p < TPW; ++p)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int64_t k = kb[p] + kk + 10 * q;
+                    const bool ok = lane < 30 && k < ke[p] && k < kb[p] + BT_BLK_PER_TRIPLE;
+                    const int64_t r = k - k0;
+                    cc[p][q] = ok ? sc[r] : -1;
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) vv[p][q][e] = ok ? sv[9 * r + 3 * c + e] : 0.0;
+                }
+#pragma unroll
+            for (int p = 0; p < TPW; ++p)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) xv[p][q] = cc[p][q] >= 0 ? op.x(3 * cc[p][q] + c) : 0.0;
+#pragma unroll
+            for (int p = 0; p < TPW; ++p) {
+                a0[p] = a1[p] = a2[p] = 0.0;
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    if (cc[p][q] >= 0) {
+                        a0[p] = fma(vv[p][q][0], xv[p][q], a0[p]);
+                        a1[p] = fma(vv[p][q][1], xv[p][q], a1[p]);
+                        a2[p] = fma(vv[p][q][2], xv[p][q], a2[p]);
+                    }
+                // rows with more than 30 blocks: the rest from global memory
+                for (int64_t kq = kb[p] + BT_BLK_PER_TRIPLE; kq < ke[p]; kq += 30)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const int64_t k = kq + kk + 10 * q;
+                        if (lane < 30 && k < ke[p]) {
+                            const double x = op.x(3 * __ldg(bci + k) + c);
+                            const double *pv = bval + 9 * k + 3 * c;
+                            a0[p] = fma(__ldg(pv), x, a0[p]);
+                            a1[p] = fma(__ldg(pv + 1), x, a1[p]);
+                            a2[p] = fma(__ldg(pv + 2), x, a2[p]);
+                        }
+                    }
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < TPW; ++p) {
+                a0[p] = a1[p] = a2[p] = 0.0;
+                for (int64_t kq = kb[p]; kq < ke[p]; kq += 30)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const int64_t k = kq + kk + 10 * q;
+                        if (lane < 30 && k < ke[p]) {
+                            const double x = op.x(3 * __ldg(bci + k) + c);
+                            const double *pv = bval + 9 * k + 3 * c;
+                            a0[p] = fma(__ldg(pv), x, a0[p]);
+                            a1[p] = fma(__ldg(pv + 1), x, a1[p]);
+                            a2[p] = fma(__ldg(pv + 2), x, a2[p]);
+                        }
+                    }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);  // the stage may be refilled
+        if (++st == stages) {
+            st = 0;
+            ph ^= 1;
+        }
+#pragma unroll
+        for (int p = 0; p < TPW; ++p) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a0[p] += __shfl_xor_sync(FULL, a0[p], o);
+                a1[p] += __shfl_xor_sync(FULL, a1[p], o);
+                a2[p] += __shfl_xor_sync(FULL, a2[p], o);
+            }
+            const int64_t I = I0 + warp * TPW + p;
+            if (I < ntrip && lane < 3 && 3 * I + lane < n)
+                ops[p].out(3 * I + lane + row_off, lane == 0 ? a0[p] : lane == 1 ? a1[p] : a2[p]);
+        }
+    }
+}
+
 struct OpY {
+    static constexpr bool kTmaDefault = true;
     static double row_bytes(const OpY &) { return 0.0; }
 
     const double *xv;
@@ -613,6 +838,7 @@ struct OpY {
     __device__ void out(int64_t i, double s) const { y[i] = s; }
 };
 struct OpResidual {
+    static constexpr bool kTmaDefault = true;
     static double row_bytes(const OpResidual &) { return 8.0; }  // b
 
     const double *xv, *b;
@@ -895,10 +1121,73 @@ struct col_bytes_of<Op, std::void_t<decltype(Op::kColBytes)>> {
     static constexpr double v = Op::kColBytes;
 };
 
+// TMA-staged block SpMV for pure BSR3 operators (PMGR_BSR_TMA=0: the
+// register-streamed k_bsr3p); PMGR_BSR_TPW triples per consumer warp and
+// tile (1 / 2), PMGR_BSR_STAGES stages, PMGR_BSR_CPS CTAs per SM
+template <class Op, int TPW>
+void launch_bsr3t_t(const CsrView &A, const Op &op, int stages, int cps, cudaStream_t s) {
+    constexpr int tpt = BT_CW * TPW;
+    const unsigned capv = (unsigned)((tpt * BT_BLK_PER_TRIPLE * 72 + 16 + 15) & ~15);
+    const unsigned capc = (unsigned)((tpt * BT_BLK_PER_TRIPLE * 4 + 16 + 15) & ~15);
+    const size_t smem = 128 + (size_t)stages * (capv + capc);
+    static size_t set_for = 0;
+    if (set_for < smem) {
+        PMGR_CUDA(cudaFuncSetAttribute(k_bsr3t<Op, TPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set_for = smem;
+    }
+    const int64_t ntiles = (A.nbrows + tpt - 1) / tpt;
+    const int64_t want = (int64_t)cps * num_sms();
+    const unsigned grid = (unsigned)(ntiles < want ? ntiles : want);
+    const int trig = grid <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
+    launch_pdl(k_bsr3t<Op, TPW>, dim3(grid), dim3(BT_THREADS), smem, s, A.nbrows, A.nbrows, A.nrows, A.bro, A.bci,
+               A.bval, op, A.row_off, trig, stages, capv, capc);
+}
+
+// epilogues with no per-row prefetch state take the TMA kernel by default
+// (measured at C4: residual pass 944 -> 884 us); the Jacobi-type epilogues
+// keep k_bsr3p, whose register budget suits them better (PMGR_BSR_TMA=2:
+// every pure block operator, for A/B runs)
+template <class Op, class = void>
+struct tma_default {
+    static constexpr bool v = false;
+};
+template <class Op>
+struct tma_default<Op, std::void_t<decltype(Op::kTmaDefault)>> {
+    static constexpr bool v = Op::kTmaDefault;
+};
+
+template <class Op>
+bool launch_bsr3t(const CsrView &A, const Op &op, cudaStream_t s) {
+    static const int on = [] {
+        const char *e = getenv("PMGR_BSR_TMA");
+        return e ? atoi(e) : 1;
+    }();
+    static const int tpw = [] {
+        const char *e = getenv("PMGR_BSR_TPW");
+        return e ? atoi(e) : 2;
+    }();
+    static const int stages = [] {
+        const char *e = getenv("PMGR_BSR_STAGES");
+        const int v = e ? atoi(e) : 2;
+        return v < 2 ? 2 : v > 8 ? 8 : v;
+    }();
+    static const int cps = [] {
+        const char *e = getenv("PMGR_BSR_CPS");
+        return e ? atoi(e) : 3;
+    }();
+    if (!on || (on == 1 && !tma_default<Op>::v) || A.rro != nullptr || A.nbrows <= 0) return false;
+    if (tpw == 1) launch_bsr3t_t<Op, 1>(A, op, stages, cps, s);
+    else if (tpw == 4) launch_bsr3t_t<Op, 4>(A, op, stages, cps, s);
+    else launch_bsr3t_t<Op, 2>(A, op, stages, cps, s);
+    PMGR_LAUNCHED();
+    return true;
+}
+
 template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
     ledger(csr_pass_bytes(A) + Op::row_bytes(op) * A.nrows + col_bytes_of<Op>::v * A.ncols);
+    if (A.nbrows > 0 && launch_bsr3t(A, op, s)) return;
     if (A.nbrows > 0) {
         const int64_t ntrip = A.rro ? (A.nrows + 2) / 3 : A.nbrows;
         const unsigned grid = grid_for(ntrip * 32, 256);

@@ -246,6 +246,61 @@ def nccl_transport(rank: int, nranks: int, dist):
     return _Handle(out, "pmgr_transport_destroy")
 
 
+def host_transport(rank: int, nranks: int, dist, group=None):
+    """Host-staged transport inside libpmgr over the caller's torch.distributed
+    group (any backend with point-to-point and all_reduce, e.g. gloo): every
+    exchange stages through host memory and synchronises, so several
+    processes may share one GPU.  Used by the multi-process tests."""
+    import torch
+
+    from . import _lib
+
+    def a2a(_ctx, sptr, sbytes, rptr, rbytes):
+        try:
+            reqs, keep = [], []
+            for p in range(nranks):
+                if p == rank:
+                    continue
+                if sbytes[p] > 0:
+                    buf = (ctypes.c_uint8 * sbytes[p]).from_address(sptr[p])
+                    t = torch.frombuffer(buf, dtype=torch.uint8)
+                    keep.append(t)
+                    reqs.append(dist.isend(t, dst=p, group=group))
+                if rbytes[p] > 0:
+                    buf = (ctypes.c_uint8 * rbytes[p]).from_address(rptr[p])
+                    t = torch.frombuffer(buf, dtype=torch.uint8)
+                    keep.append(t)
+                    reqs.append(dist.irecv(t, src=p, group=group))
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception:  # noqa: BLE001 -- reported as a library error
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    def ared(_ctx, buf, n):
+        try:
+            arr = (ctypes.c_double * n).from_address(ctypes.addressof(buf.contents))
+            t = torch.frombuffer(arr, dtype=torch.float64)
+            dist.all_reduce(t, group=group)
+            return 0
+        except Exception:  # noqa: BLE001
+            import traceback
+
+            traceback.print_exc()
+            return 1
+
+    fa, fr = _lib.ALLTOALLV_FN(a2a), _lib.ALLREDUCE_FN(ared)
+    out = ctypes.c_void_p()
+    _lib.check(_lib.lib().pmgr_transport_host_create(rank, nranks, ctypes.cast(fa, ctypes.c_void_p),
+                                                     ctypes.cast(fr, ctypes.c_void_p), None, ctypes.byref(out)))
+    h = _Handle(out, "pmgr_transport_destroy")
+    h._callbacks = (fa, fr)  # keep the trampolines alive with the transport
+    return h
+
+
 class _Handle:
     def __init__(self, h, destroy):
         self.h, self._destroy = h, destroy

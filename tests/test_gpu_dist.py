@@ -47,6 +47,51 @@ def test_distributed_apply_is_bitwise(pk, name, kw, n_max, four, nranks):
     assert np.array_equal(zd, z), f"max diff {np.abs(zd - z).max()}"
 
 
+# the production configurations' multi-cycle AMG F-relaxation (C5: two
+# V-cycles, C4: three) on the row-distributed path
+PROD_CASES = [("C5", dict(nxy=8, nz_per_gpu=4, gpus=2)), ("C4", dict(n=6))]
+
+
+@pytest.mark.parametrize("name,kw", PROD_CASES)
+@pytest.mark.parametrize("nranks", [1, 2, 3])
+def test_distributed_apply_production_is_bitwise(pk, name, kw, nranks):
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make(name, seed=3, **kw), nranks)
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    cfg = mgr.config_from_options(problems.solver_options(name, pb))
+    assert max(lv.f_relax_sweeps for lv in cfg.levels) > 1
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of), cfg)
+    v = np.random.default_rng(7).standard_normal(pb.n)
+    z = h.apply(v)
+    zd = dist.emulate_apply(h, bounds, v).cpu().numpy()
+    assert np.array_equal(zd, z), f"max diff {np.abs(zd - z).max()}"
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_distributed_gmres_matches_oracle(pk, nranks):
+    """The row-distributed GMRES (emulated ranks) against the CPU oracle on the
+    same rank-major problem: iterations +-1, solution 1e-10 when the counts
+    agree (the oracle is pinned to the reference, tests/test_oracle_golden.py)."""
+    from oracle import oracle as O
+
+    sparse, amg, mgr, krylov, dist, problems = pk
+    pb, bounds = problems.rank_major(problems.make("C5", seed=4, nxy=10, nz_per_gpu=5, gpus=2), nranks)
+    opts = problems.solver_options("C5", pb)
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of), mgr.config_from_options(opts))
+    cfg = krylov.GmresConfig(restart=opts["restart"], max_iters=opts["max_iters"], rtol=1e-6)
+    xd, its, conv = dist.emulate_gmres(h, bounds, pb.rhs, cfg)
+    xd = xd.cpu().numpy()
+    oA = O.Csr(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    oh = O.mgr_setup(oA, pb.field_of, pb.entity_of, O.config_from_options(opts))
+    xo, its_o, _, conv_o = O.gmres(lambda y: O.spmv(oA, y), oh.apply, pb.rhs, restart=opts["restart"],
+                                   max_iters=opts["max_iters"], rtol=1e-6)
+    rel = np.linalg.norm(xd - xo) / np.linalg.norm(xo)
+    print(f"[dist {nranks}] iterations {its} (oracle {its_o}) solution rel {rel:.2e}")
+    assert conv and conv_o and abs(its - its_o) <= 1
+    assert rel <= (1e-10 if its == its_o else 1e-5), rel
+
+
 def test_distributed_apply_uneven_and_empty_ranks(pk):
     """More ranks than some coarse spaces have rows: empty owned ranges."""
     sparse, amg, mgr, krylov, dist, problems = pk
@@ -163,12 +208,17 @@ from tests.test_gpu_dist import build
 from tests.test_gpu_parity import mgr_config
 from paper_1904_05960_b200 import amg, dist, krylov, mgr, problems, sparse
 pk = (sparse, amg, mgr, krylov, dist, problems)
-for name, n, n_max, four in (("C2", 12, 4, False), ("C1", 12, None, False), ("C4", 10, 4, True)):
+for name, n, n_max, four in (("C2", 12, 4, False), ("C1", 12, None, False), ("C4", 10, 4, True), ("C4p", 10, 4, True)):
     for nranks in (1, 2, 3):
-        pb, bounds = problems.rank_major(problems.make(name, seed=3, n=n), nranks)
-        A, h = build(pk, pb, n_max, four)
+        pb, bounds = problems.rank_major(problems.make(name[:2], seed=3, n=n), nranks)
+        if name == "C4p":  # production configuration: three AMG V-cycles of F-relaxation
+            cfg = mgr.config_from_options(problems.solver_options("C4", pb))
+            A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+            h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of), cfg)
+        else:
+            A, h = build(pk, pb, n_max, four)
+            cfg = mgr_config(pk[:4], pb, n_max, four)
         lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
-        cfg = mgr_config(pk[:4], pb, n_max, four)
         v = np.random.default_rng(7).standard_normal(pb.n)
         z = h.apply(v)
         zd = dist.emulate_setup_apply(A, lay, cfg, bounds, v).cpu().numpy()
@@ -202,7 +252,7 @@ def test_distributed_setup_is_bitwise():
                        timeout=900, cwd=repo)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     cases = [ln.split() for ln in r.stdout.splitlines() if ln.startswith("CASE")]
-    assert len(cases) == 9, r.stdout
+    assert len(cases) == 12, r.stdout
     bad = [c for c in cases if c[4] != "True"]
     assert not bad, r.stdout
     for ln in r.stdout.splitlines():

@@ -488,3 +488,43 @@ def test_mgr_option_variants(pk, tag):
         assert st.iterations == int(d["gmres_iters"])
         assert np.allclose(st.residual_history[:20], d["gmres_hist"][:20], rtol=1e-6)
 
+
+
+_KERNEL_AB_SCRIPT = r"""
+import sys, hashlib, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1904_05960_b200 import mgr, problems, sparse
+out = []
+for name, kw in (("C2", dict(n=16)), ("C4", dict(n=12)), ("C5", dict(nxy=12, nz_per_gpu=6, gpus=1))):
+    pb = problems.make(name, seed=2, **kw)
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of),
+                      mgr.config_from_options(problems.solver_options(name, pb)))
+    v = np.random.default_rng(5).standard_normal(pb.n)
+    z = h.apply(v)
+    out.append(hashlib.sha256(z.tobytes()).hexdigest())
+print("DIGESTS", " ".join(out))
+"""
+
+
+@pytest.mark.parametrize("env", [dict(PMGR_BSR_TPW="1"), dict(PMGR_BSR_TPW="2", PMGR_BSR_STAGES="2"),
+                                 dict(PMGR_BSR_TPW="2", PMGR_BSR_CPS="1", PMGR_BSR_STAGES="4")])
+def test_tma_block_spmv_is_bitwise(pk, env):
+    """The TMA-staged block SpMV (k_bsr3t) sums every row triple in the
+    register-streamed kernels' order: MGR applications are bitwise equal
+    with it on or off, for every pipeline shape."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(extra):
+        r = subprocess.run([sys.executable, "-c", _KERNEL_AB_SCRIPT, repo], env=dict(os.environ, **extra),
+                           capture_output=True, text=True, timeout=600, cwd=repo)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return [ln for ln in r.stdout.splitlines() if ln.startswith("DIGESTS")][0]
+
+    ref = run(dict(PMGR_BSR_TMA="0"))
+    assert ref == run(dict(PMGR_BSR_TMA="2", **env))  # every pure block operator on the TMA kernel
+    assert ref == run(dict(PMGR_BSR_TMA="1", **env))  # the default split
