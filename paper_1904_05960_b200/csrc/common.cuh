@@ -364,6 +364,9 @@ inline double csr_pass_bytes(const CsrView &A) {
 int64_t exclusive_scan_total(const int64_t *in, int64_t *out, int64_t n, cudaStream_t s);
 int64_t exclusive_scan_total_i32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
 // Sort (keys, vals) pairs within each CSR row segment by key (ascending).
+// the same over an explicit list of [sbeg[i], send[i]) segments
+void segmented_sort_pairs_list(int32_t *keys, double *vals, int64_t nnz, const int64_t *sbeg, const int64_t *send,
+                               int64_t nseg, cudaStream_t s);
 void segmented_sort_pairs(int32_t *keys, double *vals, int64_t nnz, const int64_t *ro,
                           int64_t nrows, cudaStream_t s);
 double device_max_abs(const double *x, int64_t n, cudaStream_t s);

@@ -75,9 +75,15 @@ __global__ void k_iota(int32_t *p, int64_t n) {
 }
 
 // ------------------------------------------------------------ spgemm
-constexpr int HS = 2048;          // hash slots per warp (shared path)
-constexpr int SP_WARPS = 4;       // warps per block (4 * 2048 * 12 B = 96 KB)
-constexpr int SMALL_LIMIT = HS / 2;
+// shared-memory hash tables per warp: the symbolic pass keeps keys only
+// (2048 slots, rows up to 1024 by their upper bound: 8 KB per warp), the
+// numeric pass keys and values (1024 slots, rows up to 512 by their exact
+// count: 12 KB per warp); rows beyond take a global-memory table
+constexpr int HS_SYM = 2048;
+constexpr int HS_NUM = 1024;
+constexpr int SP_WARPS = 4;       // warps per block
+constexpr int SMALL_LIMIT = HS_SYM / 2;      // symbolic: upper bound
+constexpr int SMALL_LIMIT_NUM = HS_NUM / 2;  // numeric: exact count
 
 __device__ __forceinline__ unsigned hash_k(int32_t k) { return (unsigned)k * 2654435761u; }
 
@@ -122,11 +128,11 @@ __global__ void k_spgemm_ub(int64_t n, const int64_t *xro, const int32_t *xci, c
 }
 
 // global-table sizes for big rows (0 for rows on the shared path)
-__global__ void k_table_size(int64_t n, const int64_t *ub, int64_t *tsz) {
+__global__ void k_table_size(int64_t n, const int64_t *ub, int64_t *tsz, int64_t limit) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int64_t u = ub[i];
-    if (u <= SMALL_LIMIT) {
+    if (u <= limit) {
         tsz[i] = 0;
     } else {
         int64_t t = 1;
@@ -145,14 +151,16 @@ __global__ void __launch_bounds__(SP_WARPS * 32)
              const int32_t *__restrict__ yci, const double *__restrict__ yv,
              const int64_t *__restrict__ ub, const int64_t *__restrict__ toff, int32_t *gkeys,
              double *gvals, int64_t *cnt, const int64_t *__restrict__ cro, int32_t *cci, double *cv) {
+    constexpr int HS = NUMERIC ? HS_NUM : HS_SYM;
     extern __shared__ unsigned char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     int32_t *skeys = (int32_t *)smem + warp * HS;
-    double *svals = (double *)(smem + sizeof(int32_t) * HS * SP_WARPS) + warp * HS;
+    double *svals = NUMERIC ? (double *)(smem + sizeof(int32_t) * HS * SP_WARPS) + warp * HS : nullptr;
     const int64_t nwarps = (int64_t)gridDim.x * SP_WARPS;
     for (int64_t i = blockIdx.x * (int64_t)SP_WARPS + warp; i < n; i += nwarps) {
-        const bool big = ub[i] > SMALL_LIMIT;
+        // symbolic: table by the upper bound; numeric: by the exact count
+        const bool big = NUMERIC ? cro[i + 1] - cro[i] > SMALL_LIMIT_NUM : ub[i] > SMALL_LIMIT;
         int32_t *keys;
         double *vals;
         int64_t tsz;
@@ -171,26 +179,84 @@ __global__ void __launch_bounds__(SP_WARPS * 32)
         }
         __syncwarp();
         int64_t local = 0;
-        for (int64_t jj = xro[i]; jj < xro[i + 1]; ++jj) {
-            const int32_t j = xci[jj];
-            const double xval = NUMERIC ? xv[jj] : 0.0;
-            for (int64_t kk = yro[j] + lane; kk < yro[j + 1]; kk += 32) {
-                const int32_t k = yci[kk];
-                bool ins;
-                int64_t slot = table_insert(keys, tsz, k, ins);
-                if (NUMERIC) {
-                    vals[slot] = __dadd_rn(vals[slot], __dmul_rn(xval, yv[kk]));
-                } else if (ins) {
-                    ++local;
+        // The middle index is walked in ascending order (csr_matmat's
+        // summation order), but its loads are batched: lane t fetches the
+        // t-th middle index of the batch, its X value and Y row bounds (32
+        // independent loads instead of a chain of three per index), and the
+        // first chunk of Y's row for step t+1 is loaded while step t inserts.
+        const int64_t xe = xro[i + 1];
+        for (int64_t jb = xro[i]; jb < xe; jb += 32) {
+            const int64_t jq = jb + lane;
+            const bool has = jq < xe;
+            const int32_t jl = has ? xci[jq] : 0;
+            const double xl = (NUMERIC && has) ? xv[jq] : 0.0;
+            const int64_t sl = has ? yro[jl] : 0, el = has ? yro[jl + 1] : 0;
+            const int nb = (int)(xe - jb < 32 ? xe - jb : 32);
+            int64_t st = __shfl_sync(FULL, sl, 0), en = __shfl_sync(FULL, el, 0);
+            int32_t kc = st + lane < en ? yci[st + lane] : -1;
+            double yc = (NUMERIC && kc >= 0) ? yv[st + lane] : 0.0;
+            for (int t = 0; t < nb; ++t) {
+                const double xval = __shfl_sync(FULL, xl, t);
+                // prefetch step t+1's first chunk
+                const int64_t st1 = __shfl_sync(FULL, sl, (t + 1) & 31), en1 = __shfl_sync(FULL, el, (t + 1) & 31);
+                const bool nx = t + 1 < nb && st1 + lane < en1;
+                const int32_t kn = nx ? yci[st1 + lane] : -1;
+                const double yn = (NUMERIC && nx) ? yv[st1 + lane] : 0.0;
+                if (kc >= 0) {
+                    bool ins;
+                    const int64_t slot = table_insert(keys, tsz, kc, ins);
+                    if (NUMERIC) vals[slot] = __dadd_rn(vals[slot], __dmul_rn(xval, yc));
+                    else if (ins) ++local;
                 }
+                for (int64_t kk = st + 32 + lane; kk < en; kk += 32) {
+                    const int32_t k = yci[kk];
+                    bool ins;
+                    const int64_t slot = table_insert(keys, tsz, k, ins);
+                    if (NUMERIC) vals[slot] = __dadd_rn(vals[slot], __dmul_rn(xval, yv[kk]));
+                    else if (ins) ++local;
+                }
+                __syncwarp();
+                st = st1;
+                en = en1;
+                kc = kn;
+                yc = yn;
             }
-            __syncwarp();
         }
         if (!NUMERIC) {
             local = warp_sum_i64(local);
             if (lane == 0) cnt[i] = local;
+        } else if (!big) {
+            // shared table: compact the occupied slots in place (a chunk's
+            // reads precede its writes, which land at or below the chunk),
+            // then write each entry at its rank among the row's keys -- the
+            // row comes out sorted, no segmented sort needed
+            int m = 0;
+            for (int t0 = 0; t0 < HS; t0 += 32) {
+                const int t = t0 + lane;
+                const int32_t k = keys[t];
+                const double val = vals[t];
+                const unsigned msk = __ballot_sync(FULL, k != -1);
+                __syncwarp();
+                if (k != -1) {
+                    const int pos = m + __popc(msk & ((1u << lane) - 1u));
+                    keys[pos] = k;
+                    vals[pos] = val;
+                }
+                m += __popc(msk);
+                __syncwarp();
+            }
+            const int64_t base = cro[i];
+            for (int e = lane; e < m; e += 32) {
+                const int32_t k = keys[e];
+                int r = 0;
+                for (int q = 0; q < m; ++q) r += keys[q] < k;
+                const double val = vals[e];
+                cci[base + r] = k;
+                cv[base + r] = (val == 0.0) ? 0.0 : val;
+            }
         } else {
-            // dump occupied slots (order fixed later by the segmented sort)
+            // global table: dump occupied slots (sorted afterwards by the
+            // segmented sort over the big rows)
             int64_t base = cro[i];
             for (int64_t t0 = 0; t0 < tsz; t0 += 32) {
                 int64_t t = t0 + lane;
@@ -207,6 +273,16 @@ __global__ void __launch_bounds__(SP_WARPS * 32)
         }
         __syncwarp();
     }
+}
+
+// [begin, end) of the rows with more than `limit` entries (any order)
+__global__ void k_big_segments(int64_t n, const int64_t *ro, int64_t limit, int64_t *sb, int64_t *se,
+                               unsigned long long *count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n || ro[i + 1] - ro[i] <= limit) return;
+    const unsigned long long p = atomicAdd(count, 1ull);
+    sb[p] = ro[i];
+    se[p] = ro[i + 1];
 }
 
 // Coarse products (few output columns): a dense accumulator per row in
@@ -232,15 +308,27 @@ __global__ void __launch_bounds__(DENSE_THREADS)
         if (NUMERIC)
             for (int64_t t = threadIdx.x; t < ncols; t += DENSE_THREADS) acc[t] = 0.0;
         __syncthreads();
-        for (int64_t jj = xro[i]; jj < xro[i + 1]; ++jj) {
-            const int32_t j = xci[jj];
-            const double xval = NUMERIC ? xv[jj] : 0.0;
-            for (int64_t kk = yro[j] + threadIdx.x; kk < yro[j + 1]; kk += DENSE_THREADS) {
-                const int32_t k = yci[kk];
-                atomicOr(flags + (k >> 5), 1u << (k & 31));
-                if (NUMERIC) acc[k] = __dadd_rn(acc[k], __dmul_rn(xval, yv[kk]));
+        // middle indices in ascending order, their loads batched 32 at a time
+        // (every warp fetches the same batch; lane t holds index t)
+        const int64_t xe = xro[i + 1];
+        const int lane = threadIdx.x & 31;
+        for (int64_t jb = xro[i]; jb < xe; jb += 32) {
+            const int64_t jq = jb + lane;
+            const bool has = jq < xe;
+            const int32_t jl = has ? xci[jq] : 0;
+            const double xl = (NUMERIC && has) ? xv[jq] : 0.0;
+            const int64_t sl = has ? yro[jl] : 0, el = has ? yro[jl + 1] : 0;
+            const int nb = (int)(xe - jb < 32 ? xe - jb : 32);
+            for (int t = 0; t < nb; ++t) {
+                const double xval = __shfl_sync(FULL, xl, t);
+                const int64_t st = __shfl_sync(FULL, sl, t), en = __shfl_sync(FULL, el, t);
+                for (int64_t kk = st + threadIdx.x; kk < en; kk += DENSE_THREADS) {
+                    const int32_t k = yci[kk];
+                    atomicOr(flags + (k >> 5), 1u << (k & 31));
+                    if (NUMERIC) acc[k] = __dadd_rn(acc[k], __dmul_rn(xval, yv[kk]));
+                }
+                if (NUMERIC) __syncthreads();
             }
-            if (NUMERIC) __syncthreads();
         }
         __syncthreads();
         // words [w0, w1) of this thread, in order
@@ -746,37 +834,59 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
     } else {
     k_spgemm_ub<<<grid_for(n * 32, 256), 256, 0, s>>>(n, X.ro, X.ci, Y.ro, Y.ncols, ub.p);
     PMGR_LAUNCHED();
-    k_table_size<<<grid_for(n, 256), 256, 0, s>>>(n, ub.p, tsz.p);
+    k_table_size<<<grid_for(n, 256), 256, 0, s>>>(n, ub.p, tsz.p, SMALL_LIMIT);
     PMGR_LAUNCHED();
     int64_t gtotal = exclusive_scan_total(tsz.p, toff.p, n, s);
     setup_trace("  spgemm bounds", gtotal, s);
     TBuf<int32_t> gkeys(gtotal, s);
-    TBuf<double> gvals(mode >= 0 ? gtotal : 0, s);
 
-    const size_t smem = (size_t)SP_WARPS * HS * (sizeof(int32_t) + sizeof(double));
+    const size_t smem_sym = (size_t)SP_WARPS * HS_SYM * sizeof(int32_t);
+    const size_t smem_num = (size_t)SP_WARPS * HS_NUM * (sizeof(int32_t) + sizeof(double));
     static bool attr_set = false;
     if (!attr_set) {
-        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_sym));
+        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_num));
         attr_set = true;
     }
-    int64_t want = (n + SP_WARPS - 1) / SP_WARPS;
-    int64_t cap = (int64_t)num_sms() * 2 * 16;
-    unsigned grid = (unsigned)(want < cap ? want : cap);
-    if (grid < 1) grid = 1;
+    // resident warps: the occupancy each pass's shared tables allow
+    auto grid_of = [&](const void *fn, size_t smem) {
+        int per_sm = 0;
+        PMGR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SP_WARPS * 32, smem));
+        const int64_t want = (n + SP_WARPS - 1) / SP_WARPS;
+        const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+        return (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
+    };
 
-    k_spgemm<false><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
-                                                       gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
+    k_spgemm<false><<<grid_of((const void *)k_spgemm<false>, smem_sym), SP_WARPS * 32, smem_sym, s>>>(
+        n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
     PMGR_LAUNCHED();
     total = exclusive_scan_total(cnt.p, cro.p, n, s);
     setup_trace("  spgemm symbolic", total, s);
+    // numeric tables from the exact counts
+    k_table_size<<<grid_for(n, 256), 256, 0, s>>>(n, cnt.p, tsz.p, SMALL_LIMIT_NUM);
+    PMGR_LAUNCHED();
+    const int64_t ntotal = exclusive_scan_total(tsz.p, toff.p, n, s);
+    gkeys.release();
+    TBuf<int32_t> nkeys(ntotal, s);
+    TBuf<double> nvals(ntotal, s);
     tci.alloc(total, s);
     tv.alloc(total, s);
-    k_spgemm<true><<<grid, SP_WARPS * 32, smem, s>>>(n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p,
-                                                      gkeys.p, gvals.p, nullptr, cro.p, tci.p, tv.p);
+    k_spgemm<true><<<grid_of((const void *)k_spgemm<true>, smem_num), SP_WARPS * 32, smem_num, s>>>(
+        n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, nkeys.p, nvals.p, nullptr, cro.p, tci.p, tv.p);
     PMGR_LAUNCHED();
     setup_trace("  spgemm numeric", total, s);
-    segmented_sort_pairs(tci.p, tv.p, total, cro.p, n, s);
+    // only rows with more than SMALL_LIMIT_NUM entries (global tables) are unsorted
+    {
+        TBuf<int64_t> sb(n, s), se(n, s);
+        TBuf<unsigned long long> nbig(1, s);
+        PMGR_CUDA(cudaMemsetAsync(nbig.p, 0, sizeof(unsigned long long), s));
+        k_big_segments<<<grid_for(n, 256), 256, 0, s>>>(n, cro.p, SMALL_LIMIT_NUM, sb.p, se.p, nbig.p);
+        PMGR_LAUNCHED();
+        const int64_t nb = (int64_t)read_scalar(nbig.p, s);
+        if (nb > 0) segmented_sort_pairs_list(tci.p, tv.p, total, sb.p, se.p, nb, s);
+    }
     setup_trace("  spgemm sort", total, s);
     }
     if (mode == 1) {

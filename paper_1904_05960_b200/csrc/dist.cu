@@ -397,6 +397,8 @@ struct CallbackTransport : Transport {
             so += sbytes[p];
             ro += rbytes[p];
         }
+        if (sbytes[rank] != rbytes[rank]) fail(PMGR_ERR_INVALID, "host transport: self sizes disagree");
+        if (sbytes[rank] > 0) std::memcpy(rp[rank], sp[rank], (size_t)sbytes[rank]);  // the callback skips self
         if (a2a(ctx, sp.data(), sbytes.data(), rp.data(), rbytes.data()) != 0)
             fail(PMGR_ERR_CUDA, "host transport: all-to-all callback failed");
     }

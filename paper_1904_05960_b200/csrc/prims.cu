@@ -198,6 +198,24 @@ void segmented_sort_pairs(int32_t *keys, double *vals, int64_t nnz, const int64_
     PMGR_CUDA(cudaMemcpyAsync(vals, v2.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
 }
 
+void segmented_sort_pairs_list(int32_t *keys, double *vals, int64_t nnz, const int64_t *sbeg, const int64_t *send,
+                               int64_t nseg, cudaStream_t s) {
+    if (nnz <= 1 || nseg == 0) return;
+    // the listed segments are sorted into a copy of the whole arrays (the
+    // other entries are already in place) and copied back
+    TBuf<int32_t> k2(nnz, s);
+    TBuf<double> v2(nnz, s);
+    PMGR_CUDA(cudaMemcpyAsync(k2.p, keys, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s));
+    PMGR_CUDA(cudaMemcpyAsync(v2.p, vals, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    size_t tmp = 0;
+    PMGR_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, keys, k2.p, vals, v2.p, nnz, nseg, sbeg, send, s));
+    TBuf<char> t((int64_t)tmp, s);
+    PMGR_CUDA(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, keys, k2.p, vals, v2.p, nnz, nseg, sbeg, send, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    PMGR_CUDA(cudaMemcpyAsync(keys, k2.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s));
+    PMGR_CUDA(cudaMemcpyAsync(vals, v2.p, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+}
+
 double device_max_abs(const double *x, int64_t n, cudaStream_t s) {
     if (n == 0) return 0.0;
     TBuf<unsigned long long> out(1, s);

@@ -24,6 +24,7 @@ inside libpmgr; `emulate_apply` / `emulate_gmres` run N ranks on one GPU
 from __future__ import annotations
 
 import ctypes
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -308,6 +309,8 @@ class _Handle:
     def __del__(self):
         from . import _lib
 
+        if sys.is_finalizing():  # the process is exiting: the driver reclaims everything
+            return
         if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
             getattr(_lib._lib, self._destroy)(self.h)
             self.h = None

@@ -226,15 +226,27 @@ def gmres_loop(vec, apply_A, apply_M, b, x, nonzero_x0, restart, max_iters, rtol
 
 
 def _gmres_generic(apply_A, apply_M_inv, b, x0, cfg):
-    """Reference krylov.py:39-117 over device vectors and arbitrary callables."""
+    """Reference krylov.py:39-117 over device vectors and arbitrary callables.
+
+    The Krylov vectors live on the device.  Callables see what the caller's
+    b is: float64 CUDA tensors when b is one, NumPy arrays when b is a NumPy
+    array (the reference's contract: `lambda v: lu @ v` keeps working; each
+    call then copies v to the host and the result back)."""
     host_in = not is_device_tensor(b)
     bd = to_device(b)
     n = bd.numel()
     vec = DeviceVectors()
     x = vec.zeros(n) if x0 is None else to_device(x0, n).clone()
     nonzero = x0 is not None and bool((x != 0).any())
-    x, total, hist, conv = gmres_loop(vec, lambda v: _call(apply_A, v),
-                                      None if apply_M_inv is None else (lambda v: _call(apply_M_inv, v)),
-                                      bd, x, nonzero, cfg.restart, cfg.max_iters, cfg.rtol, cfg.atol)
+
+    def wrap(op):
+        if op is None:
+            return None
+        if host_in:
+            return lambda v: _call(op, v.cpu().numpy())
+        return lambda v: _call(op, v)
+
+    x, total, hist, conv = gmres_loop(vec, wrap(apply_A), wrap(apply_M_inv), bd, x, nonzero, cfg.restart,
+                                      cfg.max_iters, cfg.rtol, cfg.atol)
     out = x.cpu().numpy() if host_in else x
     return out, SolveStats(total, hist, conv)

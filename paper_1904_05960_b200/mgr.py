@@ -6,9 +6,12 @@ block extraction, W_p = -D_FF^-1 A_FC, structural RAP with the optional
 N_max non-Galerkin dropping, AMG / Jacobi F-relaxation and the terminal AMG.
 `mgr_apply` / `MgrHierarchy.apply` run the reduction cycle of mgr.py:399-438.
 
-Options the reference offers but no BASELINE.json config uses (global
-HBGS/ILU smoothers, ideal transfers, exact solves, quasi-IMPES) raise
-NotImplementedError instead of silently running elsewhere.
+The level-2 global smoothers of default_three_level (ILU(k) and hybrid block
+Gauss-Seidel over partitions, mgr.py:275-292) run on the device.  Options
+the reference offers but no BASELINE.json config uses and the device path
+does not implement (ideal transfers, exact F / terminal solves, quasi-IMPES,
+Jacobi restriction) raise NotImplementedError instead of silently running
+elsewhere.
 """
 
 from __future__ import annotations

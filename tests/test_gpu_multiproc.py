@@ -94,8 +94,12 @@ def test_two_processes_host_transport_vs_oracle(name):
     port = _free_port()
     procs = []
     for r in range(2):
+        # coarse levels kept distributed down to 300 rows, as in
+        # test_gpu_dist.py::test_distributed_setup_is_bitwise (at the default
+        # thresholds the redundantly set-up small levels agree to ~1e-13, not
+        # bitwise: DESIGN.md §7)
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port))
+                   MASTER_PORT=str(port), PMGR_COLLAPSE_ROWS="300", PMGR_DIST_REPLICATE_ROWS="300")
         procs.append(subprocess.Popen([sys.executable, "-c", _SCRIPT, REPO, name], env=env, cwd=REPO,
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
     outs = []
@@ -106,6 +110,10 @@ def test_two_processes_host_transport_vs_oracle(name):
             p.kill()
             out, err = p.communicate()
         outs.append((p.returncode, out, err))
+    for r, (rc, out, err) in enumerate(outs):
+        if os.environ.get("PMGR_TEST_LOGDIR"):
+            with open(os.path.join(os.environ["PMGR_TEST_LOGDIR"], f"multiproc_{name}_rank{r}.log"), "w") as f:
+                f.write(f"rc={rc}\n--- stdout\n{out}\n--- stderr\n{err}\n")
     for rc, out, err in outs:
         assert rc == 0, (out[-2000:], err[-4000:])
     line = [ln for ln in outs[0][1].splitlines() if ln.startswith("RESULT")]

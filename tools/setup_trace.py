@@ -16,7 +16,7 @@ pb = problems.make(name, device=dev)
 A = pb.A if dev else sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
 cfg = mgr.config_from_options(problems.solver_options(name, pb))
 lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
-for rep in range(3):
+for rep in range(int(os.environ.get("SETUP_REPS", "3"))):
     torch.cuda.synchronize()
     t = time.time()
     h = mgr.mgr_setup(A, lay, cfg)
