@@ -148,6 +148,12 @@ struct DBuf {
     T *get() const { return p; }
 };
 
+// The device's default memory pool keeps what scratch buffers free (release
+// threshold = unlimited) instead of returning it to the driver at every
+// synchronisation: setup allocates and frees tens of GB of scratch at C4,
+// and re-mapping it cost hundreds of ms per setup.  Called once per device.
+void keep_pool_memory();
+
 // Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
 template <class T>
 struct TBuf {
@@ -176,6 +182,7 @@ struct TBuf {
         s = st;
         n = count;
         size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+        keep_pool_memory();
         PMGR_CUDA(cudaMallocAsync((void **)&p, bytes, s));
     }
     void release() {

@@ -80,7 +80,7 @@ __global__ void k_iota(int32_t *p, int64_t n) {
 // numeric pass keys and values (1024 slots, rows up to 512 by their exact
 // count: 12 KB per warp); rows beyond take a global-memory table
 constexpr int HS_SYM = 2048;
-constexpr int HS_NUM = 1024;
+constexpr int HS_NUM = 512;
 constexpr int SP_WARPS = 4;       // warps per block
 constexpr int SMALL_LIMIT = HS_SYM / 2;      // symbolic: upper bound
 constexpr int SMALL_LIMIT_NUM = HS_NUM / 2;  // numeric: exact count

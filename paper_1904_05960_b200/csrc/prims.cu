@@ -130,6 +130,19 @@ bool pdl_enabled() {
     return on;
 }
 
+void keep_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    static const bool keep_on = !(getenv("PMGR_POOL_KEEP") && getenv("PMGR_POOL_KEEP")[0] == '0');
+    cudaMemPool_t pool;
+    if (keep_on && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {
