@@ -795,31 +795,31 @@ void cycle_from_zero(pmgr_amg &h, size_t l, cudaStream_t s, double *out) {
     const double pass = csr_pass_bytes(A) + 16.0 * A.nrows;
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_SWEEP0 : PROF_KINDS, pass, s);
-        halo_exchange(L.halo.get(), L.x.p, s);
-        spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
+        with_halo(*L.A, L.halo.get(), L.x.p, s, [&](const CsrView &V) { spmv_residual(V, L.x.p, L.b.p, L.r.p, s); });
     } else {
         vec_zero(L.x.p, A.nrows, s);
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, true, s);
         spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
     }
-    halo_exchange(L.halo.get(), L.r.p, s);
     const double *e;
     if (has_next) {
         AmgLevel &N = h.levels[l + 1];
-        if (N.jacobi) spmv_restrict_div(L.R.view(), L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
-        else spmv(L.R.view(), L.r.p, N.b.p, s);
+        with_halo(L.R, L.halo.get(), L.r.p, s, [&](const CsrView &V) {
+            if (N.jacobi) spmv_restrict_div(V, L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
+            else spmv(V, L.r.p, N.b.p, s);
+        });
         cycle_from_zero(h, l + 1, s);
-        halo_exchange(N.halo.get(), N.xo.p, s);
-        e = N.xo.p;
+        with_halo(L.P, N.halo.get(), N.xo.p, s, [&](const CsrView &V) { spmv_add_pre(V, N.xo.p, L.x.p, s); });
     } else {
+        halo_exchange(L.halo.get(), L.r.p, s);
         spmv(L.R.view(), L.r.p, h.cb.p, s);
         e = coarse_solve(h, s);
+        spmv_add_pre(L.P.view(), e, L.x.p, s);
     }
-    spmv_add_pre(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
         ProfScope ps(tag ? PROF_FRELAX_JACOBI : PROF_KINDS, pass, s);
-        halo_exchange(L.halo.get(), L.x.p, s);
-        spmv_jacobi_bpre(A, L.x.p, L.b.p, L.dtilde.p, y, s);
+        with_halo(*L.A, L.halo.get(), L.x.p, s,
+                  [&](const CsrView &V) { spmv_jacobi_bpre(V, L.x.p, L.b.p, L.dtilde.p, y, s); });
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);
         vec_copy(L.x.p, y, A.nrows, s);
@@ -898,31 +898,30 @@ void amg_cycle(pmgr_amg &h, const double *b, const double *x, double *out, cudaS
     vec_copy(b + o, L.b.p + o, n, s);
     const CsrView A = L.A->view();
     if (L.jacobi) {
-        halo_exchange(L.halo.get(), const_cast<double *>(x), s);
-        spmv_jacobi(A, x, L.b.p, L.dtilde.p, L.x.p, s);
+        with_halo(*L.A, L.halo.get(), const_cast<double *>(x), s,
+                  [&](const CsrView &V) { spmv_jacobi(V, x, L.b.p, L.dtilde.p, L.x.p, s); });
     } else {
         vec_copy(x, L.x.p, n, s);
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, true, s);
     }
-    halo_exchange(L.halo.get(), L.x.p, s);
-    spmv_residual(A, L.x.p, L.b.p, L.r.p, s);
-    halo_exchange(L.halo.get(), L.r.p, s);
-    const double *e;
+    with_halo(*L.A, L.halo.get(), L.x.p, s, [&](const CsrView &V) { spmv_residual(V, L.x.p, L.b.p, L.r.p, s); });
     if (h.levels.size() > 1) {
         AmgLevel &N = h.levels[1];
-        if (N.jacobi) spmv_restrict_div(L.R.view(), L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
-        else spmv(L.R.view(), L.r.p, N.b.p, s);
+        with_halo(L.R, L.halo.get(), L.r.p, s, [&](const CsrView &V) {
+            if (N.jacobi) spmv_restrict_div(V, L.r.p, N.dtilde.p, N.b.p, N.x.p, s);
+            else spmv(V, L.r.p, N.b.p, s);
+        });
         cycle_from_zero(h, 1, s);
-        halo_exchange(N.halo.get(), N.xo.p, s);
-        e = N.xo.p;
+        with_halo(L.P, N.halo.get(), N.xo.p, s, [&](const CsrView &V) { spmv_add(V, N.xo.p, L.x.p, s); });
     } else {
+        halo_exchange(L.halo.get(), L.r.p, s);
         spmv(L.R.view(), L.r.p, h.cb.p, s);
-        e = coarse_solve(h, s);
+        const double *e = coarse_solve(h, s);
+        spmv_add(L.P.view(), e, L.x.p, s);
     }
-    spmv_add(L.P.view(), e, L.x.p, s);
     if (L.jacobi) {
-        halo_exchange(L.halo.get(), L.x.p, s);
-        spmv_jacobi(A, L.x.p, L.b.p, L.dtilde.p, out, s);
+        with_halo(*L.A, L.halo.get(), L.x.p, s,
+                  [&](const CsrView &V) { spmv_jacobi(V, L.x.p, L.b.p, L.dtilde.p, out, s); });
     } else {
         hybrid_gs(A, L.nparts, L.starts.p, L.dtilde.p, L.b.p, L.x.p, L.xpre.p, false, s);
         vec_copy(L.x.p, out, n, s);

@@ -15,6 +15,7 @@
 #include <memory>
 #include <string>
 #include <utility>
+#include <array>
 #include <vector>
 
 #include "../../include/pmgr.h"
@@ -262,6 +263,10 @@ struct Csr {
     // blocks, so the Krylov SpMV re-reads what the last F-relaxation sweep
     // left in L2)
     std::shared_ptr<const Csr> blk_src;
+    // row-distributed operators: contiguous local row ranges that read no
+    // ghost column (inner) and the rest (outer); the interior rows run while
+    // the halo exchange is in flight (with_halo, hier.cuh).  Empty: no split.
+    std::vector<std::array<int64_t, 2>> inner, outer;
     CsrView view() const {
         const Csr &b = blk_src ? *blk_src : *this;
         return CsrView{nrows,  ncols,  nnz,     ro.p,    ci.p,    v.p,      maxrow, row_off,  lanes, ci16.p,

@@ -154,6 +154,7 @@ struct LoopbackHub {
         if (++arrived == n) {
             try {
                 execute(s);
+                if (p.kind == EXCHANGE) PMGR_CUDA(cudaStreamSynchronize(s));  // see LoopbackTransport::exchange
             } catch (const Error &e) {
                 failed = true;
                 why = e.msg;
@@ -184,11 +185,16 @@ struct LoopbackTransport : Transport {
         nranks = h->n;
     }
     void exchange(Halo &h, double *ext, cudaStream_t s) override {
+        // s may be a rank's side stream (with_halo): every rank's producers
+        // must be done before the last arriver copies, and the copies done
+        // before any rank proceeds (the emulated ranks share one main stream)
+        PMGR_CUDA(cudaStreamSynchronize(s));
         LoopbackHub::Post p;
         p.kind = LoopbackHub::EXCHANGE;
         p.h = &h;
         p.p = ext;
         hub->arrive(rank, p, s);
+        PMGR_CUDA(cudaStreamSynchronize(s));
     }
     void gather(Gather &g, const double *own, double *full, cudaStream_t s) override {
         LoopbackHub::Post p;
@@ -508,6 +514,96 @@ void halo_exchange(Halo *h, double *ext, cudaStream_t s) {
     if (h && h->tr) h->tr->exchange(*h, ext, s);
 }
 
+namespace {
+struct OverlapCtx {  // per thread (one rank per thread in the emulation) and device
+    int dev = -1;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+thread_local OverlapCtx g_ov;
+
+bool overlap_enabled() {
+    static const bool on = !(getenv("PMGR_OVERLAP") && getenv("PMGR_OVERLAP")[0] == '0');
+    return on;
+}
+}  // namespace
+
+bool halo_fork(const Csr &A, Halo *h, double *x, cudaStream_t s) {
+    if (!h || !h->tr || A.inner.empty() || !overlap_enabled()) return false;
+    int dev = 0;
+    PMGR_CUDA(cudaGetDevice(&dev));
+    if (g_ov.dev != dev) {
+        PMGR_CUDA(cudaStreamCreateWithFlags(&g_ov.cs, cudaStreamNonBlocking));
+        PMGR_CUDA(cudaEventCreateWithFlags(&g_ov.fork, cudaEventDisableTiming));
+        PMGR_CUDA(cudaEventCreateWithFlags(&g_ov.join, cudaEventDisableTiming));
+        g_ov.dev = dev;
+    }
+    PMGR_CUDA(cudaEventRecord(g_ov.fork, s));
+    PMGR_CUDA(cudaStreamWaitEvent(g_ov.cs, g_ov.fork, 0));
+    h->tr->exchange(*h, x, g_ov.cs);
+    PMGR_CUDA(cudaEventRecord(g_ov.join, g_ov.cs));
+    return true;
+}
+
+void halo_join(cudaStream_t s) { PMGR_CUDA(cudaStreamWaitEvent(s, g_ov.join, 0)); }
+
+namespace {
+__global__ void k_row_ghost(int64_t n, const int64_t *__restrict__ ro, const int32_t *__restrict__ ci, int64_t lo,
+                            int64_t hi, int8_t *flag) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    int g = 0;
+    for (int64_t q = ro[i] + lane; q < ro[i + 1]; q += 32) g |= (ci[q] < lo || ci[q] >= hi);
+    g = __any_sync(FULL, g);
+    if (lane == 0) flag[i] = (int8_t)g;
+}
+}  // namespace
+
+// split a localized operator's rows into contiguous interior / boundary
+// ranges (row triples for block operators); operators whose rows interleave
+// too finely, or that route long rows through per-row blocks, keep no split
+void classify_overlap(Csr &A, int64_t col_lo, int64_t col_hi, cudaStream_t s) {
+    A.inner.clear();
+    A.outer.clear();
+    const int64_t n = A.nrows;
+    if (n == 0 || (A.long_len > 0 && A.nlong > 0)) return;
+    const bool blocks = A.nbrows > 0;
+    if (blocks && (A.nbrows * 3 != n || A.rro.p)) return;
+    TBuf<int8_t> f(n, s);
+    k_row_ghost<<<grid_for(n * 32, 256), 256, 0, s>>>(n, A.ro.p, A.ci.p, col_lo, col_hi, f.p);
+    PMGR_LAUNCHED();
+    std::vector<int8_t> h(n);
+    PMGR_CUDA(cudaMemcpyAsync(h.data(), f.p, n, cudaMemcpyDeviceToHost, s));
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    const int64_t step = blocks ? 3 : 1;
+    std::vector<std::array<int64_t, 2>> in, out;
+    for (int64_t r = 0; r < n;) {
+        int g = 0;
+        for (int64_t k = 0; k < step; ++k) g |= h[r + k];
+        int64_t e = r + step;
+        while (e < n) {
+            int ge = 0;
+            for (int64_t k = 0; k < step; ++k) ge |= h[e + k];
+            if (ge != g) break;
+            e += step;
+        }
+        (g ? out : in).push_back({r, e});
+        r = e;
+    }
+    if (in.empty() || in.size() + out.size() > 16) return;
+    static const bool stats = getenv("PMGR_HIER_STATS") && getenv("PMGR_HIER_STATS")[0] != '0';
+    if (stats) {
+        int64_t ri = 0, ro_ = 0;
+        for (auto &r : in) ri += r[1] - r[0];
+        for (auto &r : out) ro_ += r[1] - r[0];
+        fprintf(stderr, "[pmgr] overlap split %lld rows: inner %lld in %zu ranges, outer %lld in %zu ranges\n",
+                (long long)n, (long long)ri, in.size(), (long long)ro_, out.size());
+    }
+    A.inner = std::move(in);
+    A.outer = std::move(out);
+}
+
 void gather_full(Gather *g, const double *own, double *full, cudaStream_t s) {
     if (g->tr) {
         g->tr->gather(*g, own, full, s);
@@ -810,6 +906,7 @@ struct Builder {
             csr_make_bsr3(out, out.nrows, out.ncols, s, true);
             if (out.nbrows * 3 != out.nrows) fail(PMGR_ERR_INVALID, "local block copy failed");
         }
+        if (nranks > 1) classify_overlap(out, C->off(), C->off() + C->n_own(), s);
     }
 
     // owned values of a global per-entry array into an ext-length buffer
@@ -1067,8 +1164,7 @@ static void dist_spmv(DistSolver &D, const double *x_own, double *y_own, cudaStr
     D.ensure_work();
     if (D.n_own > 0)
         PMGR_CUDA(cudaMemcpyAsync(D.ze.p + D.off, x_own, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice, s));
-    halo_exchange(D.halo0.get(), D.ze.p, s);
-    spmv(D.A.view(), D.ze.p, D.we.p, s);
+    with_halo(D.A, D.halo0.get(), D.ze.p, s, [&](const CsrView &V) { spmv(V, D.ze.p, D.we.p, s); });
     if (D.n_own > 0)
         PMGR_CUDA(cudaMemcpyAsync(y_own, D.we.p + D.off, sizeof(double) * D.n_own, cudaMemcpyDeviceToDevice, s));
 }
@@ -1090,8 +1186,7 @@ void dist_gmres(DistSolver &D, const double *b, double *x, int nonzero_x0, const
     ops.capturable = D.tr && D.tr->capturable();
     ops.step = [&](cudaStream_t q) {
         mgr_apply_direct(*D.M, D.ve.p, D.ze.p, q);
-        halo_exchange(D.halo0.get(), D.ze.p, q);
-        spmv(D.A.view(), D.ze.p, D.we.p, q);
+        with_halo(D.A, D.halo0.get(), D.ze.p, q, [&](const CsrView &V) { spmv(V, D.ze.p, D.we.p, q); });
     };
     ops.spmv = [&](const double *xo, double *yo, cudaStream_t q) { dist_spmv(D, xo, yo, q); };
     ops.apply = [&](const double *uo, double *zo, cudaStream_t q) { dist_apply(D, uo, zo, q); };

@@ -37,6 +37,29 @@ struct Gather {  // all-gather of one space into its full global-order vector
     int id = -1;
 };
 void halo_exchange(Halo *h, double *ext, cudaStream_t s);
+
+// Interior / boundary overlap of a row-distributed operator: halo_fork starts
+// the exchange of x's ghosts on a side stream (forked from s) when A has a
+// row split and the halo has a transport, returning false otherwise;
+// halo_join makes s wait for it.  with_halo runs `launch` on A's interior row
+// ranges while the exchange is in flight, then on the boundary ranges.  Every
+// row keeps its lane group and summation order, so the results are bitwise
+// those of exchange-then-launch.
+bool halo_fork(const Csr &A, Halo *h, double *x, cudaStream_t s);
+void halo_join(cudaStream_t s);
+CsrView rows_view(const CsrView &A, int64_t r0, int64_t r1);
+template <class F>
+inline void with_halo(const Csr &A, Halo *h, double *x, cudaStream_t s, F &&launch) {
+    if (!halo_fork(A, h, x, s)) {
+        halo_exchange(h, x, s);
+        launch(A.view());
+        return;
+    }
+    const CsrView V = A.view();
+    for (const auto &r : A.inner) launch(rows_view(V, r[0], r[1]));
+    halo_join(s);
+    for (const auto &r : A.outer) launch(rows_view(V, r[0], r[1]));
+}
 void gather_full(Gather *g, const double *own, double *full, cudaStream_t s);
 
 // One classical-AMG level (reference amg.py:51-57).

@@ -326,14 +326,15 @@ void apply_level(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t
                 next_prefilled = true;
             }
         }
-        halo_exchange(L.halo_f.get(), L.zf.p, s);
-        spmv_resid_rows(L.A_cf.view(), L.zf.p, v, L.c_rows.p, rc, nx, s);
+        with_halo(L.A_cf, L.halo_f.get(), L.zf.p, s,
+                  [&](const CsrView &V) { spmv_resid_rows(V, L.zf.p, v, L.c_rows.p, rc, nx, s); });
     } else {
         vec_gather(v, L.c_rows.p + L.off_c, L.nc, L.rc.p + L.off_c, s);
     }
     apply_level(h, l + 1, rc, L.zc.p, s, next_prefilled);
-    halo_exchange(L.halo_c.get(), L.zc.p, s);
-    spmv_prolong_combine(L.P.view(), L.zc.p, pre ? L.zf.p : nullptr, pre ? L.f_index.p : nullptr, z, s);
+    with_halo(L.P, L.halo_c.get(), L.zc.p, s, [&](const CsrView &V) {
+        spmv_prolong_combine(V, L.zc.p, pre ? L.zf.p : nullptr, pre ? L.f_index.p : nullptr, z, s);
+    });
     if (h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
         // r = v - A z ; z[F] += M_FF^{-1} r[F]
         DBuf<double> &r = L.tmpf;  // reuse: needs n, allocated as max(n, nf)

@@ -1427,6 +1427,21 @@ __global__ void k_mul(const double *__restrict__ a, const double *__restrict__ b
 
 }  // namespace
 
+CsrView rows_view(const CsrView &A, int64_t r0, int64_t r1) {
+    CsrView v = A;
+    v.nrows = r1 - r0;
+    v.ro = A.ro + r0;
+    v.row_off = A.row_off + r0;
+    if (A.nbrows > 0) {  // pure block operator: ranges are whole row triples
+        v.bro = A.bro + r0 / 3;
+        v.nbrows = (r1 - r0) / 3;
+    }
+    v.long_len = 0;
+    v.nlong = 0;
+    v.lrows = nullptr;
+    return v;
+}
+
 void spmv(const CsrView &A, const double *x, double *y, cudaStream_t s) { launch(A, OpY{x, y}, s); }
 
 void spmv_residual(const CsrView &A, const double *x, const double *b, double *r, cudaStream_t s) {

@@ -259,3 +259,39 @@ def test_distributed_setup_is_bitwise():
         if ln.startswith("GMRES"):
             _, name, nr, its, its1, conv, rel = ln.split()
             assert conv == "True" and abs(int(its) - int(its1)) <= 1 and float(rel) < 1e-5, ln
+
+
+_OVERLAP_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1904_05960_b200 import dist, mgr, problems, sparse
+for name, base in (("C5", problems.make_c5(seed=3, nxy=10, nz_per_gpu=6, gpus=3)), ("C4", problems.make_c4(seed=3, n=12))):
+    pb, bounds = problems.rank_major(base, 3)
+    A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
+    h = mgr.mgr_setup(A, sparse.FieldLayout(pb.field_of, pb.entity_of),
+                      mgr.config_from_options(problems.solver_options(name, pb)))
+    v = np.random.default_rng(7).standard_normal(pb.n)
+    print("BITWISE", name, bool(np.array_equal(dist.emulate_apply(h, bounds, v).cpu().numpy(), h.apply(v))))
+"""
+
+
+def test_halo_overlap_split_is_bitwise(pk):
+    """Row-distributed operators split into interior and boundary row ranges
+    (the interior rows run while the halo exchange is in flight): the split
+    is taken (PMGR_HIER_STATS reports it) and the application stays bitwise
+    equal to the single-GPU one, with the overlap on and off."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for ov in ("1", "0"):
+        env = dict(os.environ, PMGR_HIER_STATS="1", PMGR_OVERLAP=ov)
+        r = subprocess.run([sys.executable, "-c", _OVERLAP_SCRIPT, repo], env=env, capture_output=True, text=True,
+                           timeout=600, cwd=repo)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[ov] = r
+        assert r.stdout.count("BITWISE") == 2 and "False" not in r.stdout, r.stdout
+    splits = [ln for ln in outs["1"].stderr.splitlines() if "overlap split" in ln]
+    assert any("outer 0 " not in ln for ln in splits), "no operator has boundary rows"
