@@ -320,7 +320,7 @@ std::shared_ptr<Csr> assemble_poromech(const pmgr_assembly &A, cudaStream_t s) {
     PMGR_LAUNCHED();
     k_asm_frows<<<grid_for((int64_t)nf * nc, 128), 128, 0, s>>>(P, n_u, nc, M->ro.p, M->ci.p, M->v.p);
     PMGR_LAUNCHED();
-    csr_finalize(*M, s);
+    csr_finalize(*M, s, false);  // sliced jagged copy: at first use (capi.cu ensure_sj)
     PMGR_CUDA(cudaStreamSynchronize(s));
     return M;
 }

@@ -121,7 +121,7 @@ int pmgr_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t *ro
             PMGR_CUDA(cudaMemcpyAsync(m->v.p, values, sizeof(double) * nnz, k, S(stream)));
         }
         if (validate) pmgr::csr_validate(m->view(), S(stream));
-        pmgr::csr_finalize(*m, S(stream));
+        pmgr::csr_finalize(*m, S(stream), false);  // sliced jagged copy: at first use (ensure_sj)
         PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         *out = wrap(std::move(m));
     });
@@ -158,9 +158,22 @@ int pmgr_csr_download(const pmgr_csr *A, int64_t *row_offsets, int32_t *col_indi
     });
 }
 
+// A caller's matrix gets its sliced jagged solve copy when it is first
+// applied: MGR setup builds it from the block-prefix copy; a matrix used
+// without one (matvec, AMG level 0, unpreconditioned GMRES) builds it here.
+static void ensure_sj(const pmgr_csr *A, void *stream) {
+    pmgr::Csr &m = *A->m;
+    if (m.sj_want && !m.sj && !m.sj_tried) {
+        pmgr::csr_make_sj(m, S(stream));
+        PMGR_CUDA(cudaStreamSynchronize(S(stream)));
+        m.sj_tried = true;  // one attempt per layout
+    }
+}
+
 int pmgr_spmv(const pmgr_csr *A, const double *x_dev, double *y_dev, void *stream) {
     return guard([&] {
         require(A != nullptr, "NULL matrix");
+        ensure_sj(A, stream);
         pmgr::spmv(A->m->view(), x_dev, y_dev, S(stream));
     });
 }
@@ -170,6 +183,7 @@ int pmgr_amg_setup(const pmgr_csr *A, const pmgr_amg_cfg *cfg, void *stream, pmg
     return guard([&] {
         require(A && cfg && out, "NULL argument");
         init_pool();
+        ensure_sj(A, stream);
         auto h = pmgr::amg_build(A->m, *cfg, S(stream));
         *out = h.release();
     });
@@ -246,6 +260,7 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
                 pmgr::csr_make_bsr3(*A->m, h->block_prefix, h->block_prefix, S(stream));
             PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         }
+        ensure_sj(A, stream);
         *out = h.release();
     });
 }
@@ -327,6 +342,7 @@ int pmgr_gmres(const pmgr_csr *A, pmgr_mgr *M, const double *b_dev, double *x_de
     return guard([&] {
         require(A && cfg && stats && b_dev && x_dev, "NULL argument");
         require(cfg->restart <= 1000, "restart above 1000 is not supported");
+        ensure_sj(A, stream);
         pmgr::gmres_device(A, M, b_dev, x_dev, nonzero_x0, *cfg, *stats, history_host, history_cap, S(stream));
     });
 }
@@ -337,6 +353,7 @@ int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_host, double
     return guard([&] {
         require(A && cfg && stats && b_host && x_host, "NULL argument");
         require(cfg->restart <= 1000, "restart above 1000 is not supported");
+        ensure_sj(A, stream);
         const int64_t n = A->m->nrows;
         const size_t bytes = sizeof(double) * (size_t)n;
         pmgr::TBuf<double> b(n, S(stream)), x(n, S(stream));
@@ -571,7 +588,7 @@ int pmgr_csr_rows(const pmgr_csr *A, int64_t lo, int64_t hi, void *stream, pmgr_
         require(lo >= 0 && lo <= hi && hi <= A->m->nrows, "row range out of bounds");
         auto m = std::make_shared<pmgr::Csr>();
         pmgr::ds_partial_rows(*A->m, lo, hi, *m, S(stream));
-        pmgr::csr_finalize(*m, S(stream));
+        pmgr::csr_finalize(*m, S(stream), false);
         *out = wrap(m);
     });
 }

@@ -206,6 +206,30 @@ inline T read_scalar(const T *dev, cudaStream_t s) {
 // device CSR
 // ---------------------------------------------------------------------------
 
+// Sliced jagged copy of an operator for the solve phase (sj.cu, spmv.cu): rows
+// (or row triples of 3x3 blocks) in slices of 32, one lane per row; a slice
+// stores position t of all its rows that have one contiguously (rows shorter
+// than t simply drop out: no padding), so thread-per-row loads are coalesced
+// and no cross-lane reduction is needed.  Scalar slices come first in
+// "triple mode" (3 per block slice: rows 3 I + g of its triples, the entries
+// outside the blocks), then over consecutive rows from row0.
+struct SjView {
+    int64_t nrows = 0;                        // rows of the whole operator
+    int64_t nbslice = 0, nbrows = 0;          // block slices / row triples
+    int64_t ntslice = 0, ncslice = 0, row0 = 0;
+    const int64_t *bptr = nullptr;            // per block slice: first block
+    const int32_t *blen = nullptr, *bci = nullptr;
+    const double *bval = nullptr;             // per position: 9 planes of k doubles
+    const int64_t *sptr = nullptr;            // per scalar slice: first entry
+    const int32_t *slen = nullptr, *sci = nullptr;
+    const double *sv = nullptr;
+    int64_t nblocks = 0, nent = 0;
+    int64_t r0 = 0, r1 = -1;                  // output row range (r1 < 0: all)
+    int64_t row_off = 0;
+    int u = 0;                                // positions per chunk of the scalar slices
+    bool on() const { return bptr != nullptr || sptr != nullptr; }
+};
+
 struct CsrView {
     int64_t nrows, ncols, nnz;
     const int64_t *ro;
@@ -232,6 +256,16 @@ struct CsrView {
     int64_t long_len = 0, nlong = 0;
     const int32_t *lrows = nullptr;
     int lanes_u = 0;  // entries per lane in flight (2 / 4; 0: from this operator's mean)
+    SjView sj;        // sliced jagged solve copy (takes precedence when present)
+};
+
+struct Sj {
+    int64_t nbslice = 0, nbrows = 0, ntslice = 0, ncslice = 0, row0 = 0, nblocks = 0, nent = 0;
+    DBuf<int64_t> bptr, sptr;
+    DBuf<int32_t> blen, bci, slen, sci;
+    DBuf<double> bval, sv;
+    std::shared_ptr<const Sj> blk_src;  // block piece borrowed from another operator (A0 <- A_uu)
+    int u = 0;
 };
 
 struct Csr {
@@ -267,11 +301,37 @@ struct Csr {
     // ghost column (inner) and the rest (outer); the interior rows run while
     // the halo exchange is in flight (with_halo, hier.cuh).  Empty: no split.
     std::vector<std::array<int64_t, 2>> inner, outer;
+    std::shared_ptr<Sj> sj;  // sliced jagged solve copy (large operators)
+    bool sj_want = false;    // the (global) operator is large enough for it
+    bool sj_tried = false;   // a caller's matrix: the lazy build ran (capi.cu)
     CsrView view() const {
         const Csr &b = blk_src ? *blk_src : *this;
-        return CsrView{nrows,  ncols,  nnz,     ro.p,    ci.p,    v.p,      maxrow, row_off,  lanes, ci16.p,
-                       nbrows, nblocks, nrem,   b.bro.p, b.bci.p, b.bval.p, rro.p,  rci.p,    rv.p,  long_len,
-                       nlong,  lrows.p, lanes_u};
+        CsrView V{nrows,  ncols,  nnz,     ro.p,    ci.p,    v.p,      maxrow, row_off,  lanes, ci16.p,
+                  nbrows, nblocks, nrem,   b.bro.p, b.bci.p, b.bval.p, rro.p,  rci.p,    rv.p,  long_len,
+                  nlong,  lrows.p, lanes_u};
+        if (sj) {
+            const Sj &bs = sj->blk_src ? *sj->blk_src : *sj;
+            SjView &J = V.sj;
+            J.nrows = nrows;
+            J.nbslice = bs.nbslice;
+            J.nbrows = bs.nbrows;
+            J.ntslice = sj->ntslice;
+            J.ncslice = sj->ncslice;
+            J.row0 = sj->row0;
+            J.bptr = bs.bptr.p;
+            J.blen = bs.blen.p;
+            J.bci = bs.bci.p;
+            J.bval = bs.bval.p;
+            J.sptr = sj->sptr.p;
+            J.slen = sj->slen.p;
+            J.sci = sj->sci.p;
+            J.sv = sj->sv.p;
+            J.nblocks = bs.nblocks;
+            J.nent = sj->nent;
+            J.row_off = row_off;
+            J.u = sj->u;
+        }
+        return V;
     }
 };
 
@@ -284,11 +344,18 @@ void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool forc
 // the block-prefix copy of A reusing src's blocks (src: a pure BSR3 operator
 // equal to A's leading prefix x prefix block); builds only A's remainder
 void csr_make_bsr3_shared(Csr &A, int64_t prefix, std::shared_ptr<const Csr> src, cudaStream_t s);
+// sliced jagged solve copy of an operator of at least PMGR_SJ_MIN_NNZ entries
+// (built from its block-prefix copy when it has one); blk: the operator whose
+// blocks are this one's block prefix and already has its own copy
+void csr_make_sj(Csr &A, cudaStream_t s, bool force = false);
 // B = P A P^T (row i of B = row perm[i] of A), columns re-sorted
 std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_host, cudaStream_t s);
 
 // record the longest row of a finished operator (setup time, synchronises)
-void csr_finalize(Csr &A, cudaStream_t s);
+// build_sj = false: only note whether the operator wants the sliced jagged
+// copy (sj_want); the caller builds it later (csr_make_sj) or never
+void csr_finalize(Csr &A, cudaStream_t s, bool build_sj = true);
+bool sj_wanted(int64_t nrows, int64_t nnz);  // PMGR_SJ_MIN_NNZ / PMGR_SJ_MIN_ROWS
 // list the rows longer than A.long_len (0: none) for the block-per-row path
 void csr_long_rows(Csr &A, cudaStream_t s);
 
@@ -362,6 +429,9 @@ inline double csr_pass_bytes(int64_t nrows, int64_t ncols, int64_t nnz) {
 }
 // one pass over the format the solve actually streams (BSR3 copy if present)
 inline double csr_pass_bytes(const CsrView &A) {
+    if (A.sj.on())  // blocks + entries + 4-byte lengths per lane + 8-byte slice starts
+        return 76.0 * A.sj.nblocks + 12.0 * A.sj.nent +
+               (4.0 * 32 + 8.0) * (A.sj.nbslice + A.sj.ntslice + A.sj.ncslice) + 8.0 * A.ncols + 8.0 * A.nrows;
     if (A.nbrows > 0)
         return 76.0 * A.nblocks + 8.0 * (A.nbrows + 1) + 12.0 * A.nrem + (A.rro ? 8.0 * (A.nrows + 1) : 0.0) +
                8.0 * A.ncols + 8.0 * A.nrows;

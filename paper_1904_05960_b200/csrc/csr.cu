@@ -570,7 +570,9 @@ __global__ void k_to16(int64_t nnz, const int32_t *ci, uint16_t *c16) {
 }
 }  // namespace
 
-void csr_finalize(Csr &A, cudaStream_t s) {
+void csr_finalize(Csr &A, cudaStream_t s, bool build_sj) {
+    A.sj.reset();
+    A.sj_want = sj_wanted(A.nrows, A.nnz);
     if (A.nrows == 0) {
         A.maxrow = 0;
         return;
@@ -598,6 +600,7 @@ void csr_finalize(Csr &A, cudaStream_t s) {
         k_to16<<<grid_for(A.nnz, 256), 256, 0, s>>>(A.nnz, A.ci.p, A.ci16.p);
         PMGR_LAUNCHED();
     }
+    if (build_sj) csr_make_sj(A, s);
     static const bool stats = getenv("PMGR_HIER_STATS") && getenv("PMGR_HIER_STATS")[0] != '0';
     if (stats)
         fprintf(stderr, "[pmgr] operator %lld x %lld nnz %lld (%.1f/row, max %lld, long rows %lld > %lld)\n",
@@ -723,6 +726,7 @@ void csr_make_bsr3(Csr &A, int64_t prow, int64_t pcol, cudaStream_t s, bool forc
     A.nbrows = nb;
     A.nblocks = nblk;
     A.nrem = nrem;
+    csr_make_sj(A, s);
 }
 
 void csr_make_bsr3_shared(Csr &A, int64_t prefix, std::shared_ptr<const Csr> src, cudaStream_t s) {
@@ -750,6 +754,7 @@ void csr_make_bsr3_shared(Csr &A, int64_t prefix, std::shared_ptr<const Csr> src
     A.nbrows = A.blk_src->nbrows;
     A.nblocks = A.blk_src->nblocks;
     A.nrem = nrem;
+    csr_make_sj(A, s);
 }
 
 void csr_copy(const CsrView &A, Csr &B, cudaStream_t s) {

@@ -892,7 +892,8 @@ struct Builder {
                                                         C->gdev.p, (int64_t)C->ghosts_me->size(), out.ro.p,
                                                         out.ci.p, out.v.p);
         PMGR_LAUNCHED();
-        csr_finalize(out, s);
+        csr_finalize(out, s, false);
+        out.sj_want = Y.sj_want;
         out.row_off = R->off();
         out.lanes = Y.lanes > 0 ? Y.lanes : spmv_lanes(Y.view());
         out.lanes_u = Y.lanes_u > 0 ? Y.lanes_u : spmv_u_for(Y.nnz, Y.nrows, out.lanes);
@@ -905,6 +906,8 @@ struct Builder {
         if (Y.nbrows > 0 && Y.nbrows * 3 == Y.nrows && !Y.rro.p) {
             csr_make_bsr3(out, out.nrows, out.ncols, s, true);
             if (out.nbrows * 3 != out.nrows) fail(PMGR_ERR_INVALID, "local block copy failed");
+        } else {
+            csr_make_sj(out, s);
         }
         if (nranks > 1) classify_overlap(out, C->off(), C->off() + C->n_own(), s);
     }

@@ -446,8 +446,11 @@ std::vector<int64_t> ds_cols_outside(const Csr &X, int64_t rlo, int64_t rhi, int
     return out;
 }
 
-void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s) {
-    csr_finalize(A, s);
+void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s, bool build_sj) {
+    // a partial (owned-rows) operator is never applied: its rank-local slices
+    // are (dist.cu), and they take the sliced jagged copy when the GLOBAL
+    // operator is large enough
+    csr_finalize(A, s, build_sj && d == nullptr);
     if (!d) return;
     // the global operator's statistics decide the lane group and long rows
     TBuf<unsigned long long> m(1, s);
@@ -467,6 +470,7 @@ void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s) {
     csr_long_rows(A, s);
     A.lanes = (A.long_len > 0 || gmax <= 16 * gm) ? gm : 32;
     A.lanes_u = spmv_u_for(gnnz, A.nrows, A.lanes);
+    A.sj_want = sj_wanted(A.nrows, gnnz);
 }
 
 int64_t ds_diag_inverse(const Csr &A, int64_t lo, int64_t hi, double *dinv, cudaStream_t s) {

@@ -58,7 +58,7 @@ std::vector<int64_t> ds_cols_outside(const Csr &X, int64_t rlo, int64_t rhi, int
                                      cudaStream_t s);
 // csr_finalize with the statistics of the whole (distributed) operator, so
 // every rank picks the single-GPU operator's SpMV lane group and long rows
-void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s);
+void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s, bool build_sj = true);
 // 1 / diag(A) on rows [lo, hi); first row with a zero or missing diagonal (-1: none)
 int64_t ds_diag_inverse(const Csr &A, int64_t lo, int64_t hi, double *dinv, cudaStream_t s);
 

@@ -455,9 +455,11 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         setup_trace("mgr blocks", li, s);
         // ---- transfers (build_transfers, mgr.py:131-187)
         const bool need_dinv = sp.interp == PMGR_INTERP_INJECTION_JACOBI || sp.f_relax == PMGR_FRELAX_JACOBI;
-        ds_finalize(dF.get(), *A_ff, s);
+        // (the sliced jagged copy of A_FF is built from its block copy when it gets one)
+        ds_finalize(dF.get(), *A_ff, s, false);
         if (sp.f_relax == PMGR_FRELAX_AMG && sp.amg_num_functions == 3)
             csr_make_bsr3(*A_ff, A_ff->nrows, A_ff->ncols, s, false, dF.get());
+        if (!dd && !A_ff->sj) csr_make_sj(*A_ff, s);
         if (li == 0 && A_ff->nbrows > 0) {
             // F rows first, then C rows: the same blocks lead A0 itself
             bool prefix = true;

@@ -972,6 +972,176 @@ struct OpProlong {
     __device__ void out(int64_t i, double s) const { z[i] = zfv + s; }
 };
 
+// ---------------------------------------------------------------------------
+// Sliced jagged kernels (SjView, sj.cu): one lane per row / row triple.
+// ---------------------------------------------------------------------------
+
+// One scalar slice: lane `lane` sums its row (len entries) onto acc, in stored
+// order with one accumulator.  Positions are taken U at a time: the next
+// chunk's (value, column) loads are issued before the current chunk's x
+// gathers are consumed.  WAIT: the PDL wait sits between the first chunk's
+// operator loads and the first gathers.
+template <int U, bool WAIT, class Op>
+__device__ __forceinline__ double sj_scalar_slice(const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                                  int64_t off, int len, bool mine, int lane, const Op &op,
+                                                  double acc, int trigger) {
+    const unsigned lt = (1u << lane) - 1u;
+    const int maxlen = __reduce_max_sync(FULL, len);
+    double nv[U];
+    int nc[U];
+    auto fetch = [&](int t0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool a = t0 + u < len;
+            const unsigned m = __ballot_sync(FULL, a);
+            const int64_t q = off + __popc(m & lt);
+            off += __popc(m);
+            const bool ld = a && mine;
+            nv[u] = ld ? __ldg(v + q) : 0.0;
+            nc[u] = ld ? __ldg(ci + q) : -1;
+        }
+    };
+    fetch(0);
+    if (WAIT) {
+        pdl_wait();
+        if (trigger) pdl_trigger();
+    }
+    for (int t0 = 0; t0 < maxlen; t0 += U) {
+        double vv[U], xs[U];
+        int cc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            vv[u] = nv[u];
+            cc[u] = nc[u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xs[u] = cc[u] >= 0 ? op.x(cc[u]) : 0.0;
+        if (t0 + U < maxlen) fetch(t0 + U);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (cc[u] >= 0) acc = fma(vv[u], xs[u], acc);
+    }
+    return acc;
+}
+
+template <int U, class Op>
+__device__ __forceinline__ void sj_role_b(const SjView &S, const Op &op, int trigger, int64_t sl, int lane,
+                                          int64_t r1) {
+    if (sl >= S.ncslice) return;
+    const int64_t gs = S.ntslice + sl;
+    const int64_t row = S.row0 + 32 * sl + lane;
+    const bool mine = row >= S.r0 && row < r1;
+    const int len = __ldg(S.slen + gs * 32 + lane);
+    const int64_t off = __ldg(S.sptr + gs);
+    Op o = op;
+    if (mine) o.pre(row + S.row_off);
+    const double acc = sj_scalar_slice<U, true>(S.sci, S.sv, off, len, mine, lane, op, 0.0, trigger);
+    if (mine) o.out(row + S.row_off, acc);
+}
+
+// role A (blockIdx.x < nblkA): a warp per block slice -- lane = row triple:
+// its 3x3 blocks (UB positions per chunk), then the three triple-mode scalar
+// slices holding the rows' entries outside the blocks.
+// role B: a warp per scalar slice over consecutive rows.
+template <int U, int UB, class Op>
+__global__ void __launch_bounds__(128) k_sj(SjView S, Op op, int trigger, unsigned nblkA, int64_t bs0, int64_t cs0) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r1 = S.r1 < 0 ? S.nrows : S.r1;
+    if (blockIdx.x < nblkA) {
+        const int64_t Sb = bs0 + (int64_t)blockIdx.x * 4 + w;
+        if (Sb >= S.nbslice) return;
+        const int64_t I = 32 * Sb + lane;
+        const int64_t row = 3 * I;
+        // whole triples only: a triple belongs to the range with its first row
+        const bool mine = row >= S.r0 && row < r1 && I < S.nbrows;
+        const int len = __ldg(S.blen + Sb * 32 + lane);
+        int64_t off = __ldg(S.bptr + Sb);
+        const unsigned lt = (1u << lane) - 1u;
+        const int maxlen = __reduce_max_sync(FULL, len);
+        int slen[3] = {0, 0, 0};
+        int64_t soff[3] = {0, 0, 0};
+        if (S.ntslice > 0) {
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+                slen[g] = __ldg(S.slen + (3 * Sb + g) * 32 + lane);
+                soff[g] = __ldg(S.sptr + 3 * Sb + g);
+            }
+        }
+        Op o0 = op, o1 = op, o2 = op;
+        if (mine) {
+            o0.pre(row + S.row_off);
+            if (row + 1 < S.nrows) o1.pre(row + 1 + S.row_off);
+            if (row + 2 < S.nrows) o2.pre(row + 2 + S.row_off);
+        }
+        double nv[UB][9];
+        int nc[UB];
+        auto fetch = [&](int t0) {
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const bool a = t0 + u < len;
+                const unsigned m = __ballot_sync(FULL, a);
+                const int k = __popc(m);
+                const int r = __popc(m & lt);
+                const bool ld = a && mine;
+                nc[u] = ld ? __ldg(S.bci + off + r) : -1;
+                const double *p = S.bval + 9 * off + r;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) nv[u][e] = ld ? __ldg(p + (int64_t)e * k) : 0.0;
+                off += k;
+            }
+        };
+        fetch(0);
+        pdl_wait();
+        if (trigger) pdl_trigger();
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int t0 = 0; t0 < maxlen; t0 += UB) {
+            double vv[UB][9], xs[UB][3];
+            int cc[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                cc[u] = nc[u];
+#pragma unroll
+                for (int e = 0; e < 9; ++e) vv[u][e] = nv[u][e];
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) xs[u][c] = cc[u] >= 0 ? op.x(3 * cc[u] + c) : 0.0;
+            if (t0 + UB < maxlen) fetch(t0 + UB);
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                if (cc[u] >= 0) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        a0 = fma(vv[u][3 * c + 0], xs[u][c], a0);
+                        a1 = fma(vv[u][3 * c + 1], xs[u][c], a1);
+                        a2 = fma(vv[u][3 * c + 2], xs[u][c], a2);
+                    }
+                }
+            }
+        }
+        if (S.ntslice > 0) {
+            a0 = sj_scalar_slice<U, false>(S.sci, S.sv, soff[0], slen[0], mine, lane, op, a0, 0);
+            a1 = sj_scalar_slice<U, false>(S.sci, S.sv, soff[1], slen[1], mine, lane, op, a1, 0);
+            a2 = sj_scalar_slice<U, false>(S.sci, S.sv, soff[2], slen[2], mine, lane, op, a2, 0);
+        }
+        if (mine) {
+            o0.out(row + S.row_off, a0);
+            if (row + 1 < S.nrows) o1.out(row + 1 + S.row_off, a1);
+            if (row + 2 < S.nrows) o2.out(row + 2 + S.row_off, a2);
+        }
+        return;
+    }
+    sj_role_b<U>(S, op, trigger, cs0 + (int64_t)(blockIdx.x - nblkA) * 4 + w, lane, r1);
+}
+
+// operators without blocks: role B only (a fraction of k_sj's registers)
+template <int U, class Op>
+__global__ void __launch_bounds__(128) k_sjs(SjView S, Op op, int trigger, int64_t cs0) {
+    const int64_t r1 = S.r1 < 0 ? S.nrows : S.r1;
+    sj_role_b<U>(S, op, trigger, cs0 + (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5), threadIdx.x & 31, r1);
+}
+
 // a kernel lets its successor launch early (PDL) only when its own grid is
 // at most this many blocks per SM (PMGR_TRIG_BPS).  Default: every grid
 // triggers (the successor's blocks take free slots during the last wave and
@@ -1183,10 +1353,69 @@ bool launch_bsr3t(const CsrView &A, const Op &op, cudaStream_t s) {
     return true;
 }
 
+// sliced jagged copy: block slices (role A) and consecutive scalar slices
+// (role B) of one launch, restricted to the slices that meet the view's row
+// range (row-distributed interior / boundary split)
+template <class Op>
+void launch_sj(const CsrView &A, const Op &op, cudaStream_t s) {
+    const SjView &J = A.sj;
+    const int64_t r0 = J.r0, r1 = J.r1 < 0 ? J.nrows : J.r1;
+    int64_t bs0 = 0, bs1 = 0, cs0 = 0, cs1 = 0;
+    if (J.nbslice > 0) {
+        const int64_t prow = 3 * J.nbrows;
+        const int64_t lo = r0 < prow ? r0 : prow, hi = r1 < prow ? r1 : prow;
+        if (hi > lo) {
+            bs0 = lo / 96;
+            bs1 = (hi + 95) / 96;
+        }
+    }
+    if (J.ncslice > 0 && r1 > J.row0) {
+        const int64_t lo = (r0 > J.row0 ? r0 : J.row0) - J.row0, hi = r1 - J.row0;
+        if (hi > lo) {
+            cs0 = lo / 32;
+            cs1 = (hi + 31) / 32;
+        }
+    }
+    const unsigned ga = (unsigned)((bs1 - bs0 + 3) / 4), gb = (unsigned)((cs1 - cs0 + 3) / 4);
+    if (ga + gb == 0) return;
+    const int trig = ga + gb <= (unsigned)(trigger_blocks_per_sm() * num_sms()) ? 1 : 0;
+    static const int ub = [] {
+        const char *e = getenv("PMGR_SJ_UB");
+        return e ? atoi(e) : 2;  // C4 outer SpMV 1.73 ms with 3 positions per chunk, 1.53 ms with 2
+    }();
+    static const int uforce = [] {
+        const char *e = getenv("PMGR_SJ_U");
+        return e ? atoi(e) : 0;
+    }();
+    const int u = uforce > 0 ? uforce : J.u;
+#define PMGR_SJ_GO(U_, UB_) \
+    launch_pdl(k_sj<U_, UB_, Op>, dim3(ga + gb), dim3(128), 0, s, J, op, trig, ga, bs0, cs0)
+    if (ga > 0 && ub == 2) {
+        if (u <= 2) PMGR_SJ_GO(2, 2);
+        else if (u <= 4) PMGR_SJ_GO(4, 2);
+        else PMGR_SJ_GO(8, 2);
+    } else if (ga > 0) {
+        if (u <= 2) PMGR_SJ_GO(2, 3);
+        else if (u <= 4) PMGR_SJ_GO(4, 3);
+        else PMGR_SJ_GO(8, 3);
+    } else {
+        if (u <= 2) launch_pdl(k_sjs<2, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else if (u <= 4) launch_pdl(k_sjs<4, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else if (u <= 8) launch_pdl(k_sjs<8, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else launch_pdl(k_sjs<16, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+    }
+#undef PMGR_SJ_GO
+    PMGR_LAUNCHED();
+}
+
 template <class Op>
 void launch(const CsrView &A, const Op &op, cudaStream_t s) {
     if (A.nrows == 0) return;
     ledger(csr_pass_bytes(A) + Op::row_bytes(op) * A.nrows + col_bytes_of<Op>::v * A.ncols);
+    if (A.sj.on()) {
+        launch_sj(A, op, s);
+        return;
+    }
     if (A.nbrows > 0 && launch_bsr3t(A, op, s)) return;
     if (A.nbrows > 0) {
         const int64_t ntrip = A.rro ? (A.nrows + 2) / 3 : A.nbrows;
@@ -1429,6 +1658,12 @@ __global__ void k_mul(const double *__restrict__ a, const double *__restrict__ b
 
 CsrView rows_view(const CsrView &A, int64_t r0, int64_t r1) {
     CsrView v = A;
+    if (A.sj.on()) {  // the copy keeps the operator's own row numbering: only the range narrows
+        v.nrows = r1 - r0;
+        v.sj.r0 = A.sj.r0 + r0;
+        v.sj.r1 = A.sj.r0 + r1;
+        return v;
+    }
     v.nrows = r1 - r0;
     v.ro = A.ro + r0;
     v.row_off = A.row_off + r0;

@@ -532,3 +532,25 @@ def test_tma_block_spmv_is_bitwise(pk, env):
     ref = run(dict(PMGR_BSR_TMA="0"))
     assert ref == run(dict(PMGR_BSR_TMA="2", **env))  # every pure block operator on the TMA kernel
     assert ref == run(dict(PMGR_BSR_TMA="1", **env))  # the default split
+
+
+@pytest.mark.parametrize("env", [dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1"), dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1", PMGR_SJ_UB="2", PMGR_SJ_U="2"),
+                                 dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1", PMGR_SJ_U="8")])
+def test_sliced_jagged_copy_parity(pk, env):
+    """The sliced jagged solve copy (one lane per row / row triple, sj.cu)
+    normally serves only the large HBM-streamed operators; forced onto EVERY
+    operator (PMGR_SJ_MIN_NNZ=1) the SpMV, AMG, MGR apply / GMRES parity tests
+    against the reference goldens and the row-distributed bitwise tests must
+    pass unchanged."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sel = ("test_spmv or test_amg_laplacian_bitwise or test_mgr_apply_and_gmres or test_mgr_option_variants "
+           "or test_all_c_level or test_empty_and_tiny or test_distributed_apply or test_halo_overlap "
+           "or test_distributed_gmres or test_apply_is_linear")
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "tests/test_gpu_dist.py", "-m", "gpu",
+                        "-x", "-q", "-k", sel, "-p", "no:cacheprovider"],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=1500, cwd=repo)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
