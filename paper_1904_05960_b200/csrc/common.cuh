@@ -227,6 +227,7 @@ struct SjView {
     int64_t r0 = 0, r1 = -1;                  // output row range (r1 < 0: all)
     int64_t row_off = 0;
     int u = 0;                                // positions per chunk of the scalar slices
+    int lg = 0;                               // consecutive slices: 2^lg lanes per row
     bool on() const { return bptr != nullptr || sptr != nullptr; }
 };
 
@@ -265,7 +266,7 @@ struct Sj {
     DBuf<int32_t> blen, bci, slen, sci;
     DBuf<double> bval, sv;
     std::shared_ptr<const Sj> blk_src;  // block piece borrowed from another operator (A0 <- A_uu)
-    int u = 0;
+    int u = 0, lg = 0;
 };
 
 struct Csr {
@@ -330,6 +331,7 @@ struct Csr {
             J.nent = sj->nent;
             J.row_off = row_off;
             J.u = sj->u;
+            J.lg = sj->lg;
         }
         return V;
     }

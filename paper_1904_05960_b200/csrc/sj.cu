@@ -21,7 +21,9 @@ namespace {
 
 // lengths of the scalar slices' lane rows and the slice totals
 // triple mode (gs < ntslice): slice gs = 3 S + g holds rows 3 (32 S + lane) + g
-__global__ void k_sj_slen(int64_t nslice, int64_t ntslice, int64_t prow, int64_t row0, int64_t n,
+// consecutive slices hold 32 >> lg rows, 2^lg lanes each: lane gl of a row
+// owns its entries g t + gl, so its length is the number of such entries
+__global__ void k_sj_slen(int64_t nslice, int64_t ntslice, int64_t prow, int64_t row0, int64_t n, int lg,
                           const int64_t *__restrict__ ro, int32_t *__restrict__ slen, int64_t *__restrict__ tot) {
     const int64_t gs = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -34,17 +36,21 @@ __global__ void k_sj_slen(int64_t nslice, int64_t ntslice, int64_t prow, int64_t
         row = 3 * (32 * S + lane) + g;
         ok = row < prow;
     } else {
-        row = row0 + 32 * (gs - ntslice) + lane;
+        row = row0 + (32 >> lg) * (gs - ntslice) + (lane >> lg);
         ok = row < n;
     }
-    const int len = ok ? (int)(ro[row + 1] - ro[row]) : 0;
+    int len = ok ? (int)(ro[row + 1] - ro[row]) : 0;
+    if (gs >= ntslice && lg > 0) {
+        const int g = 1 << lg, gl = lane & (g - 1);
+        len = len > gl ? (len - gl + g - 1) >> lg : 0;
+    }
     slen[gs * 32 + lane] = len;
     int64_t t = len;
     t = warp_sum_i64(t);
     if (lane == 0) tot[gs] = t;
 }
 
-__global__ void k_sj_sfill(int64_t nslice, int64_t ntslice, int64_t row0, const int64_t *__restrict__ ro,
+__global__ void k_sj_sfill(int64_t nslice, int64_t ntslice, int64_t row0, int lg, const int64_t *__restrict__ ro,
                            const int32_t *__restrict__ ci, const double *__restrict__ v,
                            const int64_t *__restrict__ sptr, const int32_t *__restrict__ slen,
                            int32_t *__restrict__ sci, double *__restrict__ sv) {
@@ -56,10 +62,12 @@ __global__ void k_sj_sfill(int64_t nslice, int64_t ntslice, int64_t row0, const 
         const int64_t S = gs / 3;
         row = 3 * (32 * S + lane) + (gs - 3 * S);
     } else {
-        row = row0 + 32 * (gs - ntslice) + lane;
+        row = row0 + (32 >> lg) * (gs - ntslice) + (lane >> lg);
     }
     const int len = slen[gs * 32 + lane];
-    const int64_t q0 = len > 0 ? ro[row] : 0;
+    const int sh = gs < ntslice ? 0 : lg;
+    const int gl = lane & ((1 << sh) - 1);
+    const int64_t q0 = len > 0 ? ro[row] + gl : 0;
     int maxlen = len;
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
     const unsigned lt = (1u << lane) - 1u;
@@ -69,8 +77,8 @@ __global__ void k_sj_sfill(int64_t nslice, int64_t ntslice, int64_t row0, const 
         const unsigned m = __ballot_sync(FULL, a);
         if (a) {
             const int64_t w = off + __popc(m & lt);
-            sci[w] = ci[q0 + t];
-            sv[w] = v[q0 + t];
+            sci[w] = ci[q0 + ((int64_t)t << sh)];
+            sv[w] = v[q0 + ((int64_t)t << sh)];
         }
         off += __popc(m);
     }
@@ -181,23 +189,40 @@ void csr_make_sj(Csr &A, cudaStream_t s, bool force) {
         const int64_t nbs = has_blocks ? (A.nbrows + 31) / 32 : 0;
         J->ntslice = 3 * nbs;
         J->row0 = prow;
-        J->ncslice = (A.nrows - prow + 31) / 32;
+        const double mean = (double)nent / (double)(A.nrows > 0 ? A.nrows : 1);
+        // lanes per row of the consecutive slices (PMGR_SJ_G; default by mean row length)
+        static const int gforce = [] {
+            const char *e = getenv("PMGR_SJ_G");
+            return e ? atoi(e) : 0;
+        }();
+        static const double gmean = [] {
+            const char *e = getenv("PMGR_SJ_G_MEAN");
+            return e ? atof(e) : 1e30;
+        }();
+        static const int gbig = [] {
+            const char *e = getenv("PMGR_SJ_GBIG");
+            return e ? atoi(e) : 4;
+        }();
+        int g = gforce > 0 ? gforce : (mean >= gmean ? gbig : 1);
+        J->lg = g >= 8 ? 3 : g >= 4 ? 2 : g >= 2 ? 1 : 0;
+        const int64_t R = 32 >> J->lg;
+        J->ncslice = (A.nrows - prow + R - 1) / R;
         const int64_t ns = J->ntslice + J->ncslice;
         J->nent = nent;
         J->slen.alloc(ns * 32);
         J->sptr.alloc(ns + 1);
         TBuf<int64_t> tot(ns, s);
-        k_sj_slen<<<grid_for(ns * 32, 256), 256, 0, s>>>(ns, J->ntslice, prow, J->row0, A.nrows, ro, J->slen.p,
-                                                         tot.p);
+        k_sj_slen<<<grid_for(ns * 32, 256), 256, 0, s>>>(ns, J->ntslice, prow, J->row0, A.nrows, J->lg, ro,
+                                                         J->slen.p, tot.p);
         PMGR_LAUNCHED();
         exclusive_scan_total(tot.p, J->sptr.p, ns, s);
         J->sci.alloc(nent);
         J->sv.alloc(nent);
-        k_sj_sfill<<<grid_for(ns * 32, 256), 256, 0, s>>>(ns, J->ntslice, J->row0, ro, ci, v, J->sptr.p, J->slen.p,
-                                                          J->sci.p, J->sv.p);
+        k_sj_sfill<<<grid_for(ns * 32, 256), 256, 0, s>>>(ns, J->ntslice, J->row0, J->lg, ro, ci, v, J->sptr.p,
+                                                          J->slen.p, J->sci.p, J->sv.p);
         PMGR_LAUNCHED();
-        const double mean = (double)nent / (double)(A.nrows > 0 ? A.nrows : 1);
-        J->u = mean <= 6.0 ? 2 : mean <= 24.0 ? 4 : 8;
+        const double lmean = mean / (double)(1 << J->lg);  // positions per lane
+        J->u = lmean <= 6.0 ? 2 : lmean <= 24.0 ? 4 : 8;
     }
     A.sj = J;
 }

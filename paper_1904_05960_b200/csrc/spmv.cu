@@ -983,22 +983,37 @@ struct OpProlong {
 // operator loads and the first gathers.
 template <int U, bool WAIT, class Op>
 __device__ __forceinline__ double sj_scalar_slice(const int32_t *__restrict__ ci, const double *__restrict__ v,
-                                                  int64_t off, int len, bool mine, int lane, const Op &op,
+                                                  int64_t off0, int len, bool mine, int lane, const Op &op,
                                                   double acc, int trigger) {
     const unsigned lt = (1u << lane) - 1u;
     const int maxlen = __reduce_max_sync(FULL, len);
+    const int minlen = __reduce_min_sync(FULL, len);  // positions [0, minlen) hold all 32 lanes
+    const double *vb = v + off0;
+    const int32_t *cb = ci + off0;
+    int off = 0;  // entries of the slice before the next position to fetch (warp-uniform)
     double nv[U];
     int nc[U];
     auto fetch = [&](int t0) {
+        if (t0 + U <= minlen) {  // full positions: lane-strided, immediate offsets, no ranks
+            const double *p = vb + off + lane;
+            const int32_t *pc = cb + off + lane;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const bool a = t0 + u < len;
-            const unsigned m = __ballot_sync(FULL, a);
-            const int64_t q = off + __popc(m & lt);
-            off += __popc(m);
-            const bool ld = a && mine;
-            nv[u] = ld ? __ldg(v + q) : 0.0;
-            nc[u] = ld ? __ldg(ci + q) : -1;
+            for (int u = 0; u < U; ++u) {
+                nv[u] = mine ? __ldg(p + 32 * u) : 0.0;
+                nc[u] = mine ? __ldg(pc + 32 * u) : -1;
+            }
+            off += 32 * U;
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool a = t0 + u < len;
+                const unsigned m = __ballot_sync(FULL, a);
+                const int q = off + __popc(m & lt);
+                off += __popc(m);
+                const bool ld = a && mine;
+                nv[u] = ld ? __ldg(vb + q) : 0.0;
+                nc[u] = ld ? __ldg(cb + q) : -1;
+            }
         }
     };
     fetch(0);
@@ -1024,19 +1039,25 @@ __device__ __forceinline__ double sj_scalar_slice(const int32_t *__restrict__ ci
     return acc;
 }
 
+// role B: a warp per scalar slice of 32 / g consecutive rows, g = 2^lg lanes
+// per row (lane gl of a row takes its entries g t + gl; the g partial sums
+// are added pairwise at the end)
 template <int U, class Op>
 __device__ __forceinline__ void sj_role_b(const SjView &S, const Op &op, int trigger, int64_t sl, int lane,
                                           int64_t r1) {
     if (sl >= S.ncslice) return;
+    const int lg = S.lg;
     const int64_t gs = S.ntslice + sl;
-    const int64_t row = S.row0 + 32 * sl + lane;
+    const int64_t row = S.row0 + ((32 >> lg) * sl) + (lane >> lg);
     const bool mine = row >= S.r0 && row < r1;
+    const bool head = (lane & ((1 << lg) - 1)) == 0;
     const int len = __ldg(S.slen + gs * 32 + lane);
     const int64_t off = __ldg(S.sptr + gs);
     Op o = op;
-    if (mine) o.pre(row + S.row_off);
-    const double acc = sj_scalar_slice<U, true>(S.sci, S.sv, off, len, mine, lane, op, 0.0, trigger);
-    if (mine) o.out(row + S.row_off, acc);
+    if (mine && head) o.pre(row + S.row_off);
+    double acc = sj_scalar_slice<U, true>(S.sci, S.sv, off, len, mine, lane, op, 0.0, trigger);
+    for (int w = (1 << lg) >> 1; w > 0; w >>= 1) acc += __shfl_xor_sync(FULL, acc, w);
+    if (mine && head) o.out(row + S.row_off, acc);
 }
 
 // role A (blockIdx.x < nblkA): a warp per block slice -- lane = row triple:
@@ -1372,8 +1393,9 @@ void launch_sj(const CsrView &A, const Op &op, cudaStream_t s) {
     if (J.ncslice > 0 && r1 > J.row0) {
         const int64_t lo = (r0 > J.row0 ? r0 : J.row0) - J.row0, hi = r1 - J.row0;
         if (hi > lo) {
-            cs0 = lo / 32;
-            cs1 = (hi + 31) / 32;
+            const int64_t R = 32 >> J.lg;
+            cs0 = lo / R;
+            cs1 = (hi + R - 1) / R;
         }
     }
     const unsigned ga = (unsigned)((bs1 - bs0 + 3) / 4), gb = (unsigned)((cs1 - cs0 + 3) / 4);
