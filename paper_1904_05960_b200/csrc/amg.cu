@@ -629,10 +629,16 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         if (!dd) {
             csr_transpose(lev.P.view(), lev.R, s);
             csr_finalize(lev.R, s);
-            Csr T1;
-            spgemm(lev.R.view(), Av, 0, T1, s);
-            spgemm(T1.view(), lev.P.view(), 0, *next, s);
+            setup_trace("  amg R = P^T", (int64_t)h->levels.size(), s);
+            {
+                Csr T1;
+                spgemm(lev.R.view(), Av, 0, T1, s);
+                spgemm(T1.view(), lev.P.view(), 0, *next, s);
+                setup_trace("  amg R A P", (int64_t)h->levels.size(), s);
+            }
+            setup_trace("  amg free R A", (int64_t)h->levels.size(), s);
             csr_finalize(*next, s);
+            setup_trace("  amg finalize", (int64_t)h->levels.size(), s);
         } else {
             // R = P^T: my fine rows' entries assembled at the coarse owners
             // (pieces in rank order = ascending fine index, as csr_transpose

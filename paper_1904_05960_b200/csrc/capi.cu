@@ -225,6 +225,7 @@ int pmgr_amg_export_csr(const pmgr_amg *h, int32_t level, int32_t what, void *st
             const pmgr::AmgLevel &L = amg_level(h, level);
             pmgr::csr_copy(what == 0 ? L.A->view() : L.P.view(), *m, S(stream));
         }
+        pmgr::csr_finalize(*m, S(stream), false);  // an exported operator is a matrix like any other
         PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         *out = wrap(std::move(m));
     });
@@ -261,6 +262,7 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
             PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         }
         ensure_sj(A, stream);
+        pmgr::setup_trace("mgr A0 solve copies", -1, S(stream));
         *out = h.release();
     });
 }
@@ -309,6 +311,7 @@ int pmgr_mgr_export_csr(const pmgr_mgr *h, int32_t level, int32_t what, void *st
             const pmgr::Csr &nx = (level + 1 < (int32_t)h->levels.size()) ? *h->levels[level + 1].A : *h->terminal_A;
             pmgr::csr_copy(nx.view(), *m, S(stream));
         }
+        pmgr::csr_finalize(*m, S(stream), false);
         PMGR_CUDA(cudaStreamSynchronize(S(stream)));
         *out = wrap(std::move(m));
     });

@@ -353,6 +353,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                                     const int32_t *entity_of_host, const pmgr_level_spec *specs, int nlevels,
                                     const pmgr_mgr_cfg &cfg, cudaStream_t s, const DistSetup *dist) {
     if (A0->nrows != A0->ncols) fail(PMGR_ERR_INVALID, "mgr_setup requires a square matrix");
+    setup_trace("mgr begin", -1, s);
     // distributed setup (dsetup.cuh): every operator keeps the owned rows of
     // its global row space; dd tracks the owned ranges of the level space
     std::unique_ptr<DistSetup> dd;

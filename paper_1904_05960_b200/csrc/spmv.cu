@@ -994,26 +994,28 @@ __device__ __forceinline__ double sj_scalar_slice(const int32_t *__restrict__ ci
     double nv[U];
     int nc[U];
     auto fetch = [&](int t0) {
-        if (t0 + U <= minlen) {  // full positions: lane-strided, immediate offsets, no ranks
-            const double *p = vb + off + lane;
-            const int32_t *pc = cb + off + lane;
+        int q[U];
+        unsigned act = 0;
+        if (t0 + U <= minlen) {  // full positions: lane-strided, no ranks
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                nv[u] = mine ? __ldg(p + 32 * u) : 0.0;
-                nc[u] = mine ? __ldg(pc + 32 * u) : -1;
-            }
+            for (int u = 0; u < U; ++u) q[u] = off + lane + 32 * u;
             off += 32 * U;
+            act = mine ? 0xffffffffu : 0u;
         } else {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const bool a = t0 + u < len;
                 const unsigned m = __ballot_sync(FULL, a);
-                const int q = off + __popc(m & lt);
+                q[u] = off + __popc(m & lt);
                 off += __popc(m);
-                const bool ld = a && mine;
-                nv[u] = ld ? __ldg(vb + q) : 0.0;
-                nc[u] = ld ? __ldg(cb + q) : -1;
+                if (a && mine) act |= 1u << u;
             }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ld = (act >> u) & 1u;
+            nv[u] = ld ? __ldg(vb + q[u]) : 0.0;
+            nc[u] = ld ? __ldg(cb + q[u]) : -1;
         }
     };
     fetch(0);
@@ -1157,8 +1159,9 @@ __global__ void __launch_bounds__(128) k_sj(SjView S, Op op, int trigger, unsign
 }
 
 // operators without blocks: role B only (a fraction of k_sj's registers)
+// (six blocks per SM: 80 registers; level 1 of C4 704 us, 712 us uncapped at 92)
 template <int U, class Op>
-__global__ void __launch_bounds__(128) k_sjs(SjView S, Op op, int trigger, int64_t cs0) {
+__global__ void __launch_bounds__(128, 6) k_sjs(SjView S, Op op, int trigger, int64_t cs0) {
     const int64_t r1 = S.r1 < 0 ? S.nrows : S.r1;
     sj_role_b<U>(S, op, trigger, cs0 + (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5), threadIdx.x & 31, r1);
 }
@@ -1423,8 +1426,7 @@ void launch_sj(const CsrView &A, const Op &op, cudaStream_t s) {
     } else {
         if (u <= 2) launch_pdl(k_sjs<2, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else if (u <= 4) launch_pdl(k_sjs<4, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
-        else if (u <= 8) launch_pdl(k_sjs<8, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
-        else launch_pdl(k_sjs<16, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else launch_pdl(k_sjs<8, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
     }
 #undef PMGR_SJ_GO
     PMGR_LAUNCHED();

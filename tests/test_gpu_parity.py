@@ -535,7 +535,7 @@ def test_tma_block_spmv_is_bitwise(pk, env):
 
 
 @pytest.mark.parametrize("env", [dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1"), dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1", PMGR_SJ_UB="2", PMGR_SJ_U="2"),
-                                 dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1", PMGR_SJ_U="8")])
+                                 dict(PMGR_SJ_MIN_NNZ="1", PMGR_SJ_MIN_ROWS="1", PMGR_SJ_U="8", PMGR_SJ_G="4")])
 def test_sliced_jagged_copy_parity(pk, env):
     """The sliced jagged solve copy (one lane per row / row triple, sj.cu)
     normally serves only the large HBM-streamed operators; forced onto EVERY
