@@ -1039,7 +1039,7 @@ std::shared_ptr<Csr> csr_permute(const Csr &A, const int64_t *perm_h, cudaStream
         PMGR_LAUNCHED();
     }
     segmented_sort_pairs(B->ci.p, B->v.p, B->nnz, B->ro.p, n, s);
-    csr_finalize(*B, s);
+    csr_finalize(*B, s, false);  // a caller's matrix: sliced jagged copy at first use
     PMGR_CUDA(cudaStreamSynchronize(s));
     return B;
 }

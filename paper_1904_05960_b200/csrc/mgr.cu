@@ -371,14 +371,20 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
     bool interleaved = cfg.flow_interleaved != 0;
     for (int li = 0; li < nlevels; ++li) {
         const pmgr_level_spec &sp = specs[li];
-        if (interleaved) {
+        // (only a global smoother reads the flag: levels with none at or after
+        // them skip the check -- two host sorts of the flow rows, ~40 ms per
+        // level at C4)
+        bool smoother_ahead = false;
+        for (int lj = li; lj < nlevels; ++lj) smoother_ahead |= specs[lj].global_smoother != PMGR_SMOOTHER_NONE;
+        if (interleaved && smoother_ahead) {
             std::vector<int64_t> sv, pv;
             for (int64_t i = 0; i < (int64_t)fo.size(); ++i) {
                 if (fo[i] == 1) sv.push_back(i);
                 else if (fo[i] == 2) pv.push_back(i);
             }
             auto by_ent = [&](std::vector<int64_t> &v) {
-                std::stable_sort(v.begin(), v.end(), [&](int64_t a, int64_t b) { return eo[a] < eo[b]; });
+                auto less = [&](int64_t a, int64_t b) { return eo[a] < eo[b]; };
+                if (!std::is_sorted(v.begin(), v.end(), less)) std::stable_sort(v.begin(), v.end(), less);
             };
             by_ent(sv);
             by_ent(pv);
@@ -569,6 +575,8 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         // ---- next layout
         std::vector<int8_t> fo2;
         std::vector<int32_t> eo2;
+        fo2.reserve((size_t)L.nc);
+        eo2.reserve((size_t)L.nc);
         for (int64_t i = 0; i < n; ++i)
             if ((sp.c_mask >> (fo[i] & 63)) & 1ull) {
                 fo2.push_back(fo[i]);
