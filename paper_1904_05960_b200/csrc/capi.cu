@@ -263,6 +263,7 @@ int pmgr_mgr_setup(const pmgr_csr *A, const int8_t *field_of, const int32_t *ent
         }
         ensure_sj(A, stream);
         pmgr::setup_trace("mgr A0 solve copies", -1, S(stream));
+        pmgr::host_trace_report("mgr_setup");
         *out = h.release();
     });
 }

@@ -85,6 +85,19 @@ bool pdl_enabled();
 // PMGR_SETUP_TRACE=1: synchronise and print the wall time of each setup
 // phase to stderr (diagnostics only; off by default)
 void setup_trace(const char *what, int64_t level, cudaStream_t s);
+// host-side accounting under PMGR_SETUP_TRACE: seconds spent in cudaMalloc,
+// cudaFree, pool allocations and blocking scalar reads (kind 0..3)
+bool host_trace_on();
+void host_trace_add(int kind, double seconds, double bytes);
+void host_trace_report(const char *what);
+struct HostTimer {
+    int kind;
+    double bytes;
+    bool on;
+    double t0;
+    HostTimer(int k, double b);
+    ~HostTimer();
+};
 
 template <class... KArgs, class... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -114,7 +127,18 @@ inline unsigned grid_for(int64_t threads_needed, int block) {
 // device buffers
 // ---------------------------------------------------------------------------
 
-// Persistent device buffer (cudaMalloc/cudaFree): owned by long-lived handles.
+// Persistent device buffers go through a block cache (prims.cu): cudaMalloc /
+// cudaFree of the setup's ~900 operator arrays (62 GB at C4) cost 0.2-0.6 s
+// per setup and varied box to box; freed blocks are kept (after a device
+// synchronisation -- what cudaFree did implicitly) and handed to the next
+// request of about that size, so a repeated setup allocates nothing.  The
+// cache is capped (PMGR_DBUF_CACHE_GB, default 45 % of the device) and is
+// returned to the driver when an allocation fails.  PMGR_DBUF_CACHE=0: off.
+void *dbuf_alloc(size_t bytes);
+void dbuf_free(void *p, size_t bytes);
+void dbuf_trim();  // return the cached blocks to the driver
+
+// Persistent device buffer: owned by long-lived handles.
 template <class T>
 struct DBuf {
     T *p = nullptr;
@@ -139,10 +163,10 @@ struct DBuf {
         release();
         n = count;
         size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
-        PMGR_CUDA(cudaMalloc((void **)&p, bytes));
+        p = static_cast<T *>(dbuf_alloc(bytes));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dbuf_free(p, sizeof(T) * (size_t)(n > 0 ? n : 1));
         p = nullptr;
         n = 0;
     }
@@ -184,7 +208,14 @@ struct TBuf {
         n = count;
         size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
         keep_pool_memory();
-        PMGR_CUDA(cudaMallocAsync((void **)&p, bytes, s));
+        HostTimer ht(2, (double)bytes);
+        cudaError_t e = cudaMallocAsync((void **)&p, bytes, s);
+        if (e == cudaErrorMemoryAllocation) {  // give the persistent buffers' cached blocks back and retry
+            cudaGetLastError();
+            dbuf_trim();
+            e = cudaMallocAsync((void **)&p, bytes, s);
+        }
+        if (e != cudaSuccess) fail_cuda(e, "cudaMallocAsync", __FILE__, __LINE__);
     }
     void release() {
         if (p) cudaFreeAsync(p, s);
@@ -197,6 +228,7 @@ struct TBuf {
 template <class T>
 inline T read_scalar(const T *dev, cudaStream_t s) {
     T h;
+    HostTimer ht(3, 0.0);
     PMGR_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
     PMGR_CUDA(cudaStreamSynchronize(s));
     return h;

@@ -354,6 +354,7 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                                     const pmgr_mgr_cfg &cfg, cudaStream_t s, const DistSetup *dist) {
     if (A0->nrows != A0->ncols) fail(PMGR_ERR_INVALID, "mgr_setup requires a square matrix");
     setup_trace("mgr begin", -1, s);
+    host_trace_report("before");
     // distributed setup (dsetup.cuh): every operator keeps the owned rows of
     // its global row space; dd tracks the owned ranges of the level space
     std::unique_ptr<DistSetup> dd;

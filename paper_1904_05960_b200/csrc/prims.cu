@@ -5,6 +5,9 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace pmgr {
@@ -120,6 +123,136 @@ void setup_trace(const char *what, int64_t level, cudaStream_t s) {
     fprintf(stderr, "[pmgr setup] %-28s level %3lld  %9.3f ms\n", what, (long long)level,
             std::chrono::duration<double, std::milli>(now - last).count());
     last = now;
+}
+
+namespace {
+double g_ht_sec[4] = {0, 0, 0, 0}, g_ht_bytes[4] = {0, 0, 0, 0};
+int64_t g_ht_cnt[4] = {0, 0, 0, 0};
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+bool host_trace_on() {
+    static const bool on = [] {
+        const char *e = getenv("PMGR_SETUP_TRACE");
+        return e && e[0] != '0';
+    }();
+    return on;
+}
+void host_trace_add(int kind, double seconds, double bytes) {
+    g_ht_sec[kind] += seconds;
+    g_ht_bytes[kind] += bytes;
+    ++g_ht_cnt[kind];
+}
+void host_trace_report(const char *what) {
+    if (!host_trace_on()) return;
+    static const char *names[4] = {"cudaMalloc", "cudaFree", "cudaMallocAsync", "blocking scalar reads"};
+    for (int k = 0; k < 4; ++k) {
+        fprintf(stderr, "[pmgr host] %-12s %-22s %6lld calls %9.3f ms %9.2f GB\n", what, names[k],
+                (long long)g_ht_cnt[k], 1e3 * g_ht_sec[k], g_ht_bytes[k] / 1e9);
+        g_ht_sec[k] = g_ht_bytes[k] = 0;
+        g_ht_cnt[k] = 0;
+    }
+}
+HostTimer::HostTimer(int k, double b) : kind(k), bytes(b), on(host_trace_on()), t0(on ? now_s() : 0.0) {}
+HostTimer::~HostTimer() {
+    if (on) host_trace_add(kind, now_s() - t0, bytes);
+}
+
+namespace {
+// Block cache behind the persistent buffers (DBuf): a freed block is kept
+// (per device, keyed by size) and handed to the next request of about that
+// size, so a repeated setup -- the second build of a benchmark, every Newton
+// step of a simulation -- finds its ~900 operator arrays without a single
+// cudaMalloc.  Blocks are cached only after a device synchronisation, so no
+// stream can still be using one when it is handed out again.
+struct BlockCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void *> free_blocks;
+    std::map<void *, std::pair<int, size_t>> live;  // handed out: device, block size
+    size_t cached = 0;
+    size_t cap() {
+        static const size_t c = [] {
+            if (const char *e = getenv("PMGR_DBUF_CACHE_GB")) return (size_t)(atof(e) * 1e9);
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) tot = (size_t)64 << 30;
+            return (size_t)(0.45 * (double)tot);
+        }();
+        return c;
+    }
+    // return every cached block to the driver (out of memory, or on request)
+    void trim() {
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto &kv : free_blocks) cudaFree(kv.second);
+        free_blocks.clear();
+        cached = 0;
+    }
+};
+BlockCache &block_cache() {
+    static BlockCache *c = new BlockCache;  // never destroyed: buffers may outlive static teardown
+    return *c;
+}
+}  // namespace
+
+void dbuf_trim() { block_cache().trim(); }
+
+void *dbuf_alloc(size_t bytes) {
+    HostTimer ht(0, (double)bytes);
+    BlockCache &C = block_cache();
+    const size_t want = (bytes + 511) & ~(size_t)511;
+    int dev = 0;
+    PMGR_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lock(C.mu);
+        auto it = C.free_blocks.lower_bound({dev, want});
+        if (it != C.free_blocks.end() && it->first.first == dev &&
+            it->first.second <= want + want / 8 + (64 << 10)) {
+            void *p = it->second;
+            C.live[p] = it->first;
+            C.cached -= it->first.second;
+            C.free_blocks.erase(it);
+            return p;
+        }
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        C.trim();
+        e = cudaMalloc(&p, want);
+    }
+    if (e != cudaSuccess) fail_cuda(e, "cudaMalloc", __FILE__, __LINE__);
+    std::lock_guard<std::mutex> lock(C.mu);
+    C.live[p] = {dev, want};
+    return p;
+}
+
+void dbuf_free(void *p, size_t bytes) {
+    HostTimer ht(1, (double)bytes);
+    BlockCache &C = block_cache();
+    std::pair<int, size_t> key{-1, 0};
+    {
+        std::lock_guard<std::mutex> lock(C.mu);
+        auto it = C.live.find(p);
+        if (it != C.live.end()) {
+            key = it->second;
+            C.live.erase(it);
+        }
+    }
+    static const bool cache_on = !(getenv("PMGR_DBUF_CACHE") && getenv("PMGR_DBUF_CACHE")[0] == '0');
+    if (key.first < 0 || !cache_on || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);  // unknown block, cache off, or the context is shutting down
+        return;
+    }
+    std::lock_guard<std::mutex> lock(C.mu);
+    if (C.cached + key.second > C.cap()) {
+        cudaFree(p);
+        return;
+    }
+    C.free_blocks.emplace(key, p);
+    C.cached += key.second;
 }
 
 bool pdl_enabled() {
