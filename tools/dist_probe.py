@@ -1,3 +1,8 @@
+"""Row-distributed apply against the single-GPU apply on small C5 / C4 problems
+at the DEFAULT replication / collapse thresholds (the tests pin the thresholds
+that keep the coarse levels distributed): prints whether the sliced and the
+distributed-setup applications are bitwise equal and the largest difference.
+    python tools/dist_probe.py"""
 import sys, numpy as np
 sys.path.insert(0, ".")
 from paper_1904_05960_b200 import dist as D, mgr, problems, sparse
