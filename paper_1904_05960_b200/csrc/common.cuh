@@ -337,6 +337,10 @@ struct Csr {
     std::shared_ptr<Sj> sj;  // sliced jagged solve copy (large operators)
     bool sj_want = false;    // the (global) operator is large enough for it
     bool sj_tried = false;   // a caller's matrix: the lazy build ran (capi.cu)
+    // the GLOBAL operator's rows / entries when this is a rank's slice or a
+    // partial (owned-rows) operator (0: its own): the lanes-per-row choice of
+    // the sliced jagged copy fixes the summation order, so slices follow it
+    int64_t g_rows = 0, g_nnz = 0;
     CsrView view() const {
         const Csr &b = blk_src ? *blk_src : *this;
         CsrView V{nrows,  ncols,  nnz,     ro.p,    ci.p,    v.p,      maxrow, row_off,  lanes, ci16.p,

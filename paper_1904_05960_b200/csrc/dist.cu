@@ -894,6 +894,8 @@ struct Builder {
         PMGR_LAUNCHED();
         csr_finalize(out, s, false);
         out.sj_want = Y.sj_want;
+        out.g_rows = Y.g_rows > 0 ? Y.g_rows : Y.nrows;
+        out.g_nnz = Y.g_nnz > 0 ? Y.g_nnz : Y.nnz;
         out.row_off = R->off();
         out.lanes = Y.lanes > 0 ? Y.lanes : spmv_lanes(Y.view());
         out.lanes_u = Y.lanes_u > 0 ? Y.lanes_u : spmv_u_for(Y.nnz, Y.nrows, out.lanes);

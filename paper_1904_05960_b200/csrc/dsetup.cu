@@ -471,6 +471,8 @@ void ds_finalize(const DistSetup *d, Csr &A, cudaStream_t s, bool build_sj) {
     A.lanes = (A.long_len > 0 || gmax <= 16 * gm) ? gm : 32;
     A.lanes_u = spmv_u_for(gnnz, A.nrows, A.lanes);
     A.sj_want = sj_wanted(A.nrows, gnnz);
+    A.g_rows = A.nrows;
+    A.g_nnz = gnnz;
 }
 
 int64_t ds_diag_inverse(const Csr &A, int64_t lo, int64_t hi, double *dinv, cudaStream_t s) {

@@ -190,21 +190,31 @@ void csr_make_sj(Csr &A, cudaStream_t s, bool force) {
         J->ntslice = 3 * nbs;
         J->row0 = prow;
         const double mean = (double)nent / (double)(A.nrows > 0 ? A.nrows : 1);
-        // lanes per row of the consecutive slices (PMGR_SJ_G; default by mean row length)
+        // lanes per row of the consecutive slices (PMGR_SJ_G): four for long-row
+        // operators of fewer than PMGR_SJ_G_ROWS rows, which one lane per row
+        // leaves short of warps (C4 AMG level 2, 573k rows x 164: 270 -> 252 us;
+        // level 1, 2.4M rows: 737 us with one lane, 741 with four), decided on
+        // the global operator's statistics
+        const int64_t grows = A.g_rows > 0 ? A.g_rows : A.nrows;
+        const double gmean_rows = (double)(A.g_nnz > 0 ? A.g_nnz : A.nnz) / (double)(grows > 0 ? grows : 1);
         static const int gforce = [] {
             const char *e = getenv("PMGR_SJ_G");
             return e ? atoi(e) : 0;
         }();
         static const double gmean = [] {
             const char *e = getenv("PMGR_SJ_G_MEAN");
-            return e ? atof(e) : 1e30;
+            return e ? atof(e) : 64.0;
+        }();
+        static const int64_t grows_max = [] {
+            const char *e = getenv("PMGR_SJ_G_ROWS");
+            return e ? atoll(e) : (int64_t)1000000;
         }();
         static const int gbig = [] {
             const char *e = getenv("PMGR_SJ_GBIG");
             return e ? atoi(e) : 4;
         }();
-        int g = gforce > 0 ? gforce : (mean >= gmean ? gbig : 1);
-        J->lg = g >= 8 ? 3 : g >= 4 ? 2 : g >= 2 ? 1 : 0;
+        int g = gforce > 0 ? gforce : (!has_blocks && gmean_rows >= gmean && grows < grows_max ? gbig : 1);
+        J->lg = g >= 32 ? 5 : g >= 16 ? 4 : g >= 8 ? 3 : g >= 4 ? 2 : g >= 2 ? 1 : 0;
         const int64_t R = 32 >> J->lg;
         J->ncslice = (A.nrows - prow + R - 1) / R;
         const int64_t ns = J->ntslice + J->ncslice;
