@@ -144,7 +144,13 @@ __global__ void k_table_size(int64_t n, const int64_t *ub, int64_t *tsz, int64_t
 // NUMERIC = false: count distinct columns per row into cnt[i].
 // NUMERIC = true : accumulate and dump (key, value) pairs unsorted into
 //                  C at cro[i]; structural mode stores zero sums as +0.0.
-template <bool NUMERIC>
+// FLAT (products whose right factor has short rows, e.g. (R A) P with two
+// entries per row of P): instead of one middle index per step -- two busy
+// lanes out of 32 -- the (middle index, entry) pairs of a batch of 32 middle
+// indices are flattened in (j, entry) order and taken 32 per step; pairs of
+// one step that hit the same output column are added by the lowest lane in
+// lane order, i.e. in ascending j, so every sum is still csr_matmat's.
+template <bool NUMERIC, bool FLAT = false>
 __global__ void __launch_bounds__(SP_WARPS * 32)
     k_spgemm(int64_t n, const int64_t *__restrict__ xro, const int32_t *__restrict__ xci,
              const double *__restrict__ xv, const int64_t *__restrict__ yro,
@@ -191,6 +197,58 @@ __global__ void __launch_bounds__(SP_WARPS * 32)
             const int32_t jl = has ? xci[jq] : 0;
             const double xl = (NUMERIC && has) ? xv[jq] : 0.0;
             const int64_t sl = has ? yro[jl] : 0, el = has ? yro[jl + 1] : 0;
+            if constexpr (FLAT) {
+                const int len = (int)(el - sl);
+                int inc = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                const int excl = inc - len;
+                const int T = __shfl_sync(FULL, inc, 31);
+                for (int q0 = 0; q0 < T; q0 += 32) {
+                    const int q = q0 + lane;
+                    const bool act = q < T;
+                    int t = 0;  // the last middle index of the batch whose pairs start at or before q
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int cand = t + step;
+                        const int ev = __shfl_sync(FULL, excl, cand & 31);
+                        if (cand < 32 && ev <= q) t = cand;
+                    }
+                    const int e = q - __shfl_sync(FULL, excl, t);
+                    const int64_t ys = __shfl_sync(FULL, sl, t);
+                    const double xval = __shfl_sync(FULL, xl, t);
+                    int32_t k = -1;
+                    double prod = 0.0;
+                    if (act) {
+                        k = yci[ys + e];
+                        if (NUMERIC) prod = __dmul_rn(xval, yv[ys + e]);
+                    }
+                    int64_t slot = -1;
+                    bool ins = false;
+                    if (act) slot = table_insert(keys, tsz, k, ins);
+                    if (!NUMERIC) {
+                        if (ins) ++local;
+                    } else {
+                        __syncwarp();
+                        const unsigned grp = __match_any_sync(FULL, act ? (int)slot : -1 - lane);
+                        const int gsz = __popc(grp);
+                        const int maxg = __reduce_max_sync(FULL, act ? gsz : 0);
+                        const bool leader = act && (__ffs(grp) - 1 == lane);
+                        double sacc = leader ? vals[slot] : 0.0;
+                        for (int r = 0; r < maxg; ++r) {
+                            const unsigned src = __fns(grp, 0, r + 1);
+                            const double pv = __shfl_sync(FULL, prod, src & 31u);
+                            if (leader && r < gsz) sacc = __dadd_rn(sacc, pv);
+                        }
+                        if (leader) vals[slot] = sacc;
+                    }
+                    __syncwarp();
+                }
+                continue;
+            }
             const int nb = (int)(xe - jb < 32 ? xe - jb : 32);
             int64_t st = __shfl_sync(FULL, sl, 0), en = __shfl_sync(FULL, el, 0);
             int32_t kc = st + lane < en ? yci[st + lane] : -1;
@@ -292,7 +350,13 @@ __global__ void k_big_segments(int64_t n, const int64_t *ro, int64_t limit, int6
 constexpr int DENSE_COLS = 12288;
 constexpr int DENSE_THREADS = 256;
 
-template <bool NUMERIC>
+// FLAT (numeric pass, right factors with short rows): no block barrier per
+// middle index.  Every warp walks the row's flattened (middle index, entry)
+// pairs, 32 per step in (j, entry) order, and accumulates the output columns
+// k with k mod 8 = its warp number; pairs of a step that hit one column are
+// added by the lowest lane in lane order (ascending j), so the sums are
+// unchanged bit for bit.
+template <bool NUMERIC, bool FLAT = false>
 __global__ void __launch_bounds__(DENSE_THREADS)
     k_spgemm_dense(int64_t n, int64_t ncols, const int64_t *__restrict__ xro, const int32_t *__restrict__ xci,
                    const double *__restrict__ xv, const int64_t *__restrict__ yro, const int32_t *__restrict__ yci,
@@ -318,6 +382,56 @@ __global__ void __launch_bounds__(DENSE_THREADS)
             const int32_t jl = has ? xci[jq] : 0;
             const double xl = (NUMERIC && has) ? xv[jq] : 0.0;
             const int64_t sl = has ? yro[jl] : 0, el = has ? yro[jl + 1] : 0;
+            if constexpr (NUMERIC && FLAT) {
+                static_assert(DENSE_THREADS == 256, "eight warps share the output columns");
+                const int warp = threadIdx.x >> 5;
+                const int len = (int)(el - sl);
+                int inc = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                const int excl = inc - len;
+                const int T = __shfl_sync(FULL, inc, 31);
+                for (int q0 = 0; q0 < T; q0 += 32) {
+                    const int q = q0 + lane;
+                    const bool act = q < T;
+                    int t = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int cand = t + step;
+                        const int ev = __shfl_sync(FULL, excl, cand & 31);
+                        if (cand < 32 && ev <= q) t = cand;
+                    }
+                    const int e = q - __shfl_sync(FULL, excl, t);
+                    const int64_t ys = __shfl_sync(FULL, sl, t);
+                    const double xval = __shfl_sync(FULL, xl, t);
+                    int32_t k = -1;
+                    double prod = 0.0;
+                    if (act) {
+                        k = yci[ys + e];
+                        prod = __dmul_rn(xval, yv[ys + e]);
+                    }
+                    const bool mine = act && ((k & 7) == warp);
+                    const unsigned grp = __match_any_sync(FULL, mine ? k : -1 - lane);
+                    const int gsz = __popc(grp);
+                    const int maxg = __reduce_max_sync(FULL, mine ? gsz : 0);
+                    const bool leader = mine && (__ffs(grp) - 1 == lane);
+                    double sacc = leader ? acc[k] : 0.0;
+                    for (int r = 0; r < maxg; ++r) {
+                        const unsigned src = __fns(grp, 0, r + 1);
+                        const double pv = __shfl_sync(FULL, prod, src & 31u);
+                        if (leader && r < gsz) sacc = __dadd_rn(sacc, pv);
+                    }
+                    if (leader) {
+                        acc[k] = sacc;
+                        atomicOr(flags + (k >> 5), 1u << (k & 31));
+                    }
+                    __syncwarp();
+                }
+                continue;
+            }
             const int nb = (int)(xe - jb < 32 ? xe - jb : 32);
             for (int t = 0; t < nb; ++t) {
                 const double xval = __shfl_sync(FULL, xl, t);
@@ -832,8 +946,25 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
         total = exclusive_scan_total(cnt.p, cro.p, n, s);
         tci.alloc(total, s);
         tv.alloc(total, s);
-        k_spgemm_dense<true><<<g, DENSE_THREADS, smem_num, s>>>(n, Y.ncols, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v,
-                                                                nullptr, cro.p, tci.p, tv.p);
+        // PMGR_SPGEMM_DENSE_FLAT: the barrier-free numeric pass when the right
+        // factor's rows average at most this many entries (0: never)
+        static const double dflat_mean = [] {
+            const char *e = getenv("PMGR_SPGEMM_DENSE_FLAT");
+            return e ? atof(e) : 8.0;  // C4: 153 -> 139 ms of dense products at 8, 221 ms at 64
+        }();
+        static bool dense_flat_attr = false;
+        if (!dense_flat_attr) {
+            const int maxs = (int)(sizeof(unsigned) * DENSE_COLS / 32 + 8 + sizeof(double) * DENSE_COLS);
+            PMGR_CUDA(cudaFuncSetAttribute(k_spgemm_dense<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           maxs));
+            dense_flat_attr = true;
+        }
+        if (dflat_mean > 0.0 && Y.nrows > 0 && (double)Y.nnz <= dflat_mean * (double)Y.nrows)
+            k_spgemm_dense<true, true><<<g, DENSE_THREADS, smem_num, s>>>(n, Y.ncols, X.ro, X.ci, X.v, Y.ro, Y.ci,
+                                                                          Y.v, nullptr, cro.p, tci.p, tv.p);
+        else
+            k_spgemm_dense<true><<<g, DENSE_THREADS, smem_num, s>>>(n, Y.ncols, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v,
+                                                                    nullptr, cro.p, tci.p, tv.p);
         PMGR_LAUNCHED();
         setup_trace("  spgemm dense", total, s);
     } else {
@@ -853,8 +984,19 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
                                        (int)smem_sym));
         PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_num));
+        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_sym));
+        PMGR_CUDA(cudaFuncSetAttribute(k_spgemm<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_num));
         attr_set = true;
     }
+    // PMGR_SPGEMM_FLAT: flattened (middle index, entry) pairs when the right
+    // factor's rows average at most this many entries (0: never)
+    static const double flat_mean = [] {
+        const char *e = getenv("PMGR_SPGEMM_FLAT");
+        return e ? atof(e) : 8.0;
+    }();
+    const bool flat = flat_mean > 0.0 && Y.nrows > 0 && (double)Y.nnz <= flat_mean * (double)Y.nrows;
     // resident warps: the occupancy each pass's shared tables allow
     auto grid_of = [&](const void *fn, size_t smem) {
         int per_sm = 0;
@@ -864,8 +1006,12 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
         return (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
     };
 
-    k_spgemm<false><<<grid_of((const void *)k_spgemm<false>, smem_sym), SP_WARPS * 32, smem_sym, s>>>(
-        n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
+    if (flat)
+        k_spgemm<false, true><<<grid_of((const void *)k_spgemm<false, true>, smem_sym), SP_WARPS * 32, smem_sym, s>>>(
+            n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
+    else
+        k_spgemm<false><<<grid_of((const void *)k_spgemm<false>, smem_sym), SP_WARPS * 32, smem_sym, s>>>(
+            n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, gkeys.p, nullptr, cnt.p, nullptr, nullptr, nullptr);
     PMGR_LAUNCHED();
     total = exclusive_scan_total(cnt.p, cro.p, n, s);
     setup_trace("  spgemm symbolic", total, s);
@@ -878,8 +1024,12 @@ void spgemm(const CsrView &X, const CsrView &Y, int mode, Csr &C, cudaStream_t s
     TBuf<double> nvals(ntotal, s);
     tci.alloc(total, s);
     tv.alloc(total, s);
-    k_spgemm<true><<<grid_of((const void *)k_spgemm<true>, smem_num), SP_WARPS * 32, smem_num, s>>>(
-        n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, nkeys.p, nvals.p, nullptr, cro.p, tci.p, tv.p);
+    if (flat)
+        k_spgemm<true, true><<<grid_of((const void *)k_spgemm<true, true>, smem_num), SP_WARPS * 32, smem_num, s>>>(
+            n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, nkeys.p, nvals.p, nullptr, cro.p, tci.p, tv.p);
+    else
+        k_spgemm<true><<<grid_of((const void *)k_spgemm<true>, smem_num), SP_WARPS * 32, smem_num, s>>>(
+            n, X.ro, X.ci, X.v, Y.ro, Y.ci, Y.v, ub.p, toff.p, nkeys.p, nvals.p, nullptr, cro.p, tci.p, tv.p);
     PMGR_LAUNCHED();
     setup_trace("  spgemm numeric", total, s);
     // only rows with more than SMALL_LIMIT_NUM entries (global tables) are unsorted
