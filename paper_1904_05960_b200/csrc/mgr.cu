@@ -37,6 +37,29 @@ __global__ void k_split(int64_t n, const int8_t *field, uint64_t cmask, int8_t *
     f64[i] = 1 - c;
 }
 
+// which field tags occur, and how many rows the C mask selects
+__global__ void k_field_stats(int64_t n, const int8_t *field, uint64_t cmask, int *seen, unsigned long long *nc) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long c = 0;
+    if (i < n) {
+        const int8_t t = field[i];
+        if (!seen[(uint8_t)t]) seen[(uint8_t)t] = 1;  // benign race: every writer stores 1
+        c = (cmask >> (t & 63)) & 1ull;
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(nc, c);
+}
+
+// the next level's layout: field / entity of the C rows, in order
+__global__ void k_restrict_layout(int64_t nc, const int64_t *c_rows, const int8_t *field, const int32_t *entity,
+                                  int8_t *field2, int32_t *entity2) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nc) return;
+    const int64_t i = c_rows[k];
+    field2[k] = field[i];
+    entity2[k] = entity[i];
+}
+
 __global__ void k_index_maps(int64_t n, const int8_t *is_c, const int64_t *cscan, const int64_t *fscan,
                              int64_t *c_index, int64_t *f_index, int64_t *c_rows, int64_t *f_rows) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -364,8 +387,22 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
     h->terminal_cycles = cfg.terminal_cycles > 1 ? cfg.terminal_cycles : 1;
     if (const char *e = getenv("PMGR_NO_GRAPHS")) h->use_graphs = (e[0] == '0');
     h->f_relax_post = cfg.f_relax_post;
-    std::vector<int8_t> fo(field_of_host, field_of_host + A0->nrows);
-    std::vector<int32_t> eo(entity_of_host, entity_of_host + A0->nrows);
+    // the layout (field tag and entity per row) lives on the device and is
+    // restricted to the C rows level by level there; the host copies exist
+    // only while a global smoother needs them (12.7M-row host loops cost
+    // ~100 ms per C4 setup)
+    TBuf<int8_t> dfo(A0->nrows, s);
+    TBuf<int32_t> deo(A0->nrows, s);
+    PMGR_CUDA(cudaMemcpyAsync(dfo.p, field_of_host, (size_t)A0->nrows, cudaMemcpyHostToDevice, s));
+    PMGR_CUDA(cudaMemcpyAsync(deo.p, entity_of_host, sizeof(int32_t) * (size_t)A0->nrows, cudaMemcpyHostToDevice, s));
+    bool any_smoother = false;
+    for (int lj = 0; lj < nlevels; ++lj) any_smoother |= specs[lj].global_smoother != PMGR_SMOOTHER_NONE;
+    std::vector<int8_t> fo;
+    std::vector<int32_t> eo;
+    if (any_smoother) {
+        fo.assign(field_of_host, field_of_host + A0->nrows);
+        eo.assign(entity_of_host, entity_of_host + A0->nrows);
+    }
     std::shared_ptr<const Csr> cur = A0;
     // FieldLayout ordering: interleaved while every restriction keeps the S/P
     // pairing, else downgraded (the mgr.py:359 x sparse.py:180-189 shim)
@@ -394,9 +431,23 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
             if (!ok) interleaved = false;
         }
         std::set<int> present;
+        int64_t nc_h = 0;
         {
-            bool seen[256] = {};
-            for (int8_t t : fo) seen[(uint8_t)t] = true;
+            const int64_t nl = cur->nrows;
+            TBuf<int> dseen(256, s);
+            TBuf<unsigned long long> dnc(1, s);
+            PMGR_CUDA(cudaMemsetAsync(dseen.p, 0, sizeof(int) * 256, s));
+            PMGR_CUDA(cudaMemsetAsync(dnc.p, 0, sizeof(unsigned long long), s));
+            if (nl > 0) {
+                k_field_stats<<<grid_for(nl, 256), 256, 0, s>>>(nl, dfo.p, sp.c_mask, dseen.p, dnc.p);
+                PMGR_LAUNCHED();
+            }
+            int seen[256];
+            unsigned long long ncv = 0;
+            PMGR_CUDA(cudaMemcpyAsync(seen, dseen.p, sizeof(seen), cudaMemcpyDeviceToHost, s));
+            PMGR_CUDA(cudaMemcpyAsync(&ncv, dnc.p, sizeof(ncv), cudaMemcpyDeviceToHost, s));
+            PMGR_CUDA(cudaStreamSynchronize(s));
+            nc_h = (int64_t)ncv;
             for (int t = 0; t < 256; ++t)
                 if (seen[t]) present.insert((int)(int8_t)t);
         }
@@ -417,8 +468,6 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         if (sp.f_relax == PMGR_FRELAX_EXACT) fail(PMGR_ERR_NOT_SUPPORTED, "exact F-relaxation is not on the device path");
         if (sp.quasi_impes) fail(PMGR_ERR_NOT_SUPPORTED, "quasi-IMPES is not on the device path");
         const int64_t n = cur->nrows;
-        int64_t nc_h = 0;
-        for (int8_t t : fo) nc_h += (sp.c_mask >> (t & 63)) & 1ull;
         if (nc_h == n) {
             if (present.size() != 1) fail(PMGR_ERR_INVALID, "an all-C level requires a single remaining field");
             break;  // reduction-free limit (mgr.py:347-352)
@@ -429,11 +478,9 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         L.nc = nc_h;
         L.nf = n - nc_h;
         // ---- split and index maps
-        TBuf<int8_t> field(n, s);
-        PMGR_CUDA(cudaMemcpyAsync(field.p, fo.data(), n, cudaMemcpyHostToDevice, s));
         L.is_c.alloc(n);
         TBuf<int64_t> c64(n, s), f64(n, s), cscan(n + 1, s), fscan(n + 1, s), c_index(n, s);
-        k_split<<<grid_for(n, 256), 256, 0, s>>>(n, field.p, sp.c_mask, L.is_c.p, c64.p, f64.p);
+        k_split<<<grid_for(n, 256), 256, 0, s>>>(n, dfo.p, sp.c_mask, L.is_c.p, c64.p, f64.p);
         PMGR_LAUNCHED();
         exclusive_scan_total(c64.p, cscan.p, n, s);
         exclusive_scan_total(f64.p, fscan.p, n, s);
@@ -470,8 +517,8 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         if (!dd && !A_ff->sj) csr_make_sj(*A_ff, s);
         if (li == 0 && A_ff->nbrows > 0) {
             // F rows first, then C rows: the same blocks lead A0 itself
-            bool prefix = true;
-            for (int64_t i = 0; i < n && prefix; ++i) prefix = (((sp.c_mask >> (fo[i] & 63)) & 1ull) != 0) == (i >= L.nf);
+            // (the C rows are the last nc rows exactly when the first of them is row nf)
+            const bool prefix = L.nc > 0 && read_scalar(L.c_rows.p, s) == L.nf;
             if (prefix) {
                 h->block_prefix = L.nf;
                 if (!dd) h->block_src = A_ff;
@@ -555,11 +602,9 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
                 Csr corr, kept;
                 csr_subtract(A_cc.view(), T.view(), corr, s);
                 TBuf<int32_t> ent(L.nc, s);
-                std::vector<int32_t> ec;
-                ec.reserve(L.nc);
-                for (int64_t i = 0; i < n; ++i)
-                    if ((sp.c_mask >> (fo[i] & 63)) & 1ull) ec.push_back(eo[i]);
-                PMGR_CUDA(cudaMemcpyAsync(ent.p, ec.data(), sizeof(int32_t) * L.nc, cudaMemcpyHostToDevice, s));
+                TBuf<int8_t> fdummy(L.nc, s);
+                k_restrict_layout<<<grid_for(L.nc, 256), 256, 0, s>>>(L.nc, L.c_rows.p, dfo.p, deo.p, fdummy.p, ent.p);
+                PMGR_LAUNCHED();
                 csr_sparsify(corr.view(), ent.p, sp.n_max, kept, s);
                 csr_subtract(A_cc.view(), kept.view(), *coarse, s);
                 PMGR_CUDA(cudaStreamSynchronize(s));
@@ -574,17 +619,29 @@ std::unique_ptr<pmgr_mgr> mgr_build(std::shared_ptr<const Csr> A0, const int8_t 
         L.zc.alloc(L.nc);
         L.tmpf.alloc(n > L.nf ? n : L.nf);
         // ---- next layout
-        std::vector<int8_t> fo2;
-        std::vector<int32_t> eo2;
-        fo2.reserve((size_t)L.nc);
-        eo2.reserve((size_t)L.nc);
-        for (int64_t i = 0; i < n; ++i)
-            if ((sp.c_mask >> (fo[i] & 63)) & 1ull) {
-                fo2.push_back(fo[i]);
-                eo2.push_back(eo[i]);
+        {
+            TBuf<int8_t> dfo2(L.nc, s);
+            TBuf<int32_t> deo2(L.nc, s);
+            if (L.nc > 0) {
+                k_restrict_layout<<<grid_for(L.nc, 256), 256, 0, s>>>(L.nc, L.c_rows.p, dfo.p, deo.p, dfo2.p, deo2.p);
+                PMGR_LAUNCHED();
             }
-        fo.swap(fo2);
-        eo.swap(eo2);
+            dfo = std::move(dfo2);
+            deo = std::move(deo2);
+        }
+        if (any_smoother) {
+            std::vector<int8_t> fo2;
+            std::vector<int32_t> eo2;
+            fo2.reserve((size_t)L.nc);
+            eo2.reserve((size_t)L.nc);
+            for (int64_t i = 0; i < n; ++i)
+                if ((sp.c_mask >> (fo[i] & 63)) & 1ull) {
+                    fo2.push_back(fo[i]);
+                    eo2.push_back(eo[i]);
+                }
+            fo.swap(fo2);
+            eo.swap(eo2);
+        }
         h->levels.push_back(std::move(L));
         cur = coarse;
         if (dd) dd->start = dC->start;
