@@ -60,6 +60,11 @@ PMGR_API const char *pmgr_last_error(void);
 PMGR_API int64_t pmgr_last_error_index(void);
 /* Number of kernel launches issued by this library so far (bench evidence). */
 PMGR_API int64_t pmgr_launch_count(void);
+/* Device memory of destroyed matrices / hierarchies is kept in a block cache
+ * and reused by the next setup (a repeated setup then allocates nothing);
+ * this returns the cached blocks to the driver.  The reference has no
+ * counterpart (NumPy arrays are freed by the garbage collector). */
+PMGR_API int pmgr_release_cached_memory(void);
 
 /* ---- sparse core (sparse.py) ------------------------------------------- */
 /* Copy a CSR matrix (host or device arrays) into library-owned device memory.

@@ -88,6 +88,7 @@ SIGNATURES = {
     "pmgr_last_error": (ctypes.c_char_p, []),
     "pmgr_last_error_index": (ctypes.c_int64, []),
     "pmgr_launch_count": (ctypes.c_int64, []),
+    "pmgr_release_cached_memory": (ctypes.c_int, []),
     "pmgr_csr_create": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, vp, vp, vp, ctypes.c_int,
                                        ctypes.c_int, vp, ctypes.POINTER(vp)]),
     "pmgr_csr_destroy": (ctypes.c_int, [vp]),
@@ -196,3 +197,9 @@ def check(status: int):
 
 def launch_count() -> int:
     return int(lib().pmgr_launch_count())
+
+
+def release_cached_memory() -> None:
+    """Return the device blocks libpmgr keeps for reuse (memory of destroyed
+    matrices and hierarchies) to the CUDA driver."""
+    check(lib().pmgr_release_cached_memory())

@@ -389,6 +389,13 @@ int pmgr_gmres_host(const pmgr_csr *A, pmgr_mgr *M, const double *b_host, double
     });
 }
 
+int pmgr_release_cached_memory(void) {
+    return guard([&] {
+        PMGR_CUDA(cudaDeviceSynchronize());
+        pmgr::dbuf_trim();
+    });
+}
+
 int pmgr_prof_enable(int on) {
     return guard([&] { pmgr::prof_enable(on != 0); });
 }
