@@ -90,6 +90,18 @@ __device__ __forceinline__ void block_sum2(double &a, double &b, double *sh) {
 constexpr int AO_THREADS = 256;
 constexpr int AO_UM = 10;  // phase 1: double2 loads per lane per basis vector batch
 constexpr int AO_WARPS = AO_THREADS / 32;
+// rows per shared-memory tile of the projection phase when the block's slice
+// does not fit (PMGR_ARNOLDI_TILE, multiple of 32; 0: off)
+inline int arnoldi_tile() {
+    static const int t = [] {
+        const char *e = getenv("PMGR_ARNOLDI_TILE");
+        int v = e ? atoi(e) : 2048;
+        if (v < 0) v = 0;
+        if (v > 8192) v = 8192;
+        return v / 32 * 32;
+    }();
+    return t;
+}
 
 struct AoParams {
     double *V;
@@ -107,6 +119,9 @@ struct AoParams {
     // split modes (row-distributed GMRES): projections and the squared norm
     // leave the kernel for a cross-rank all-reduce
     double *red, *nrm2;
+    // SM = false: rows per shared-memory tile of the projection phase (0: the
+    // w / V_j slices are re-read from L2 for every pair of basis vectors)
+    int tile;
 };
 
 __device__ __forceinline__ void stamp(const AoParams &P, int slot) {
@@ -170,7 +185,84 @@ __global__ void __launch_bounds__(AO_THREADS, 2) k_arnoldi(AoParams P) {
     // vectors at a time and issues every 16-byte load of both slices before
     // consuming them (one memory latency per pair for slices up to 640 rows);
     // slices are 256-byte aligned (ldv, chunk multiples of 32).
-    if constexpr (MODE == 0 || MODE == 1) {
+    if constexpr (!SM && (MODE == 0 || MODE == 1)) {
+        // large n: the block's slice does not fit shared memory.  Walk it in
+        // tiles of P.tile rows whose w / V_j parts are staged in shared memory
+        // once and reused by every pair of basis vectors (streaming them from
+        // L2 per pair doubled the phase's L2 traffic: 2.55 ms against 1.95 ms
+        // for the update phase at C4); the per-vector partials of the tiles
+        // are summed in tile order in hs / as_ (free until phase 2b).
+        if (P.tile > 0) {
+            const int tile = P.tile;
+            for (int k = threadIdx.x; k <= j; k += AO_THREADS) {
+                hs[k] = 0.0;
+                as_[k] = 0.0;
+            }
+            __syncthreads();
+            for (int64_t t0 = lo; t0 < hi; t0 += tile) {
+                const int64_t t1 = t0 + tile < hi ? t0 + tile : hi;
+                const int len = (int)(t1 - t0), len2 = len >> 1;
+                for (int64_t i = t0 + threadIdx.x; i < t1; i += AO_THREADS) {
+                    slice[i - t0] = P.w[i];
+                    slice[tile + (i - t0)] = vjg[i];
+                }
+                __syncthreads();
+                const double2 *w2 = reinterpret_cast<const double2 *>(slice);
+                const double2 *v2 = reinterpret_cast<const double2 *>(slice + tile);
+                for (int k = 2 * warp; k <= j; k += 2 * AO_WARPS) {
+                    double a0[2] = {0.0, 0.0}, a1[2] = {0.0, 0.0}, g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+                    for (int base = 0; base < len2; base += 32 * AO_UM) {
+                        double2 xs[2][AO_UM];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const double2 *x2 = reinterpret_cast<const double2 *>(P.V + (int64_t)(k + q) * ldv + t0);
+#pragma unroll
+                            for (int u = 0; u < AO_UM; ++u) {
+                                const int p = base + lane + 32 * u;
+                                xs[q][u] = (k + q <= j && p < len2) ? x2[p] : make_double2(0.0, 0.0);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < AO_UM; ++u) {
+                            const int p = base + lane + 32 * u;
+                            if (p < len2) {
+                                const double2 ww = w2[p], vv = v2[p];
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) {
+                                    a0[q] = fma(xs[q][u].x, ww.x, a0[q]);
+                                    a1[q] = fma(xs[q][u].y, ww.y, a1[q]);
+                                    g0[q] = fma(xs[q][u].x, vv.x, g0[q]);
+                                    g1[q] = fma(xs[q][u].y, vv.y, g1[q]);
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        if ((len & 1) && lane == 0 && k + q <= j) {  // odd last tile: its final row
+                            const double xl = P.V[(int64_t)(k + q) * ldv + t1 - 1];
+                            a0[q] = fma(xl, slice[len - 1], a0[q]);
+                            g0[q] = fma(xl, slice[tile + len - 1], g0[q]);
+                        }
+                        const double sa = warp_sum(a0[q] + a1[q]);
+                        const double sg = warp_sum(g0[q] + g1[q]);
+                        if (lane == 0 && k + q <= j) {  // this warp owns k and k + 1 in every tile
+                            hs[k + q] += sa;
+                            as_[k + q] += sg;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            for (int k = threadIdx.x; k <= j; k += AO_THREADS) {
+                P.pa[(int64_t)k * nblk + b] = hs[k];
+                P.pg[(int64_t)k * nblk + b] = as_[k];
+            }
+            __syncthreads();
+        }
+    }
+    if constexpr (MODE == 0 || MODE == 1)
+    if (SM || P.tile <= 0) {
         const int len = (int)(hi - lo), len2 = len >> 1;
         const double2 *w2 = reinterpret_cast<const double2 *>(SM ? wsl : P.w + lo);
         const double2 *v2 = reinterpret_cast<const double2 *>(SM ? vsl : vjg + lo);
@@ -610,6 +702,7 @@ struct Ws {
     int nblk = 1, nupd = 1;
     int64_t ldv = 0, chunk = 0;
     bool use_smem = false;
+    int tile = 0;  // projection tile rows of the global-memory variant
     size_t smem = 0;
     DBuf<double> V, w, z, r, vin, u;
     DBuf<double> H, G, cs, sn, g, a, h, y, hist, pa, pg, pn, beta;
@@ -693,6 +786,20 @@ Ws &workspace(const pmgr_csr *A, pmgr_mgr *M, int m, int max_iters, int64_t n) {
             cudaGetLastError();
             w->use_smem = false;
             w->smem = 0;
+            // projection tiles of the global-memory variant
+            const int tile = arnoldi_tile();
+            int per_sm_t = 0;
+            if (tile > 0 && chunk > tile &&
+                cudaFuncSetAttribute(k_arnoldi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * tile) ==
+                    cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, k_arnoldi<false>, AO_THREADS,
+                                                              (size_t)16 * tile) == cudaSuccess &&
+                (int64_t)per_sm_t * num_sms() >= w->nblk) {
+                w->tile = tile;
+                w->smem = (size_t)16 * tile;
+            } else {
+                cudaGetLastError();
+            }
         }
     }
     w->pa.alloc((int64_t)(m + 1) * w->nblk);
@@ -758,6 +865,7 @@ void arnoldi_step(const CsrView &Av, Ws &W, cudaStream_t s, cudaGraphConditional
     P.cond = cond;
     P.use_cond = use_cond;
     P.stamps = W.stamps.p;
+    P.tile = W.use_smem ? 0 : W.tile;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(W.nblk);
     cfg.blockDim = dim3(AO_THREADS);
@@ -1060,10 +1168,19 @@ void gmres_split(SplitOps &ops, const double *b, double *x, int nonzero_x0, cons
         PMGR_CUDA(cudaFuncSetAttribute(k_arnoldi<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         PMGR_CUDA(cudaFuncSetAttribute(k_arnoldi<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
+    size_t smem_t = 0;
+    if (!sm && n > 0 && arnoldi_tile() > 0 && chunk > arnoldi_tile() &&
+        cudaFuncSetAttribute(k_arnoldi<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             16 * arnoldi_tile()) == cudaSuccess) {
+        P.tile = arnoldi_tile();
+        smem_t = (size_t)16 * P.tile;
+    } else {
+        cudaGetLastError();
+    }
     auto step = [&](cudaStream_t st) {
         ops.step(st);  // w = A M vin
         if (sm) k_arnoldi<true, 1><<<nblk, AO_THREADS, smem, st>>>(P);
-        else k_arnoldi<false, 1><<<nblk, AO_THREADS, 0, st>>>(P);
+        else k_arnoldi<false, 1><<<nblk, AO_THREADS, smem_t, st>>>(P);
         PMGR_LAUNCHED();
         k_arnoldi<false, 2><<<nblk, AO_THREADS, 0, st>>>(P);
         PMGR_LAUNCHED();
