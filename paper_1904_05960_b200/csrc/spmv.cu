@@ -1160,8 +1160,8 @@ __global__ void __launch_bounds__(128) k_sj(SjView S, Op op, int trigger, unsign
 
 // operators without blocks: role B only (a fraction of k_sj's registers)
 // (six blocks per SM: 80 registers; level 1 of C4 704 us, 712 us uncapped at 92)
-template <int U, class Op>
-__global__ void __launch_bounds__(128, 6) k_sjs(SjView S, Op op, int trigger, int64_t cs0) {
+template <int U, class Op, int MINB = 6>
+__global__ void __launch_bounds__(128, MINB) k_sjs(SjView S, Op op, int trigger, int64_t cs0) {
     const int64_t r1 = S.r1 < 0 ? S.nrows : S.r1;
     sj_role_b<U>(S, op, trigger, cs0 + (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5), threadIdx.x & 31, r1);
 }
@@ -1424,7 +1424,21 @@ void launch_sj(const CsrView &A, const Op &op, cudaStream_t s) {
         else if (u <= 4) PMGR_SJ_GO(4, 3);
         else PMGR_SJ_GO(8, 3);
     } else {
-        if (u <= 2) launch_pdl(k_sjs<2, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        // PMGR_SJ_SHORT_MINB: blocks per SM the short-row variants (two / four
+        // positions per chunk: prolongations, restrictions, the 7-point
+        // pressure levels) are compiled for: their one or two chunks per row
+        // are a chain of dependent round trips, so more resident warps help
+        // (12 blocks = 40 registers: C4 MGR apply 15.64 -> 15.54 ms, the AMG
+        // prolongation 98 -> 86 us)
+        static const int short_minb = [] {
+            const char *e = getenv("PMGR_SJ_SHORT_MINB");
+            return e ? atoi(e) : 12;
+        }();
+        if (u <= 2 && short_minb == 12) launch_pdl(k_sjs<2, Op, 12>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else if (u <= 2 && short_minb == 10) launch_pdl(k_sjs<2, Op, 10>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else if (u <= 4 && short_minb == 12) launch_pdl(k_sjs<4, Op, 12>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else if (u <= 4 && short_minb == 10) launch_pdl(k_sjs<4, Op, 10>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
+        else if (u <= 2) launch_pdl(k_sjs<2, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else if (u <= 4) launch_pdl(k_sjs<4, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else launch_pdl(k_sjs<8, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
     }
