@@ -1424,9 +1424,8 @@ void launch_sj(const CsrView &A, const Op &op, cudaStream_t s) {
         else if (u <= 4) PMGR_SJ_GO(4, 3);
         else PMGR_SJ_GO(8, 3);
     } else {
-        // PMGR_SJ_SHORT_MINB: blocks per SM the short-row variants (two / four
-        // positions per chunk: prolongations, restrictions, the 7-point
-        // pressure levels) are compiled for: their one or two chunks per row
+        // PMGR_SJ_SHORT_MINB: blocks per SM the shortest-row variant (two
+        // positions per chunk: prolongations, restrictions) is compiled for: their one or two chunks per row
         // are a chain of dependent round trips, so more resident warps help
         // (12 blocks = 40 registers: C4 MGR apply 15.64 -> 15.54 ms, the AMG
         // prolongation 98 -> 86 us)
@@ -1434,10 +1433,11 @@ void launch_sj(const CsrView &A, const Op &op, cudaStream_t s) {
             const char *e = getenv("PMGR_SJ_SHORT_MINB");
             return e ? atoi(e) : 12;
         }();
+        // (the four-position variant spills at 40 registers and measured slower:
+        // it keeps six blocks per SM; a persistent grid-stride grid for the
+        // short-row operators measured 15.65-15.80 ms against 15.61)
         if (u <= 2 && short_minb == 12) launch_pdl(k_sjs<2, Op, 12>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else if (u <= 2 && short_minb == 10) launch_pdl(k_sjs<2, Op, 10>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
-        else if (u <= 4 && short_minb == 12) launch_pdl(k_sjs<4, Op, 12>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
-        else if (u <= 4 && short_minb == 10) launch_pdl(k_sjs<4, Op, 10>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else if (u <= 2) launch_pdl(k_sjs<2, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else if (u <= 4) launch_pdl(k_sjs<4, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
         else launch_pdl(k_sjs<8, Op>, dim3(gb), dim3(128), 0, s, J, op, trig, cs0);
