@@ -494,9 +494,18 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
     if (dist && dist->nranks > 1) dd.reset(new DistSetup(*dist));
     auto replicate = [&](bool force) {
         if (dd && (force || cur->nrows <= dd->replicate_below)) {
+            // a pure block operator (the node-blocked displacement block) keeps
+            // its 3x3 block copy when gathered: the block kernels sum in another
+            // order than the CSR ones, and the gathered level must apply exactly
+            // like the single-GPU hierarchy's
+            const bool blocks = cur->nbrows > 0 && cur->nbrows * 3 == cur->nrows && cur->nrem == 0;
             auto full = std::make_shared<Csr>();
             ds_gather_rows(*dd, *cur, *full, s);
-            csr_finalize(*full, s);
+            csr_finalize(*full, s, !blocks);
+            if (blocks) {
+                csr_make_bsr3(*full, full->nrows, full->ncols, s, true);
+                if (!full->sj) csr_make_sj(*full, s);
+            }
             cur = full;
             dd.reset();
         }
