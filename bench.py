@@ -320,7 +320,16 @@ def run_gpu_dist(args, rank, world, local_rank):
     # weak scaling = the C5 slab stack (ns^3 cells per GPU), strong scaling =
     # the fixed C4 128^3 problem
     ns = args.slab
-    if not args.weak:
+    c3 = (not args.weak) and args.config == "C3"
+    if c3:
+        # C3 (64^3, "1 GPU and 2 GPUs"): its production configuration has an
+        # ILU(1) global smoother, which the row distribution takes from a
+        # hierarchy built whole on every rank (the partitions of 16 flow rows
+        # fall on the z-slab boundaries); 1.3M dofs set up in 0.13 s
+        base = problems.make("C3", seed=args.seed, device=True)
+        opts = problems.solver_options("C3", base, variant=args.dist_variant)
+        args.replicated_setup = True
+    elif not args.weak:
         base = problems.make_c4(seed=args.seed, n=128, device=True)
         opts = problems.solver_options("C4", base, variant=args.dist_variant)
     else:
@@ -424,7 +433,9 @@ def run_gpu_dist(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, paper_1904_05960_b200/problems.py)",
-            "config": {"workload": ("C4: three-phase poromechanics 128^3 over " + f"{world} GPU(s) (rank-major z-slabs)"
+            "config": {"workload": ("C3: two-phase layered poromechanics 64^3 over " + f"{world} GPU(s) (rank-major z-slabs)"
+                                    if c3 else
+                                    "C4: three-phase poromechanics 128^3 over " + f"{world} GPU(s) (rank-major z-slabs)"
                                     if not args.weak else
                                     f"C5: two-phase poromechanics {ns}x{ns}x{ns * world} ({ns}^3 cells per GPU, "
                                     "rank-major z-slabs)") + " -- MGR-preconditioned GMRES to rtol 1e-6",

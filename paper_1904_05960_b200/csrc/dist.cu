@@ -1058,7 +1058,8 @@ std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, cons
     if (M->f_relax_post || M->terminal_cycles != 1)
         fail(PMGR_ERR_NOT_SUPPORTED, "row distribution supports pre F-relaxation and one terminal cycle");
     for (const MgrLevel &L : M->levels) {
-        if (L.smoother) fail(PMGR_ERR_NOT_SUPPORTED, "row distribution of a level with a global smoother");
+        if (L.smoother && partial)
+            fail(PMGR_ERR_NOT_SUPPORTED, "distributed setup of a level with a global smoother");
         if (L.f_relax == PMGR_FRELAX_NONE || (L.f_relax_sweeps != 1 && L.f_relax != PMGR_FRELAX_AMG))
             fail(PMGR_ERR_NOT_SUPPORTED,
                  "row distribution supports AMG F-relaxation (any number of cycles) or single-sweep Jacobi");
@@ -1080,6 +1081,10 @@ std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, cons
         Ms.push_back(C);
         B.read(F, &L.A_cf, C);
         B.read(C, &L.P, Ms[l]);
+        if (L.smoother) {  // the smoothed iterate is read by the level operator and its C rows
+            B.read(Ms[l], L.A.get(), Ms[l]);
+            B.read(Ms[l], &L.A_c, C);
+        }
         if (L.f_relax == PMGR_FRELAX_AMG) plan_amg(B, *L.amg, F, fplans[l]);
     }
     AmgPlan tplan;
@@ -1132,6 +1137,19 @@ std::unique_ptr<DistSolver> dist_build_impl(const pmgr_csr *A, pmgr_mgr *M, cons
         B.ext_buffer(C, L.rc);
         B.ext_buffer(C, L.zc);
         if (G.f_relax == PMGR_FRELAX_AMG) L.amg = build_amg(B, fplans[l]);
+        if (G.smoother) {
+            // ILU partitions live whole on their ranks: the rank's factors are
+            // rows of the global ones, the level operator and its C rows are
+            // localised like every other operator
+            L.smoother = smoother_slice(*G.smoother, Mi->lo, Mi->hi, s);
+            L.halo_m = Mi->halo;
+            auto Al = std::make_shared<Csr>();
+            B.localize(*G.A, Mi, Mi, *Al);
+            L.A = Al;
+            B.localize(G.A_c, C, Mi, L.A_c);
+            B.ext_buffer(Mi, L.zs);
+            B.ext_buffer(Mi, L.rr);
+        }
     }
     h->terminal = build_amg(B, tplan);
     PMGR_CUDA(cudaStreamSynchronize(s));

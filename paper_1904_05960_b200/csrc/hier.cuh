@@ -143,6 +143,11 @@ std::unique_ptr<GlobalSmoother> smoother_build(std::shared_ptr<const Csr> A, int
                                                int64_t npartitions, bool interleaved, const int8_t *field_of,
                                                const int32_t *entity_of, cudaStream_t s);
 void smoother_apply(GlobalSmoother &g, const double *v, double *z, cudaStream_t s);
+// the smoother of the rows [lo, hi) of g's level for a rank that owns them:
+// ILU(k) with one thread per partition only, and only when the partition
+// boundaries fall on lo and hi (every partition then lives on one rank, the
+// factors are the global ones row for row and the application is local)
+std::unique_ptr<GlobalSmoother> smoother_slice(const GlobalSmoother &g, int64_t lo, int64_t hi, cudaStream_t s);
 
 // One MGR reduction level (reference mgr.py:300-311).
 struct MgrLevel {
@@ -167,6 +172,7 @@ struct MgrLevel {
     // of the F space (read by A_CF) and of the C space (read by P)
     int64_t off = 0, off_f = 0, off_c = 0;
     std::shared_ptr<Halo> halo_f, halo_c;
+    std::shared_ptr<Halo> halo_m;  // of the level space itself (read by A and A_c behind a global smoother)
 };
 
 }  // namespace pmgr

@@ -255,35 +255,40 @@ void f_relax_apply(MgrLevel &L, const double *vf, double *zf, cudaStream_t s) {
 // A level with a global smoother (mgr.py:411-429): z = S v; F-relaxation on
 // the residual v - A z; C residual of the smoothed z; coarse correction.
 void apply_level_smoothed(pmgr_mgr &h, size_t l, const double *v, double *z, cudaStream_t s) {
+    // vectors in the level's ext layout (row-distributed: owned range at
+    // L.off, the smoother local to the rank's partitions, ghosts of zs
+    // exchanged before A and A_c read them; offsets 0 and no-ops on one GPU)
     MgrLevel &L = h.levels[l];
-    const int64_t n = L.n;
-    smoother_apply(*L.smoother, v, L.zs.p, s);
+    const int64_t o = L.off, of = L.off_f;
+    smoother_apply(*L.smoother, v + o, L.zs.p + o, s);
     auto f_relax_on = [&](const double *r, double *zacc) {  // zacc[F] += M_FF^{-1} r[F]
         bool done = false;
         if (L.f_relax_sweeps == 1) {
             if (L.f_relax == PMGR_FRELAX_AMG) {
                 done = amg_cycle_rows(*L.amg, r, L.f_rows.p, L.zf.p, s);
             } else {
-                vec_scale_gather(r, L.f_rows.p, L.dinv_ff.p, L.nf, L.zf.p, s);
+                vec_scale_gather(r, L.f_rows.p + of, L.dinv_ff.p + of, L.nf, L.zf.p + of, s);
                 done = true;
             }
         }
         if (!done) {
-            vec_gather(r, L.f_rows.p, L.nf, L.vf.p, s);
+            vec_gather(r, L.f_rows.p + of, L.nf, L.vf.p + of, s);
             f_relax_apply(L, L.vf.p, L.zf.p, s);
         }
         ledger(32.0 * L.nf);
-        k_scatter_add<<<grid_for(L.nf, 256), 256, 0, s>>>(L.zf.p, L.f_rows.p, L.nf, zacc);
+        k_scatter_add<<<grid_for(L.nf, 256), 256, 0, s>>>(L.zf.p + of, L.f_rows.p + of, L.nf, zacc);
         PMGR_LAUNCHED();
     };
     if (!h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
-        spmv_residual(L.A->view(), L.zs.p, v, L.rr.p, s);
+        with_halo(*L.A, L.halo_m.get(), L.zs.p, s,
+                  [&](const CsrView &V) { spmv_residual(V, L.zs.p, v, L.rr.p, s); });
         f_relax_on(L.rr.p, L.zs.p);
     }
-    spmv_resid_rows(L.A_c.view(), L.zs.p, v, L.c_rows.p, L.rc.p, ResidNext{}, s);
+    with_halo(L.A_c, L.halo_m.get(), L.zs.p, s,
+              [&](const CsrView &V) { spmv_resid_rows(V, L.zs.p, v, L.c_rows.p, L.rc.p, ResidNext{}, s); });
     apply_level(h, l + 1, L.rc.p, L.zc.p, s, false);
-    vec_copy(L.zs.p, z, n, s);
-    spmv_add(L.P.view(), L.zc.p, z, s);
+    vec_copy(L.zs.p + o, z + o, L.n, s);
+    with_halo(L.P, L.halo_c.get(), L.zc.p, s, [&](const CsrView &V) { spmv_add(V, L.zc.p, z, s); });
     if (h.f_relax_post && L.f_relax != PMGR_FRELAX_NONE) {
         spmv_residual(L.A->view(), z, v, L.rr.p, s);
         f_relax_on(L.rr.p, z);

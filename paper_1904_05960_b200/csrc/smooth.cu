@@ -650,6 +650,52 @@ std::unique_ptr<GlobalSmoother> smoother_build(std::shared_ptr<const Csr> A, int
 }
 
 // z = S v (x0 = 0); z may not alias v
+namespace {
+__global__ void k_lu_slice(int64_t n, int64_t lo, int64_t e0, const int64_t *ro, const int32_t *ci, const double *v,
+                           const int64_t *dpos, int64_t *oro, int32_t *oci, double *ov, int64_t *odpos) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    oro[i] = ro[lo + i] - e0;
+    if (i == n) return;
+    odpos[i] = dpos[lo + i] - e0;
+    for (int64_t q = ro[lo + i]; q < ro[lo + i + 1]; ++q) {
+        oci[q - e0] = ci[q] - (int32_t)lo;
+        ov[q - e0] = v[q];
+    }
+}
+}  // namespace
+
+std::unique_ptr<GlobalSmoother> smoother_slice(const GlobalSmoother &g, int64_t lo, int64_t hi, cudaStream_t s) {
+    if (g.kind != PMGR_SMOOTHER_ILU || g.leveled)
+        fail(PMGR_ERR_NOT_SUPPORTED,
+             "row distribution of a global smoother supports ILU(k) over short partitions (one thread per partition)");
+    std::vector<int64_t> st((size_t)g.nparts + 1);
+    PMGR_CUDA(cudaMemcpyAsync(st.data(), g.starts.p, sizeof(int64_t) * st.size(), cudaMemcpyDeviceToHost, s));
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    const auto a = std::lower_bound(st.begin(), st.end(), lo), b = std::lower_bound(st.begin(), st.end(), hi);
+    if (a == st.end() || *a != lo || b == st.end() || *b != hi)
+        fail(PMGR_ERR_NOT_SUPPORTED,
+             "row distribution of an ILU smoother needs its partition boundaries on the rank boundaries");
+    auto out = std::make_unique<GlobalSmoother>();
+    out->kind = PMGR_SMOOTHER_ILU;
+    out->n = hi - lo;
+    std::vector<int64_t> ls(a, b + 1);
+    for (int64_t &x : ls) x -= lo;
+    out->nparts = (int64_t)ls.size() - 1;
+    upload(out->starts, ls, s);
+    const int64_t n = hi - lo;
+    int64_t e0 = 0, e1 = 0;
+    PMGR_CUDA(cudaMemcpyAsync(&e0, g.lu.ro.p + lo, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PMGR_CUDA(cudaMemcpyAsync(&e1, g.lu.ro.p + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PMGR_CUDA(cudaStreamSynchronize(s));
+    out->lu.alloc(n, n, e1 - e0);
+    out->dpos.alloc(n);
+    k_lu_slice<<<grid_for(n + 1, 128), 128, 0, s>>>(n, lo, e0, g.lu.ro.p, g.lu.ci.p, g.lu.v.p, g.dpos.p, out->lu.ro.p,
+                                                    out->lu.ci.p, out->lu.v.p, out->dpos.p);
+    PMGR_LAUNCHED();
+    return out;
+}
+
 void smoother_apply(GlobalSmoother &g, const double *v, double *z, cudaStream_t s) {
     const int64_t n = g.n;
     if (n == 0) return;
