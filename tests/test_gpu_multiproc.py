@@ -33,6 +33,8 @@ from paper_1904_05960_b200 import dist as D, krylov, mgr, problems, sparse
 name = sys.argv[2]
 if name == "C5":
     base = problems.make_c5(seed=4, nxy=10, nz_per_gpu=5, gpus=2)
+elif name == "C3":
+    base = problems.make("C3", seed=4, n=8)
 else:
     base = problems.make_c4(seed=4, n=8)
 pb, bounds = problems.rank_major(base, world)
@@ -42,7 +44,12 @@ A = sparse.CsrMatrix(pb.n, pb.n, pb.row_offsets, pb.col_indices, pb.values)
 lay = sparse.FieldLayout(pb.field_of, pb.entity_of)
 tr = D.host_transport(rank, world, tdist)
 lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-solver = D.DeviceDistSetupSolver(D.row_slice(A, lo, hi), lay, cfg, bounds, rank, world, tr)
+if name == "C3":
+    # ILU(1) global smoother level: sliced from a hierarchy built whole in every process
+    h_whole = mgr.mgr_setup(A, lay, cfg)
+    solver = D.DeviceDistSolver(h_whole, bounds, rank, world, tr)
+else:
+    solver = D.DeviceDistSetupSolver(D.row_slice(A, lo, hi), lay, cfg, bounds, rank, world, tr)
 assert (solver.lo, solver.n_own) == (lo, hi - lo)
 v = np.random.default_rng(11).standard_normal(pb.n)
 z_own = solver.apply(v[lo:hi]).cpu()
@@ -83,7 +90,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name", ["C5", "C4"])
+@pytest.mark.parametrize("name", ["C5", "C4", "C3"])
 def test_two_processes_host_transport_vs_oracle(name):
     import json
 
