@@ -64,6 +64,7 @@ PROD_CASES = {
 FULL_CASES = {
     "c3_64p": ("C3", dict(n=64)),
     "c4_128p": ("C4", dict(n=128)),
+    "c5_128p": ("C5", dict(nxy=128, nz_per_gpu=128, gpus=1)),
 }
 
 
