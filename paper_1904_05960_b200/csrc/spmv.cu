@@ -1014,8 +1014,10 @@ __device__ __forceinline__ double sj_scalar_slice(const int32_t *__restrict__ ci
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const bool ld = (act >> u) & 1u;
-            nv[u] = ld ? __ldg(vb + q[u]) : 0.0;
-            nc[u] = ld ? __ldg(cb + q[u]) : -1;
+            // streamed once per pass: evict-first, so the gathered vector keeps
+            // its lines (C4 AMG level 1: 737 -> 725 us, MGR apply -0.09 ms)
+            nv[u] = ld ? __ldcs(vb + q[u]) : 0.0;
+            nc[u] = ld ? __ldcs(cb + q[u]) : -1;
         }
     };
     fetch(0);
