@@ -3,6 +3,7 @@
 // Every entry point catches pmgr::Error and converts it into a status code
 // plus a thread-local message / row index that the Python layer turns back
 // into the reference's exception (ValueError / RuntimeError / ...).
+#include <mutex>
 #include <cstring>
 #include <string>
 
@@ -162,6 +163,8 @@ int pmgr_csr_download(const pmgr_csr *A, int64_t *row_offsets, int32_t *col_indi
 // applied: MGR setup builds it from the block-prefix copy; a matrix used
 // without one (matvec, AMG level 0, unpreconditioned GMRES) builds it here.
 static void ensure_sj(const pmgr_csr *A, void *stream) {
+    static std::mutex mu;  // two threads may apply the same matrix for the first time
+    std::lock_guard<std::mutex> lock(mu);
     pmgr::Csr &m = *A->m;
     if (m.sj_want && !m.sj && !m.sj_tried) {
         pmgr::csr_make_sj(m, S(stream));
