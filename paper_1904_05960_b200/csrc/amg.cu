@@ -744,29 +744,19 @@ std::unique_ptr<pmgr_amg> amg_build(std::shared_ptr<const Csr> A0, const pmgr_am
         } else {
             TBuf<int64_t> piv(1, s);
             const unsigned gx = grid_for(nc, 256);
-            // 5 nc dependent launches: recorded once as a CUDA graph (launch
-            // latency ~1 us per node instead of ~5 us per stream launch)
-            cudaStream_t cs;
-            PMGR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-            cudaGraph_t graph = nullptr;
-            PMGR_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            // five dependent launches per pivot, straight on the stream: the
+            // kernels of one pivot take ~30 us, more than their launches cost,
+            // so a recorded CUDA graph bought nothing (70 ms either way at
+            // nc = 2,034) and its capture broke when several ranks' host
+            // threads set up at once (the emulated-rank harness)
             for (int64_t k = 0; k < nc; ++k) {
-                k_gj_pivot<<<1, 1024, 0, cs>>>(nc, k, M.p, piv.p, sing.p);
-                k_gj_swap<<<gx, 256, 0, cs>>>(nc, k, piv.p, M.p, h->coarse_inv.p);
-                k_gj_col<<<gx, 256, 0, cs>>>(nc, k, M.p, colk.p);
-                k_gj_scale<<<gx, 256, 0, cs>>>(nc, k, colk.p, M.p, h->coarse_inv.p);
-                k_gj_elim<<<dim3(gx, (unsigned)nc), 256, 0, cs>>>(nc, k, colk.p, M.p, h->coarse_inv.p);
+                k_gj_pivot<<<1, 1024, 0, s>>>(nc, k, M.p, piv.p, sing.p);
+                k_gj_swap<<<gx, 256, 0, s>>>(nc, k, piv.p, M.p, h->coarse_inv.p);
+                k_gj_col<<<gx, 256, 0, s>>>(nc, k, M.p, colk.p);
+                k_gj_scale<<<gx, 256, 0, s>>>(nc, k, colk.p, M.p, h->coarse_inv.p);
+                k_gj_elim<<<dim3(gx, (unsigned)nc), 256, 0, s>>>(nc, k, colk.p, M.p, h->coarse_inv.p);
             }
-            const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-            if (ce != cudaSuccess) fail_cuda(ce, "capture of the coarsest inverse", __FILE__, __LINE__);
-            cudaGraphExec_t ex = nullptr;
-            PMGR_CUDA(cudaGraphInstantiate(&ex, graph, 0));
-            PMGR_CUDA(cudaStreamSynchronize(s));  // M, colk, piv were produced on s
-            PMGR_CUDA(cudaGraphLaunch(ex, s));
-            PMGR_CUDA(cudaStreamSynchronize(s));
-            PMGR_CUDA(cudaGraphExecDestroy(ex));
-            PMGR_CUDA(cudaGraphDestroy(graph));
-            PMGR_CUDA(cudaStreamDestroy(cs));
+            PMGR_CUDA(cudaPeekAtLastError());
             g_launches.fetch_add(5 * nc, std::memory_order_relaxed);
         }
         PMGR_CUDA(cudaStreamSynchronize(s));
