@@ -3,7 +3,7 @@ one GPU (loopback transport): the application against the single-GPU
 hierarchy's (bitwise at the default thresholds) and the distributed GMRES's
 iteration count.  The only way to run the multi-rank setup at the headline
 size on a one-GPU box.
-    python tools/c4_dist_probe.py [nranks]"""
+    python tools/c4_dist_probe.py [nranks] [C4|C5 [slab]]"""
 import os
 import sys
 import time
@@ -17,7 +17,11 @@ from paper_1904_05960_b200 import dist as D, krylov, mgr, problems, sparse  # no
 
 nranks = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 name = sys.argv[2] if len(sys.argv) > 2 else "C4"
-base = problems.make(name, device=True)
+if name == "C5":  # the weak-scaling stack: a 128^3 slab per rank
+    ns = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+    base = problems.make_c5(seed=0, nxy=ns, nz_per_gpu=ns, gpus=nranks, device=True)
+else:
+    base = problems.make(name, device=True)
 pb, bounds = problems.rank_major(base, nranks)
 del base
 opts = problems.solver_options(name, pb)
@@ -27,16 +31,18 @@ h = mgr.mgr_setup(pb.A, lay, cfg)
 v = torch.randn(pb.n, dtype=torch.float64, device="cuda")
 z = h.apply(v)
 torch.cuda.synchronize()
+b = torch.from_numpy(pb.rhs).cuda()
+gcfg = krylov.GmresConfig(restart=opts["restart"], max_iters=opts["max_iters"], rtol=opts["rtol"])
+x1, st = krylov.gmres(pb.A, h.apply, b, cfg=gcfg)
+del h  # the emulated ranks need the memory
+from paper_1904_05960_b200 import _lib  # noqa: E402
+_lib.release_cached_memory()
 t = time.time()
 zs = D.emulate_setup_apply(pb.A, lay, cfg, bounds, v)
 torch.cuda.synchronize()
 print(f"{name} over {nranks} emulated ranks: distributed setup + apply {time.time() - t:.1f} s; bitwise",
       bool(torch.equal(zs, z)), "max diff", float((zs - z).abs().max()), flush=True)
 del zs
-gcfg = krylov.GmresConfig(restart=opts["restart"], max_iters=opts["max_iters"], rtol=opts["rtol"])
-b = torch.from_numpy(pb.rhs).cuda()
-x1, st = krylov.gmres(pb.A, h.apply, b, cfg=gcfg)
-del h
 torch.cuda.synchronize()
 t = time.time()
 xd, its, conv = D.emulate_setup_gmres(pb.A, lay, cfg, bounds, b, gcfg)
